@@ -1,0 +1,233 @@
+"""CPU oracle for the RailS hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import this package.  It shares no code with the
+CUDA path (``paper_2510_19262_b200``) and never imports it.
+
+The arithmetic lives in ``oracle.c`` (plain C, one function per paper step, each
+citing the PAPER.md passage it follows); this module only marshals numpy arrays
+through ctypes and strings the per-node steps together in the paper's order
+(Alg. 2).  ``brute.py`` holds the exhaustive optimum for tiny inputs.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc (no FP contraction: R#25)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(
+            ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fPIC", "-shared",
+             "-o", _LIB, _SRC])
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        P = ctypes.c_void_p
+        i32, i64, u64, dbl = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
+        L.orc_mix64.restype = u64
+        L.orc_mix64.argtypes = [u64]
+        L.orc_ecmp_rail.restype = i32
+        L.orc_ecmp_rail.argtypes = [u64, i64, i64, i32]
+        L.orc_histogram_node.restype = ctypes.c_int
+        L.orc_histogram_node.argtypes = [i32, i32, i32, i32, i32, P, P, i32, i64, P, P, P]
+        L.orc_chunk_count.restype = i64
+        L.orc_chunk_count.argtypes = [i32, i64, P, i64]
+        L.orc_split.restype = i64
+        L.orc_split.argtypes = [i32, i64, P, i64, P, P, P, P]
+        L.orc_lpt.restype = None
+        L.orc_lpt.argtypes = [i64, i32, P, P, P, P, P]
+        L.orc_compact.restype = None
+        L.orc_compact.argtypes = [i32, i64, P, i64, i64, P, P, P, P, P, P, P, P, P, P, P]
+        L.orc_mse.restype = dbl
+        L.orc_mse.argtypes = [i32, P]
+        L.orc_nmse.restype = dbl
+        L.orc_nmse.argtypes = [i32, P]
+        L.orc_eval.restype = None
+        L.orc_eval.argtypes = [i32, i32, dbl, u64, P, i64, P, P, P, P, P, P, P, P, P, P, P, P]
+        L.orc_pack_node.restype = ctypes.c_int
+        L.orc_pack_node.argtypes = [i32, i32, i32, i32, i32, i64, i64, P, P, P, P, i64,
+                                    P, P, P, P, P, P, P, P, i64]
+        _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    assert a.flags["C_CONTIGUOUS"], "oracle arrays must be C-contiguous"
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _c(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+DEFAULT_ECMP_SEED = 0x9E3779B97F4A7C15  # R#14
+
+
+# ------------------------------------------------------------------ scalars
+def mix64(z: int) -> int:
+    return int(lib().orc_mix64(z & 0xFFFFFFFFFFFFFFFF))
+
+
+def ecmp_rail(seed: int, src: int, dst: int, N: int) -> int:
+    return int(lib().orc_ecmp_rail(seed & 0xFFFFFFFFFFFFFFFF, src, dst, N))
+
+
+def mse(loads) -> float:
+    L = _c(loads, np.int64)
+    return float(lib().orc_mse(len(L), _p(L)))
+
+
+def nmse(loads) -> float:
+    L = _c(loads, np.int64)
+    return float(lib().orc_nmse(len(L), _p(L)))
+
+
+# ------------------------------------------------------------------ steps
+def histogram_node(M, N, d, T, k, topk_node, lut, row_bytes, with_rank=True):
+    """a1 for node d: topk_node int32 [N][T][k] -> counts [N][G], msg [N][G], rank."""
+    G = M * N
+    topk_node = _c(topk_node, np.int32)
+    lut = _c(lut, np.int32)
+    counts = np.zeros((N, G), np.int32)
+    msg = np.zeros((N, G), np.int64)
+    rank = np.zeros((N, T, k), np.int32) if with_rank else None
+    rc = lib().orc_histogram_node(M, N, d, T, k, _p(topk_node), _p(lut), len(lut), row_bytes,
+                                  _p(counts), _p(msg), _p(rank) if with_rank else None)
+    if rc != 0:
+        raise ValueError("oracle histogram: routing id out of range")
+    return counts, msg, rank
+
+
+def split(msg_node, C):
+    """a2: msg_node int64 [N][G] -> chunk arrays in emission order (g, h, c)."""
+    msg_node = _c(msg_node, np.int64)
+    N, G = msg_node.shape
+    F = int(lib().orc_chunk_count(N, G, _p(msg_node), C))
+    ch = dict(g=np.zeros(F, np.int32), h=np.zeros(F, np.int32),
+              c=np.zeros(F, np.int64), size=np.zeros(F, np.int64))
+    F2 = lib().orc_split(N, G, _p(msg_node), C, _p(ch["g"]), _p(ch["h"]), _p(ch["c"]),
+                         _p(ch["size"]))
+    assert F2 == F
+    return ch
+
+
+def lpt(w, N):
+    """Alg. 2 steps 2-3 on weights given in tie-break order.
+    Returns (order, rail, off, load)."""
+    w = _c(w, np.int64)
+    F = len(w)
+    order = np.zeros(F, np.int64)
+    rail = np.zeros(F, np.int32)
+    off = np.zeros(F, np.int64)
+    load = np.zeros(N, np.int64)
+    lib().orc_lpt(F, N, _p(w), _p(order), _p(rail), _p(off), _p(load))
+    return order, rail, off, load
+
+
+def compact(msg_node, C, ch, rail, off):
+    msg_node = _c(msg_node, np.int64)
+    N, G = msg_node.shape
+    F = len(ch["size"])
+    full_base = np.zeros((N, G), np.int64)
+    rem_rail = np.zeros((N, G), np.int8)
+    rem_off = np.zeros((N, G), np.int64)
+    n_full = np.zeros(1, np.int64)
+    n_rem = np.zeros(1, np.int32)
+    lib().orc_compact(N, G, _p(msg_node), C, F, _p(ch["g"]), _p(ch["h"]), _p(ch["c"]),
+                      _p(ch["size"]), _p(rail), _p(off), _p(full_base), _p(rem_rail),
+                      _p(rem_off), _p(n_full), _p(n_rem))
+    return dict(full_base=full_base, rem_rail=rem_rail, rem_off=rem_off,
+                n_full=int(n_full[0]), n_rem=int(n_rem[0]))
+
+
+def schedule_node(msg_node, C):
+    """a2-a4 for one node: chunks, LPT per chunk, compact schedule, LoadState."""
+    msg_node = _c(msg_node, np.int64)
+    N = msg_node.shape[0]
+    ch = split(msg_node, C)
+    order, rail, off, load = lpt(ch["size"], N)
+    comp = compact(msg_node, C, ch, rail, off)
+    return dict(chunks=ch, order=order, rail=rail, off=off, send_load=load, **comp)
+
+
+def eval_unit(M, N, R2, ecmp_seed, msg_unit, ch_d, ch_h, ch_size, ch_rail):
+    """a5 for one unit from an explicit per-chunk assignment (any policy)."""
+    msg_unit = _c(msg_unit, np.int64)
+    ch_d, ch_h = _c(ch_d, np.int32), _c(ch_h, np.int32)
+    ch_size, ch_rail = _c(ch_size, np.int64), _c(ch_rail, np.int32)
+    S = np.zeros((M, N), np.int64); R = np.zeros((M, N), np.int64)
+    S_e = np.zeros((M, N), np.int64); R_e = np.zeros((M, N), np.int64)
+    ints = np.zeros(6, np.int64); dbl = np.zeros(5, np.float64)
+    ms = np.zeros(M, np.float64); nms = np.zeros(M, np.float64)
+    lib().orc_eval(M, N, float(R2), ecmp_seed & 0xFFFFFFFFFFFFFFFF, _p(msg_unit), len(ch_size),
+                   _p(ch_d), _p(ch_h), _p(ch_size), _p(ch_rail), _p(S), _p(R), _p(S_e), _p(R_e),
+                   _p(ints), _p(dbl), _p(ms), _p(nms))
+    return dict(S=S, R=R, S_e=S_e, R_e=R_e, maxload=int(ints[0]), maxload_e=int(ints[1]),
+                total=int(ints[2]), rowmax=int(ints[3]), colmax=int(ints[4]),
+                total_e=int(ints[5]), T=float(dbl[0]), T_e=float(dbl[1]),
+                T_star=float(dbl[2]), busbw=float(dbl[3]), busbw_e=float(dbl[4]),
+                mse=ms, nmse=nms)
+
+
+def pack_node(M, N, d, T, k, row_bytes, C, x_node, topk_node, lut, msg_node, sched,
+              rail_base, out_cap):
+    """a7 for one node by definition; returns the output byte buffer."""
+    x_node = _c(x_node, np.uint8)
+    topk_node, lut = _c(topk_node, np.int32), _c(lut, np.int32)
+    msg_node = _c(msg_node, np.int64)
+    ch = sched["chunks"]
+    rail_base = _c(rail_base, np.int64)
+    out = np.zeros(int(out_cap), np.uint8)
+    rc = lib().orc_pack_node(M, N, d, T, k, row_bytes, C, _p(x_node), _p(topk_node), _p(lut),
+                             _p(msg_node), len(ch["size"]), _p(ch["g"]), _p(ch["h"]),
+                             _p(ch["c"]), _p(ch["size"]), _p(_c(sched["rail"], np.int32)),
+                             _p(_c(sched["off"], np.int64)), _p(rail_base), _p(out), out_cap)
+    if rc != 0:
+        raise RuntimeError(f"oracle pack failed rc={rc}")
+    return out
+
+
+# ------------------------------------------------------------------ whole unit
+def run_unit_matrix(M, N, C, R2, ecmp_seed, msg_unit):
+    """Schedule + eval one unit given D^(1) bytes msg_unit [M][N][G]."""
+    msg_unit = _c(msg_unit, np.int64)
+    scheds = []
+    cd, chh, cs, cr = [], [], [], []
+    for d in range(M):
+        s = schedule_node(msg_unit[d], C)
+        scheds.append(s)
+        F = len(s["chunks"]["size"])
+        cd.append(np.full(F, d, np.int32)); chh.append(s["chunks"]["h"])
+        cs.append(s["chunks"]["size"]); cr.append(s["rail"])
+    ev = eval_unit(M, N, R2, ecmp_seed, msg_unit, np.concatenate(cd), np.concatenate(chh),
+                   np.concatenate(cs), np.concatenate(cr))
+    return scheds, ev
+
+
+def run_unit_routing(M, N, T, k, row_bytes, C, R2, ecmp_seed, topk_unit, lut):
+    """Histogram + schedule + eval for one unit given routing topk_unit [M][N][T][k]."""
+    G = M * N
+    counts = np.zeros((M, N, G), np.int32)
+    msg = np.zeros((M, N, G), np.int64)
+    rank = np.zeros((M, N, T, k), np.int32)
+    for d in range(M):
+        counts[d], msg[d], rank[d] = histogram_node(M, N, d, T, k, topk_unit[d], lut, row_bytes)
+    scheds, ev = run_unit_matrix(M, N, C, R2, ecmp_seed, msg)
+    return dict(counts=counts, msg=msg, rank=rank, scheds=scheds, eval=ev)

@@ -1,0 +1,82 @@
+"""Input generators: determinism, CPU/torch agreement, recipe invariants (not gpu)."""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import gen
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_examples.json")))
+
+
+def test_mix64_torch_matches_numpy_and_int():
+    z = np.array([0, 1, 2, 12345, (1 << 63) + 5, (1 << 64) - 1], dtype=np.uint64)
+    a = gen.mix64_np(z)
+    b = gen.mix64_t(torch.from_numpy(z.view(np.int64).copy())).numpy().view(np.uint64)
+    assert np.array_equal(a, b)
+    assert [gen.mix64_int(int(v)) for v in z] == [int(v) for v in a]
+    assert gen.mix64_int(0) == 0xE220A8397B1DCDAF
+
+
+@pytest.mark.parametrize("ex", GOLD["zipf"])
+def test_zipf_weights_worked(ex):
+    w = gen.zipf_weights(ex["s"], ex["n"])
+    want = ex["w"] if "w" in ex else [a / ex["w_den"] for a in ex["w_num"]]
+    assert np.allclose(w, want, rtol=1e-12, atol=0)
+    assert abs(w.sum() - 1) < 1e-12
+
+
+def test_routing_deterministic_sliceable_and_valid():
+    M, N, T, k, E = 5, 4, 37, 2, 8
+    full = gen.routing(M, N, T, k, E, 99, u=3)
+    again = gen.routing(M, N, T, k, E, 99, u=3)
+    assert torch.equal(full, again)
+    part = gen.routing(M, N, T, k, E, 99, u=3, d0=2, nd=2)
+    assert torch.equal(full[2:4], part)
+    assert not torch.equal(full, gen.routing(M, N, T, k, E, 99, u=4))
+    inst = full.long()
+    assert inst.min() >= 0 and inst.max() < M * E
+    e = inst % E
+    assert (e[..., 0] != e[..., 1]).all()  # distinct experts per token (R#24)
+    lut = gen.inst_lut(M, N, E)
+    assert lut.shape == (M * E,) and int(lut.max()) < M * N
+    assert int(lut[2 * E + 5]) == 2 * N + (5 % N)
+
+
+def test_routing_topk_general_k():
+    r = gen.routing(3, 2, 50, 4, 6, 1, 0)
+    e = (r.long() % 6).reshape(-1, 4)
+    assert all(len(set(row.tolist())) == 4 for row in e)
+
+
+def test_payload_counter_based():
+    a = gen.payload(4, 2, 5, 64, 7, 0, 0, 4)
+    b = gen.payload(4, 2, 5, 64, 7, 0, 1, 2)
+    assert torch.equal(a[1:3], b)
+
+
+@pytest.mark.parametrize("fn", ["receiver", "sender", "uniform"])
+def test_d1_rows_and_intra(fn):
+    M, N, V = 6, 4, 10 ** 7 + 3
+    if fn == "receiver":
+        D = gen.d1_receiver_skew(M, N, V, 1.2, 5, 0)
+    elif fn == "sender":
+        D = gen.d1_sender_skew(M, N, V, 1.2, 5, 0)
+    else:
+        D = gen.d1_uniform(M, N, V)
+    assert D.dtype == np.int64 and (D >= 0).all()
+    for d in range(M):
+        assert (D[d, :, d * N:(d + 1) * N] == 0).all()
+    if fn != "sender":
+        assert (D.sum(axis=2) == V).all()  # S:223 conservation
+    g2 = gen.d1_receiver_skew(M, N, V, 1.2, 5, 0)
+    if fn == "receiver":
+        assert np.array_equal(D, g2)
+
+
+def test_receiver_skew_is_skewed():
+    D = gen.d1_receiver_skew(16, 8, 256 << 20, 1.2, 1, 0)
+    col = D.sum(axis=(0, 1))
+    assert col.max() > 20 * np.median(col)
