@@ -1,0 +1,240 @@
+/*
+ * rails.h -- C ABI of the B200-native RailS hot path (arXiv 2510.19262).
+ *
+ * The library (paper_2510_19262_b200/librails.so) implements, in hand-written
+ * sm_100a CUDA kernels, the per-node LPT spraying scheduler of RailS and the
+ * payload packing it drives:
+ *
+ *   a1 rails_histogram      MoE top-k routing -> per-node D^(1) send histogram
+ *   a2-a4 rails_lpt_schedule chunking, size-descending sort, greedy LPT on N rails
+ *   a5 rails_eval/_finalize per-rail send/receive loads, completion time, T*,
+ *                           bus bandwidth, MSE, ECMP-hash baseline
+ *   a7 rails_pack           token rows -> rail-ordered send buffers
+ *
+ * Citations: P:n = PAPER.md line n; R#n = reading n of DESIGN.md section 3.
+ *
+ * Conventions (all entry points):
+ *  - Array arguments are DEVICE pointers owned by the caller (e.g. torch tensors);
+ *    the library never allocates, frees or retains them.  Struct arguments
+ *    (rails_topo_t etc.) are HOST pointers read during the call only.
+ *  - Every compute call is asynchronous on `stream` (a cudaStream_t passed as
+ *    void*; NULL = legacy default stream) and returns after enqueueing.
+ *  - Return value: RAILS_OK or a negative code.  Argument errors are detected on
+ *    the host before anything is enqueued (nothing is written).  Errors that
+ *    depend on device data (out-of-range routing ids, undersized output buffers)
+ *    are recorded in a device-side flag; the affected items are skipped, and
+ *    rails_check() reports the first such error after synchronising.
+ *  - rails_last_error() returns a thread-local message for the last failure.
+ *  - No exceptions cross the ABI; calls on distinct streams may run concurrently
+ *    (the device error flag is process-wide; see rails_check).
+ *
+ * Index notation: M nodes (domains), N rails = GPUs = NICs
+ * per node, G = M*N global GPUs, h = f*N + m a global destination
+ * GPU on node f, g a local source GPU, U units (all-to-all rounds, R#6).
+ * A call covers the source nodes d0 .. d0+nd-1 of U units; arrays indexed by
+ * source node use the LOCAL node index dl = d - d0, outermost dims [U][nd].
+ */
+#ifndef RAILS_H
+#define RAILS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    RAILS_OK = 0,
+    RAILS_EINVAL = -1,    /* bad argument (null pointer, size, alignment, topology) */
+    RAILS_ERANGE = -2,    /* routing id / LUT value / negative byte count out of range */
+    RAILS_ENOSPC = -3,    /* workspace or output buffer too small, or size limit hit */
+    RAILS_EOVERFLOW = -4, /* a load would overflow int64 */
+    RAILS_ECUDA = -5      /* CUDA launch or runtime failure (see rails_last_error) */
+};
+
+/* Topology and method parameters -- the paper's problem statement (section 4.1). */
+typedef struct {
+    int32_t M;            /* nodes (computing domains), >= 2   */
+    int32_t N;            /* rails = GPUs = NICs per node, 1..32 */
+    int64_t chunk_bytes;  /* C: fixed chunk size, 1 .. 2^31   */
+    double R2;            /* inter-domain rate per rail and direction, B/s, > 0 */
+    double R1;            /* intra-domain rate; 0 = unspecified, else must be > R2 */
+    uint64_t ecmp_seed;   /* seed of the ECMP-hash baseline (R#14)   */
+} rails_topo_t;
+
+/* Which (unit, source node) block a call covers. */
+typedef struct {
+    int32_t U;   /* units (all-to-all rounds) in the call, >= 1   (R#6) */
+    int32_t d0;  /* first source node held by the caller, >= 0          */
+    int32_t nd;  /* number of source nodes held, >= 1, d0 + nd <= M     */
+} rails_shard_t;
+
+/* ------------------------------------------------------------------ a1 */
+/* Per-node send histogram (D^(1) row block; Alg. 1 "Select input slices
+ * for local experts according to Gate and E") with the stable in-bucket
+ * rank the pack needs (R#18).
+ *   topk_inst  int32 [U][nd][N][T][k]  expert-instance id of slot s of token t of
+ *              local GPU g (values in [0, n_inst));
+ *   inst_to_gpu int32 [n_inst]         instance -> global destination GPU in [0, G);
+ *   row_bytes  payload bytes per token row (RB), >= 1;
+ *   counts     int32 [U][nd][N][G]     number of (t,s) of GPU g routed to GPU h,
+ *              intra-node included (R#2);
+ *   msg_bytes  int64 [U][nd][N][G]     counts * RB for remote h, 0 when h is on the
+ *              source node (R#2);
+ *   row_rank   int32 [U][nd][N][T][k]  number of earlier (t',s') (in (t,s) order)
+ *              of the same GPU g with the same destination h; may be NULL.
+ * Out-of-range ids set RAILS_ERANGE in the device flag; such slots are skipped. */
+int rails_histogram(const rails_topo_t* topo, const rails_shard_t* shard,
+                    int32_t T, int32_t k, const int32_t* topk_inst,
+                    const int32_t* inst_to_gpu, int32_t n_inst, int64_t row_bytes,
+                    int32_t* counts, int64_t* msg_bytes, int32_t* row_rank,
+                    void* stream);
+
+/* ------------------------------------------------------------------ a2-a4 */
+/* Compact LPT schedule of every (unit, node).  Chunking (R#3): message
+ * B = msg_bytes[u][dl][g][h] is cut into floor(B/C) full chunks and one remainder
+ * chunk of B mod C bytes when nonzero.  Sort (Alg. 2 step 2): size
+ * descending, ties by (g, h, chunk index) ascending (R#4).  Assignment (Alg. 2
+ * step 3): LoadState[0..N) = 0; each chunk goes to the lowest-index
+ * argmin rail (R#5) at byte offset LoadState[j*] (R#19); LoadState[j*] += size.
+ * Because every full chunk is larger than every remainder and full chunks come in
+ * (g,h,c) order, the i-th full chunk of a node (i = full_base[g][h] + c) lands on
+ * rail i mod N at offset floor(i/N)*C; remainders are recorded per message.
+ *   full_base  int64 [U][nd][N][G]  full chunks of the node emitted before (g,h);
+ *   rem_rail   int8  [U][nd][N][G]  rail of the remainder chunk, -1 if none;
+ *   rem_off    int64 [U][nd][N][G]  its byte offset in the rail buffer, 0 if none;
+ *   send_load  int64 [U][nd][N]     final LoadState (= S[d][.], Eq. 4);
+ *   n_full     int64 [U][nd]        number of full chunks of the node;
+ *   n_rem      int32 [U][nd]        number of remainder chunks of the node.     */
+typedef struct {
+    int64_t* full_base;
+    int8_t* rem_rail;
+    int64_t* rem_off;
+    int64_t* send_load;
+    int64_t* n_full;
+    int32_t* n_rem;
+} rails_sched_t;
+
+/* Device workspace (bytes) rails_lpt_schedule needs for this topology/shard. */
+int rails_schedule_workspace(const rails_topo_t* topo, const rails_shard_t* shard,
+                             size_t* workspace_bytes);
+
+/* msg_bytes int64 [U][nd][N][G] (>= 0; negative values flag RAILS_ERANGE and
+ * count as 0).  workspace: device buffer of at least rails_schedule_workspace()
+ * bytes, 256-byte aligned, not used concurrently by another call. */
+int rails_lpt_schedule(const rails_topo_t* topo, const rails_shard_t* shard,
+                       const int64_t* msg_bytes, const rails_sched_t* out,
+                       void* workspace, size_t workspace_bytes, void* stream);
+
+/* Generic atomic-flow LPT ("small application-layer messages" P:603):
+ * n_seg independent flow sets, set s = flows seg_off[s] .. seg_off[s+1]-1
+ * (seg_off: device int64 [n_seg+1], non-decreasing, seg_off[0] = 0, last = F).
+ * Order within a set: weight descending, then flow index ascending; each flow to
+ * the lowest-index argmin rail.  w int64 [F] >= 0; rail int8-range int32 [F];
+ * off int64 [F] (LoadState before the update); load int64 [n_seg][N]. */
+int rails_assign_workspace(int32_t n_seg, int64_t F, size_t* workspace_bytes);
+int rails_lpt_assign(int32_t N, int32_t n_seg, const int64_t* seg_off, int64_t F,
+                     const int64_t* w, int32_t* rail, int64_t* off, int64_t* load,
+                     void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------ a5 */
+/* Loads and balance of the shard's nodes plus reduction buffers for the global
+ * quantities.  Load model (R#7): a chunk of node d on rail j bound for node
+ * f = h/N adds to S[d][j] (Eq. 4) and R[f][j] (Eq. 5).  ECMP baseline (R#13,
+ * R#14): each whole message (d,g,h) goes on rail ecmp(d*N+g, h).
+ *   S, S_e    int64 [U][nd][N]   send loads (LPT, ECMP) of the shard's nodes;
+ *   mse, nmse double [U][nd]     Eq. 6 of S[d][.] about its mean, exact
+ *                                form sum_j (N*S_j - sum S)^2 / N^3 (R#11); nMSE =
+ *                                mse / (sum S)^2, 0 if sum S = 0 (R#12);
+ *   red_sum   int64 [U][RAILS_RED_SUM_LEN(M,N)]  PARTIAL sums over the shard's
+ *             nodes, layout: R[M][N], R_e[M][N], colsum[M] (bytes into node f),
+ *             total, total_e.  Overwritten (zeroed then accumulated) by the call.
+ *   red_max   int64 [U][RAILS_RED_MAX_LEN]  PARTIAL maxima: max S, max S_e,
+ *             max row sum (bytes out of one node), 0.
+ * With the nodes of a unit split over ranks, all-reduce red_sum (SUM) and
+ * red_max (MAX) across ranks before rails_eval_finalize (a6). */
+#define RAILS_RED_SUM_LEN(M, N) (2 * (int64_t)(M) * (int64_t)(N) + (int64_t)(M) + 2)
+#define RAILS_RED_MAX_LEN 4
+typedef struct {
+    int64_t* S;
+    int64_t* S_e;
+    double* mse;
+    double* nmse;
+    int64_t* red_sum;
+    int64_t* red_max;
+} rails_eval_t;
+
+int rails_eval(const rails_topo_t* topo, const rails_shard_t* shard,
+               const int64_t* msg_bytes, const rails_sched_t* sched,
+               const rails_eval_t* out, void* stream);
+
+/* Per-unit results from fully reduced red_sum / red_max ([U][...] as above):
+ *   maxload   = max(max S, max R)        (most loaded NIC, send or receive)
+ *   T         = maxload / R2             (R#8)
+ *   total     = inter-node bytes;  busbw = total / T, 0 if total = 0   (R#10)
+ *   rowmax, colmax = max row / column sum of D^(2) (Eq. 1);
+ *   T_star    = max(rowmax, colmax) / (N * R2)   (Thm 2 + Thm 3)
+ *   *_e       = the same for the ECMP-hash baseline.
+ * All outputs are device arrays of length U (int64 or double). */
+typedef struct {
+    int64_t* maxload;
+    int64_t* maxload_e;
+    int64_t* total;
+    int64_t* rowmax;
+    int64_t* colmax;
+    double* T;
+    double* T_e;
+    double* T_star;
+    double* busbw;
+    double* busbw_e;
+} rails_final_t;
+
+int rails_eval_finalize(const rails_topo_t* topo, int32_t U, const int64_t* red_sum,
+                        const int64_t* red_max, const rails_final_t* out, void* stream);
+
+/* ------------------------------------------------------------------ a7 */
+/* Rail buffer placement: rail_base int64 [U][nd][N] = exclusive prefix sum of
+ * send_load in (u, dl, j) order, i.e. the byte offset of rail j of node d in one
+ * contiguous output buffer; total int64 [1] = the buffer size needed. */
+int rails_rail_offsets(const rails_topo_t* topo, const rails_shard_t* shard,
+                       const int64_t* send_load, int64_t* rail_base, int64_t* total,
+                       void* stream);
+
+/* Scatter token rows into rail-ordered send buffers (R#18-R#20).  Message (g,h)
+ * is the concatenation, in ascending (t,s), of the RB-byte rows x[g][t] of every
+ * REMOTE slot routed to h; the copy with rank rho occupies message bytes
+ * [rho*RB, (rho+1)*RB).  Chunk c of the message (bytes [c*C, c*C+size)) is
+ * written to out + rail_base[u][dl][rail(c)] + off(c) with (rail, off) from the
+ * compact schedule.  Each source row is read once.  Payload is opaque bytes.
+ *   x         [U][nd][N][T][row_bytes] device bytes, 16-byte aligned;
+ *   row_bytes multiple of 16; chunk_bytes multiple of 16;
+ *   topk_inst, inst_to_gpu, row_rank, msg_bytes: as produced/consumed above;
+ *   out       device buffer of out_cap bytes, 16-byte aligned.
+ * A destination beyond out_cap sets RAILS_ENOSPC (that piece is skipped). */
+int rails_pack(const rails_topo_t* topo, const rails_shard_t* shard, int32_t T,
+               int32_t k, const void* x, const int32_t* topk_inst,
+               const int32_t* inst_to_gpu, int32_t n_inst, const int32_t* row_rank,
+               const int64_t* msg_bytes, int64_t row_bytes, const rails_sched_t* sched,
+               const int64_t* rail_base, void* out, int64_t out_cap, void* stream);
+
+/* ------------------------------------------------------------------ misc */
+/* Synchronise `stream`, then return (and clear) the first device-side error
+ * recorded since the last check: RAILS_OK, RAILS_ERANGE, RAILS_ENOSPC or
+ * RAILS_EOVERFLOW; RAILS_ECUDA if the stream reports a CUDA error. */
+int rails_check(void* stream);
+
+/* Thread-local description of the last failed call ("" if none). */
+const char* rails_last_error(void);
+
+/* Number of kernel launches this thread's calls have enqueued since the last
+ * reset (reset = nonzero).  For benchmark accounting. */
+int64_t rails_launch_count(int32_t reset);
+
+/* ABI version (major*100 + minor). */
+int32_t rails_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RAILS_H */

@@ -306,8 +306,9 @@ void orc_eval(int32_t M, int32_t N, double R2, uint64_t ecmp_seed,
     int64_t lb = rowmax > colmax ? rowmax : colmax;
     double T_star = (double)lb / ((double)N * R2);
     dbl[0] = T; dbl[1] = T_e; dbl[2] = T_star;
-    dbl[3] = (double)total / T;         /* busbw = total bytes / T (R#10) */
-    dbl[4] = (double)total_e / T_e;
+    /* busbw = total bytes / T (R#10); 0 when nothing crosses the rails */
+    dbl[3] = (total > 0) ? (double)total / T : 0.0;
+    dbl[4] = (total_e > 0) ? (double)total_e / T_e : 0.0;
     for (int32_t d = 0; d < M; d++) {
         mse[d] = orc_mse(N, S + (int64_t)d * N);
         nmse[d] = orc_nmse(N, S + (int64_t)d * N);

@@ -1,0 +1,258 @@
+// abi.cu -- the extern "C" boundary declared in include/rails.h.
+//
+// Host-side argument validation (nothing is enqueued on an argument error), the
+// device error flag behind rails_check, the thread-local last-error string and the
+// launch counter.  All compute is in k_*.cu; this file only validates and launches.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "common.cuh"
+
+__device__ int g_rails_err;  // process-wide device error flag (per device)
+
+namespace rails {
+static thread_local char t_err[512] = "";
+static thread_local long long t_launches = 0;
+void count_launch(int n) { t_launches += n; }
+
+static int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(t_err, sizeof(t_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+static std::mutex g_mu;
+static int* g_err_ptr[64];
+static int g_sms[64];
+
+static int ctx(void* stream, LaunchCtx* c) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return fail(RAILS_ECUDA, "cudaGetDevice: %s", cudaGetErrorString(e));
+  if (dev < 0 || dev >= 64) return fail(RAILS_ECUDA, "device index %d unsupported", dev);
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g_err_ptr[dev]) {
+    void* p = nullptr;
+    e = cudaGetSymbolAddress(&p, g_rails_err);
+    if (e != cudaSuccess)
+      return fail(RAILS_ECUDA, "cudaGetSymbolAddress: %s (is this an sm_100 device?)",
+                  cudaGetErrorString(e));
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    g_err_ptr[dev] = (int*)p;
+    g_sms[dev] = sms > 0 ? sms : 148;
+  }
+  c->stream = (cudaStream_t)stream;
+  c->err = g_err_ptr[dev];
+  c->num_sms = g_sms[dev];
+  return RAILS_OK;
+}
+
+static int cuda_rc(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return RAILS_OK;
+  return fail(RAILS_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+static int check_topo(const rails_topo_t* t) {
+  if (!t) return fail(RAILS_EINVAL, "topo is NULL");
+  if (t->M < 2) return fail(RAILS_EINVAL, "M=%d: need at least 2 nodes (P:184)", t->M);
+  if (t->N < 1 || t->N > 32) return fail(RAILS_EINVAL, "N=%d: need 1 <= N <= 32", t->N);
+  if ((long long)t->M * t->N > (1LL << 20))
+    return fail(RAILS_EINVAL, "M*N=%lld exceeds 2^20 GPUs", (long long)t->M * t->N);
+  if (t->chunk_bytes < 1 || t->chunk_bytes > (1LL << 31))
+    return fail(RAILS_EINVAL, "chunk_bytes=%lld: need 1 <= C <= 2^31", (long long)t->chunk_bytes);
+  if (!(t->R2 > 0) || !std::isfinite(t->R2)) return fail(RAILS_EINVAL, "R2 must be > 0");
+  if (t->R1 != 0 && !(t->R1 > t->R2))
+    return fail(RAILS_EINVAL, "R1 must exceed R2 (P:333) or be 0");
+  return RAILS_OK;
+}
+
+static int check_shard(const rails_topo_t* t, const rails_shard_t* s) {
+  if (!s) return fail(RAILS_EINVAL, "shard is NULL");
+  if (s->U < 1) return fail(RAILS_EINVAL, "U=%d: need >= 1", s->U);
+  if (s->nd < 1 || s->d0 < 0 || (long long)s->d0 + s->nd > t->M)
+    return fail(RAILS_EINVAL, "shard nodes [%d, %d) outside [0, %d)", s->d0, s->d0 + s->nd, t->M);
+  const long long NG = (long long)t->N * t->M * t->N;
+  if ((long long)s->U * s->nd * NG > (1LL << 40))
+    return fail(RAILS_EINVAL, "U*nd*N*G too large");
+  return RAILS_OK;
+}
+
+static bool al(const void* p, size_t a) { return ((uintptr_t)p % a) == 0; }
+}  // namespace rails
+
+using namespace rails;
+
+extern "C" {
+
+int32_t rails_version(void) { return 100; }
+
+const char* rails_last_error(void) { return t_err; }
+
+int64_t rails_launch_count(int32_t reset) {
+  long long v = t_launches;
+  if (reset) t_launches = 0;
+  return v;
+}
+
+int rails_check(void* stream) {
+  LaunchCtx c;
+  int rc = ctx(stream, &c);
+  if (rc) return rc;
+  cudaError_t e = cudaStreamSynchronize(c.stream);
+  if (e != cudaSuccess) return cuda_rc(e, "stream");
+  int flag = 0;
+  e = cudaMemcpy(&flag, c.err, sizeof(int), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_rc(e, "read error flag");
+  if (flag) {
+    int zero = 0;
+    cudaMemcpy(c.err, &zero, sizeof(int), cudaMemcpyHostToDevice);
+  }
+  if (flag & ERR_RANGE) return fail(RAILS_ERANGE, "device: value out of range (routing id, LUT, rank or byte count)");
+  if (flag & ERR_NOSPC) return fail(RAILS_ENOSPC, "device: output buffer too small");
+  if (flag & ERR_OVERFLOW) return fail(RAILS_EOVERFLOW, "device: load overflow");
+  return RAILS_OK;
+}
+
+int rails_histogram(const rails_topo_t* topo, const rails_shard_t* sh, int32_t T, int32_t k,
+                    const int32_t* topk_inst, const int32_t* inst_to_gpu, int32_t n_inst,
+                    int64_t row_bytes, int32_t* counts, int64_t* msg_bytes, int32_t* row_rank,
+                    void* stream) {
+  int rc = check_topo(topo);
+  if (rc || (rc = check_shard(topo, sh))) return rc;
+  if (T < 1 || k < 1 || k > 32) return fail(RAILS_EINVAL, "need T >= 1 and 1 <= k <= 32");
+  if ((long long)T * k > (1LL << 30)) return fail(RAILS_EINVAL, "T*k too large");
+  if (n_inst < 1 || row_bytes < 1) return fail(RAILS_EINVAL, "need n_inst >= 1, row_bytes >= 1");
+  if (!topk_inst || !inst_to_gpu || !counts || !msg_bytes)
+    return fail(RAILS_EINVAL, "NULL array argument");
+  if ((long long)topo->M * topo->N > 49152)
+    return fail(RAILS_ENOSPC, "G=%lld: histogram bins exceed shared memory",
+                (long long)topo->M * topo->N);
+  LaunchCtx c;
+  if ((rc = ctx(stream, &c))) return rc;
+  return cuda_rc(launch_histogram(c, sh->U, sh->nd, sh->d0, topo->M, topo->N, T, k, topk_inst,
+                                  inst_to_gpu, n_inst, row_bytes, counts, msg_bytes, row_rank),
+                 "rails_histogram launch");
+}
+
+int rails_schedule_workspace(const rails_topo_t* topo, const rails_shard_t* sh, size_t* bytes) {
+  int rc = check_topo(topo);
+  if (rc || (rc = check_shard(topo, sh))) return rc;
+  if (!bytes) return fail(RAILS_EINVAL, "bytes is NULL");
+  *bytes = schedule_workspace_bytes(sh->U, sh->nd, (long long)topo->N * topo->M * topo->N);
+  return RAILS_OK;
+}
+
+int rails_lpt_schedule(const rails_topo_t* topo, const rails_shard_t* sh,
+                       const int64_t* msg_bytes, const rails_sched_t* out, void* ws,
+                       size_t ws_bytes, void* stream) {
+  int rc = check_topo(topo);
+  if (rc || (rc = check_shard(topo, sh))) return rc;
+  if (!msg_bytes || !out || !out->full_base || !out->rem_rail || !out->rem_off ||
+      !out->send_load || !out->n_full || !out->n_rem || !ws)
+    return fail(RAILS_EINVAL, "NULL argument");
+  if (!al(ws, 256)) return fail(RAILS_EINVAL, "workspace must be 256-byte aligned");
+  const size_t need =
+      schedule_workspace_bytes(sh->U, sh->nd, (long long)topo->N * topo->M * topo->N);
+  if (ws_bytes < need) return fail(RAILS_ENOSPC, "workspace %zu < %zu bytes", ws_bytes, need);
+  LaunchCtx c;
+  if ((rc = ctx(stream, &c))) return rc;
+  return cuda_rc(launch_schedule(c, sh->U, sh->nd, sh->d0, topo->M, topo->N, topo->chunk_bytes,
+                                 msg_bytes, *out, ws),
+                 "rails_lpt_schedule launch");
+}
+
+int rails_assign_workspace(int32_t n_seg, int64_t F, size_t* bytes) {
+  if (n_seg < 1 || F < 0 || !bytes) return fail(RAILS_EINVAL, "bad arguments");
+  *bytes = assign_workspace_bytes(n_seg, F);
+  return RAILS_OK;
+}
+
+int rails_lpt_assign(int32_t N, int32_t n_seg, const int64_t* seg_off, int64_t F,
+                     const int64_t* w, int32_t* rail, int64_t* off, int64_t* load, void* ws,
+                     size_t ws_bytes, void* stream) {
+  if (N < 1 || N > 32) return fail(RAILS_EINVAL, "N=%d: need 1 <= N <= 32", N);
+  if (n_seg < 1 || F < 0 || F > (1LL << 31) - 1) return fail(RAILS_EINVAL, "bad n_seg or F");
+  if (!seg_off || !load || !ws || (F > 0 && (!w || !rail || !off)))
+    return fail(RAILS_EINVAL, "NULL argument");
+  if (!al(ws, 256)) return fail(RAILS_EINVAL, "workspace must be 256-byte aligned");
+  if (ws_bytes < assign_workspace_bytes(n_seg, F))
+    return fail(RAILS_ENOSPC, "workspace too small");
+  LaunchCtx c;
+  int rc;
+  if ((rc = ctx(stream, &c))) return rc;
+  return cuda_rc(launch_assign(c, N, n_seg, seg_off, F, w, rail, off, load, ws),
+                 "rails_lpt_assign launch");
+}
+
+int rails_eval(const rails_topo_t* topo, const rails_shard_t* sh, const int64_t* msg_bytes,
+               const rails_sched_t* sched, const rails_eval_t* out, void* stream) {
+  int rc = check_topo(topo);
+  if (rc || (rc = check_shard(topo, sh))) return rc;
+  if (!msg_bytes || !sched || !sched->full_base || !sched->rem_rail || !out || !out->S ||
+      !out->S_e || !out->mse || !out->nmse || !out->red_sum || !out->red_max)
+    return fail(RAILS_EINVAL, "NULL argument");
+  LaunchCtx c;
+  if ((rc = ctx(stream, &c))) return rc;
+  return cuda_rc(launch_eval(c, sh->U, sh->nd, sh->d0, topo->M, topo->N, topo->chunk_bytes,
+                             topo->ecmp_seed, msg_bytes, *sched, *out),
+                 "rails_eval launch");
+}
+
+int rails_eval_finalize(const rails_topo_t* topo, int32_t U, const int64_t* red_sum,
+                        const int64_t* red_max, const rails_final_t* out, void* stream) {
+  int rc = check_topo(topo);
+  if (rc) return rc;
+  if (U < 1 || !red_sum || !red_max || !out) return fail(RAILS_EINVAL, "bad argument");
+  LaunchCtx c;
+  if ((rc = ctx(stream, &c))) return rc;
+  return cuda_rc(launch_finalize(c, U, topo->M, topo->N, topo->R2, red_sum, red_max, *out),
+                 "rails_eval_finalize launch");
+}
+
+int rails_rail_offsets(const rails_topo_t* topo, const rails_shard_t* sh,
+                       const int64_t* send_load, int64_t* rail_base, int64_t* total,
+                       void* stream) {
+  int rc = check_topo(topo);
+  if (rc || (rc = check_shard(topo, sh))) return rc;
+  if (!send_load || !rail_base || !total) return fail(RAILS_EINVAL, "NULL argument");
+  LaunchCtx c;
+  if ((rc = ctx(stream, &c))) return rc;
+  return cuda_rc(launch_rail_offsets(c, (long long)sh->U * sh->nd * topo->N, send_load,
+                                     rail_base, total),
+                 "rails_rail_offsets launch");
+}
+
+int rails_pack(const rails_topo_t* topo, const rails_shard_t* sh, int32_t T, int32_t k,
+               const void* x, const int32_t* topk_inst, const int32_t* inst_to_gpu,
+               int32_t n_inst, const int32_t* row_rank, const int64_t* msg_bytes,
+               int64_t row_bytes, const rails_sched_t* sched, const int64_t* rail_base,
+               void* out, int64_t out_cap, void* stream) {
+  int rc = check_topo(topo);
+  if (rc || (rc = check_shard(topo, sh))) return rc;
+  if (T < 1 || k < 1 || k > 32 || n_inst < 1) return fail(RAILS_EINVAL, "bad T, k or n_inst");
+  if (row_bytes < 16 || row_bytes % 16 || row_bytes > (1LL << 30))
+    return fail(RAILS_EINVAL, "row_bytes=%lld must be a positive multiple of 16",
+                (long long)row_bytes);
+  if (topo->chunk_bytes % 16)
+    return fail(RAILS_EINVAL, "pack needs chunk_bytes %% 16 == 0 (16-byte vector copies)");
+  if (!x || !topk_inst || !inst_to_gpu || !row_rank || !msg_bytes || !sched ||
+      !sched->full_base || !sched->rem_rail || !sched->rem_off || !rail_base ||
+      (!out && out_cap > 0))
+    return fail(RAILS_EINVAL, "NULL argument");
+  if (!al(x, 16) || (out && !al(out, 16))) return fail(RAILS_EINVAL, "x/out must be 16-byte aligned");
+  if (out_cap < 0) return fail(RAILS_EINVAL, "out_cap < 0");
+  LaunchCtx c;
+  if ((rc = ctx(stream, &c))) return rc;
+  return cuda_rc(launch_pack(c, sh->U, sh->nd, sh->d0, topo->M, topo->N, T, k, topo->chunk_bytes,
+                             x, topk_inst, inst_to_gpu, n_inst, row_rank, msg_bytes, row_bytes,
+                             *sched, rail_base, out, out_cap, 0),
+                 "rails_pack launch");
+}
+
+}  // extern "C"

@@ -1,0 +1,158 @@
+// common.cuh -- internal helpers of the B200 RailS kernels (sm_100a only).
+// Not part of the ABI; see include/rails.h.  No code here is shared with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/rails.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "librails is written for sm_100a (B200) only"
+#endif
+
+namespace rails {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// Device error bits, OR-ed into the flag word passed to every kernel.
+enum : int { ERR_RANGE = 1, ERR_NOSPC = 2, ERR_OVERFLOW = 4 };
+
+__device__ __forceinline__ void flag_error(int* err, int bit) {
+  if ((*(volatile int*)err & bit) == 0) atomicOr(err, bit);
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Warp-inclusive scan helpers (int64 and int32).
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T n = __shfl_up_sync(FULL, v, o);
+    if (lane >= o) v += n;
+  }
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    T n = __shfl_xor_sync(FULL, v, o);
+    v = n > v ? n : v;
+  }
+  return v;
+}
+
+// Block-wide exclusive scan of one int64 per thread; returns the exclusive prefix
+// and writes the block total to *total.  scratch: >= 33 int64 in shared memory.
+__device__ __forceinline__ long long block_excl_scan(long long v, long long* scratch,
+                                                     long long* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+  long long inc = warp_incl_scan(v);
+  if (lane == 31) scratch[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    long long s = lane < nw ? scratch[lane] : 0;
+    long long si = warp_incl_scan(s);
+    if (lane < nw) scratch[lane] = si - s;
+    if (lane == 31) scratch[32] = si;
+  }
+  __syncthreads();
+  long long r = scratch[wid] + inc - v;
+  *total = scratch[32];
+  __syncthreads();
+  return r;
+}
+
+// ECMP rail (R#14): splitmix64 output step, this library's own copy.
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ int ecmp_rail(uint64_t seed, long long src, long long dst, int N) {
+  uint64_t key = ((uint64_t)src << 32) | (uint64_t)dst;
+  uint32_t hi = (uint32_t)(mix64(key ^ seed) >> 32);
+  return (int)(hi % (uint32_t)N);
+}
+
+// Division by the chunk size C: shift when C is a power of two.
+struct ChunkDiv {
+  long long C;
+  int shift;  // >= 0 when C == 1 << shift, else -1
+  __device__ __forceinline__ long long div(long long b) const {
+    return shift >= 0 ? (b >> shift) : (b / C);
+  }
+};
+
+// Streaming 16-byte global accesses (opaque payload bytes; never touched as floats).
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_stream(uint4* p, const uint4& v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+}  // namespace rails
+
+// ---------------------------------------------------------------- host launchers
+// (defined in the kernel .cu files, called by abi.cu after validation)
+namespace rails {
+struct LaunchCtx {
+  cudaStream_t stream;
+  int* err;      // device error flag
+  int num_sms;
+};
+
+cudaError_t launch_histogram(const LaunchCtx&, int U, int nd, int d0, int M, int N, int T,
+                             int k, const int32_t* topk, const int32_t* lut, int n_inst,
+                             long long row_bytes, int32_t* counts, int64_t* msg,
+                             int32_t* rank);
+
+size_t schedule_workspace_bytes(int U, int nd, long long NG);
+cudaError_t launch_schedule(const LaunchCtx&, int U, int nd, int d0, int M, int N, long long C,
+                            const int64_t* msg, const rails_sched_t& s, void* ws);
+
+size_t assign_workspace_bytes(int n_seg, long long F);
+cudaError_t launch_assign(const LaunchCtx&, int N, int n_seg, const int64_t* seg_off,
+                          long long F, const int64_t* w, int32_t* rail, int64_t* off,
+                          int64_t* load, void* ws);
+
+cudaError_t launch_eval(const LaunchCtx&, int U, int nd, int d0, int M, int N, long long C,
+                        uint64_t seed, const int64_t* msg, const rails_sched_t& s,
+                        const rails_eval_t& e);
+cudaError_t launch_finalize(const LaunchCtx&, int U, int M, int N, double R2,
+                            const int64_t* red_sum, const int64_t* red_max,
+                            const rails_final_t& f);
+
+cudaError_t launch_rail_offsets(const LaunchCtx&, long long n, const int64_t* send_load,
+                                int64_t* rail_base, int64_t* total);
+cudaError_t launch_pack(const LaunchCtx&, int U, int nd, int d0, int M, int N, int T, int k,
+                        long long C, const void* x, const int32_t* topk, const int32_t* lut,
+                        int n_inst, const int32_t* rank, const int64_t* msg,
+                        long long row_bytes, const rails_sched_t& s, const int64_t* rail_base,
+                        void* out, long long out_cap, int impl);
+
+void count_launch(int n);
+}  // namespace rails

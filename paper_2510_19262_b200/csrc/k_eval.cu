@@ -1,0 +1,252 @@
+// k_eval.cu -- a5: loads, completion time, T*, busbw, MSE, ECMP baseline (sm_100a).
+//
+// Load model (Eq. 4-5; rail pairing NIC(k,n) -> NIC(f,n), R#7):
+// a chunk of node d on rail j bound for node f adds to S[d][j] and R[f][j].
+// From the compact schedule, message (g,h) with n = floor(B/C) full chunks
+// starting at node-global full index fb puts q*C on every rail plus C on the r
+// rails fb mod N, fb+1 mod N, ... (q = n div N, r = n mod N), and its remainder on
+// rem_rail.  So eval is O(messages * N), never O(chunks).
+//
+// k_eval_node: one CTA per (unit, node); warp w handles destination nodes f = w,
+// w+W, ...; lane j accumulates R_d[f][j] (bytes of node d into NIC (f,j)) over the
+// N*N messages into f, which 32 lanes load cooperatively and broadcast by shuffle.
+// Then R[f][j] += R_d[f][j] (int64 atomics: order-independent, hence
+// deterministic), S[d][j] = sum_f R_d[f][j], colsum[f] += sum_j R_d[f][j].  The ECMP
+// baseline (R#13-R#14) hashes each whole message onto one rail.
+// MSE (Eq. 6; Alg. 2 step 6; R#11) is the exact integer
+// sum_j (N*S_j - sum S)^2 over N^3, converted once (R#25).
+// k_eval_finalize: per unit, max over the reduced R, T = maxload/R2,
+// T* = max(rowmax, colmax)/(N*R2) (Thm 2 + Thm 3), busbw = total/T (R#10).
+#include "common.cuh"
+
+namespace rails {
+
+constexpr int EVAL_WARPS = 8;
+
+__device__ __forceinline__ double u128_to_double(unsigned __int128 v) {
+  const unsigned long long hi = (unsigned long long)(v >> 64), lo = (unsigned long long)v;
+  if (hi == 0) return __ull2double_rn(lo);
+  return __dadd_rn(__dmul_rn(__ull2double_rn(hi), 18446744073709551616.0), __ull2double_rn(lo));
+}
+
+__global__ void __launch_bounds__(EVAL_WARPS * 32)
+    k_eval_node(int M, int N, int nd, int d0, long long C, int cshift, uint64_t seed,
+                const int64_t* __restrict__ msg, const int64_t* __restrict__ full_base,
+                const int8_t* __restrict__ rem_rail, int64_t* __restrict__ S,
+                int64_t* __restrict__ S_e, double* __restrict__ mse,
+                double* __restrict__ nmse, int64_t* __restrict__ red_sum,
+                int64_t* __restrict__ red_max, long long rsl) {
+  __shared__ long long sS[EVAL_WARPS][32], sSe[EVAL_WARPS][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long seg = blockIdx.x;
+  const long long u = seg / nd;
+  const int d = d0 + (int)(seg % nd);
+  const long long G = (long long)M * N, NG = (long long)N * G;
+  const ChunkDiv cd{C, cshift};
+  const int64_t* __restrict__ mg = msg + seg * NG;
+  const int64_t* __restrict__ fbp = full_base + seg * NG;
+  const int8_t* __restrict__ rrp = rem_rail + seg * NG;
+  unsigned long long* rs = (unsigned long long*)(red_sum + u * rsl);
+  unsigned long long* R = rs;
+  unsigned long long* Re = rs + M * (long long)N;
+  unsigned long long* col = Re + M * (long long)N;
+  unsigned long long* tot = col + M;
+
+  long long Sj = 0, Sej = 0;
+  const int NN = N * N;
+  for (int f = wid; f < M; f += EVAL_WARPS) {
+    if (f == d) continue;  // intra-node traffic never crosses the rails (R#2)
+    long long Rf = 0, Ref = 0;
+    for (int b0 = 0; b0 < NN; b0 += 32) {
+      const int l = b0 + lane;
+      long long B = 0, q = 0, rem = 0;
+      int r = 0, st = 0, rr = -1, e = -1;
+      if (l < NN) {
+        const int g = l / N, m = l - (l / N) * N;
+        const long long idx = (long long)g * G + (long long)f * N + m;
+        B = mg[idx];
+        if (B > 0) {
+          const long long nf = cd.div(B);
+          rem = B - nf * C;
+          const long long fb = fbp[idx];
+          q = nf / N;
+          r = (int)(nf - q * N);
+          st = (int)(fb % N);
+          rr = (rem > 0) ? (int)rrp[idx] : -1;
+          e = ecmp_rail(seed, (long long)d * N + g, (long long)f * N + m, N);
+        } else {
+          B = 0;
+        }
+      }
+      const int cnt = min(32, NN - b0);
+      for (int b = 0; b < cnt; ++b) {
+        const long long Bb = __shfl_sync(FULL, B, b);
+        if (Bb == 0) continue;
+        const long long qb = __shfl_sync(FULL, q, b);
+        const long long remb = __shfl_sync(FULL, rem, b);
+        const int rb = __shfl_sync(FULL, r, b);
+        const int stb = __shfl_sync(FULL, st, b);
+        const int rrb = __shfl_sync(FULL, rr, b);
+        const int eb = __shfl_sync(FULL, e, b);
+        if (lane < N) {
+          int dj = lane - stb;
+          if (dj < 0) dj += N;
+          Rf += qb * C + (dj < rb ? C : 0) + (lane == rrb ? remb : 0);
+          if (lane == eb) Ref += Bb;
+        }
+      }
+    }
+    if (lane < N) {
+      if (Rf) atomicAdd(R + (long long)f * N + lane, (unsigned long long)Rf);
+      if (Ref) atomicAdd(Re + (long long)f * N + lane, (unsigned long long)Ref);
+      Sj += Rf;
+      Sej += Ref;
+    }
+    const long long cf = warp_sum(lane < N ? Rf : 0LL);
+    if (lane == 0 && cf) atomicAdd(col + f, (unsigned long long)cf);
+  }
+  sS[wid][lane] = Sj;
+  sSe[wid][lane] = Sej;
+  __syncthreads();
+  if (wid != 0) return;
+  long long s = 0, se = 0;
+#pragma unroll
+  for (int w = 0; w < EVAL_WARPS; ++w) {
+    s += sS[w][lane];
+    se += sSe[w][lane];
+  }
+  if (lane >= N) s = se = 0;
+  if (lane < N) {
+    S[seg * N + lane] = s;
+    S_e[seg * N + lane] = se;
+  }
+  const long long total = warp_sum(s), total_e = warp_sum(se);
+  const long long mx = warp_max(s), mxe = warp_max(se);
+  unsigned __int128 sq = 0;
+  for (int j = 0; j < N; ++j) {
+    const long long sj = __shfl_sync(FULL, s, j);
+    const __int128 dv = (__int128)N * sj - (__int128)total;
+    sq += (unsigned __int128)(dv * dv);
+  }
+  if (lane == 0) {
+    const double dN = (double)N;
+    const double m = __ddiv_rn(u128_to_double(sq), __dmul_rn(__dmul_rn(dN, dN), dN));
+    mse[seg] = m;
+    nmse[seg] =
+        total == 0 ? 0.0
+                   : __ddiv_rn(m, __dmul_rn(__ll2double_rn(total), __ll2double_rn(total)));
+    if (total) atomicAdd(tot, (unsigned long long)total);
+    if (total_e) atomicAdd(tot + 1, (unsigned long long)total_e);
+    atomicMax((long long*)red_max + u * RAILS_RED_MAX_LEN + 0, mx);
+    atomicMax((long long*)red_max + u * RAILS_RED_MAX_LEN + 1, mxe);
+    atomicMax((long long*)red_max + u * RAILS_RED_MAX_LEN + 2, total);
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    k_eval_finalize(int M, int N, double R2, long long rsl, const int64_t* __restrict__ red_sum,
+                    const int64_t* __restrict__ red_max, rails_final_t out) {
+  __shared__ long long s3[3][8];
+  const long long u = blockIdx.x;
+  const int64_t* rs = red_sum + u * rsl;
+  const long long MN = (long long)M * N;
+  long long mR = 0, mRe = 0, mc = 0;
+  for (long long i = threadIdx.x; i < MN; i += blockDim.x) {
+    mR = max(mR, (long long)rs[i]);
+    mRe = max(mRe, (long long)rs[MN + i]);
+  }
+  for (long long i = threadIdx.x; i < M; i += blockDim.x) mc = max(mc, (long long)rs[2 * MN + i]);
+  mR = warp_max(mR);
+  mRe = warp_max(mRe);
+  mc = warp_max(mc);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    s3[0][wid] = mR;
+    s3[1][wid] = mRe;
+    s3[2][wid] = mc;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+    mR = max(mR, s3[0][w]);
+    mRe = max(mRe, s3[1][w]);
+    mc = max(mc, s3[2][w]);
+  }
+  const int64_t* rm = red_max + u * RAILS_RED_MAX_LEN;
+  const long long maxload = max((long long)rm[0], mR);
+  const long long maxload_e = max((long long)rm[1], mRe);
+  const long long rowmax = rm[2];
+  const long long total = rs[2 * MN + M], total_e = rs[2 * MN + M + 1];
+  const double T = __ddiv_rn(__ll2double_rn(maxload), R2);
+  const double T_e = __ddiv_rn(__ll2double_rn(maxload_e), R2);
+  const long long lb = max(rowmax, mc);
+  const double T_star = __ddiv_rn(__ll2double_rn(lb), __dmul_rn((double)N, R2));
+  if (out.maxload) out.maxload[u] = maxload;
+  if (out.maxload_e) out.maxload_e[u] = maxload_e;
+  if (out.total) out.total[u] = total;
+  if (out.rowmax) out.rowmax[u] = rowmax;
+  if (out.colmax) out.colmax[u] = mc;
+  if (out.T) out.T[u] = T;
+  if (out.T_e) out.T_e[u] = T_e;
+  if (out.T_star) out.T_star[u] = T_star;
+  if (out.busbw) out.busbw[u] = total > 0 ? __ddiv_rn(__ll2double_rn(total), T) : 0.0;
+  if (out.busbw_e) out.busbw_e[u] = total_e > 0 ? __ddiv_rn(__ll2double_rn(total_e), T_e) : 0.0;
+}
+
+// Exclusive prefix of send_load in (u, dl, j) order -> rail_base; total bytes.
+__global__ void __launch_bounds__(1024)
+    k_rail_offsets(long long n, const int64_t* __restrict__ send_load,
+                   int64_t* __restrict__ rail_base, int64_t* __restrict__ total) {
+  __shared__ long long scratch[33];
+  long long carry = 0;
+  for (long long t0 = 0; t0 < n; t0 += blockDim.x) {
+    const long long i = t0 + threadIdx.x;
+    const long long v = i < n ? send_load[i] : 0;
+    long long tot;
+    const long long ex = block_excl_scan(v, scratch, &tot);
+    if (i < n) rail_base[i] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) *total = carry;
+}
+
+static int pow2_shift(long long C) {
+  if (C <= 0 || (C & (C - 1))) return -1;
+  int s = 0;
+  while ((1LL << s) < C) ++s;
+  return s;
+}
+
+cudaError_t launch_eval(const LaunchCtx& c, int U, int nd, int d0, int M, int N, long long C,
+                        uint64_t seed, const int64_t* msg, const rails_sched_t& s,
+                        const rails_eval_t& e) {
+  const long long rsl = RAILS_RED_SUM_LEN(M, N);
+  cudaError_t err =
+      cudaMemsetAsync(e.red_sum, 0, (size_t)U * rsl * sizeof(int64_t), c.stream);
+  if (err != cudaSuccess) return err;
+  err = cudaMemsetAsync(e.red_max, 0, (size_t)U * RAILS_RED_MAX_LEN * sizeof(int64_t), c.stream);
+  if (err != cudaSuccess) return err;
+  k_eval_node<<<(unsigned)((long long)U * nd), EVAL_WARPS * 32, 0, c.stream>>>(
+      M, N, nd, d0, C, pow2_shift(C), seed, msg, s.full_base, s.rem_rail, e.S, e.S_e, e.mse,
+      e.nmse, e.red_sum, e.red_max, rsl);
+  count_launch(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(const LaunchCtx& c, int U, int M, int N, double R2,
+                            const int64_t* red_sum, const int64_t* red_max,
+                            const rails_final_t& f) {
+  k_eval_finalize<<<(unsigned)U, 256, 0, c.stream>>>(M, N, R2, RAILS_RED_SUM_LEN(M, N), red_sum,
+                                                     red_max, f);
+  count_launch(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rail_offsets(const LaunchCtx& c, long long n, const int64_t* send_load,
+                                int64_t* rail_base, int64_t* total) {
+  k_rail_offsets<<<1, 1024, 0, c.stream>>>(n, send_load, rail_base, total);
+  count_launch(1);
+  return cudaGetLastError();
+}
+
+}  // namespace rails

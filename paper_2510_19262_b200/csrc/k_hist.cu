@@ -1,0 +1,152 @@
+// k_hist.cu -- a1: per-node send histogram + stable in-bucket rank (sm_100a).
+//
+// D^(1) row block of one source GPU (Alg. 1 "Select input slices for local
+// experts according to Gate and E"): counts[g][h] = #(t,s) routed to global
+// GPU h; msg_bytes = counts * RB for remote h (R#2); row_rank = position of (t,s)
+// among the earlier slots of GPU g with the same h (R#18), which the pack needs.
+//
+// Design (B200): one CTA per (unit, node, source GPU).  The T*k routing entries are
+// split into W contiguous warp segments.  Pass 1: each warp walks its segment in
+// 32-entry groups; __match_any_sync groups equal destinations and the lowest peer
+// adds the group count into the warp's private shared-memory sub-histogram (no
+// atomics, no cross-warp races).  Scan: per bin, an exclusive prefix across warps
+// turns the sub-histograms into the warp's starting rank; the column total is the
+// count.  Pass 2 re-walks the segment (L1/L2-resident) and emits
+// rank = warp base + running count + peers below in the group: deterministic and
+// identical to the sequential definition.  HBM traffic per CTA: read 4*T*k B of
+// routing, write 4*T*k B of ranks + 12*G B of counts/bytes.
+#include "common.cuh"
+
+namespace rails {
+
+template <int W, int UNR>
+__global__ void __launch_bounds__(W * 32)
+    k_hist_rank(const int32_t* __restrict__ topk, const int32_t* __restrict__ lut, int n_inst,
+                int M, int N, int d0, int nd, int T, int k, long long RB,
+                int32_t* __restrict__ counts, int64_t* __restrict__ msg,
+                int32_t* __restrict__ rank, int* err) {
+  extern __shared__ int32_t cnt[];  // [W][G]
+  const int G = M * N;
+  const long long cta = blockIdx.x;  // ((u*nd) + dl)*N + g
+  const long long ul = cta / N;
+  const int d = d0 + (int)(ul % nd);
+  const long long ne = (long long)T * k;
+  const int32_t* __restrict__ src = topk + cta * ne;
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  for (int i = threadIdx.x; i < W * G; i += W * 32) cnt[i] = 0;
+  __syncthreads();
+
+  const long long seg = (((ne + W - 1) / W) + 31) & ~31LL;
+  const long long beg = (long long)wid * seg;
+  const long long end = min(ne, beg + seg);
+  int32_t* my = cnt + wid * G;
+
+  // ---- pass 1: per-warp sub-histogram
+  for (long long base = beg; base < end; base += 32 * UNR) {
+    int hv[UNR];
+#pragma unroll
+    for (int j = 0; j < UNR; ++j) {
+      long long e = base + j * 32 + lane;
+      hv[j] = (e < end) ? __ldg(src + e) : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < UNR; ++j) {
+      long long e = base + j * 32 + lane;
+      int h = -1;
+      if (e < end) {
+        int inst = hv[j];
+        if (inst >= 0 && inst < n_inst) {
+          h = __ldg(lut + inst);
+          if (h < 0 || h >= G) h = -1;
+        }
+        if (h < 0) flag_error(err, ERR_RANGE);
+      }
+      unsigned peers = __match_any_sync(FULL, h);
+      if (h >= 0 && lane == __ffs(peers) - 1) my[h] += __popc(peers);
+    }
+  }
+  __syncthreads();
+
+  // ---- scan across warps per bin; totals are the counts
+  for (int h = threadIdx.x; h < G; h += W * 32) {
+    int run = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      int c = cnt[w * G + h];
+      cnt[w * G + h] = run;
+      run += c;
+    }
+    counts[cta * G + h] = run;
+    msg[cta * G + h] = (h / N == d) ? 0LL : (long long)run * RB;
+  }
+  if (rank == nullptr) return;
+  __syncthreads();
+
+  // ---- pass 2: stable ranks
+  int32_t* __restrict__ dst = rank + cta * ne;
+  for (long long base = beg; base < end; base += 32 * UNR) {
+    int hv[UNR];
+#pragma unroll
+    for (int j = 0; j < UNR; ++j) {
+      long long e = base + j * 32 + lane;
+      hv[j] = (e < end) ? __ldg(src + e) : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < UNR; ++j) {
+      long long e = base + j * 32 + lane;
+      int h = -1;
+      if (e < end) {
+        int inst = hv[j];
+        if (inst >= 0 && inst < n_inst) {
+          h = __ldg(lut + inst);
+          if (h < 0 || h >= G) h = -1;
+        }
+      }
+      unsigned peers = __match_any_sync(FULL, h);
+      int r = -1;
+      if (h >= 0) r = my[h] + __popc(peers & lanemask_lt());
+      __syncwarp();
+      if (h >= 0 && lane == __ffs(peers) - 1) my[h] += __popc(peers);
+      __syncwarp();
+      if (e < end) dst[e] = r;
+    }
+  }
+}
+
+template <int W>
+static cudaError_t launch_w(const LaunchCtx& c, long long grid, int M, int N, int d0, int nd,
+                            int T, int k, const int32_t* topk, const int32_t* lut, int n_inst,
+                            long long RB, int32_t* counts, int64_t* msg, int32_t* rank) {
+  size_t smem = (size_t)W * M * N * sizeof(int32_t);
+  auto kern = k_hist_rank<W, 8>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<(unsigned)grid, W * 32, smem, c.stream>>>(topk, lut, n_inst, M, N, d0, nd, T, k, RB,
+                                                    counts, msg, rank, c.err);
+  count_launch(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_histogram(const LaunchCtx& c, int U, int nd, int d0, int M, int N, int T,
+                             int k, const int32_t* topk, const int32_t* lut, int n_inst,
+                             long long row_bytes, int32_t* counts, int64_t* msg,
+                             int32_t* rank) {
+  const long long grid = (long long)U * nd * N;
+  const long long G = (long long)M * N;
+  // Warps per CTA: as many private sub-histograms as fit in 64 KiB (>= 1).
+  if (G * 8 * 4 <= 65536)
+    return launch_w<8>(c, grid, M, N, d0, nd, T, k, topk, lut, n_inst, row_bytes, counts, msg,
+                       rank);
+  if (G * 4 * 4 <= 65536)
+    return launch_w<4>(c, grid, M, N, d0, nd, T, k, topk, lut, n_inst, row_bytes, counts, msg,
+                       rank);
+  if (G * 2 * 4 <= 98304)
+    return launch_w<2>(c, grid, M, N, d0, nd, T, k, topk, lut, n_inst, row_bytes, counts, msg,
+                       rank);
+  return launch_w<1>(c, grid, M, N, d0, nd, T, k, topk, lut, n_inst, row_bytes, counts, msg,
+                     rank);
+}
+
+}  // namespace rails

@@ -1,0 +1,444 @@
+// k_sched.cu -- a2 chunking, a3 segmented radix sort, a4 LPT chain (sm_100a).
+//
+// a2 (R#3): message B of (g,h) -> floor(B/C) full chunks + one remainder of
+//    B mod C bytes.  Full chunks are never materialised: every full chunk (size C)
+//    is larger than every remainder (< C) and full chunks are emitted in (g,h,c)
+//    order, so under Alg. 2's sort (size desc, ties by GPU index, R#4) they form
+//    the prefix of the sorted list in emission order, and LPT with all-zero start
+//    loads deals them round-robin: full chunk i -> rail i mod N at offset
+//    floor(i/N)*C (lowest-index argmin, R#5).  k_chunk_sort emits
+//    full_base = exclusive prefix of floor(B/C) in (g,h) order and compacts the
+//    remainders (at most one per message) into a list in (g,h) order.
+// a3: the remainder list is sorted by size descending with a stable
+//    LSD radix sort on key = C-1-size (8-bit digits, passes whose digit is constant
+//    over the segment are skipped).  Stability keeps (g,h) order among equal sizes,
+//    which is exactly the tie-break R#4.  One CTA per (unit, node); the segment
+//    lives in shared memory when it fits (generic pointers, global otherwise).
+// a4: one warp per (unit, node) runs the serial argmin chain over the
+//    sorted remainders.  Lane j holds rail j's load relative to a running base
+//    (the current minimum); with rel <= C < 2^26 the 32-bit key (rel << 5) | j
+//    makes argmin-with-lowest-index-tie a single redux.sync.min.u32.  Offsets are
+//    base + rel of the chosen rail before the add (R#19).
+#include <climits>
+
+#include "common.cuh"
+
+namespace rails {
+
+// ---------------------------------------------------------------- block radix pass
+// Stable counting pass over n items on digit (key >> shift) & 255.  Warp w owns
+// the contiguous item range [w*seg, (w+1)*seg); per-warp digit counters in
+// shared memory `hist` ([W][256] int32), `sc` >= 16 ints of scratch.
+// Requires blockDim.x >= 256 and a multiple of 32.
+template <typename KeyT, typename IdxT>
+__device__ void radix_pass(const KeyT* kin, const IdxT* iin, KeyT* kout, IdxT* iout, int n,
+                           int shift, int* hist, int* sc) {
+  const int W = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int seg = (((n + W - 1) / W) + 31) & ~31;
+  const int beg = wid * seg, end = min(n, beg + seg);
+  for (int i = threadIdx.x; i < W * 256; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  int* my = hist + wid * 256;
+  for (int base = beg; base < end; base += 32) {
+    int i = base + lane;
+    unsigned dg = (i < end) ? (unsigned)((kin[i] >> shift) & 255) : 0xffffffffu;
+    unsigned peers = __match_any_sync(FULL, dg);
+    if (i < end && lane == __ffs(peers) - 1) my[dg] += __popc(peers);
+  }
+  __syncthreads();
+  // digit totals -> exclusive digit bases -> per-warp starting positions
+  // (threads 0..255 = warps 0..7, one digit each)
+  int tot = 0, inc = 0;
+  if (threadIdx.x < 256) {
+    for (int w = 0; w < W; ++w) tot += hist[w * 256 + threadIdx.x];
+    inc = warp_incl_scan(tot);
+    if (lane == 31) sc[wid] = inc;
+  }
+  __syncthreads();
+  if (threadIdx.x < 256) {
+    int run = inc - tot;
+    for (int w = 0; w < wid; ++w) run += sc[w];
+    for (int w = 0; w < W; ++w) {
+      int c = hist[w * 256 + threadIdx.x];
+      hist[w * 256 + threadIdx.x] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  for (int base = beg; base < end; base += 32) {
+    int i = base + lane;
+    unsigned dg = (i < end) ? (unsigned)((kin[i] >> shift) & 255) : 0xffffffffu;
+    unsigned peers = __match_any_sync(FULL, dg);
+    int pos = 0;
+    if (i < end) pos = my[dg] + __popc(peers & lanemask_lt());
+    __syncwarp();
+    if (i < end && lane == __ffs(peers) - 1) my[dg] += __popc(peers);
+    __syncwarp();
+    if (i < end) {
+      kout[pos] = kin[i];
+      iout[pos] = iin[i];
+    }
+  }
+  __syncthreads();
+}
+
+// Sort n (key, idx) pairs ascending by key, stably.  Returns 0 if the result is in
+// the A buffers, 1 if in the B buffers.  kor/kand: OR and AND of all keys.
+template <typename KeyT, typename IdxT>
+__device__ int radix_sort(KeyT* kA, IdxT* iA, KeyT* kB, IdxT* iB, int n, KeyT kor, KeyT kand,
+                          int nbits, int* hist, int* sc) {
+  int cur = 0;
+  if (n <= 1) return 0;
+  const KeyT diff = kor ^ kand;
+  for (int shift = 0; shift < nbits; shift += 8) {
+    if (((diff >> shift) & 255) == 0) continue;  // digit constant: pass is identity
+    if (cur == 0)
+      radix_pass<KeyT, IdxT>(kA, iA, kB, iB, n, shift, hist, sc);
+    else
+      radix_pass<KeyT, IdxT>(kB, iB, kA, iA, n, shift, hist, sc);
+    cur ^= 1;
+  }
+  return cur;
+}
+
+template <typename T>
+__device__ __forceinline__ T block_reduce_or(T v, T* s) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v |= __shfl_xor_sync(FULL, v, o);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (lane == 0) s[wid] = v;
+  __syncthreads();
+  T r = 0;
+  for (int w = 0; w < nw; ++w) r |= s[w];
+  __syncthreads();
+  return r;
+}
+template <typename T>
+__device__ __forceinline__ T block_reduce_and(T v, T* s) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v &= __shfl_xor_sync(FULL, v, o);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (lane == 0) s[wid] = v;
+  __syncthreads();
+  T r = ~(T)0;
+  for (int w = 0; w < nw; ++w) r &= s[w];
+  __syncthreads();
+  return r;
+}
+
+// ---------------------------------------------------------------- a2 + a3
+constexpr int SORT_THREADS = 512;
+constexpr int SORT_SMEM_ITEMS = 16384;  // items per CTA kept in shared memory
+
+template <typename IdxT>
+__global__ void __launch_bounds__(SORT_THREADS)
+    k_chunk_sort(const int64_t* __restrict__ msg, long long NG, int N, int d0, int nd,
+                 long long C, int cshift, int nbits, int64_t* __restrict__ full_base, int8_t* __restrict__ rem_rail,
+                 int64_t* __restrict__ rem_off, int64_t* __restrict__ n_full_out,
+                 int32_t* __restrict__ n_rem_out, uint32_t* __restrict__ ws_w,
+                 uint32_t* __restrict__ ws_m, uint8_t* __restrict__ ws_scratch, int use_smem,
+                 int* err) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ long long scan_scratch[33];
+  __shared__ int hist[(SORT_THREADS / 32) * 256];
+  __shared__ int sc[32];
+  __shared__ uint32_t red32[32];
+
+  const long long seg = blockIdx.x;
+  const ChunkDiv cd{C, cshift};
+  const int64_t* __restrict__ mg = msg + seg * NG;
+  const long long G = NG / N;
+  const int d = d0 + (int)(seg % nd);
+
+  uint32_t *kA, *kB;
+  IdxT *iA, *iB;
+  {
+    const long long cap = NG;
+    uint8_t* base = use_smem ? smem : (ws_scratch + seg * (cap * (8 + 2 * sizeof(IdxT)) + 64));
+    kA = (uint32_t*)base;
+    kB = kA + cap;
+    iA = (IdxT*)(kB + cap);
+    iB = iA + cap;
+  }
+
+  long long carry_full = 0;
+  int carry_rem = 0;
+  uint32_t kor = 0, kand = 0xffffffffu;
+  for (long long t0 = 0; t0 < NG; t0 += SORT_THREADS) {
+    const long long m = t0 + threadIdx.x;
+    long long B = 0;
+    if (m < NG) {
+      B = mg[m];
+      // negative bytes, or bytes to a GPU of the source node (R#2), are invalid
+      if (B < 0 || (B != 0 && (m % G) / N == d)) {
+        flag_error(err, ERR_RANGE);
+        B = 0;
+      }
+    }
+    const long long nf = cd.div(B);
+    const long long rem = B - nf * C;
+    const int fl = rem > 0;
+    if (nf >= (1LL << 40)) flag_error(err, ERR_OVERFLOW);
+    long long tot;
+    const long long ex = block_excl_scan((nf << 16) | fl, scan_scratch, &tot);
+    if (m < NG) {
+      full_base[seg * NG + m] = carry_full + (ex >> 16);
+      if (fl) {
+        const int pos = carry_rem + (int)(ex & 0xffff);
+        const uint32_t key = (uint32_t)(C - 1 - rem);
+        kA[pos] = key;
+        iA[pos] = (IdxT)m;
+        kor |= key;
+        kand &= key;
+      } else {
+        rem_rail[seg * NG + m] = -1;
+        rem_off[seg * NG + m] = 0;
+      }
+    }
+    carry_full += tot >> 16;
+    carry_rem += (int)(tot & 0xffff);
+  }
+  kor = block_reduce_or(kor, red32);
+  kand = block_reduce_and(kand, red32);
+  if (threadIdx.x == 0) {
+    n_full_out[seg] = carry_full;
+    n_rem_out[seg] = carry_rem;
+  }
+  __syncthreads();
+  const int n = carry_rem;
+  const int which = radix_sort<uint32_t, IdxT>(kA, iA, kB, iB, n, kor, kand, nbits, hist, sc);
+  const uint32_t* ks = which ? kB : kA;
+  const IdxT* is = which ? iB : iA;
+  for (int i = threadIdx.x; i < n; i += SORT_THREADS) {
+    ws_w[seg * NG + i] = (uint32_t)(C - 1 - (long long)ks[i]);
+    ws_m[seg * NG + i] = (uint32_t)is[i];
+  }
+}
+
+// ---------------------------------------------------------------- a4 chain
+constexpr int CHAIN_WARPS = 4;
+
+__global__ void __launch_bounds__(CHAIN_WARPS * 32)
+    k_lpt_chain(long long nseg, int N, long long C, long long NG,
+                const int64_t* __restrict__ n_full, const int32_t* __restrict__ n_rem,
+                const uint32_t* __restrict__ ws_w, const uint32_t* __restrict__ ws_m,
+                int8_t* __restrict__ rem_rail, int64_t* __restrict__ rem_off,
+                int64_t* __restrict__ send_load, int* err) {
+  const int lane = threadIdx.x & 31;
+  const long long seg = (long long)blockIdx.x * CHAIN_WARPS + (threadIdx.x >> 5);
+  if (seg >= nseg) return;
+  const long long nf = n_full[seg];
+  const long long q = nf / N;
+  const int r = (int)(nf - q * N);
+  const int nr = n_rem[seg];
+  const uint32_t* __restrict__ sw = ws_w + seg * NG;
+  const uint32_t* __restrict__ sm = ws_m + seg * NG;
+  int8_t* __restrict__ rr = rem_rail + seg * NG;
+  int64_t* __restrict__ ro = rem_off + seg * NG;
+
+  if (C < (1LL << 26)) {
+    // Fast path: relative loads, single redux.sync per step.
+    long long base = C * q;  // current minimum load (full-chunk closed form)
+    uint32_t rel = (lane < r) ? (uint32_t)C : 0u;
+    for (int i0 = 0; i0 < nr; i0 += 32) {
+      uint32_t wv = 0, mv = 0;
+      if (i0 + lane < nr) {
+        wv = sw[i0 + lane];
+        mv = sm[i0 + lane];
+      }
+      const int cnt = min(32, nr - i0);
+      for (int b = 0; b < cnt; ++b) {
+        const uint32_t wb = __shfl_sync(FULL, wv, b);
+        const uint32_t mb = __shfl_sync(FULL, mv, b);
+        const uint32_t key = (lane < N) ? ((rel << 5) | (uint32_t)lane) : 0xffffffffu;
+        const uint32_t kmin = __reduce_min_sync(FULL, key);
+        const int j = (int)(kmin & 31u);
+        const uint32_t mrel = kmin >> 5;
+        if (lane == j) {
+          rel += wb;
+          rr[mb] = (int8_t)j;
+          ro[mb] = base + mrel;
+        }
+        rel -= mrel;
+        base += mrel;
+      }
+    }
+    if (lane < N) send_load[seg * N + lane] = base + rel;
+  } else {
+    // General path: 64-bit loads, butterfly argmin over (load, lane).
+    long long L = (lane < N) ? C * (q + (lane < r ? 1 : 0)) : LLONG_MAX;
+    for (int i0 = 0; i0 < nr; i0 += 32) {
+      uint32_t wv = 0, mv = 0;
+      if (i0 + lane < nr) {
+        wv = sw[i0 + lane];
+        mv = sm[i0 + lane];
+      }
+      const int cnt = min(32, nr - i0);
+      for (int b = 0; b < cnt; ++b) {
+        const uint32_t wb = __shfl_sync(FULL, wv, b);
+        const uint32_t mb = __shfl_sync(FULL, mv, b);
+        long long v = L;
+        int ix = lane;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          long long ov = __shfl_xor_sync(FULL, v, o);
+          int oi = __shfl_xor_sync(FULL, ix, o);
+          if (ov < v || (ov == v && oi < ix)) {
+            v = ov;
+            ix = oi;
+          }
+        }
+        if (lane == ix) {
+          rr[mb] = (int8_t)ix;
+          ro[mb] = v;
+          L += wb;
+        }
+      }
+    }
+    if (lane < N) {
+      if (L < 0) flag_error(err, ERR_OVERFLOW);
+      send_load[seg * N + lane] = L;
+    }
+  }
+}
+
+static int ceil_log2(long long x) {  // bits needed for values 0..x-1
+  int b = 0;
+  while ((1LL << b) < x) ++b;
+  return b;
+}
+
+size_t schedule_workspace_bytes(int U, int nd, long long NG) {
+  const long long nseg = (long long)U * nd;
+  size_t sorted = (size_t)nseg * NG * 8;  // ws_w + ws_m
+  size_t scratch = (NG <= SORT_SMEM_ITEMS) ? 0 : (size_t)nseg * (NG * (8 + 2 * 4) + 64);
+  return 256 + sorted + scratch;
+}
+
+cudaError_t launch_schedule(const LaunchCtx& c, int U, int nd, int d0, int M, int N, long long C,
+                            const int64_t* msg, const rails_sched_t& s, void* ws) {
+  const long long nseg = (long long)U * nd;
+  const long long NG = (long long)N * M * N;
+  int cshift = -1;
+  if ((C & (C - 1)) == 0) cshift = ceil_log2(C);
+  const int nbits = ceil_log2(C > 1 ? C - 1 : 1) + 1;
+  uint8_t* w8 = (uint8_t*)ws;
+  uint32_t* ws_w = (uint32_t*)(w8 + 256);
+  uint32_t* ws_m = ws_w + nseg * NG;
+  uint8_t* scratch = (uint8_t*)(ws_m + nseg * NG);
+  cudaError_t e;
+  if (NG <= SORT_SMEM_ITEMS) {
+    const size_t smem = (size_t)NG * (8 + 2 * sizeof(uint16_t));
+    auto kern = k_chunk_sort<uint16_t>;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<(unsigned)nseg, SORT_THREADS, smem, c.stream>>>(
+        msg, NG, N, d0, nd, C, cshift, nbits, s.full_base, s.rem_rail, s.rem_off, s.n_full, s.n_rem, ws_w,
+        ws_m, nullptr, 1, c.err);
+  } else {
+    k_chunk_sort<uint32_t><<<(unsigned)nseg, SORT_THREADS, 0, c.stream>>>(
+        msg, NG, N, d0, nd, C, cshift, nbits, s.full_base, s.rem_rail, s.rem_off, s.n_full, s.n_rem, ws_w,
+        ws_m, scratch, 0, c.err);
+  }
+  count_launch(1);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  const unsigned grid = (unsigned)((nseg + CHAIN_WARPS - 1) / CHAIN_WARPS);
+  k_lpt_chain<<<grid, CHAIN_WARPS * 32, 0, c.stream>>>(nseg, N, C, NG, s.n_full, s.n_rem, ws_w,
+                                                       ws_m, s.rem_rail, s.rem_off,
+                                                       s.send_load, c.err);
+  count_launch(1);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- generic assign
+// One CTA per flow set: stable radix sort of ~w (64-bit keys) then the 64-bit
+// argmin chain on warp 0.  Workspace holds the per-set key/index buffers.
+__global__ void __launch_bounds__(SORT_THREADS)
+    k_assign(int N, const int64_t* __restrict__ seg_off, const int64_t* __restrict__ w,
+             int32_t* __restrict__ rail, int64_t* __restrict__ off, int64_t* __restrict__ load,
+             uint64_t* kA, uint64_t* kB, uint32_t* iA, uint32_t* iB, int* err) {
+  __shared__ int hist[(SORT_THREADS / 32) * 256];
+  __shared__ int sc[32];
+  __shared__ uint64_t red64[32];
+  const int s = blockIdx.x;
+  const long long b0 = seg_off[s], b1 = seg_off[s + 1];
+  const int n = (int)(b1 - b0);
+  kA += b0;
+  kB += b0;
+  iA += b0;
+  iB += b0;
+  uint64_t kor = 0, kand = ~0ull;
+  for (int i = threadIdx.x; i < n; i += SORT_THREADS) {
+    long long wi = w[b0 + i];
+    if (wi < 0) {
+      flag_error(err, ERR_RANGE);
+      wi = 0;
+    }
+    const uint64_t key = ~(uint64_t)wi;
+    kA[i] = key;
+    iA[i] = (uint32_t)i;
+    kor |= key;
+    kand &= key;
+  }
+  kor = block_reduce_or(kor, red64);
+  kand = block_reduce_and(kand, red64);
+  __syncthreads();
+  const int which = radix_sort<uint64_t, uint32_t>(kA, iA, kB, iB, n, kor, kand, 64, hist, sc);
+  const uint64_t* ks = which ? kB : kA;
+  const uint32_t* is = which ? iB : iA;
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  long long L = (lane < N) ? 0 : LLONG_MAX;
+  for (int i0 = 0; i0 < n; i0 += 32) {
+    long long wv = 0;
+    uint32_t mv = 0;
+    if (i0 + lane < n) {
+      wv = (long long)(~ks[i0 + lane]);
+      mv = is[i0 + lane];
+    }
+    const int cnt = min(32, n - i0);
+    for (int b = 0; b < cnt; ++b) {
+      const long long wb = __shfl_sync(FULL, wv, b);
+      const uint32_t mb = __shfl_sync(FULL, mv, b);
+      long long v = L;
+      int ix = lane;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        long long ov = __shfl_xor_sync(FULL, v, o);
+        int oi = __shfl_xor_sync(FULL, ix, o);
+        if (ov < v || (ov == v && oi < ix)) {
+          v = ov;
+          ix = oi;
+        }
+      }
+      if (lane == ix) {
+        rail[b0 + mb] = ix;
+        off[b0 + mb] = v;
+        if (L > LLONG_MAX - wb) flag_error(err, ERR_OVERFLOW);
+        L += wb;
+      }
+    }
+  }
+  if (lane < N) load[(long long)s * N + lane] = L;
+}
+
+size_t assign_workspace_bytes(int n_seg, long long F) {
+  (void)n_seg;
+  return 256 + (size_t)F * (8 + 8 + 4 + 4) + 64;
+}
+
+cudaError_t launch_assign(const LaunchCtx& c, int N, int n_seg, const int64_t* seg_off,
+                          long long F, const int64_t* w, int32_t* rail, int64_t* off,
+                          int64_t* load, void* ws) {
+  uint8_t* w8 = (uint8_t*)ws + 256;
+  uint64_t* kA = (uint64_t*)w8;
+  uint64_t* kB = kA + F;
+  uint32_t* iA = (uint32_t*)(kB + F);
+  uint32_t* iB = iA + F;
+  k_assign<<<(unsigned)n_seg, SORT_THREADS, 0, c.stream>>>(N, seg_off, w, rail, off, load, kA,
+                                                           kB, iA, iB, c.err);
+  count_launch(1);
+  return cudaGetLastError();
+}
+
+}  // namespace rails

@@ -1,0 +1,91 @@
+"""One pass of the whole hot path (all SURVEY section 8(a) rows) over preallocated buffers.
+
+Routing configs (C1, C3, C4):  a1 histogram -> a2-a4 LPT schedule -> a5 eval ->
+[a6 cross-rank reduction] -> finalize -> a7 rail offsets + pack.
+Matrix configs (C2, C5):       a2-a4 -> a5 -> [a6] -> finalize.
+
+Only buffer management and call sequencing live here; every step is a C-ABI call
+into librails.so (``rails.py``).  ``reduce`` is the a6 hook: a callable taking
+(red_sum, red_max) int64 tensors and all-reducing them (SUM, MAX) across the ranks
+that hold different source nodes of the same units (torch.distributed / NCCL).
+"""
+from __future__ import annotations
+
+from typing import Callable
+
+import torch
+
+from . import rails
+
+
+class RoutingPipeline:
+    def __init__(self, M: int, N: int, T: int, k: int, row_bytes: int, chunk_bytes: int,
+                 U: int, d0: int, nd: int, n_inst: int, device, R2: float = 5.0e10,
+                 ecmp_seed: int = 0x9E3779B97F4A7C15, out_cap: int | None = None):
+        self.tp = rails.topo(M, N, chunk_bytes, R2, 0.0, ecmp_seed)
+        self.sh = rails.shard(U, d0, nd)
+        self.M, self.N, self.T, self.k, self.RB, self.C = M, N, T, k, row_bytes, chunk_bytes
+        self.U, self.d0, self.nd = U, d0, nd
+        dev = torch.device(device)
+        G = M * N
+        self.counts = torch.empty((U, nd, N, G), dtype=torch.int32, device=dev)
+        self.msg = torch.empty((U, nd, N, G), dtype=torch.int64, device=dev)
+        self.rank = torch.empty((U, nd, N, T, k), dtype=torch.int32, device=dev)
+        self.sched = rails.Schedule.empty(self.tp, self.sh, dev)
+        self.ws = torch.empty(rails.schedule_workspace(self.tp, self.sh), dtype=torch.uint8,
+                              device=dev)
+        self.ev = rails.EvalOut.empty(self.tp, self.sh, dev)
+        self.final = rails.empty_final(U, dev)
+        self.rail_base = torch.empty((U, nd, N), dtype=torch.int64, device=dev)
+        self.total = torch.empty(1, dtype=torch.int64, device=dev)
+        # every remote (t,s) copy is at most one row: a tight upper bound needing no sync
+        cap = out_cap if out_cap is not None else U * nd * N * T * k * row_bytes
+        self.out = torch.empty(cap, dtype=torch.uint8, device=dev)
+
+    def schedule_part(self, topk: torch.Tensor, lut: torch.Tensor, stream=None):
+        rails.histogram(self.tp, self.sh, topk, lut, self.RB,
+                        out=(self.counts, self.msg, self.rank), stream=stream)
+        rails.lpt_schedule(self.tp, self.sh, self.msg, out=self.sched, workspace=self.ws,
+                           stream=stream)
+        rails.eval(self.tp, self.sh, self.msg, self.sched, out=self.ev, stream=stream)
+
+    def finalize_part(self, reduce: Callable | None = None, stream=None):
+        if reduce is not None:
+            reduce(self.ev.red_sum, self.ev.red_max)
+        rails.eval_finalize(self.tp, self.U, self.ev.red_sum, self.ev.red_max, out=self.final,
+                            stream=stream)
+
+    def pack_part(self, topk, lut, x, stream=None):
+        rails.rail_offsets(self.tp, self.sh, self.sched.send_load, self.rail_base, self.total,
+                           stream=stream)
+        rails.pack(self.tp, self.sh, self.T, self.k, x, topk, lut, self.rank, self.msg, self.RB,
+                   self.sched, self.rail_base, self.out, stream=stream)
+
+    def step(self, topk, lut, x, reduce: Callable | None = None, stream=None):
+        self.schedule_part(topk, lut, stream)
+        self.finalize_part(reduce, stream)
+        self.pack_part(topk, lut, x, stream)
+
+
+class MatrixPipeline:
+    """Schedule + eval for D^(1) byte matrices msg [U][nd][N][G] (no routing, no pack)."""
+
+    def __init__(self, M: int, N: int, chunk_bytes: int, U: int, d0: int, nd: int, device,
+                 R2: float = 5.0e10, ecmp_seed: int = 0x9E3779B97F4A7C15):
+        self.tp = rails.topo(M, N, chunk_bytes, R2, 0.0, ecmp_seed)
+        self.sh = rails.shard(U, d0, nd)
+        self.U = U
+        dev = torch.device(device)
+        self.sched = rails.Schedule.empty(self.tp, self.sh, dev)
+        self.ws = torch.empty(rails.schedule_workspace(self.tp, self.sh), dtype=torch.uint8,
+                              device=dev)
+        self.ev = rails.EvalOut.empty(self.tp, self.sh, dev)
+        self.final = rails.empty_final(U, dev)
+
+    def step(self, msg: torch.Tensor, reduce: Callable | None = None, stream=None):
+        rails.lpt_schedule(self.tp, self.sh, msg, out=self.sched, workspace=self.ws, stream=stream)
+        rails.eval(self.tp, self.sh, msg, self.sched, out=self.ev, stream=stream)
+        if reduce is not None:
+            reduce(self.ev.red_sum, self.ev.red_max)
+        rails.eval_finalize(self.tp, self.U, self.ev.red_sum, self.ev.red_max, out=self.final,
+                            stream=stream)

@@ -1,0 +1,318 @@
+"""ctypes binding of include/rails.h -- argument marshalling only.
+
+Every function here has the name of a C entry point (without the ``rails_``
+prefix), checks tensor dtypes/devices/shapes, passes ``tensor.data_ptr()`` and the
+current CUDA stream, and raises :class:`RailsError` on a nonzero return code.  All
+computation happens in librails.so's sm_100a kernels; there is no CPU fallback:
+loading fails loudly when the library is missing, and calls require CUDA tensors.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librails.so")
+
+RAILS_OK, RAILS_EINVAL, RAILS_ERANGE, RAILS_ENOSPC, RAILS_EOVERFLOW, RAILS_ECUDA = 0, -1, -2, -3, -4, -5
+_NAMES = {-1: "EINVAL", -2: "ERANGE", -3: "ENOSPC", -4: "EOVERFLOW", -5: "ECUDA"}
+RED_MAX_LEN = 4
+
+
+def red_sum_len(M: int, N: int) -> int:
+    return 2 * M * N + M + 2
+
+
+class RailsError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"RAILS_{_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+class Topo(ctypes.Structure):
+    _fields_ = [("M", ctypes.c_int32), ("N", ctypes.c_int32), ("chunk_bytes", ctypes.c_int64),
+                ("R2", ctypes.c_double), ("R1", ctypes.c_double), ("ecmp_seed", ctypes.c_uint64)]
+
+
+class Shard(ctypes.Structure):
+    _fields_ = [("U", ctypes.c_int32), ("d0", ctypes.c_int32), ("nd", ctypes.c_int32)]
+
+
+class _Sched(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in
+                ("full_base", "rem_rail", "rem_off", "send_load", "n_full", "n_rem")]
+
+
+class _Eval(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("S", "S_e", "mse", "nmse", "red_sum", "red_max")]
+
+
+_FINAL_FIELDS = ("maxload", "maxload_e", "total", "rowmax", "colmax", "T", "T_e", "T_star",
+                 "busbw", "busbw_e")
+
+
+class _Final(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in _FINAL_FIELDS]
+
+
+_lib = None
+
+
+def lib():
+    """Load librails.so (raises if it has not been built: no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        P, i32, i64, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+        PT, PS = ctypes.POINTER(Topo), ctypes.POINTER(Shard)
+        L.rails_histogram.argtypes = [PT, PS, i32, i32, P, P, i32, i64, P, P, P, P]
+        L.rails_schedule_workspace.argtypes = [PT, PS, ctypes.POINTER(sz)]
+        L.rails_lpt_schedule.argtypes = [PT, PS, P, ctypes.POINTER(_Sched), P, sz, P]
+        L.rails_assign_workspace.argtypes = [i32, i64, ctypes.POINTER(sz)]
+        L.rails_lpt_assign.argtypes = [i32, i32, P, i64, P, P, P, P, P, sz, P]
+        L.rails_eval.argtypes = [PT, PS, P, ctypes.POINTER(_Sched), ctypes.POINTER(_Eval), P]
+        L.rails_eval_finalize.argtypes = [PT, i32, P, P, ctypes.POINTER(_Final), P]
+        L.rails_rail_offsets.argtypes = [PT, PS, P, P, P, P]
+        L.rails_pack.argtypes = [PT, PS, i32, i32, P, P, P, i32, P, P, i64,
+                                 ctypes.POINTER(_Sched), P, P, i64, P]
+        L.rails_check.argtypes = [P]
+        L.rails_last_error.restype = ctypes.c_char_p
+        L.rails_launch_count.argtypes = [i32]
+        L.rails_launch_count.restype = i64
+        L.rails_version.restype = i32
+        for n in ("rails_histogram", "rails_schedule_workspace", "rails_lpt_schedule",
+                  "rails_assign_workspace", "rails_lpt_assign", "rails_eval",
+                  "rails_eval_finalize", "rails_rail_offsets", "rails_pack", "rails_check"):
+            getattr(L, n).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _ok(rc: int):
+    if rc != RAILS_OK:
+        raise RailsError(rc, lib().rails_last_error().decode())
+
+
+def _stream(stream=None) -> ctypes.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t: torch.Tensor | None, dtype=None, what="tensor"):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError(f"{what} must be a CUDA tensor (no CPU fallback)")
+    if dtype is not None and t.dtype != dtype:
+        raise ValueError(f"{what} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{what} must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def topo(M: int, N: int, chunk_bytes: int, R2: float = 5.0e10, R1: float = 0.0,
+         ecmp_seed: int = 0x9E3779B97F4A7C15) -> Topo:
+    return Topo(M, N, chunk_bytes, R2, R1, ecmp_seed)
+
+
+def shard(U: int, d0: int, nd: int) -> Shard:
+    return Shard(U, d0, nd)
+
+
+# ---------------------------------------------------------------- a1
+def histogram(tp: Topo, sh: Shard, topk: torch.Tensor, lut: torch.Tensor, row_bytes: int,
+              with_rank: bool = True, out=None, stream=None):
+    """topk int32 [U][nd][N][T][k] -> (counts int32, msg_bytes int64 [U][nd][N][G], rank)."""
+    U, nd, N, T, k = topk.shape
+    G = tp.M * tp.N
+    assert (U, nd, N) == (sh.U, sh.nd, tp.N), "topk shape must be [U][nd][N][T][k]"
+    dev = topk.device
+    if out is None:
+        counts = torch.empty((U, nd, N, G), dtype=torch.int32, device=dev)
+        msg = torch.empty((U, nd, N, G), dtype=torch.int64, device=dev)
+        rank = torch.empty((U, nd, N, T, k), dtype=torch.int32, device=dev) if with_rank else None
+    else:
+        counts, msg, rank = out
+    _ok(lib().rails_histogram(ctypes.byref(tp), ctypes.byref(sh), T, k,
+                              _ptr(topk, torch.int32, "topk"), _ptr(lut, torch.int32, "lut"),
+                              lut.numel(), row_bytes, _ptr(counts, torch.int32, "counts"),
+                              _ptr(msg, torch.int64, "msg"), _ptr(rank, torch.int32, "rank"),
+                              _stream(stream)))
+    return counts, msg, rank
+
+
+# ---------------------------------------------------------------- a2-a4
+@dataclass
+class Schedule:
+    full_base: torch.Tensor  # int64 [U][nd][N][G]
+    rem_rail: torch.Tensor   # int8  [U][nd][N][G]
+    rem_off: torch.Tensor    # int64 [U][nd][N][G]
+    send_load: torch.Tensor  # int64 [U][nd][N]
+    n_full: torch.Tensor     # int64 [U][nd]
+    n_rem: torch.Tensor      # int32 [U][nd]
+
+    @staticmethod
+    def empty(tp: Topo, sh: Shard, device) -> "Schedule":
+        U, nd, N, G = sh.U, sh.nd, tp.N, tp.M * tp.N
+        z = dict(device=device)
+        return Schedule(torch.empty((U, nd, N, G), dtype=torch.int64, **z),
+                        torch.empty((U, nd, N, G), dtype=torch.int8, **z),
+                        torch.empty((U, nd, N, G), dtype=torch.int64, **z),
+                        torch.empty((U, nd, N), dtype=torch.int64, **z),
+                        torch.empty((U, nd), dtype=torch.int64, **z),
+                        torch.empty((U, nd), dtype=torch.int32, **z))
+
+    def c(self) -> _Sched:
+        return _Sched(_ptr(self.full_base, torch.int64, "full_base"),
+                      _ptr(self.rem_rail, torch.int8, "rem_rail"),
+                      _ptr(self.rem_off, torch.int64, "rem_off"),
+                      _ptr(self.send_load, torch.int64, "send_load"),
+                      _ptr(self.n_full, torch.int64, "n_full"),
+                      _ptr(self.n_rem, torch.int32, "n_rem"))
+
+
+def schedule_workspace(tp: Topo, sh: Shard) -> int:
+    n = ctypes.c_size_t(0)
+    _ok(lib().rails_schedule_workspace(ctypes.byref(tp), ctypes.byref(sh), ctypes.byref(n)))
+    return int(n.value)
+
+
+def lpt_schedule(tp: Topo, sh: Shard, msg: torch.Tensor, out: Schedule | None = None,
+                 workspace: torch.Tensor | None = None, stream=None) -> Schedule:
+    if out is None:
+        out = Schedule.empty(tp, sh, msg.device)
+    need = schedule_workspace(tp, sh)
+    if workspace is None:
+        workspace = torch.empty(need, dtype=torch.uint8, device=msg.device)
+    cs = out.c()
+    _ok(lib().rails_lpt_schedule(ctypes.byref(tp), ctypes.byref(sh), _ptr(msg, torch.int64, "msg"),
+                                 ctypes.byref(cs), _ptr(workspace, torch.uint8, "workspace"),
+                                 workspace.numel(), _stream(stream)))
+    return out
+
+
+def lpt_assign(N: int, seg_off: torch.Tensor, w: torch.Tensor, stream=None):
+    """Generic atomic-flow LPT: returns (rail int32 [F], off int64 [F], load int64 [n_seg][N])."""
+    n_seg = seg_off.numel() - 1
+    F = w.numel()
+    dev = w.device
+    n = ctypes.c_size_t(0)
+    _ok(lib().rails_assign_workspace(n_seg, F, ctypes.byref(n)))
+    ws = torch.empty(int(n.value), dtype=torch.uint8, device=dev)
+    rail = torch.empty(F, dtype=torch.int32, device=dev)
+    off = torch.empty(F, dtype=torch.int64, device=dev)
+    load = torch.empty((n_seg, N), dtype=torch.int64, device=dev)
+    _ok(lib().rails_lpt_assign(N, n_seg, _ptr(seg_off, torch.int64, "seg_off"), F,
+                               _ptr(w, torch.int64, "w"), _ptr(rail), _ptr(off), _ptr(load),
+                               _ptr(ws), ws.numel(), _stream(stream)))
+    return rail, off, load
+
+
+# ---------------------------------------------------------------- a5
+@dataclass
+class EvalOut:
+    S: torch.Tensor        # int64 [U][nd][N]
+    S_e: torch.Tensor      # int64 [U][nd][N]
+    mse: torch.Tensor      # float64 [U][nd]
+    nmse: torch.Tensor     # float64 [U][nd]
+    red_sum: torch.Tensor  # int64 [U][2MN+M+2]
+    red_max: torch.Tensor  # int64 [U][4]
+
+    @staticmethod
+    def empty(tp: Topo, sh: Shard, device) -> "EvalOut":
+        U, nd, N = sh.U, sh.nd, tp.N
+        z = dict(device=device)
+        return EvalOut(torch.empty((U, nd, N), dtype=torch.int64, **z),
+                       torch.empty((U, nd, N), dtype=torch.int64, **z),
+                       torch.empty((U, nd), dtype=torch.float64, **z),
+                       torch.empty((U, nd), dtype=torch.float64, **z),
+                       torch.empty((U, red_sum_len(tp.M, N)), dtype=torch.int64, **z),
+                       torch.empty((U, RED_MAX_LEN), dtype=torch.int64, **z))
+
+    def c(self) -> _Eval:
+        return _Eval(_ptr(self.S, torch.int64), _ptr(self.S_e, torch.int64),
+                     _ptr(self.mse, torch.float64), _ptr(self.nmse, torch.float64),
+                     _ptr(self.red_sum, torch.int64), _ptr(self.red_max, torch.int64))
+
+    def R(self, M: int, N: int) -> torch.Tensor:
+        return self.red_sum[:, :M * N].view(-1, M, N)
+
+    def R_e(self, M: int, N: int) -> torch.Tensor:
+        return self.red_sum[:, M * N:2 * M * N].view(-1, M, N)
+
+    def colsum(self, M: int, N: int) -> torch.Tensor:
+        return self.red_sum[:, 2 * M * N:2 * M * N + M]
+
+
+def eval(tp: Topo, sh: Shard, msg: torch.Tensor, sched: Schedule, out: EvalOut | None = None,
+         stream=None) -> EvalOut:  # noqa: A001 - the C entry point is rails_eval
+    if out is None:
+        out = EvalOut.empty(tp, sh, msg.device)
+    cs, ce = sched.c(), out.c()
+    _ok(lib().rails_eval(ctypes.byref(tp), ctypes.byref(sh), _ptr(msg, torch.int64, "msg"),
+                         ctypes.byref(cs), ctypes.byref(ce), _stream(stream)))
+    return out
+
+
+def empty_final(U: int, device) -> dict:
+    f = {}
+    for n in _FINAL_FIELDS:
+        dt = torch.float64 if n in ("T", "T_e", "T_star", "busbw", "busbw_e") else torch.int64
+        f[n] = torch.empty(U, dtype=dt, device=device)
+    return f
+
+
+def eval_finalize(tp: Topo, U: int, red_sum: torch.Tensor, red_max: torch.Tensor,
+                  out: dict | None = None, stream=None) -> dict:
+    if out is None:
+        out = empty_final(U, red_sum.device)
+    cf = _Final(*[_ptr(out[n]) for n in _FINAL_FIELDS])
+    _ok(lib().rails_eval_finalize(ctypes.byref(tp), U, _ptr(red_sum, torch.int64, "red_sum"),
+                                  _ptr(red_max, torch.int64, "red_max"), ctypes.byref(cf),
+                                  _stream(stream)))
+    return out
+
+
+# ---------------------------------------------------------------- a7
+def rail_offsets(tp: Topo, sh: Shard, send_load: torch.Tensor, rail_base=None, total=None,
+                 stream=None):
+    if rail_base is None:
+        rail_base = torch.empty_like(send_load)
+    if total is None:
+        total = torch.empty(1, dtype=torch.int64, device=send_load.device)
+    _ok(lib().rails_rail_offsets(ctypes.byref(tp), ctypes.byref(sh),
+                                 _ptr(send_load, torch.int64, "send_load"),
+                                 _ptr(rail_base, torch.int64, "rail_base"),
+                                 _ptr(total, torch.int64, "total"), _stream(stream)))
+    return rail_base, total
+
+
+def pack(tp: Topo, sh: Shard, T: int, k: int, x: torch.Tensor, topk: torch.Tensor,
+         lut: torch.Tensor, rank: torch.Tensor, msg: torch.Tensor, row_bytes: int,
+         sched: Schedule, rail_base: torch.Tensor, out: torch.Tensor, stream=None):
+    cs = sched.c()
+    _ok(lib().rails_pack(ctypes.byref(tp), ctypes.byref(sh), T, k, _ptr(x, None, "x"),
+                         _ptr(topk, torch.int32, "topk"), _ptr(lut, torch.int32, "lut"),
+                         lut.numel(), _ptr(rank, torch.int32, "rank"),
+                         _ptr(msg, torch.int64, "msg"), row_bytes, ctypes.byref(cs),
+                         _ptr(rail_base, torch.int64, "rail_base"), _ptr(out, None, "out"),
+                         out.numel() * out.element_size(), _stream(stream)))
+
+
+# ---------------------------------------------------------------- misc
+def check(stream=None):
+    """Synchronise and raise on any device-side error recorded since the last check."""
+    _ok(lib().rails_check(_stream(stream)))
+
+
+def launch_count(reset: bool = False) -> int:
+    return int(lib().rails_launch_count(1 if reset else 0))
+
+
+def version() -> int:
+    return int(lib().rails_version())

@@ -1,0 +1,399 @@
+"""CUDA path (through the C ABI) vs the CPU oracle, element by element (-m gpu).
+
+Integers (counts, bytes, ranks, schedules, loads, packed bytes) must be bit-exact;
+derived floats (T, T*, busbw, MSE) within 1e-6 relative (BASELINE.json), and the
+max observed error is printed.  Inputs are seeded; sizes span several tiles plus
+ragged tails and include the degenerate cases of the method.
+"""
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+import gen
+import oracle
+from helpers import (R2, SEED, compare_schedule, oracle_eval_from_scheds, random_msg, rel_err,
+                     routing_inputs)
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2510_19262_b200 import rails
+    from paper_2510_19262_b200.pipeline import MatrixPipeline, RoutingPipeline
+
+DEV = "cuda:0"
+FLOAT_TOL = 1e-6
+MAX_ERR = {"v": 0.0}
+
+
+@pytest.fixture(autouse=True)
+def _need_cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    yield
+    rails.check()
+
+
+def _cmp_float(a, b, what):
+    e = rel_err(float(a), float(b))
+    MAX_ERR["v"] = max(MAX_ERR["v"], e)
+    assert e <= FLOAT_TOL, f"{what}: gpu {a!r} oracle {b!r} rel {e:g}"
+
+
+# ------------------------------------------------------------------ a1 histogram
+@pytest.mark.parametrize("M,N,T,k,E,U,d0,nd", [
+    (4, 4, 4096, 2, 8, 1, 0, 4),      # C1 shape
+    (3, 5, 777, 3, 7, 2, 1, 2),       # ragged, N not a power of 2, shard
+    (2, 1, 100, 1, 3, 1, 0, 2),       # N = 1, k = 1
+    (9, 8, 333, 2, 8, 2, 3, 4),       # G = 72, multi-unit
+    (64, 8, 513, 2, 8, 1, 60, 4),     # C3-sized bins (G = 512), ragged tokens
+    (300, 8, 64, 2, 8, 1, 0, 2),      # G = 2400 -> 4-warp histogram variant
+])
+def test_histogram_parity(M, N, T, k, E, U, d0, nd):
+    topk_all, lut = routing_inputs(M, N, T, k, E, 11, 0, U)
+    topk = topk_all[:, d0:d0 + nd].contiguous()
+    tp = rails.topo(M, N, 65536)
+    sh = rails.shard(U, d0, nd)
+    RB = 8192
+    counts, msg, rank = rails.histogram(tp, sh, topk.to(DEV), lut.to(DEV), RB)
+    counts, msg, rank = counts.cpu().numpy(), msg.cpu().numpy(), rank.cpu().numpy()
+    for u in range(U):
+        for dl in range(nd):
+            c, m, r = oracle.histogram_node(M, N, d0 + dl, T, k, topk[u, dl].numpy(), lut.numpy(), RB)
+            assert np.array_equal(counts[u, dl], c)
+            assert np.array_equal(msg[u, dl], m)
+            assert np.array_equal(rank[u, dl], r)
+
+
+def test_histogram_range_error_flagged():
+    M, N, T, k = 2, 2, 64, 2
+    topk = torch.zeros((1, 2, N, T, k), dtype=torch.int32)
+    topk[0, 1, 1, 7, 1] = 99  # instance id out of range
+    lut = torch.tensor([0, 1, 2, 3], dtype=torch.int32)
+    rails.histogram(rails.topo(M, N, 4096), rails.shard(1, 0, 2), topk.to(DEV), lut.to(DEV), 16)
+    with pytest.raises(rails.RailsError) as ei:
+        rails.check()
+    assert ei.value.code == rails.RAILS_ERANGE
+    rails.check()  # flag cleared
+
+
+# ------------------------------------------------------------------ a2-a4 schedule
+@pytest.mark.parametrize("M,N,C,U,d0,nd,p,hi,mult", [
+    (4, 4, 65536, 2, 0, 4, 0.7, 500000, 1),
+    (16, 8, 1 << 20, 2, 0, 16, 0.9, 30 << 20, 1),     # C2-like sizes
+    (5, 3, 1000, 1, 0, 5, 0.5, 20000, 1),            # C not a power of two
+    (6, 7, 16, 1, 2, 3, 0.3, 2000, 1),               # tiny chunks, many full chunks
+    (3, 2, 1, 1, 0, 3, 0.5, 50, 1),                  # C = 1: no remainders
+    (4, 8, 1 << 30, 1, 0, 4, 0.8, 100000, 1),        # C > every message: all remainders
+    (70, 8, 32768, 1, 0, 3, 0.9, 300000, 1),         # NG = 4480 remainder sort
+    (3, 4, 96, 1, 0, 3, 0.8, 10, 32),                # many equal sizes (ties)
+    (2, 1, 4096, 3, 0, 2, 1.0, 100000, 1),           # N = 1
+    (300, 8, 4096, 1, 0, 2, 0.9, 50000, 1),          # NG = 19200 > smem: global-scratch sort
+])
+def test_schedule_parity(M, N, C, U, d0, nd, p, hi, mult):
+    rng = np.random.default_rng(M * 1000 + N * 10 + U)
+    msg = random_msg(rng, U, M, N, p=p, hi=hi, mult=mult, nodes=range(d0, d0 + nd))
+    tp = rails.topo(M, N, C)
+    sh = rails.shard(U, d0, nd)
+    s = rails.lpt_schedule(tp, sh, torch.from_numpy(msg).to(DEV))
+    for u in range(U):
+        for dl in range(nd):
+            compare_schedule(s, u, dl, oracle.schedule_node(msg[u, dl], C), f"u{u} d{dl}")
+
+
+def test_schedule_general_path_large_chunks():
+    # C >= 2^26 uses the 64-bit argmin chain
+    rng = np.random.default_rng(5)
+    M, N, C = 3, 4, 1 << 27
+    msg = random_msg(rng, 1, M, N, p=0.9, hi=1 << 29)
+    s = rails.lpt_schedule(rails.topo(M, N, C), rails.shard(1, 0, M), torch.from_numpy(msg).to(DEV))
+    for d in range(M):
+        compare_schedule(s, 0, d, oracle.schedule_node(msg[0, d], C), f"d{d}")
+
+
+def test_schedule_all_zero_and_empty_nodes():
+    M, N, C = 4, 4, 4096
+    msg = np.zeros((2, M, N, M * N), np.int64)
+    msg[1, 2, 3, 5] = 12345
+    s = rails.lpt_schedule(rails.topo(M, N, C), rails.shard(2, 0, M), torch.from_numpy(msg).to(DEV))
+    for u in range(2):
+        for d in range(M):
+            compare_schedule(s, u, d, oracle.schedule_node(msg[u, d], C))
+
+
+def test_schedule_intra_node_bytes_flagged():
+    M, N = 2, 2
+    msg = np.zeros((1, M, N, M * N), np.int64)
+    msg[0, 0, 0, 1] = 100  # node 0 -> its own GPU 1: not inter-domain (R#2)
+    rails.lpt_schedule(rails.topo(M, N, 64), rails.shard(1, 0, M), torch.from_numpy(msg).to(DEV))
+    with pytest.raises(rails.RailsError):
+        rails.check()
+
+
+@pytest.mark.parametrize("skew", ["receiver", "sender", "uniform"])
+def test_schedule_eval_c2_reduced(skew):
+    cfg = dict(gen.CONFIGS["c2"], skew=skew)
+    U = 3
+    msg = gen.d1_units(cfg, gen.config_seed(2), 0, U)
+    M, N, C = cfg["M"], cfg["N"], cfg["C"]
+    pipe = MatrixPipeline(M, N, C, U, 0, M, DEV)
+    pipe.step(torch.from_numpy(msg).to(DEV))
+    torch.cuda.synchronize()
+    for u in range(U):
+        scheds = [oracle.schedule_node(msg[u, d], C) for d in range(M)]
+        for d in range(M):
+            compare_schedule(pipe.sched, u, d, scheds[d], f"u{u} d{d}")
+        ev = oracle_eval_from_scheds(M, N, msg[u], scheds)
+        _compare_eval(pipe, u, 0, M, M, N, ev)
+
+
+# ------------------------------------------------------------------ generic LPT
+def test_lpt_assign_parity():
+    rng = np.random.default_rng(9)
+    sets = [[5, 4, 3, 3, 2], [3, 3, 2, 2, 2], [7, 7, 6, 6, 5, 5, 4, 4, 4], [], [0, 0, 5],
+            list(rng.integers(1, 10 ** 6, size=1000)), list(rng.integers(1, 4, size=333)),
+            list(rng.integers(1, 1 << 40, size=77))]
+    for N in (1, 2, 3, 8, 32):
+        w = np.concatenate([np.asarray(s, np.int64) for s in sets])
+        off = np.concatenate([[0], np.cumsum([len(s) for s in sets])]).astype(np.int64)
+        rail, o, load = rails.lpt_assign(N, torch.from_numpy(off).to(DEV), torch.from_numpy(w).to(DEV))
+        rail, o, load = rail.cpu().numpy(), o.cpu().numpy(), load.cpu().numpy()
+        for i, s in enumerate(sets):
+            _, r_o, o_o, l_o = oracle.lpt(np.asarray(s, np.int64), N)
+            a, b = off[i], off[i + 1]
+            assert np.array_equal(rail[a:b], r_o), (N, i)
+            assert np.array_equal(o[a:b], o_o), (N, i)
+            assert np.array_equal(load[i], l_o), (N, i)
+
+
+# ------------------------------------------------------------------ a5 eval
+def _compare_eval(pipe, u, d0, nd, M, N, ev):
+    e = pipe.ev
+    S = e.S[u].cpu().numpy()
+    assert np.array_equal(S, ev["S"][d0:d0 + nd])
+    assert np.array_equal(e.S_e[u].cpu().numpy(), ev["S_e"][d0:d0 + nd])
+    assert np.array_equal(e.R(M, N)[u].cpu().numpy(), ev["R"])
+    assert np.array_equal(e.R_e(M, N)[u].cpu().numpy(), ev["R_e"])
+    # send_load from the LPT chain equals S recomputed from the schedule
+    assert np.array_equal(pipe.sched.send_load[u].cpu().numpy(), S)
+    f = {k: v[u].item() for k, v in pipe.final.items()}
+    for key in ("maxload", "maxload_e", "total", "rowmax", "colmax"):
+        assert f[key] == ev[key], key
+    for key in ("T", "T_e", "T_star", "busbw", "busbw_e"):
+        _cmp_float(f[key], ev[key], key)
+    for dl in range(nd):
+        _cmp_float(e.mse[u, dl].item(), ev["mse"][d0 + dl], "mse")
+        _cmp_float(e.nmse[u, dl].item(), ev["nmse"][d0 + dl], "nmse")
+
+
+@pytest.mark.parametrize("M,N,C,U", [(4, 4, 65536, 2), (7, 3, 1000, 1), (5, 8, 4096, 2),
+                                     (2, 1, 64, 1), (33, 8, 32768, 1)])
+def test_eval_parity(M, N, C, U):
+    rng = np.random.default_rng(M + N + C)
+    msg = random_msg(rng, U, M, N, p=0.5, hi=300000)
+    pipe = MatrixPipeline(M, N, C, U, 0, M, DEV)
+    pipe.step(torch.from_numpy(msg).to(DEV))
+    for u in range(U):
+        scheds = [oracle.schedule_node(msg[u, d], C) for d in range(M)]
+        _compare_eval(pipe, u, 0, M, M, N, oracle_eval_from_scheds(M, N, msg[u], scheds))
+
+
+def test_eval_no_traffic():
+    M, N = 3, 2
+    msg = np.zeros((1, M, N, M * N), np.int64)
+    pipe = MatrixPipeline(M, N, 4096, 1, 0, M, DEV)
+    pipe.step(torch.from_numpy(msg).to(DEV))
+    assert pipe.final["total"].item() == 0 and pipe.final["busbw"].item() == 0.0
+    assert pipe.final["T"].item() == 0.0 and pipe.ev.nmse.abs().sum().item() == 0
+
+
+def test_sharded_eval_equals_unsharded():
+    # a6: partial red_sum (SUM) / red_max (MAX) over node shards == one-shot result
+    rng = np.random.default_rng(21)
+    M, N, C, U = 9, 4, 8192, 2
+    msg = random_msg(rng, U, M, N, p=0.6, hi=100000)
+    full = MatrixPipeline(M, N, C, U, 0, M, DEV)
+    full.step(torch.from_numpy(msg).to(DEV))
+    cuts = [0, 2, 7, 9]
+    parts = []
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        p = MatrixPipeline(M, N, C, U, a, b - a, DEV)
+        p.step(torch.from_numpy(msg[:, a:b].copy()).to(DEV))
+        parts.append(p)
+        assert torch.equal(p.sched.send_load, full.sched.send_load[:, a:b])
+        assert torch.equal(p.sched.rem_off, full.sched.rem_off[:, a:b])
+    rs = sum(p.ev.red_sum for p in parts)
+    rm = torch.stack([p.ev.red_max for p in parts]).amax(0)
+    assert torch.equal(rs, full.ev.red_sum) and torch.equal(rm, full.ev.red_max)
+    fin = rails.eval_finalize(full.tp, U, rs.contiguous(), rm.contiguous())
+    for k in fin:
+        assert torch.equal(fin[k], full.final[k]), k
+
+
+# ------------------------------------------------------------------ a7 pack
+def _oracle_pack_check(pipe, topk, lut, x, u, dl, scheds_oracle=None):
+    M, N, T, k, RB, C = pipe.M, pipe.N, pipe.T, pipe.k, pipe.RB, pipe.C
+    d = pipe.d0 + dl
+    c, m, r = oracle.histogram_node(M, N, d, T, k, topk[u, dl].numpy(), lut.numpy(), RB)
+    s = oracle.schedule_node(m, C) if scheds_oracle is None else scheds_oracle
+    base_all = pipe.rail_base[u, dl].cpu().numpy()
+    start = int(base_all[0])
+    L = s["send_load"]
+    base = np.concatenate([[0], np.cumsum(L)[:-1]]).astype(np.int64)
+    assert np.array_equal(base_all - start, base)
+    want = oracle.pack_node(M, N, d, T, k, RB, C, x[u, dl].numpy().view(np.uint8), topk[u, dl].numpy(),
+                            lut.numpy(), m, s, base, int(L.sum()))
+    got = pipe.out[start:start + int(L.sum())].cpu().numpy()
+    assert got.shape == want.shape
+    if not np.array_equal(got, want):
+        bad = np.nonzero(got != want)[0]
+        raise AssertionError(f"pack mismatch u{u} d{d}: {len(bad)} bytes differ, first at {bad[0]}")
+
+
+@pytest.mark.parametrize("M,N,T,k,E,RB,C,U,d0,nd", [
+    (4, 4, 512, 2, 8, 1024, 4096, 1, 0, 4),     # C >= RB, 2-piece path
+    (3, 2, 300, 2, 4, 4096, 1024, 1, 0, 3),     # C < RB: multi-piece path
+    (3, 5, 211, 3, 6, 48, 80, 2, 1, 2),         # C not a power of two, ragged T, 3 slots
+    (2, 1, 100, 1, 3, 16, 16, 1, 0, 2),         # N = 1, smallest rows/chunks
+    (5, 8, 128, 2, 8, 12288, 32768, 1, 0, 5),   # C4 row size (12 KiB) straddling 32 KiB
+    (3, 2, 40, 2, 4, 20480, 8192, 1, 0, 3),     # rows > 16 KiB window, multi-piece
+])
+def test_pack_parity(M, N, T, k, E, RB, C, U, d0, nd):
+    topk_all, lut = routing_inputs(M, N, T, k, E, 7, 0, U)
+    topk = topk_all[:, d0:d0 + nd].contiguous()
+    x = torch.stack([gen.payload(M, N, T, RB, 3, u, d0, nd) for u in range(U)])
+    pipe = RoutingPipeline(M, N, T, k, RB, C, U, d0, nd, lut.numel(), DEV)
+    pipe.step(topk.to(DEV), lut.to(DEV), x.to(DEV))
+    torch.cuda.synchronize()
+    assert int(pipe.total.item()) == int(pipe.sched.send_load.sum().item())
+    for u in range(U):
+        for dl in range(nd):
+            _oracle_pack_check(pipe, topk, lut, x, u, dl)
+
+
+def test_pack_enospc_flagged():
+    M, N, T, k, E, RB, C = 2, 2, 64, 2, 4, 256, 4096
+    topk, lut = routing_inputs(M, N, T, k, E, 1, 0, 1)
+    x = gen.payload(M, N, T, RB, 3, 0, 0, M)[None]
+    pipe = RoutingPipeline(M, N, T, k, RB, C, 1, 0, M, lut.numel(), DEV, out_cap=1024)
+    pipe.step(topk.to(DEV), lut.to(DEV), x.to(DEV))
+    with pytest.raises(rails.RailsError) as ei:
+        rails.check()
+    assert ei.value.code == rails.RAILS_ENOSPC
+
+
+# ------------------------------------------------------------------ full configs
+def _routing_full(cfg_name, U=None, sample_nodes=None, pack_nodes=(0,), seed_off=0, eval_full=True):
+    cfg = gen.CONFIGS[cfg_name]
+    M, N, T, k, E, C = cfg["M"], cfg["N"], cfg["T"], cfg["k"], cfg["E"], cfg["C"]
+    U = cfg["U"] if U is None else U
+    RB = cfg["H"] * 2
+    seed = gen.config_seed(int(cfg_name[1])) + seed_off
+    topk = torch.stack([gen.routing(M, N, T, k, E, seed, u, device=DEV) for u in range(U)])
+    lut = gen.inst_lut(M, N, E).to(DEV)
+    x = torch.empty((U, M, N, T, RB // 8), dtype=torch.int64, device=DEV)
+    for u in range(U):
+        gen.payload(M, N, T, RB, seed, u, 0, M, device=DEV, out=x[u])
+    pipe = RoutingPipeline(M, N, T, k, RB, C, U, 0, M, lut.numel(), DEV)
+    pipe.step(topk, lut, x)
+    torch.cuda.synchronize()
+    topk_c, lut_c = topk.cpu(), lut.cpu()
+    for u in range(U):
+        nodes = range(M) if sample_nodes is None else sample_nodes
+        if eval_full:
+            res = oracle.run_unit_routing(M, N, T, k, RB, C, R2, SEED, topk_c[u].numpy(), lut_c.numpy())
+            assert np.array_equal(pipe.counts[u].cpu().numpy(), res["counts"])
+            assert np.array_equal(pipe.msg[u].cpu().numpy(), res["msg"])
+            assert np.array_equal(pipe.rank[u].cpu().numpy(), res["rank"])
+            for d in nodes:
+                compare_schedule(pipe.sched, u, d, res["scheds"][d], f"u{u} d{d}")
+            _compare_eval(pipe, u, 0, M, M, N, res["eval"])
+            scheds = res["scheds"]
+        else:
+            scheds = {}
+            for d in nodes:
+                c, m, r = oracle.histogram_node(M, N, d, T, k, topk_c[u, d].numpy(), lut_c.numpy(), RB)
+                assert np.array_equal(pipe.msg[u, d].cpu().numpy(), m)
+                assert np.array_equal(pipe.rank[u, d].cpu().numpy(), r)
+                scheds[d] = oracle.schedule_node(m, C)
+                compare_schedule(pipe.sched, u, d, scheds[d], f"u{u} d{d}")
+        for d in pack_nodes:
+            xs = x[u:u + 1, d:d + 1].cpu()
+            _oracle_pack_check_node(pipe, topk_c, lut_c, xs, u, d, scheds[d])
+    return pipe
+
+
+def _oracle_pack_check_node(pipe, topk, lut, x_node, u, d, sched):
+    M, N, T, k, RB, C = pipe.M, pipe.N, pipe.T, pipe.k, pipe.RB, pipe.C
+    _, m, _ = oracle.histogram_node(M, N, d, T, k, topk[u, d].numpy(), lut.numpy(), RB)
+    L = sched["send_load"]
+    base_all = pipe.rail_base[u, d].cpu().numpy()
+    start = int(base_all[0])
+    base = np.concatenate([[0], np.cumsum(L)[:-1]]).astype(np.int64)
+    assert np.array_equal(base_all - start, base)
+    want = oracle.pack_node(M, N, d, T, k, RB, C, x_node[0, 0].numpy().view(np.uint8),
+                            topk[u, d].numpy(), lut.numpy(), m, sched, base, int(L.sum()))
+    got = pipe.out[start:start + int(L.sum())].cpu().numpy()
+    assert hashlib.sha256(got.tobytes()).digest() == hashlib.sha256(want.tobytes()).digest(), \
+        f"pack mismatch u{u} d{d}"
+
+
+def test_config_c1_full():
+    _routing_full("c1", pack_nodes=(0, 1, 2, 3))
+
+
+@pytest.mark.slow
+def test_config_c3_full_eval_sampled_pack():
+    # BASELINE config 3 at full size in the launch configuration bench.py times;
+    # oracle: every node's histogram/schedule/eval, pack on sampled nodes.
+    _routing_full("c3", pack_nodes=(0, 37, 63))
+
+
+@pytest.mark.slow
+def test_config_c4_sampled_units():
+    # config 4 (U=32 layers x 128 nodes): GPU runs 4 layers at once; oracle on
+    # sampled nodes (histogram, rank, schedule) and one sampled pack.
+    _routing_full("c4", U=4, sample_nodes=(0, 77, 127), pack_nodes=(77,), eval_full=False)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("C", [4 << 10, 64 << 10, 1 << 20, 4 << 20])
+def test_config_c5_sweep_sampled(C):
+    cfg = gen.CONFIGS["c5"]
+    M, N = cfg["M"], cfg["N"]
+    msg = gen.d1_units(cfg, gen.config_seed(5), 0, 1)
+    pipe = MatrixPipeline(M, N, C, 1, 0, M, DEV)
+    pipe.step(torch.from_numpy(msg).to(DEV))
+    torch.cuda.synchronize()
+    for d in (0, 100, 255):
+        compare_schedule(pipe.sched, 0, d, oracle.schedule_node(msg[0, d], C), f"d{d}")
+    if C >= (1 << 20):
+        scheds = [oracle.schedule_node(msg[0, d], C) for d in range(M)]
+        _compare_eval(pipe, 0, 0, M, M, N, oracle_eval_from_scheds(M, N, msg[0], scheds))
+    else:
+        # property at any size: sum S = sum R = total; T >= T*; send_load == S
+        f = pipe.final
+        assert f["T"].item() >= f["T_star"].item()
+        assert int(pipe.ev.S.sum()) == int(msg.sum()) == f["total"].item()
+        assert torch.equal(pipe.ev.S, pipe.sched.send_load)
+
+
+def test_determinism_repeat():
+    M, N, T, k, E, RB, C = 6, 4, 700, 2, 8, 2048, 8192
+    topk, lut = routing_inputs(M, N, T, k, E, 5, 0, 2)
+    x = torch.stack([gen.payload(M, N, T, RB, 5, u, 0, M) for u in range(2)])
+    outs = []
+    for _ in range(2):
+        pipe = RoutingPipeline(M, N, T, k, RB, C, 2, 0, M, lut.numel(), DEV)
+        pipe.out.zero_()
+        pipe.step(topk.to(DEV), lut.to(DEV), x.to(DEV))
+        torch.cuda.synchronize()
+        outs.append((pipe.rank.clone(), pipe.sched.rem_off.clone(), pipe.ev.red_sum.clone(),
+                     pipe.out[:int(pipe.total.item())].clone()))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+
+
+def test_report_max_float_error():
+    print(f"max relative float error observed vs oracle: {MAX_ERR['v']:.3g}")
