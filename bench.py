@@ -1,0 +1,405 @@
+#!/usr/bin/env python
+"""Benchmark of the RailS hot path on B200 (one JSON line on rank 0).
+
+Workload (default, --workload c3): BASELINE.json config 3, Mixtral 8x7B expert-
+parallel routing shape -- 64 nodes x 8 rails, T = 4096 tokens per GPU, top-2 of 8
+experts, H = 4096 bf16 rows (RB = 8 KiB), 32 KiB chunks.  It is the configuration
+that exercises every row of SURVEY section 8(a) (routing -> histogram -> chunk ->
+sort -> LPT -> eval -> reduction -> pack) and fits one GPU; configs[1] (C2) is a
+byte matrix with no routing or payload, so it cannot run a1/a7 (available as
+--workload c2, schedule+eval only).
+
+A step = one pass of the whole path over one batch: every rank holds M/P source
+nodes of each of U = P units (weak scaling: 64 (unit, node) schedules + packs per
+GPU per step); a6 all-reduces the partial receive loads (NCCL SUM) and maxima (MAX).
+value = (unit, node) pairs completed by all ranks / max-over-ranks device time.
+
+Timing: W untimed warm-up steps, then K steps bracketed by barrier +
+cuda.synchronize, CUDA events on the launching stream; the payload (16 GiB) and rail
+buffers (31.5 GiB) per rank exceed L2 (126 MB), so every step streams from HBM.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import gen  # noqa: E402
+
+METRIC = ("LPT-scheduled nodes/sec and pack GB/s (vs HBM peak) at 1/2/4/8 B200; "
+          "makespan/OPT")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c3", choices=["c3", "c2", "c1", "c4"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        time.sleep(0.2)
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- oracle (CPU) arm
+def oracle_sample(cfg_name: str, budget_s: float = 12.0, max_nodes: int = 16):
+    """Time the CPU oracle, as it stands, on a bounded sample of the same workload:
+    the full path (histogram, chunk, sort, LPT, eval, pack) for sampled nodes of unit 0."""
+    import oracle
+
+    cfg = gen.CONFIGS[cfg_name]
+    M, N, C = cfg["M"], cfg["N"], cfg["C"]
+    seed = gen.config_seed(int(cfg_name[1]))
+    done, t_used = 0, 0.0
+    if cfg["kind"] == "routing":
+        T, k, E, RB = cfg["T"], cfg["k"], cfg["E"], cfg["H"] * 2
+        lut = gen.inst_lut(M, N, E).numpy()
+        while done < max_nodes and t_used < budget_s:
+            d = (done * 37) % M
+            topk = gen.routing(M, N, T, k, E, seed, 0, d, 1)[0].numpy()
+            x = gen.payload(M, N, T, RB, seed, 0, d, 1)[0].numpy().view(np.uint8)
+            t0 = time.perf_counter()
+            c, m, r = oracle.histogram_node(M, N, d, T, k, topk, lut, RB)
+            s = oracle.schedule_node(m, C)
+            ch = s["chunks"]
+            oracle.eval_unit(M, N, 5.0e10, gen.ECMP_SEED, np.pad(m[None], ((d, M - d - 1), (0, 0), (0, 0))),
+                             np.full(len(ch["size"]), d, np.int32), ch["h"], ch["size"], s["rail"])
+            L = s["send_load"]
+            base = np.concatenate([[0], np.cumsum(L)[:-1]]).astype(np.int64)
+            oracle.pack_node(M, N, d, T, k, RB, C, x, topk, lut, m, s, base, int(L.sum()))
+            t_used += time.perf_counter() - t0
+            done += 1
+        sample = f"{done} sampled nodes of unit 0 (full path incl. pack), single-threaded C oracle"
+    else:
+        msg = gen.d1_units(cfg, seed, 0, 1)[0]
+        while done < max_nodes * 4 and t_used < budget_s:
+            d = done % M
+            t0 = time.perf_counter()
+            s = oracle.schedule_node(msg[d], C)
+            ch = s["chunks"]
+            oracle.eval_unit(M, N, 5.0e10, gen.ECMP_SEED, msg,
+                             np.full(len(ch["size"]), d, np.int32), ch["h"], ch["size"], s["rail"])
+            t_used += time.perf_counter() - t0
+            done += 1
+        sample = f"{done} sampled nodes of unit 0 (schedule + eval), single-threaded C oracle"
+    return {"value": done / t_used, "unit": "nodes/s", "cores": 1, "kind": "oracle",
+            "sample": sample, "seconds": round(t_used, 3)}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    vals = []
+    for _ in range(args.warmup):
+        oracle_sample(args.workload, budget_s=2.0, max_nodes=1)
+    t0 = time.perf_counter()
+    info = None
+    for _ in range(args.steps):
+        info = oracle_sample(args.workload, budget_s=8.0, max_nodes=4)
+        vals.append(info["value"])
+    wall = time.perf_counter() - t0
+    v = statistics.median(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "nodes/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * wall / max(1, args.steps), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": args.workload}, "gpu_launches": 0,
+            "cpu_baseline": dict(info, value=v),
+            "e2e": {"value": v, "unit": "nodes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    from paper_2510_19262_b200 import rails
+    from paper_2510_19262_b200.pipeline import MatrixPipeline, RoutingPipeline
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    cfg = gen.CONFIGS[args.workload]
+    M, N = cfg["M"], cfg["N"]
+    P = world
+    assert M % P == 0, "M must divide over ranks"
+    nd = M // P
+    d0 = rank * nd
+    U = P  # weak scaling: per GPU, M/P nodes of each of P units = M node schedules
+    seed = gen.config_seed(int(args.workload[1]))
+    C = cfg["C"]
+
+    def reduce(red_sum, red_max):
+        if dist is not None:
+            dist.all_reduce(red_sum, op=dist.ReduceOp.SUM)
+            dist.all_reduce(red_max, op=dist.ReduceOp.MAX)
+
+    stream = torch.cuda.current_stream()
+    if cfg["kind"] == "routing":
+        T, k, E, RB = cfg["T"], cfg["k"], cfg["E"], cfg["H"] * 2
+        topk = torch.empty((U, nd, N, T, k), dtype=torch.int32, device=dev)
+        for u in range(U):
+            topk[u] = gen.routing(M, N, T, k, E, seed, u, d0, nd, device=dev)
+        lut = gen.inst_lut(M, N, E).to(dev)
+        x = torch.empty((U, nd, N, T, RB // 8), dtype=torch.int64, device=dev)
+        for u in range(U):
+            gen.payload(M, N, T, RB, seed, u, d0, nd, device=dev, out=x[u])
+        pipe = RoutingPipeline(M, N, T, k, RB, C, U, d0, nd, lut.numel(), dev)
+
+        def step(ev_p0, ev_p1):
+            pipe.schedule_part(topk, lut)
+            pipe.finalize_part(reduce if dist is not None else None)
+            rails.rail_offsets(pipe.tp, pipe.sh, pipe.sched.send_load, pipe.rail_base, pipe.total)
+            ev_p0.record(stream)
+            rails.pack(pipe.tp, pipe.sh, T, k, x, topk, lut, pipe.rank, pipe.msg, RB, pipe.sched,
+                       pipe.rail_base, pipe.out)
+            ev_p1.record(stream)
+    else:
+        msg = torch.from_numpy(gen.d1_units(cfg, seed, 0, U)[:, d0:d0 + nd].copy()).to(dev)
+        pipe = MatrixPipeline(M, N, C, U, d0, nd, dev)
+
+        def step(ev_p0, ev_p1):
+            ev_p0.record(stream)
+            pipe.step(msg, reduce if dist is not None else None)
+            ev_p1.record(stream)
+
+    def evpair():
+        return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    for _ in range(max(args.warmup, 1)):
+        step(*evpair())
+    rails.check()
+
+    # timed region
+    # per-step events around the dominant kernel (k_pack), on its launch stream
+    kev = [evpair() for _ in range(args.steps)]
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    rails.launch_count(reset=True)
+    with ClockSampler(local) as clk:
+        t_all0 = torch.cuda.Event(enable_timing=True)
+        t_all1 = torch.cuda.Event(enable_timing=True)
+        t_all0.record(stream)
+        for i in range(args.steps):
+            step(*kev[i])
+        t_all1.record(stream)
+        torch.cuda.synchronize()
+    launches = rails.launch_count(reset=True)
+    if dist is not None:
+        dist.barrier()
+    total_ms = t_all0.elapsed_time(t_all1)
+    kern_avg_ms = sum(a.elapsed_time(b) for a, b in kev) / len(kev)
+    pack_avg_ms = kern_avg_ms
+    rails.check()
+
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    nodes = U * M  # all ranks together: U units x M nodes
+    value = nodes * args.steps / (total_ms / 1000.0)
+    peak, peak_kind = measured_peaks()
+
+    out = {"metric": METRIC, "value": value, "unit": "nodes/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+           "data": "synthetic"}
+    fin = {kk: vv.cpu() for kk, vv in pipe.final.items()}
+    quality = {"T_lpt_over_Tstar": float((fin["T"] / fin["T_star"]).max()),
+               "T_ecmp_over_Tstar": float((fin["T_e"] / fin["T_star"]).max()),
+               "busbw_lpt_over_ecmp": float((fin["busbw"] / fin["busbw_e"]).min())}
+    if cfg["kind"] == "routing":
+        tokens = U * nd * N * T
+        pack_bytes = tokens * RB + int(pipe.total.item())  # read each row once + write copies
+        t2 = torch.tensor([pack_bytes], dtype=torch.float64, device=dev)
+        pk_t = torch.tensor([pack_avg_ms], dtype=torch.float64, device=dev)
+        if dist is not None:
+            dist.all_reduce(t2)
+            dist.all_reduce(pk_t, op=dist.ReduceOp.MAX)
+        pack_gbs = float(t2.item()) / (float(pk_t.item()) / 1000.0) / 1e9
+        per_gpu_pack = pack_bytes / (pack_avg_ms / 1000.0) / 1e9
+        out["pack_gbs"] = pack_gbs
+        out["config"] = {"workload": "c3: Mixtral 8x7B EP routing shape, 64 nodes x 8 rails, "
+                         "T=4096 tokens/GPU, top-2 of 8 experts, H=4096 bf16 rows (8 KiB), "
+                         "32 KiB chunks" if args.workload == "c3" else args.workload,
+                         "units": U, "nodes_per_rank": nd * U, "M": M, "N": N, "T": T, "k": k,
+                         "row_bytes": RB, "chunk_bytes": C, "parallelism": f"nodes{P}",
+                         "l2": "inputs larger than L2: 16 GiB payload + 31.5 GiB rail buffers "
+                               "streamed per step per GPU"}
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "pack_traffic.json")
+        if os.path.exists(tp):
+            try:
+                traffic = json.load(open(tp)).get(args.workload)
+            except Exception:
+                traffic = None
+        out["roofline"] = {"kernel": "k_pack", "bound": "hbm", "achieved": per_gpu_pack,
+                           "peak": peak, "unit": "GB/s", "frac": per_gpu_pack / peak,
+                           "peak_kind": peak_kind, "traffic": traffic,
+                           "algorithmic_bytes_per_launch": pack_bytes,
+                           "avg_launch_ms": pack_avg_ms,
+                           "share_of_step": pack_avg_ms / (total_ms / args.steps)}
+    else:
+        out["config"] = {"workload": args.workload, "units": U, "nodes_per_rank": nd * U,
+                         "M": M, "N": N, "chunk_bytes": C, "parallelism": f"nodes{P}"}
+    out["quality"] = quality
+    out["clocks"] = clk.summary()
+    out["gpu_launches"] = int(launches)
+
+    # ---- e2e: host buffers, H2D of the step's inputs + D2H of its results, timed
+    if not args.no_e2e:
+        out["e2e"] = e2e(args, cfg, pipe, rails, stream, dist, world, locals())
+    # ---- cpu baseline (rank 0, N = 1 only)
+    if world == 1 and not args.no_cpu:
+        out["cpu_baseline"] = oracle_sample(args.workload)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def e2e(args, cfg, pipe, rails, stream, dist, world, env):
+    """Same metric through the public API with pinned HOST inputs/outputs."""
+    import psutil
+    dev = env["dev"]
+    steps = max(1, args.e2e_steps)
+    if cfg["kind"] == "routing":
+        topk, x, lut = env["topk"], env["x"], env["lut"]
+        need = topk.numel() * 4 + x.numel() * 8
+        local_ranks = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+        if psutil.virtual_memory().available < 2.5 * need * local_ranks:
+            return {"value": None, "unit": "nodes/s", "note": "insufficient host RAM for pinned inputs"}
+        h_topk = torch.empty(topk.shape, dtype=topk.dtype, pin_memory=True)
+        h_x = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+        h_topk.copy_(topk)
+        h_x.copy_(x)
+        h_res = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in pipe.final.items()}
+
+        def one():
+            topk.copy_(h_topk, non_blocking=True)
+            x.copy_(h_x, non_blocking=True)
+            pipe.step(topk, lut, x, env["reduce"] if dist is not None else None)
+            for kk, vv in pipe.final.items():
+                h_res[kk].copy_(vv, non_blocking=True)
+        h2d = h_topk.numel() * 4 + h_x.numel() * 8
+    else:
+        msg = env["msg"]
+        h_msg = torch.empty(msg.shape, dtype=msg.dtype, pin_memory=True)
+        h_msg.copy_(msg)
+        h_res = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in pipe.final.items()}
+
+        def one():
+            msg.copy_(h_msg, non_blocking=True)
+            pipe.step(msg, env["reduce"] if dist is not None else None)
+            for kk, vv in pipe.final.items():
+                h_res[kk].copy_(vv, non_blocking=True)
+        h2d = h_msg.numel() * 8
+    d2h = sum(v.numel() * v.element_size() for v in pipe.final.values())
+    one()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        one()
+    e1.record(stream)
+    e1.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    nodes = env["U"] * env["M"]
+    return {"value": nodes * steps / (float(ms.item()) / 1000.0), "unit": "nodes/s",
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": steps}
+
+
+if __name__ == "__main__":
+    main()

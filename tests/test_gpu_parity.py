@@ -284,18 +284,20 @@ def test_pack_enospc_flagged():
 
 
 # ------------------------------------------------------------------ full configs
-def _routing_full(cfg_name, U=None, sample_nodes=None, pack_nodes=(0,), seed_off=0, eval_full=True):
+def _routing_full(cfg_name, U=None, sample_nodes=None, pack_nodes=(0,), seed_off=0,
+                  eval_full=True, d0=0, nd=None):
     cfg = gen.CONFIGS[cfg_name]
     M, N, T, k, E, C = cfg["M"], cfg["N"], cfg["T"], cfg["k"], cfg["E"], cfg["C"]
     U = cfg["U"] if U is None else U
+    nd = M - d0 if nd is None else nd
     RB = cfg["H"] * 2
     seed = gen.config_seed(int(cfg_name[1])) + seed_off
-    topk = torch.stack([gen.routing(M, N, T, k, E, seed, u, device=DEV) for u in range(U)])
+    topk = torch.stack([gen.routing(M, N, T, k, E, seed, u, d0, nd, device=DEV) for u in range(U)])
     lut = gen.inst_lut(M, N, E).to(DEV)
-    x = torch.empty((U, M, N, T, RB // 8), dtype=torch.int64, device=DEV)
+    x = torch.empty((U, nd, N, T, RB // 8), dtype=torch.int64, device=DEV)
     for u in range(U):
-        gen.payload(M, N, T, RB, seed, u, 0, M, device=DEV, out=x[u])
-    pipe = RoutingPipeline(M, N, T, k, RB, C, U, 0, M, lut.numel(), DEV)
+        gen.payload(M, N, T, RB, seed, u, d0, nd, device=DEV, out=x[u])
+    pipe = RoutingPipeline(M, N, T, k, RB, C, U, d0, nd, lut.numel(), DEV)
     pipe.step(topk, lut, x)
     torch.cuda.synchronize()
     topk_c, lut_c = topk.cpu(), lut.cpu()
@@ -313,27 +315,29 @@ def _routing_full(cfg_name, U=None, sample_nodes=None, pack_nodes=(0,), seed_off
         else:
             scheds = {}
             for d in nodes:
-                c, m, r = oracle.histogram_node(M, N, d, T, k, topk_c[u, d].numpy(), lut_c.numpy(), RB)
-                assert np.array_equal(pipe.msg[u, d].cpu().numpy(), m)
-                assert np.array_equal(pipe.rank[u, d].cpu().numpy(), r)
+                dl = d - d0
+                c, m, r = oracle.histogram_node(M, N, d, T, k, topk_c[u, dl].numpy(), lut_c.numpy(), RB)
+                assert np.array_equal(pipe.msg[u, dl].cpu().numpy(), m)
+                assert np.array_equal(pipe.rank[u, dl].cpu().numpy(), r)
                 scheds[d] = oracle.schedule_node(m, C)
-                compare_schedule(pipe.sched, u, d, scheds[d], f"u{u} d{d}")
+                compare_schedule(pipe.sched, u, dl, scheds[d], f"u{u} d{d}")
         for d in pack_nodes:
-            xs = x[u:u + 1, d:d + 1].cpu()
+            xs = x[u:u + 1, d - d0:d - d0 + 1].cpu()
             _oracle_pack_check_node(pipe, topk_c, lut_c, xs, u, d, scheds[d])
     return pipe
 
 
 def _oracle_pack_check_node(pipe, topk, lut, x_node, u, d, sched):
     M, N, T, k, RB, C = pipe.M, pipe.N, pipe.T, pipe.k, pipe.RB, pipe.C
-    _, m, _ = oracle.histogram_node(M, N, d, T, k, topk[u, d].numpy(), lut.numpy(), RB)
+    dl = d - pipe.d0
+    _, m, _ = oracle.histogram_node(M, N, d, T, k, topk[u, dl].numpy(), lut.numpy(), RB)
     L = sched["send_load"]
-    base_all = pipe.rail_base[u, d].cpu().numpy()
+    base_all = pipe.rail_base[u, dl].cpu().numpy()
     start = int(base_all[0])
     base = np.concatenate([[0], np.cumsum(L)[:-1]]).astype(np.int64)
     assert np.array_equal(base_all - start, base)
     want = oracle.pack_node(M, N, d, T, k, RB, C, x_node[0, 0].numpy().view(np.uint8),
-                            topk[u, d].numpy(), lut.numpy(), m, sched, base, int(L.sum()))
+                            topk[u, dl].numpy(), lut.numpy(), m, sched, base, int(L.sum()))
     got = pipe.out[start:start + int(L.sum())].cpu().numpy()
     assert hashlib.sha256(got.tobytes()).digest() == hashlib.sha256(want.tobytes()).digest(), \
         f"pack mismatch u{u} d{d}"
@@ -352,9 +356,11 @@ def test_config_c3_full_eval_sampled_pack():
 
 @pytest.mark.slow
 def test_config_c4_sampled_units():
-    # config 4 (U=32 layers x 128 nodes): GPU runs 4 layers at once; oracle on
-    # sampled nodes (histogram, rank, schedule) and one sampled pack.
-    _routing_full("c4", U=4, sample_nodes=(0, 77, 127), pack_nodes=(77,), eval_full=False)
+    # config 4 (U=32 layers x 128 nodes, sharded over 8 GPUs): one GPU's shard of
+    # the sharded launch -- 4 layers x 16 nodes (the per-rank block at P = 8);
+    # oracle on sampled nodes (histogram, rank, schedule) and a sampled pack.
+    _routing_full("c4", U=4, d0=64, nd=16, sample_nodes=(64, 70, 79), pack_nodes=(77,),
+                  eval_full=False)
 
 
 @pytest.mark.slow
