@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--nd", type=int, default=None,
+                    help="nodes per rank override (profiling runs only; not a bench line)")
     return ap.parse_args()
 
 
@@ -210,6 +212,8 @@ def main():
     assert M % P == 0, "M must divide over ranks"
     nd = M // P
     d0 = rank * nd
+    if args.nd is not None:
+        nd = min(nd, args.nd)
     U = P  # weak scaling: per GPU, M/P nodes of each of P units = M node schedules
     seed = gen.config_seed(int(args.workload[1]))
     C = cfg["C"]
@@ -282,7 +286,7 @@ def main():
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
-    nodes = U * M  # all ranks together: U units x M nodes
+    nodes = U * nd * P  # all ranks together: U units x (nd per rank) nodes
     value = nodes * args.steps / (total_ms / 1000.0)
     peak, peak_kind = measured_peaks()
 
@@ -396,7 +400,7 @@ def e2e(args, cfg, pipe, rails, stream, dist, world, env):
     ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     if dist is not None:
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    nodes = env["U"] * env["M"]
+    nodes = env["U"] * env["nd"] * env["P"]
     return {"value": nodes * steps / (float(ms.item()) / 1000.0), "unit": "nodes/s",
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "steps": steps}
 

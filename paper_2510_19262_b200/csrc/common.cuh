@@ -27,6 +27,21 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
+// Lanes of the warp holding the same key (a "multi-split" match): one ballot per
+// key bit, so the cost is nbits ballots whatever the number of distinct keys
+// (__match_any_sync serialises over distinct values).  All 32 lanes must call it;
+// invalid lanes get 0 and are excluded from every valid lane's mask.
+__device__ __forceinline__ unsigned warp_match_bits(unsigned key, int nbits, bool valid) {
+  unsigned peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll 4
+  for (int b = 0; b < nbits; ++b) {
+    const bool bit = (key >> b) & 1u;
+    const unsigned bal = __ballot_sync(0xffffffffu, bit);
+    peers &= bit ? bal : ~bal;
+  }
+  return valid ? peers : 0u;
+}
+
 // Warp-inclusive scan helpers (int64 and int32).
 template <typename T>
 __device__ __forceinline__ T warp_incl_scan(T v) {

@@ -17,6 +17,8 @@
 // sum_j (N*S_j - sum S)^2 over N^3, converted once (R#25).
 // k_eval_finalize: per unit, max over the reduced R, T = maxload/R2,
 // T* = max(rowmax, colmax)/(N*R2) (Thm 2 + Thm 3), busbw = total/T (R#10).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace rails {
@@ -143,6 +145,171 @@ __global__ void __launch_bounds__(EVAL_WARPS * 32)
   }
 }
 
+
+// ---------------------------------------------------------------- tiled eval (v2)
+// Same outputs as k_eval_node.  The node's messages are processed in tiles of FT
+// destination nodes.  Stage 1 (thread per message): B, remainder, its rail and the
+// ECMP rail go to shared memory, plus, per (g, f), the node-global full-chunk
+// index where the block of messages (g, f*N .. f*N+N-1) starts, as (q, r) = divmod
+// by N.  Messages of fixed g and f are contiguous in (g,h) order, so their full
+// chunks form ONE index range [a, b); rail j receives cnt(b) - cnt(a) of them with
+// cnt(x) = floor(x/N) + (j < x mod N).  Stage 2 (thread per (f, j)): R_d[f][j] =
+// C * sum_g (cnt(b) - cnt(a)) + sum of remainders on j, R_e likewise from the ECMP
+// rails; then R[f][j] += R_d[f][j] (one global atomic), S_j, S_e_j and colsum[f]
+// accumulate in shared memory.
+constexpr int EV2_THREADS = 256;
+
+__device__ __forceinline__ void divmod_n(long long a, int N, long long& q, int& r) {
+  if (a >= 0 && a < (1LL << 32)) {
+    const unsigned ua = (unsigned)a;
+    const unsigned uq = ua / (unsigned)N;
+    q = uq;
+    r = (int)(ua - uq * (unsigned)N);
+  } else {
+    q = a / N;
+    r = (int)(a - q * N);
+  }
+}
+
+__global__ void __launch_bounds__(EV2_THREADS)
+    k_eval_node2(int M, int N, int nd, int d0, long long C, int cshift, uint64_t seed, int FT,
+                 const int64_t* __restrict__ msg, const int64_t* __restrict__ full_base,
+                 const int8_t* __restrict__ rem_rail, const int64_t* __restrict__ n_full,
+                 int64_t* __restrict__ S, int64_t* __restrict__ S_e, double* __restrict__ mse,
+                 double* __restrict__ nmse, int64_t* __restrict__ red_sum,
+                 int64_t* __restrict__ red_max, long long rsl) {
+  extern __shared__ __align__(16) uint8_t ev_smem[];
+  __shared__ unsigned long long sS[32], sSe[32];
+  const long long seg = blockIdx.x;
+  const long long u = seg / nd;
+  const int d = d0 + (int)(seg % nd);
+  const long long G = (long long)M * N, NG = (long long)N * G;
+  const ChunkDiv cd{C, cshift};
+  const int64_t* __restrict__ mg = msg + seg * NG;
+  const int64_t* __restrict__ fbp = full_base + seg * NG;
+  const int8_t* __restrict__ rrp = rem_rail + seg * NG;
+  const long long nfull_node = n_full[seg];
+  unsigned long long* rs = (unsigned long long*)(red_sum + u * rsl);
+  unsigned long long* R = rs;
+  unsigned long long* Re = rs + M * (long long)N;
+  unsigned long long* col = Re + M * (long long)N;
+  unsigned long long* tot = col + M;
+
+  const int TM = N * FT * N;          // messages per tile
+  long long* sB = (long long*)ev_smem;                 // [TM]
+  uint32_t* sRem = (uint32_t*)(sB + TM);               // [TM]
+  int8_t* sRr = (int8_t*)(sRem + TM);                  // [TM]
+  int8_t* sE = sRr + TM;                               // [TM]
+  long long* sQ = (long long*)(((uintptr_t)(sE + TM) + 15) & ~(uintptr_t)15);  // [N][FT+1]
+  int* sR = (int*)(sQ + N * (FT + 1));                 // [N][FT+1]
+  __shared__ unsigned long long sCol[64];
+
+  if (threadIdx.x < 32) {
+    sS[threadIdx.x] = 0;
+    sSe[threadIdx.x] = 0;
+  }
+  for (int f0 = 0; f0 < M; f0 += FT) {
+    const int ft = min(FT, M - f0);
+    const int tm = N * ft * N;
+    __syncthreads();
+    if (threadIdx.x < 64) sCol[threadIdx.x] = 0;
+    // stage 1: per-message fields, t -> (g, fl, m) with h contiguous for fixed g
+    for (int t = threadIdx.x; t < tm; t += EV2_THREADS) {
+      const int g = t / (ft * N);
+      const int rest = t - g * (ft * N);
+      const long long h = (long long)f0 * N + rest;
+      const long long idx = (long long)g * G + h;
+      long long B = mg[idx];
+      uint32_t rem = 0;
+      int rr = -1, e = -1;
+      if (B > 0 && (int)(h / N) != d) {
+        const long long nf = cd.div(B);
+        rem = (uint32_t)(B - nf * C);
+        if (rem) rr = rrp[idx];
+        e = ecmp_rail(seed, (long long)d * N + g, h, N);
+      } else {
+        B = 0;
+      }
+      sB[t] = B;
+      sRem[t] = rem;
+      sRr[t] = (int8_t)rr;
+      sE[t] = (int8_t)e;
+    }
+    // block boundaries: full index at message (g, (f0+fl)*N), fl = 0..ft
+    for (int t = threadIdx.x; t < N * (ft + 1); t += EV2_THREADS) {
+      const int g = t / (ft + 1), fl = t - g * (ft + 1);
+      const long long p = (long long)g * G + (long long)(f0 + fl) * N;
+      const long long a = (p < NG) ? fbp[p] : nfull_node;
+      long long q;
+      int r;
+      divmod_n(a, N, q, r);
+      sQ[g * (FT + 1) + fl] = q;
+      sR[g * (FT + 1) + fl] = r;
+    }
+    __syncthreads();
+    // stage 2: thread per (fl, j)
+    for (int t = threadIdx.x; t < ft * N; t += EV2_THREADS) {
+      const int fl = t / N, j = t - (t / N) * N;
+      const int f = f0 + fl;
+      long long full = 0, Rv = 0, Rev = 0;
+      if (f != d) {
+        for (int g = 0; g < N; ++g) {
+          const long long qa = sQ[g * (FT + 1) + fl], qb = sQ[g * (FT + 1) + fl + 1];
+          const int ra = sR[g * (FT + 1) + fl], rb = sR[g * (FT + 1) + fl + 1];
+          full += (qb - qa) + (j < rb ? 1 : 0) - (j < ra ? 1 : 0);
+          const int mb = g * (ft * N) + fl * N;
+          for (int m = 0; m < N; ++m) {
+            if (sRr[mb + m] == j) Rv += sRem[mb + m];
+            if (sE[mb + m] == j) Rev += sB[mb + m];
+          }
+        }
+        Rv += full * C;
+      }
+      if (Rv) {
+        atomicAdd(R + (long long)f * N + j, (unsigned long long)Rv);
+        atomicAdd(&sS[j], (unsigned long long)Rv);
+        atomicAdd(&sCol[fl], (unsigned long long)Rv);
+      }
+      if (Rev) {
+        atomicAdd(Re + (long long)f * N + j, (unsigned long long)Rev);
+        atomicAdd(&sSe[j], (unsigned long long)Rev);
+      }
+    }
+    __syncthreads();
+    for (int fl = threadIdx.x; fl < ft; fl += EV2_THREADS)
+      if (sCol[fl]) atomicAdd(col + f0 + fl, sCol[fl]);
+  }
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  long long s = lane < N ? (long long)sS[lane] : 0, se = lane < N ? (long long)sSe[lane] : 0;
+  if (lane < N) {
+    S[seg * N + lane] = s;
+    S_e[seg * N + lane] = se;
+  }
+  const long long total = warp_sum(s), total_e = warp_sum(se);
+  const long long mx = warp_max(s), mxe = warp_max(se);
+  unsigned __int128 sq = 0;
+  for (int j = 0; j < N; ++j) {
+    const long long sj = __shfl_sync(FULL, s, j);
+    const __int128 dv = (__int128)N * sj - (__int128)total;
+    sq += (unsigned __int128)(dv * dv);
+  }
+  if (lane == 0) {
+    const double dN = (double)N;
+    const double m = __ddiv_rn(u128_to_double(sq), __dmul_rn(__dmul_rn(dN, dN), dN));
+    mse[seg] = m;
+    nmse[seg] =
+        total == 0 ? 0.0
+                   : __ddiv_rn(m, __dmul_rn(__ll2double_rn(total), __ll2double_rn(total)));
+    if (total) atomicAdd(tot, (unsigned long long)total);
+    if (total_e) atomicAdd(tot + 1, (unsigned long long)total_e);
+    atomicMax((long long*)red_max + u * RAILS_RED_MAX_LEN + 0, mx);
+    atomicMax((long long*)red_max + u * RAILS_RED_MAX_LEN + 1, mxe);
+    atomicMax((long long*)red_max + u * RAILS_RED_MAX_LEN + 2, total);
+  }
+}
+
 __global__ void __launch_bounds__(256)
     k_eval_finalize(int M, int N, double R2, long long rsl, const int64_t* __restrict__ red_sum,
                     const int64_t* __restrict__ red_max, rails_final_t out) {
@@ -226,9 +393,22 @@ cudaError_t launch_eval(const LaunchCtx& c, int U, int nd, int d0, int M, int N,
   if (err != cudaSuccess) return err;
   err = cudaMemsetAsync(e.red_max, 0, (size_t)U * RAILS_RED_MAX_LEN * sizeof(int64_t), c.stream);
   if (err != cudaSuccess) return err;
-  k_eval_node<<<(unsigned)((long long)U * nd), EVAL_WARPS * 32, 0, c.stream>>>(
-      M, N, nd, d0, C, pow2_shift(C), seed, msg, s.full_base, s.rem_rail, e.S, e.S_e, e.mse,
-      e.nmse, e.red_sum, e.red_max, rsl);
+  const char* ev = getenv("RAILS_EVAL_IMPL");
+  if (ev && ev[0] == '1') {
+    k_eval_node<<<(unsigned)((long long)U * nd), EVAL_WARPS * 32, 0, c.stream>>>(
+        M, N, nd, d0, C, pow2_shift(C), seed, msg, s.full_base, s.rem_rail, e.S, e.S_e, e.mse,
+        e.nmse, e.red_sum, e.red_max, rsl);
+  } else {
+    const int FT = (EV2_THREADS / N) < 64 ? (EV2_THREADS / N) : 64;
+    const size_t tm = (size_t)N * FT * N;
+    const size_t smem = tm * (8 + 4 + 1 + 1) + 16 + (size_t)N * (FT + 1) * (8 + 4);
+    err = cudaFuncSetAttribute(k_eval_node2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem);
+    if (err != cudaSuccess) return err;
+    k_eval_node2<<<(unsigned)((long long)U * nd), EV2_THREADS, smem, c.stream>>>(
+        M, N, nd, d0, C, pow2_shift(C), seed, FT, msg, s.full_base, s.rem_rail, s.n_full, e.S,
+        e.S_e, e.mse, e.nmse, e.red_sum, e.red_max, rsl);
+  }
   count_launch(1);
   return cudaGetLastError();
 }

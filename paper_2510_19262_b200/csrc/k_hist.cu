@@ -6,14 +6,14 @@
 // among the earlier slots of GPU g with the same h (R#18), which the pack needs.
 //
 // Design (B200): one CTA per (unit, node, source GPU).  The T*k routing entries are
-// split into W contiguous warp segments.  Pass 1: each warp walks its segment in
-// 32-entry groups; __match_any_sync groups equal destinations and the lowest peer
-// adds the group count into the warp's private shared-memory sub-histogram (no
-// atomics, no cross-warp races).  Scan: per bin, an exclusive prefix across warps
+// split into W contiguous warp segments.  Pass 1: each warp counts its segment
+// into its private shared-memory sub-histogram (shared atomics that only ever
+// collide within the warp; counts are order-free).  Scan: per bin, an exclusive prefix across warps
 // turns the sub-histograms into the warp's starting rank; the column total is the
-// count.  Pass 2 re-walks the segment (L1/L2-resident) and emits
-// rank = warp base + running count + peers below in the group: deterministic and
-// identical to the sequential definition.  HBM traffic per CTA: read 4*T*k B of
+// count.  Pass 2 re-walks the segment (L1/L2-resident) in 32-entry groups; a
+// ballot-per-bit multi-split (warp_match_bits) finds the lanes with the same
+// destination, and rank = warp base + running count + peers below in the group:
+// deterministic and identical to the sequential definition.  HBM traffic per CTA: read 4*T*k B of
 // routing, write 4*T*k B of ranks + 12*G B of counts/bytes.
 #include "common.cuh"
 
@@ -41,6 +41,8 @@ __global__ void __launch_bounds__(W * 32)
   const long long beg = (long long)wid * seg;
   const long long end = min(ne, beg + seg);
   int32_t* my = cnt + wid * G;
+  int hbits = 0;
+  while ((1 << hbits) < G) ++hbits;
 
   // ---- pass 1: per-warp sub-histogram
   for (long long base = beg; base < end; base += 32 * UNR) {
@@ -62,8 +64,7 @@ __global__ void __launch_bounds__(W * 32)
         }
         if (h < 0) flag_error(err, ERR_RANGE);
       }
-      unsigned peers = __match_any_sync(FULL, h);
-      if (h >= 0 && lane == __ffs(peers) - 1) my[h] += __popc(peers);
+      if (h >= 0) atomicAdd(&my[h], 1);  // private to this warp: order-free count
     }
   }
   __syncthreads();
@@ -103,7 +104,7 @@ __global__ void __launch_bounds__(W * 32)
           if (h < 0 || h >= G) h = -1;
         }
       }
-      unsigned peers = __match_any_sync(FULL, h);
+      const unsigned peers = warp_match_bits((unsigned)h, hbits, h >= 0);
       int r = -1;
       if (h >= 0) r = my[h] + __popc(peers & lanemask_lt());
       __syncwarp();

@@ -20,6 +20,7 @@
 //    makes argmin-with-lowest-index-tie a single redux.sync.min.u32.  Offsets are
 //    base + rel of the chosen rail before the add (R#19).
 #include <climits>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -41,9 +42,7 @@ __device__ void radix_pass(const KeyT* kin, const IdxT* iin, KeyT* kout, IdxT* i
   int* my = hist + wid * 256;
   for (int base = beg; base < end; base += 32) {
     int i = base + lane;
-    unsigned dg = (i < end) ? (unsigned)((kin[i] >> shift) & 255) : 0xffffffffu;
-    unsigned peers = __match_any_sync(FULL, dg);
-    if (i < end && lane == __ffs(peers) - 1) my[dg] += __popc(peers);
+    if (i < end) atomicAdd(&my[(unsigned)((kin[i] >> shift) & 255)], 1);  // warp-private
   }
   __syncthreads();
   // digit totals -> exclusive digit bases -> per-warp starting positions
@@ -67,8 +66,8 @@ __device__ void radix_pass(const KeyT* kin, const IdxT* iin, KeyT* kout, IdxT* i
   __syncthreads();
   for (int base = beg; base < end; base += 32) {
     int i = base + lane;
-    unsigned dg = (i < end) ? (unsigned)((kin[i] >> shift) & 255) : 0xffffffffu;
-    unsigned peers = __match_any_sync(FULL, dg);
+    const unsigned dg = (i < end) ? (unsigned)((kin[i] >> shift) & 255) : 0u;
+    const unsigned peers = warp_match_bits(dg, 8, i < end);
     int pos = 0;
     if (i < end) pos = my[dg] + __popc(peers & lanemask_lt());
     __syncwarp();
@@ -302,6 +301,105 @@ __global__ void __launch_bounds__(CHAIN_WARPS * 32)
   }
 }
 
+
+// Thread-per-chain variant (N = NT in {2, 4, 8, 16}, C < 2^26): the N rail keys
+// (rel << 5) | rail live in registers kept SORTED ascending, so the argmin of
+// Alg. 2 step 3 is simply K[0] (lowest rail on equal load because the rail index
+// is the low key bits, R#5).  Assigning w moves K[0] to K[0] + (w << 5), which is
+// merged back into K[1..NT-1] by a branch-free compare/select network.  Loads are
+// kept relative to `base` (an exact int64) and rebased when the minimum exceeds
+// 2^26, so keys stay below 2^32 (rel <= min + C <= 2^27).
+// Chains are spread cpw per warp (cpw <= 32, chosen from the SM count) so that a
+// few long chains (C3: 64, C5: 256) occupy many SMs instead of sharing one LSU.
+template <int NT>
+__global__ void __launch_bounds__(128)
+    k_lpt_thread(long long nseg, int cpw, long long C, long long NG,
+                 const int64_t* __restrict__ n_full, const int32_t* __restrict__ n_rem,
+                 const uint32_t* __restrict__ ws_w, const uint32_t* __restrict__ ws_m,
+                 int8_t* __restrict__ rem_rail, int64_t* __restrict__ rem_off,
+                 int64_t* __restrict__ send_load) {
+  const int lane = threadIdx.x & 31;
+  const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long long seg = gw * cpw + lane;
+  if (lane >= cpw || seg >= nseg) return;
+  const long long nf = n_full[seg];
+  const long long q = nf / NT;
+  const int r = (int)(nf - q * NT);
+  const int nr = n_rem[seg];
+  const uint32_t* __restrict__ sw = ws_w + seg * NG;
+  const uint32_t* __restrict__ sm = ws_m + seg * NG;
+  int8_t* __restrict__ rr = rem_rail + seg * NG;
+  int64_t* __restrict__ ro = rem_off + seg * NG;
+  // full-chunk closed form: rails 0..r-1 hold C*(q+1), the rest C*q.  Sorted by
+  // (load, rail): rails r..NT-1 (rel 0) first, then rails 0..r-1 (rel C).
+  long long base = C * q;
+  uint32_t K[NT];
+#pragma unroll
+  for (int i = 0; i < NT; ++i) {
+    const int rail = (i < NT - r) ? (r + i) : (i - (NT - r));
+    const uint32_t rel = (i < NT - r) ? 0u : (uint32_t)C;
+    K[i] = (rel << 5) | (uint32_t)rail;
+  }
+  constexpr int PF = 8;
+  int i = 0;
+  for (; i + PF <= nr; i += PF) {
+    uint32_t wv[PF], mv[PF];
+#pragma unroll
+    for (int p = 0; p < PF; ++p) {
+      wv[p] = __ldg(sw + i + p);
+      mv[p] = __ldg(sm + i + p);
+    }
+#pragma unroll
+    for (int p = 0; p < PF; ++p) {
+      const uint32_t head = K[0];
+      const uint32_t x = head + (wv[p] << 5);
+      rr[mv[p]] = (int8_t)(head & 31u);
+      ro[mv[p]] = base + (long long)(head >> 5);
+      // merge x into K[1..NT-1] -> K[0..NT-1]
+      bool cprev = true;
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        const bool c = (j < NT - 1) ? (K[j + 1] < x) : false;
+        const uint32_t a = (j < NT - 1) ? K[j + 1] : 0u;
+        const uint32_t b = (j > 0) ? K[j] : 0u;  // old K[j] (= A[j-1])
+        K[j] = c ? a : (cprev ? x : b);
+        cprev = c;
+      }
+      const uint32_t mrel = K[0] >> 5;
+      if (mrel > (1u << 26)) {
+#pragma unroll
+        for (int j = 0; j < NT; ++j) K[j] -= mrel << 5;
+        base += mrel;
+      }
+    }
+  }
+  for (; i < nr; ++i) {
+    const uint32_t w = __ldg(sw + i), m = __ldg(sm + i);
+    const uint32_t head = K[0];
+    const uint32_t x = head + (w << 5);
+    rr[m] = (int8_t)(head & 31u);
+    ro[m] = base + (long long)(head >> 5);
+    bool cprev = true;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      const bool c = (j < NT - 1) ? (K[j + 1] < x) : false;
+      const uint32_t a = (j < NT - 1) ? K[j + 1] : 0u;
+      const uint32_t b = (j > 0) ? K[j] : 0u;
+      K[j] = c ? a : (cprev ? x : b);
+      cprev = c;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NT; ++j) send_load[seg * NT + (K[j] & 31u)] = base + (long long)(K[j] >> 5);
+}
+
+// LPT chain implementation: 0 = thread-per-chain when N allows (default),
+// 1 = warp-per-chain (RAILS_CHAIN_IMPL=1, kept as the reference path).
+static int chain_impl() {
+  const char* e = getenv("RAILS_CHAIN_IMPL");
+  return (e && e[0] == '1') ? 1 : 0;
+}
+
 static int ceil_log2(long long x) {  // bits needed for values 0..x-1
   int b = 0;
   while ((1LL << b) < x) ++b;
@@ -342,10 +440,28 @@ cudaError_t launch_schedule(const LaunchCtx& c, int U, int nd, int d0, int M, in
   }
   count_launch(1);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  const unsigned grid = (unsigned)((nseg + CHAIN_WARPS - 1) / CHAIN_WARPS);
-  k_lpt_chain<<<grid, CHAIN_WARPS * 32, 0, c.stream>>>(nseg, N, C, NG, s.n_full, s.n_rem, ws_w,
-                                                       ws_m, s.rem_rail, s.rem_off,
-                                                       s.send_load, c.err);
+  if (C < (1LL << 26) && chain_impl() == 0 && (N == 2 || N == 4 || N == 8 || N == 16)) {
+    // chains per warp: fill ~8 warps per SM before packing lanes (LSU sharing)
+    long long cpw = nseg / ((long long)c.num_sms * 8);
+    cpw = cpw < 1 ? 1 : (cpw > 32 ? 32 : cpw);
+    const long long nwarp = (nseg + cpw - 1) / cpw;
+    const unsigned tgrid = (unsigned)((nwarp + 3) / 4);
+#define RAILS_THREAD_CHAIN(NT)                                                            \
+  if (N == NT)                                                                            \
+    k_lpt_thread<NT><<<tgrid, 128, 0, c.stream>>>(nseg, (int)cpw, C, NG, s.n_full, s.n_rem, \
+                                                  ws_w, ws_m, s.rem_rail, s.rem_off,      \
+                                                  s.send_load);
+    RAILS_THREAD_CHAIN(2)
+    RAILS_THREAD_CHAIN(4)
+    RAILS_THREAD_CHAIN(8)
+    RAILS_THREAD_CHAIN(16)
+#undef RAILS_THREAD_CHAIN
+  } else {
+    const unsigned grid = (unsigned)((nseg + CHAIN_WARPS - 1) / CHAIN_WARPS);
+    k_lpt_chain<<<grid, CHAIN_WARPS * 32, 0, c.stream>>>(nseg, N, C, NG, s.n_full, s.n_rem, ws_w,
+                                                         ws_m, s.rem_rail, s.rem_off,
+                                                         s.send_load, c.err);
+  }
   count_launch(1);
   return cudaGetLastError();
 }

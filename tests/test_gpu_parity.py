@@ -359,7 +359,7 @@ def test_config_c4_sampled_units():
     # config 4 (U=32 layers x 128 nodes, sharded over 8 GPUs): one GPU's shard of
     # the sharded launch -- 4 layers x 16 nodes (the per-rank block at P = 8);
     # oracle on sampled nodes (histogram, rank, schedule) and a sampled pack.
-    _routing_full("c4", U=4, d0=64, nd=16, sample_nodes=(64, 70, 79), pack_nodes=(77,),
+    _routing_full("c4", U=4, d0=64, nd=16, sample_nodes=(64, 70, 79), pack_nodes=(70,),
                   eval_full=False)
 
 

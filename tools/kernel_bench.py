@@ -1,0 +1,167 @@
+#!/usr/bin/env python
+"""Per-kernel timing on representative batched launches (CUDA events, warm-up,
+inputs larger than L2 or L2 flushed between iterations).  Writes one JSON object.
+
+  pack      C3 launch (64 nodes), impl 1 (LDG/STG registers) vs 2 (TMA bulk)
+  histogram C4 iteration (32 layers x 128 nodes, 1 GiB routing) -- HBM roofline
+  schedule  C2 (1000 iterations x 16 nodes = 16000 chains), C3, C5 sweep points
+  eval      same launches as schedule
+Not a bench line: bench.py is.  Used to fill DESIGN.md section 7 and profiles/.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import gen  # noqa: E402
+from paper_2510_19262_b200 import rails  # noqa: E402
+from paper_2510_19262_b200.pipeline import MatrixPipeline, RoutingPipeline  # noqa: E402
+
+DEV = "cuda:0"
+PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+    os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+_flush = None
+
+
+def flush_l2():
+    global _flush
+    if _flush is None:
+        _flush = torch.empty(256 << 20, dtype=torch.uint8, device=DEV)
+    _flush.random_(0, 255)
+
+
+def timeit(fn, iters=10, warm=3, flush=True):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(iters):
+        if flush:
+            flush_l2()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    ts.sort()
+    return {"median_ms": ts[len(ts) // 2], "best_ms": ts[0]}
+
+
+def bench_pack(res):
+    cfg = gen.CONFIGS["c3"]
+    M, N, T, k, E, C = cfg["M"], cfg["N"], cfg["T"], cfg["k"], cfg["E"], cfg["C"]
+    RB = cfg["H"] * 2
+    seed = gen.config_seed(3)
+    topk = gen.routing(M, N, T, k, E, seed, 0, device=DEV)[None].contiguous()
+    lut = gen.inst_lut(M, N, E).to(DEV)
+    x = gen.payload(M, N, T, RB, seed, 0, 0, M, device=DEV)[None].contiguous()
+    pipe = RoutingPipeline(M, N, T, k, RB, C, 1, 0, M, lut.numel(), DEV)
+    pipe.step(topk, lut, x)
+    torch.cuda.synchronize()
+    total = int(pipe.total.item())
+    algo = M * N * T * RB + total
+    ref = None
+    for impl in ("1", "2"):
+        os.environ["RAILS_PACK_IMPL"] = impl
+        pipe.out.zero_()
+        t = timeit(lambda: rails.pack(pipe.tp, pipe.sh, T, k, x, topk, lut, pipe.rank, pipe.msg, RB,
+                                      pipe.sched, pipe.rail_base, pipe.out), flush=False)
+        rails.check()
+        h = torch.sum(pipe.out[:total].view(torch.int64) * 0 + 1).item()  # touch
+        snap = pipe.out[:total:4099].clone()
+        if ref is None:
+            ref = snap
+        same = bool(torch.equal(ref, snap))
+        gbs = algo / (t["median_ms"] / 1e3) / 1e9
+        res[f"pack_impl{impl}"] = dict(t, gbs=gbs, frac=gbs / PEAK, bytes=algo, same_as_impl1=same)
+        del h
+    os.environ.pop("RAILS_PACK_IMPL", None)
+    # schedule-side kernels of the same C3 unit
+    res["c3_schedule"] = timeit(lambda: rails.lpt_schedule(pipe.tp, pipe.sh, pipe.msg, out=pipe.sched,
+                                                           workspace=pipe.ws))
+    res["c3_histogram"] = timeit(lambda: rails.histogram(pipe.tp, pipe.sh, topk, lut, RB,
+                                                         out=(pipe.counts, pipe.msg, pipe.rank)))
+    res["c3_eval"] = timeit(lambda: rails.eval(pipe.tp, pipe.sh, pipe.msg, pipe.sched, out=pipe.ev))
+    del pipe, x
+    torch.cuda.empty_cache()
+
+
+def bench_hist_c4(res):
+    cfg = gen.CONFIGS["c4"]
+    M, N, T, k, E = cfg["M"], cfg["N"], cfg["T"], cfg["k"], cfg["E"]
+    U = cfg["U"]
+    seed = gen.config_seed(4)
+    topk = torch.empty((U, M, N, T, k), dtype=torch.int32, device=DEV)
+    for u in range(U):
+        topk[u] = gen.routing(M, N, T, k, E, seed, u, device=DEV)
+    lut = gen.inst_lut(M, N, E).to(DEV)
+    tp, sh = rails.topo(M, N, cfg["C"]), rails.shard(U, 0, M)
+    G = M * N
+    out = (torch.empty((U, M, N, G), dtype=torch.int32, device=DEV),
+           torch.empty((U, M, N, G), dtype=torch.int64, device=DEV),
+           torch.empty((U, M, N, T, k), dtype=torch.int32, device=DEV))
+    t = timeit(lambda: rails.histogram(tp, sh, topk, lut, cfg["H"] * 2, out=out))
+    algo = U * M * N * (T * k * 4 * 2 + G * 12)
+    gbs = algo / (t["median_ms"] / 1e3) / 1e9
+    res["hist_c4_iteration"] = dict(t, gbs=gbs, frac=gbs / PEAK, bytes=algo)
+    # schedule + eval over the whole C4 iteration (4096 chains of ~7K remainders)
+    msg = out[1]
+    pipe = MatrixPipeline(M, N, cfg["C"], U, 0, M, DEV)
+    res["c4_schedule"] = timeit(lambda: rails.lpt_schedule(pipe.tp, pipe.sh, msg, out=pipe.sched,
+                                                           workspace=pipe.ws))
+    res["c4_eval"] = timeit(lambda: rails.eval(pipe.tp, pipe.sh, msg, pipe.sched, out=pipe.ev))
+    del topk, out, msg, pipe
+    torch.cuda.empty_cache()
+
+
+def bench_matrix(res, name, C=None, U=None):
+    cfg = gen.CONFIGS[name]
+    M, N = cfg["M"], cfg["N"]
+    C = cfg["C"] if C is None else C
+    U = cfg["U"] if U is None else U
+    msg = torch.from_numpy(gen.d1_units(cfg, gen.config_seed(int(name[1])), 0, U)).to(DEV)
+    pipe = MatrixPipeline(M, N, C, U, 0, M, DEV)
+    ts = timeit(lambda: rails.lpt_schedule(pipe.tp, pipe.sh, msg, out=pipe.sched, workspace=pipe.ws))
+    te = timeit(lambda: rails.eval(pipe.tp, pipe.sh, msg, pipe.sched, out=pipe.ev))
+    tf = timeit(lambda: pipe.step(msg))
+    fin = {k: v.cpu() for k, v in pipe.final.items()}
+    res[f"{name}_C{C}"] = {"schedule": ts, "eval": te, "step": tf,
+                           "nodes_per_s": U * M / (tf["median_ms"] / 1e3),
+                           "n_rem_mean": float(pipe.sched.n_rem.float().mean()),
+                           "T_over_Tstar": float((fin["T"] / fin["T_star"]).max()),
+                           "Te_over_Tstar": float((fin["T_e"] / fin["T_star"]).max())}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--only", default="pack,hist,c2,c5")
+    a = ap.parse_args()
+    res = {"device": torch.cuda.get_device_name(0), "peak_gbs": PEAK}
+    only = a.only.split(",")
+    if "pack" in only:
+        bench_pack(res)
+    if "hist" in only:
+        bench_hist_c4(res)
+    if "c2" in only:
+        bench_matrix(res, "c2")
+    if "c5" in only:
+        for C in (4 << 10, 64 << 10, 1 << 20, 4 << 20):
+            bench_matrix(res, "c5", C=C)
+    s = json.dumps(res, indent=1)
+    print(s)
+    if a.out:
+        open(a.out, "w").write(s)
+
+
+if __name__ == "__main__":
+    main()
