@@ -42,6 +42,20 @@ __device__ __forceinline__ unsigned warp_match_bits(unsigned key, int nbits, boo
   return valid ? peers : 0u;
 }
 
+// Same with the key width known at compile time (fully unrolled: one VOTE and one
+// LOP3 per bit plus the bit-mask extraction).
+template <int NB>
+__device__ __forceinline__ unsigned warp_match_nb(unsigned key, bool valid) {
+  unsigned peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const unsigned m = (unsigned)(((int)(key << (31 - b))) >> 31);  // bit b -> 0 / ~0
+    const unsigned bal = __ballot_sync(0xffffffffu, m != 0u);
+    peers &= ~(bal ^ m);
+  }
+  return valid ? peers : 0u;
+}
+
 // Warp-inclusive scan helpers (int64 and int32).
 template <typename T>
 __device__ __forceinline__ T warp_incl_scan(T v) {

@@ -19,7 +19,7 @@
 
 namespace rails {
 
-template <int W, int UNR>
+template <int W, int UNR, int HB>
 __global__ void __launch_bounds__(W * 32)
     k_hist_rank(const int32_t* __restrict__ topk, const int32_t* __restrict__ lut, int n_inst,
                 int M, int N, int d0, int nd, int T, int k, long long RB,
@@ -41,8 +41,6 @@ __global__ void __launch_bounds__(W * 32)
   const long long beg = (long long)wid * seg;
   const long long end = min(ne, beg + seg);
   int32_t* my = cnt + wid * G;
-  int hbits = 0;
-  while ((1 << hbits) < G) ++hbits;
 
   // ---- pass 1: per-warp sub-histogram
   for (long long base = beg; base < end; base += 32 * UNR) {
@@ -104,7 +102,7 @@ __global__ void __launch_bounds__(W * 32)
           if (h < 0 || h >= G) h = -1;
         }
       }
-      const unsigned peers = warp_match_bits((unsigned)h, hbits, h >= 0);
+      const unsigned peers = warp_match_nb<HB>((unsigned)h, h >= 0);
       int r = -1;
       if (h >= 0) r = my[h] + __popc(peers & lanemask_lt());
       __syncwarp();
@@ -115,12 +113,12 @@ __global__ void __launch_bounds__(W * 32)
   }
 }
 
-template <int W>
-static cudaError_t launch_w(const LaunchCtx& c, long long grid, int M, int N, int d0, int nd,
-                            int T, int k, const int32_t* topk, const int32_t* lut, int n_inst,
-                            long long RB, int32_t* counts, int64_t* msg, int32_t* rank) {
+template <int W, int HB>
+static cudaError_t launch_wh(const LaunchCtx& c, long long grid, int M, int N, int d0, int nd,
+                             int T, int k, const int32_t* topk, const int32_t* lut, int n_inst,
+                             long long RB, int32_t* counts, int64_t* msg, int32_t* rank) {
   size_t smem = (size_t)W * M * N * sizeof(int32_t);
-  auto kern = k_hist_rank<W, 8>;
+  auto kern = k_hist_rank<W, 8, HB>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
@@ -128,6 +126,27 @@ static cudaError_t launch_w(const LaunchCtx& c, long long grid, int M, int N, in
                                                     counts, msg, rank, c.err);
   count_launch(1);
   return cudaGetLastError();
+}
+
+// key width (bits of the largest bin index) as a template parameter
+template <int W>
+static cudaError_t launch_w(const LaunchCtx& c, long long grid, int M, int N, int d0, int nd,
+                            int T, int k, const int32_t* topk, const int32_t* lut, int n_inst,
+                            long long RB, int32_t* counts, int64_t* msg, int32_t* rank) {
+  int hb = 0;
+  while ((1LL << hb) < (long long)M * N) ++hb;
+  switch (hb) {
+#define RAILS_HB(B)                                                                         \
+  case B:                                                                                   \
+    return launch_wh<W, B>(c, grid, M, N, d0, nd, T, k, topk, lut, n_inst, RB, counts, msg, \
+                           rank);
+    RAILS_HB(1) RAILS_HB(2) RAILS_HB(3) RAILS_HB(4) RAILS_HB(5) RAILS_HB(6) RAILS_HB(7)
+    RAILS_HB(8) RAILS_HB(9) RAILS_HB(10) RAILS_HB(11) RAILS_HB(12) RAILS_HB(13) RAILS_HB(14)
+    RAILS_HB(15) RAILS_HB(16)
+#undef RAILS_HB
+    default:
+      return cudaErrorInvalidValue;
+  }
 }
 
 cudaError_t launch_histogram(const LaunchCtx& c, int U, int nd, int d0, int M, int N, int T,

@@ -67,7 +67,7 @@ __device__ void radix_pass(const KeyT* kin, const IdxT* iin, KeyT* kout, IdxT* i
   for (int base = beg; base < end; base += 32) {
     int i = base + lane;
     const unsigned dg = (i < end) ? (unsigned)((kin[i] >> shift) & 255) : 0u;
-    const unsigned peers = warp_match_bits(dg, 8, i < end);
+    const unsigned peers = warp_match_nb<8>(dg, i < end);
     int pos = 0;
     if (i < end) pos = my[dg] + __popc(peers & lanemask_lt());
     __syncwarp();
@@ -302,6 +302,114 @@ __global__ void __launch_bounds__(CHAIN_WARPS * 32)
 }
 
 
+
+// LPT network step shared by the chain kernels: K sorted ascending holds the N
+// rail keys (rel << 5) | rail; the chunk of size w goes to K[0]'s rail (argmin,
+// lowest rail on ties) at offset base + rel, and K[0] + (w << 5) is merged back.
+template <int NT>
+__device__ __forceinline__ void lpt_step(uint32_t (&K)[NT], uint32_t w, uint32_t m,
+                                         long long base, int8_t* __restrict__ rr,
+                                         int64_t* __restrict__ ro) {
+  const uint32_t head = K[0];
+  const uint32_t x = head + (w << 5);
+  rr[m] = (int8_t)(head & 31u);
+  ro[m] = base + (long long)(head >> 5);
+  bool cprev = true;
+#pragma unroll
+  for (int j = 0; j < NT; ++j) {
+    const bool c = (j < NT - 1) ? (K[j + 1] < x) : false;
+    const uint32_t a = (j < NT - 1) ? K[j + 1] : 0u;
+    const uint32_t b = (j > 0) ? K[j] : 0u;
+    K[j] = c ? a : (cprev ? x : b);
+    cprev = c;
+  }
+}
+
+template <int NT>
+__device__ __forceinline__ void lpt_rebase(uint32_t (&K)[NT], long long& base) {
+  const uint32_t mrel = K[0] >> 5;
+  if (mrel > (1u << 26)) {
+#pragma unroll
+    for (int j = 0; j < NT; ++j) K[j] -= mrel << 5;
+    base += mrel;
+  }
+}
+
+// Few long chains (C3: 64, C5: 256): one chain per warp.  All 32 lanes stream the
+// sorted remainder list through a double-buffered shared-memory stage with
+// coalesced loads, one batch ahead; lane 0 runs the register compare network,
+// so the serial chain never waits on global memory.
+constexpr int WS_WARPS = 4;
+constexpr int WS_BATCH = 256;
+
+template <int NT>
+__global__ void __launch_bounds__(WS_WARPS * 32)
+    k_lpt_wstage(long long nseg, long long C, long long NG, const int64_t* __restrict__ n_full,
+                 const int32_t* __restrict__ n_rem, const uint32_t* __restrict__ ws_w,
+                 const uint32_t* __restrict__ ws_m, int8_t* __restrict__ rem_rail,
+                 int64_t* __restrict__ rem_off, int64_t* __restrict__ send_load) {
+  __shared__ uint32_t sW[WS_WARPS][2][WS_BATCH], sM[WS_WARPS][2][WS_BATCH];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long seg = (long long)blockIdx.x * WS_WARPS + wid;
+  if (seg >= nseg) return;
+  const long long nf = n_full[seg];
+  const long long q = nf / NT;
+  const int r = (int)(nf - q * NT);
+  const int nr = n_rem[seg];
+  const uint32_t* __restrict__ gw = ws_w + seg * NG;
+  const uint32_t* __restrict__ gm = ws_m + seg * NG;
+  int8_t* __restrict__ rr = rem_rail + seg * NG;
+  int64_t* __restrict__ ro = rem_off + seg * NG;
+  long long base = C * q;
+  uint32_t K[NT];
+#pragma unroll
+  for (int i = 0; i < NT; ++i) {
+    const int rail = (i < NT - r) ? (r + i) : (i - (NT - r));
+    K[i] = (((i < NT - r) ? 0u : (uint32_t)C) << 5) | (uint32_t)rail;
+  }
+  constexpr int PL = WS_BATCH / 32;
+  uint32_t pw[PL], pm[PL];
+#pragma unroll
+  for (int p = 0; p < PL; ++p) {
+    const int i = p * 32 + lane;
+    pw[p] = i < nr ? gw[i] : 0u;
+    pm[p] = i < nr ? gm[i] : 0u;
+  }
+  int cur = 0;
+  for (int b0 = 0; b0 < nr; b0 += WS_BATCH) {
+#pragma unroll
+    for (int p = 0; p < PL; ++p) {
+      sW[wid][cur][p * 32 + lane] = pw[p];
+      sM[wid][cur][p * 32 + lane] = pm[p];
+    }
+    __syncwarp();
+    const int nb = b0 + WS_BATCH;  // prefetch the next batch while lane 0 works
+#pragma unroll
+    for (int p = 0; p < PL; ++p) {
+      const int i = nb + p * 32 + lane;
+      pw[p] = i < nr ? gw[i] : 0u;
+      pm[p] = i < nr ? gm[i] : 0u;
+    }
+    if (lane == 0) {
+      const int cnt = min(WS_BATCH, nr - b0);
+      const uint32_t* w_ = sW[wid][cur];
+      const uint32_t* m_ = sM[wid][cur];
+#pragma unroll 4
+      for (int i = 0; i < cnt; ++i) {
+        lpt_step<NT>(K, w_[i], m_[i], base, rr, ro);
+        lpt_rebase<NT>(K, base);
+      }
+    }
+    __syncwarp();
+    cur ^= 1;
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+      send_load[seg * NT + (K[j] & 31u)] = base + (long long)(K[j] >> 5);
+  }
+}
+
 // Thread-per-chain variant (N = NT in {2, 4, 8, 16}, C < 2^26): the N rail keys
 // (rel << 5) | rail live in registers kept SORTED ascending, so the argmin of
 // Alg. 2 step 3 is simply K[0] (lowest rail on equal load because the rail index
@@ -342,52 +450,36 @@ __global__ void __launch_bounds__(128)
   }
   constexpr int PF = 8;
   int i = 0;
-  for (; i + PF <= nr; i += PF) {
-    uint32_t wv[PF], mv[PF];
+  uint32_t wv[PF], mv[PF];
+  if (PF <= nr) {
 #pragma unroll
     for (int p = 0; p < PF; ++p) {
-      wv[p] = __ldg(sw + i + p);
-      mv[p] = __ldg(sm + i + p);
+      wv[p] = __ldg(sw + p);
+      mv[p] = __ldg(sm + p);
+    }
+  }
+  for (; i + PF <= nr; i += PF) {
+    uint32_t wn[PF], mn[PF];  // next batch in flight while this one is assigned
+    const bool more = i + 2 * PF <= nr;
+#pragma unroll
+    for (int p = 0; p < PF; ++p) {
+      wn[p] = more ? __ldg(sw + i + PF + p) : 0u;
+      mn[p] = more ? __ldg(sm + i + PF + p) : 0u;
     }
 #pragma unroll
     for (int p = 0; p < PF; ++p) {
-      const uint32_t head = K[0];
-      const uint32_t x = head + (wv[p] << 5);
-      rr[mv[p]] = (int8_t)(head & 31u);
-      ro[mv[p]] = base + (long long)(head >> 5);
-      // merge x into K[1..NT-1] -> K[0..NT-1]
-      bool cprev = true;
+      lpt_step<NT>(K, wv[p], mv[p], base, rr, ro);
+      lpt_rebase<NT>(K, base);
+    }
 #pragma unroll
-      for (int j = 0; j < NT; ++j) {
-        const bool c = (j < NT - 1) ? (K[j + 1] < x) : false;
-        const uint32_t a = (j < NT - 1) ? K[j + 1] : 0u;
-        const uint32_t b = (j > 0) ? K[j] : 0u;  // old K[j] (= A[j-1])
-        K[j] = c ? a : (cprev ? x : b);
-        cprev = c;
-      }
-      const uint32_t mrel = K[0] >> 5;
-      if (mrel > (1u << 26)) {
-#pragma unroll
-        for (int j = 0; j < NT; ++j) K[j] -= mrel << 5;
-        base += mrel;
-      }
+    for (int p = 0; p < PF; ++p) {
+      wv[p] = wn[p];
+      mv[p] = mn[p];
     }
   }
   for (; i < nr; ++i) {
-    const uint32_t w = __ldg(sw + i), m = __ldg(sm + i);
-    const uint32_t head = K[0];
-    const uint32_t x = head + (w << 5);
-    rr[m] = (int8_t)(head & 31u);
-    ro[m] = base + (long long)(head >> 5);
-    bool cprev = true;
-#pragma unroll
-    for (int j = 0; j < NT; ++j) {
-      const bool c = (j < NT - 1) ? (K[j + 1] < x) : false;
-      const uint32_t a = (j < NT - 1) ? K[j + 1] : 0u;
-      const uint32_t b = (j > 0) ? K[j] : 0u;
-      K[j] = c ? a : (cprev ? x : b);
-      cprev = c;
-    }
+    lpt_step<NT>(K, __ldg(sw + i), __ldg(sm + i), base, rr, ro);
+    lpt_rebase<NT>(K, base);
   }
 #pragma unroll
   for (int j = 0; j < NT; ++j) send_load[seg * NT + (K[j] & 31u)] = base + (long long)(K[j] >> 5);
@@ -440,7 +532,20 @@ cudaError_t launch_schedule(const LaunchCtx& c, int U, int nd, int d0, int M, in
   }
   count_launch(1);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  if (C < (1LL << 26) && chain_impl() == 0 && (N == 2 || N == 4 || N == 8 || N == 16)) {
+  if (C < (1LL << 26) && chain_impl() == 0 && (N == 2 || N == 4 || N == 8 || N == 16) &&
+      nseg <= (long long)c.num_sms * 8) {
+    const unsigned wgrid = (unsigned)((nseg + WS_WARPS - 1) / WS_WARPS);
+#define RAILS_WS_CHAIN(NT)                                                                  \
+  if (N == NT)                                                                              \
+    k_lpt_wstage<NT><<<wgrid, WS_WARPS * 32, 0, c.stream>>>(nseg, C, NG, s.n_full, s.n_rem, \
+                                                           ws_w, ws_m, s.rem_rail, s.rem_off, \
+                                                           s.send_load);
+    RAILS_WS_CHAIN(2)
+    RAILS_WS_CHAIN(4)
+    RAILS_WS_CHAIN(8)
+    RAILS_WS_CHAIN(16)
+#undef RAILS_WS_CHAIN
+  } else if (C < (1LL << 26) && chain_impl() == 0 && (N == 2 || N == 4 || N == 8 || N == 16)) {
     // chains per warp: fill ~8 warps per SM before packing lanes (LSU sharing)
     long long cpw = nseg / ((long long)c.num_sms * 8);
     cpw = cpw < 1 ? 1 : (cpw > 32 ? 32 : cpw);

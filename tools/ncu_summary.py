@@ -1,0 +1,45 @@
+#!/usr/bin/env python
+"""Summarise an .ncu-rep (raw page) per launch: time, DRAM bytes, throughput,
+occupancy, issue activity and the top stall reasons."""
+import csv
+import io
+import subprocess
+import sys
+
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+        "launch__occupancy_limit_shared_mem", "launch__occupancy_limit_registers",
+        "smsp__inst_executed.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+        "lts__t_bytes.sum"]
+
+
+def main(path):
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    h, units = rows[0], rows[1]
+    out = []
+    for r in rows[2:]:
+        name = r[h.index("Kernel Name")][:70]
+        out.append(f"== {name}")
+        for k in KEYS:
+            if k in h:
+                out.append(f"   {k} = {r[h.index(k)]} {units[h.index(k)]}")
+        st = []
+        for i, k in enumerate(h):
+            if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio"):
+                try:
+                    st.append((float(r[i]), k[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]))
+                except ValueError:
+                    pass
+        st.sort(reverse=True)
+        out.append("   stalls/issue: " + ", ".join(f"{n}={v:.2f}" for v, n in st[:6]))
+    print("\n".join(out))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
