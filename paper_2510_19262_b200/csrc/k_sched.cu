@@ -328,7 +328,7 @@ __device__ __forceinline__ void lpt_step(uint32_t (&K)[NT], uint32_t w, uint32_t
 template <int NT>
 __device__ __forceinline__ void lpt_rebase(uint32_t (&K)[NT], long long& base) {
   const uint32_t mrel = K[0] >> 5;
-  if (mrel > (1u << 26)) {
+  if (mrel > (1u << 23)) {
 #pragma unroll
     for (int j = 0; j < NT; ++j) K[j] -= mrel << 5;
     base += mrel;
@@ -394,8 +394,33 @@ __global__ void __launch_bounds__(WS_WARPS * 32)
       const int cnt = min(WS_BATCH, nr - b0);
       const uint32_t* w_ = sW[wid][cur];
       const uint32_t* m_ = sM[wid][cur];
-#pragma unroll 4
-      for (int i = 0; i < cnt; ++i) {
+      // groups of 8 items held in registers, the next group loaded before the
+      // current one is assigned (global stores would otherwise order the loads)
+      constexpr int GB = 8;
+      uint32_t cw[GB], cm[GB];
+#pragma unroll
+      for (int p = 0; p < GB; ++p) {
+        cw[p] = w_[p];
+        cm[p] = m_[p];
+      }
+      int i = 0;
+      for (; i + GB <= cnt; i += GB) {
+        uint32_t nw[GB], nm[GB];
+#pragma unroll
+        for (int p = 0; p < GB; ++p) {
+          nw[p] = w_[(i + GB + p) & (WS_BATCH - 1)];
+          nm[p] = m_[(i + GB + p) & (WS_BATCH - 1)];
+        }
+#pragma unroll
+        for (int p = 0; p < GB; ++p) lpt_step<NT>(K, cw[p], cm[p], base, rr, ro);
+        lpt_rebase<NT>(K, base);
+#pragma unroll
+        for (int p = 0; p < GB; ++p) {
+          cw[p] = nw[p];
+          cm[p] = nm[p];
+        }
+      }
+      for (; i < cnt; ++i) {
         lpt_step<NT>(K, w_[i], m_[i], base, rr, ro);
         lpt_rebase<NT>(K, base);
       }
@@ -410,13 +435,14 @@ __global__ void __launch_bounds__(WS_WARPS * 32)
   }
 }
 
-// Thread-per-chain variant (N = NT in {2, 4, 8, 16}, C < 2^26): the N rail keys
+// Thread-per-chain variant (N = NT in {2, 4, 8, 16}, C < 2^23): the N rail keys
 // (rel << 5) | rail live in registers kept SORTED ascending, so the argmin of
 // Alg. 2 step 3 is simply K[0] (lowest rail on equal load because the rail index
 // is the low key bits, R#5).  Assigning w moves K[0] to K[0] + (w << 5), which is
 // merged back into K[1..NT-1] by a branch-free compare/select network.  Loads are
 // kept relative to `base` (an exact int64) and rebased when the minimum exceeds
-// 2^26, so keys stay below 2^32 (rel <= min + C <= 2^27).
+// 2^23; with at most 8 steps between rebases and C < 2^23, rel < 2^23 + 9*C < 2^27,
+// so keys stay below 2^32.
 // Chains are spread cpw per warp (cpw <= 32, chosen from the SM count) so that a
 // few long chains (C3: 64, C5: 256) occupy many SMs instead of sharing one LSU.
 template <int NT>
@@ -532,7 +558,7 @@ cudaError_t launch_schedule(const LaunchCtx& c, int U, int nd, int d0, int M, in
   }
   count_launch(1);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  if (C < (1LL << 26) && chain_impl() == 0 && (N == 2 || N == 4 || N == 8 || N == 16) &&
+  if (C < (1LL << 23) && chain_impl() == 0 && (N == 2 || N == 4 || N == 8 || N == 16) &&
       nseg <= (long long)c.num_sms * 8) {
     const unsigned wgrid = (unsigned)((nseg + WS_WARPS - 1) / WS_WARPS);
 #define RAILS_WS_CHAIN(NT)                                                                  \
@@ -545,7 +571,7 @@ cudaError_t launch_schedule(const LaunchCtx& c, int U, int nd, int d0, int M, in
     RAILS_WS_CHAIN(8)
     RAILS_WS_CHAIN(16)
 #undef RAILS_WS_CHAIN
-  } else if (C < (1LL << 26) && chain_impl() == 0 && (N == 2 || N == 4 || N == 8 || N == 16)) {
+  } else if (C < (1LL << 23) && chain_impl() == 0 && (N == 2 || N == 4 || N == 8 || N == 16)) {
     // chains per warp: fill ~8 warps per SM before packing lanes (LSU sharing)
     long long cpw = nseg / ((long long)c.num_sms * 8);
     cpw = cpw < 1 ? 1 : (cpw > 32 ? 32 : cpw);

@@ -85,6 +85,18 @@ def bench_pack(res):
         res[f"pack_impl{impl}"] = dict(t, gbs=gbs, frac=gbs / PEAK, bytes=algo, same_as_impl1=same)
         del h
     os.environ.pop("RAILS_PACK_IMPL", None)
+    # context only (NOT the roofline denominator): the same 1-read : 2-write byte
+    # mix as the pack, done by a plain torch broadcast copy of every 8 KiB row into
+    # two adjacent slots (second read of a row hits L2)
+    xs = x.view(-1, RB // 8)
+    nrow = min(xs.shape[0], pipe.out.numel() // (2 * RB))
+    dst = pipe.out[:nrow * 2 * RB].view(torch.int64).view(nrow, 2, RB // 8)
+    t = timeit(lambda: dst.copy_(xs[:nrow, None, :].expand(nrow, 2, RB // 8)), flush=False)
+    b = nrow * RB * 3
+    res["torch_dup_copy_1r2w"] = dict(t, gbs=b / (t["median_ms"] / 1e3) / 1e9, bytes=b)
+    t = timeit(lambda: dst[:, 0, :].copy_(xs[:nrow]), flush=False)
+    b = nrow * RB * 2
+    res["torch_copy_1r1w_strided"] = dict(t, gbs=b / (t["median_ms"] / 1e3) / 1e9, bytes=b)
     # schedule-side kernels of the same C3 unit
     res["c3_schedule"] = timeit(lambda: rails.lpt_schedule(pipe.tp, pipe.sh, pipe.msg, out=pipe.sched,
                                                            workspace=pipe.ws))
