@@ -116,6 +116,84 @@ __global__ void __launch_bounds__(W * 32)
 }
 
 
+
+// ---------------------------------------------------------------- warp-per-segment variant
+// Default for batched launches (T*k <= 65535, >= 16 segments per SM).  One warp
+// owns one (unit, node, source GPU): it walks
+// the T*k routing entries once, in order, 32 at a time, with a private running
+// count per bin in shared memory, so rank = running count + equal destinations
+// among lower lanes and no cross-warp scan or second pass is needed.  Equal
+// destinations inside a group are found with a tag write/read-back (each lane
+// writes its lane id at tag[h]; a lane that reads another id, or whose id was
+// overwritten by a loser's mark, has a duplicate) and match.any runs only over
+// those lanes.  Ranks are stored as they are produced (coalesced 128 B per group);
+// counts and bytes are written once at the end.
+constexpr int HW_WARPS = 4;
+
+template <int UNR>
+__global__ void __launch_bounds__(HW_WARPS * 32)
+    k_hist_w1(const int32_t* __restrict__ topk, const int32_t* __restrict__ lut, int n_inst,
+              int M, int N, int d0, int nd, int T, int k, long long RB, long long nsegs,
+              int32_t* __restrict__ counts, int64_t* __restrict__ msg,
+              int32_t* __restrict__ rank, int* err) {
+  extern __shared__ __align__(16) uint16_t sm3[];
+  const int G = M * N;
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long sg = (long long)blockIdx.x * HW_WARPS + wid;  // ((u*nd)+dl)*N + g
+  uint16_t* cnt = sm3 + wid * G;  // running counts (< 2^16: T*k <= 65535)
+  uint8_t* tg = (uint8_t*)(sm3 + HW_WARPS * G) + wid * G;
+  if (sg >= nsegs) return;
+  const long long ul = sg / N;
+  const int d = d0 + (int)(ul % nd);
+  const int ne = T * k;
+  const int32_t* __restrict__ src = topk + sg * (long long)ne;
+  int32_t* __restrict__ dst = rank ? rank + sg * (long long)ne : nullptr;
+  for (int i = lane; i < G; i += 32) cnt[i] = 0;
+  __syncwarp();
+  for (int base = 0; base < ne; base += 32 * UNR) {
+    int hv[UNR];
+#pragma unroll
+    for (int j = 0; j < UNR; ++j) {
+      const int e = base + j * 32 + lane;
+      hv[j] = (e < ne) ? __ldg(src + e) : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < UNR; ++j) {
+      const int e = base + j * 32 + lane;
+      int h = -1;
+      const int inst = hv[j];
+      if (inst >= 0 && inst < n_inst) {
+        h = __ldg(lut + inst);
+        if (h < 0 || h >= G) h = -1;
+      }
+      if (e < ne && h < 0) flag_error(err, ERR_RANGE);
+      const bool valid = h >= 0;
+      if (valid) tg[h] = (uint8_t)lane;
+      __syncwarp();
+      bool dup = valid && tg[h] != lane;  // lost the write: an equal key exists
+      __syncwarp();
+      if (dup) tg[h] = (uint8_t)(32 | lane);  // mark it for the winner
+      __syncwarp();
+      if (valid && !dup) dup = tg[h] != lane;
+      const unsigned dmask = __ballot_sync(FULL, dup);
+      unsigned peers = valid ? (1u << lane) : 0u;
+      if (dup) peers = __match_any_sync(dmask, h);
+      int r = -1;
+      if (valid) r = cnt[h] + __popc(peers & lanemask_lt());
+      __syncwarp();
+      if (valid && lane == __ffs(peers) - 1) cnt[h] = (uint16_t)(cnt[h] + __popc(peers));
+      __syncwarp();
+      if (dst && e < ne) dst[e] = r;
+    }
+  }
+  __syncwarp();
+  for (int h = lane; h < G; h += 32) {
+    const int c = cnt[h];
+    counts[sg * G + h] = c;
+    msg[sg * G + h] = (h / N == d) ? 0LL : (long long)c * RB;
+  }
+}
+
 // ---------------------------------------------------------------- single-read variant
 // Same contract.  One read of the routing: for each 32-entry group of its segment
 // a warp finds equal destinations with a shared-memory tag write/read-back (every
@@ -261,7 +339,22 @@ cudaError_t launch_histogram(const LaunchCtx& c, int U, int nd, int d0, int M, i
   const long long G = (long long)M * N;
   const char* hv = getenv("RAILS_HIST_IMPL");
   const long long ne = (long long)T * k;
-  if (!(hv && hv[0] == '1') && ne <= HIST2_MAX_NE && G <= 65535) {
+  // warp-per-segment when there are enough segments to fill the GPU (>= 16 warps
+  // per SM); otherwise the multi-warp-per-segment kernels keep latency down
+  const bool many = grid >= (long long)c.num_sms * 16;
+  if (!(hv && (hv[0] == '1' || hv[0] == '2')) && G <= 12288 && ne <= 65535 &&
+      (many || (hv && hv[0] == '3'))) {
+    const size_t smem = (size_t)HW_WARPS * G * 3;
+    auto kern = k_hist_w1<8>;
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<(unsigned)((grid + HW_WARPS - 1) / HW_WARPS), HW_WARPS * 32, smem, c.stream>>>(
+        topk, lut, n_inst, M, N, d0, nd, T, k, row_bytes, grid, counts, msg, rank, c.err);
+    count_launch(1);
+    return cudaGetLastError();
+  }
+  if (hv && hv[0] == '2' && ne <= HIST2_MAX_NE && G <= 65535) {
     // single-read variant: W warps, smem = W*G*4 (counts) + ne*4 (packed) + W*G (tags)
     int W = 8;
     while (W > 1 && (size_t)W * G * 5 + ne * 4 > 160 * 1024) W >>= 1;
