@@ -218,6 +218,48 @@ int rails_pack(const rails_topo_t* topo, const rails_shard_t* shard, int32_t T,
                const int64_t* msg_bytes, int64_t row_bytes, const rails_sched_t* sched,
                const int64_t* rail_base, void* out, int64_t out_cap, void* stream);
 
+/* ------------------------------------------------------------------ NEXT f2 */
+/* Rail-owner variant (one multi-GPU box = one RailS node): NIC j hangs off GPU j
+ * (P:184), so rail j's send buffer lives in GPU j's HBM and traffic of GPU g on
+ * rail j != g crosses the intra-domain network first.  A
+ * process holding source GPUs g0 .. g0+ng-1 of each node histograms its own rows,
+ * the node's msg_bytes rows are all-gathered (caller, NCCL), every process runs the
+ * same node-wide rails_lpt_schedule, and rails_pack_owner writes each chunk piece
+ * straight into the rail owner's buffer through peer-mapped pointers (NVLink /
+ * NVSwitch): the intra-node hop is fused into the pack.
+ *
+ * rails_histogram_gpus: as rails_histogram for source GPUs g0..g0+ng-1 only;
+ *   topk_inst/row_rank [U][nd][ng][T][k], counts/msg_bytes [U][nd][ng][G].        */
+int rails_histogram_gpus(const rails_topo_t* topo, const rails_shard_t* shard, int32_t g0,
+                         int32_t ng, int32_t T, int32_t k, const int32_t* topk_inst,
+                         const int32_t* inst_to_gpu, int32_t n_inst, int64_t row_bytes,
+                         int32_t* counts, int64_t* msg_bytes, int32_t* row_rank, void* stream);
+
+/* rail_base int64 [U][nd][N]: offset of block (u, dl) inside RAIL j's own buffer
+ * (exclusive prefix of send_load over (u, dl) for each j); rail_total int64 [N]:
+ * bytes each rail buffer needs. */
+int rails_rail_offsets_owner(const rails_topo_t* topo, const rails_shard_t* shard,
+                             const int64_t* send_load, int64_t* rail_base, int64_t* rail_total,
+                             void* stream);
+
+/* Pack the rows of source GPUs g0..g0+ng-1 (x, topk_inst, row_rank in the local
+ * [U][nd][ng][...] layout) into the rail buffers rail_ptr[j] (host array of N
+ * device pointers, peer-mapped where rail j is owned by another GPU; each 16-byte
+ * aligned, rail_cap[j] bytes, host array).  msg_bytes and sched are node-wide
+ * ([U][nd][N][G]); a piece of chunk c on rail j goes to
+ * rail_ptr[j] + rail_base[u][dl][j] + off(c).  Beyond rail_cap -> RAILS_ENOSPC. */
+int rails_pack_owner(const rails_topo_t* topo, const rails_shard_t* shard, int32_t g0,
+                     int32_t ng, int32_t T, int32_t k, const void* x, const int32_t* topk_inst,
+                     const int32_t* inst_to_gpu, int32_t n_inst, const int32_t* row_rank,
+                     const int64_t* msg_bytes, int64_t row_bytes, const rails_sched_t* sched,
+                     const int64_t* rail_base, void* const* rail_ptr, const int64_t* rail_cap,
+                     void* stream);
+
+/* Enable direct loads/stores from kernels on the current device to memory of
+ * `peer_device` (cudaDeviceEnablePeerAccess; "already enabled" is not an error).
+ * RAILS_ECUDA if the devices cannot reach each other. */
+int rails_enable_peer_access(int32_t peer_device);
+
 /* ------------------------------------------------------------------ misc */
 /* Synchronise `stream`, then return (and clear) the first device-side error
  * recorded since the last check: RAILS_OK, RAILS_ERANGE, RAILS_ENOSPC or

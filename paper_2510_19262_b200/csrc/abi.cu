@@ -143,7 +143,8 @@ int rails_histogram(const rails_topo_t* topo, const rails_shard_t* sh, int32_t T
                 (long long)topo->M * topo->N);
   LaunchCtx c;
   if ((rc = ctx(stream, &c))) return rc;
-  return cuda_rc(launch_histogram(c, sh->U, sh->nd, sh->d0, topo->M, topo->N, T, k, topk_inst,
+  return cuda_rc(launch_histogram(c, sh->U, sh->nd, sh->d0, topo->M, topo->N, topo->N, T, k,
+                                  topk_inst,
                                   inst_to_gpu, n_inst, row_bytes, counts, msg_bytes, row_rank),
                  "rails_histogram launch");
 }
@@ -261,6 +262,94 @@ int rails_pack(const rails_topo_t* topo, const rails_shard_t* sh, int32_t T, int
                              x, topk_inst, inst_to_gpu, n_inst, row_rank, msg_bytes, row_bytes,
                              *sched, rail_base, out, out_cap, pack_impl()),
                  "rails_pack launch");
+}
+
+int rails_histogram_gpus(const rails_topo_t* topo, const rails_shard_t* sh, int32_t g0,
+                         int32_t ng, int32_t T, int32_t k, const int32_t* topk_inst,
+                         const int32_t* inst_to_gpu, int32_t n_inst, int64_t row_bytes,
+                         int32_t* counts, int64_t* msg_bytes, int32_t* row_rank, void* stream) {
+  int rc = check_topo(topo);
+  if (rc || (rc = check_shard(topo, sh))) return rc;
+  if (g0 < 0 || ng < 1 || g0 + ng > topo->N)
+    return fail(RAILS_EINVAL, "GPU range [%d, %d) outside [0, %d)", g0, g0 + ng, topo->N);
+  if (T < 1 || k < 1 || k > 32) return fail(RAILS_EINVAL, "need T >= 1 and 1 <= k <= 32");
+  if ((long long)T * k > (1LL << 30)) return fail(RAILS_EINVAL, "T*k too large");
+  if (n_inst < 1 || row_bytes < 1) return fail(RAILS_EINVAL, "need n_inst >= 1, row_bytes >= 1");
+  if (!topk_inst || !inst_to_gpu || !counts || !msg_bytes)
+    return fail(RAILS_EINVAL, "NULL array argument");
+  if ((long long)topo->M * topo->N > 49152)
+    return fail(RAILS_ENOSPC, "G=%lld: histogram bins exceed shared memory",
+                (long long)topo->M * topo->N);
+  LaunchCtx c;
+  if ((rc = ctx(stream, &c))) return rc;
+  return cuda_rc(launch_histogram(c, sh->U, sh->nd, sh->d0, topo->M, topo->N, ng, T, k,
+                                  topk_inst, inst_to_gpu, n_inst, row_bytes, counts, msg_bytes,
+                                  row_rank),
+                 "rails_histogram_gpus launch");
+}
+
+int rails_rail_offsets_owner(const rails_topo_t* topo, const rails_shard_t* sh,
+                             const int64_t* send_load, int64_t* rail_base, int64_t* rail_total,
+                             void* stream) {
+  int rc = check_topo(topo);
+  if (rc || (rc = check_shard(topo, sh))) return rc;
+  if (!send_load || !rail_base || !rail_total) return fail(RAILS_EINVAL, "NULL argument");
+  LaunchCtx c;
+  if ((rc = ctx(stream, &c))) return rc;
+  return cuda_rc(launch_rail_offsets_owner(c, (long long)sh->U * sh->nd, topo->N, send_load,
+                                           rail_base, rail_total),
+                 "rails_rail_offsets_owner launch");
+}
+
+int rails_pack_owner(const rails_topo_t* topo, const rails_shard_t* sh, int32_t g0, int32_t ng,
+                     int32_t T, int32_t k, const void* x, const int32_t* topk_inst,
+                     const int32_t* inst_to_gpu, int32_t n_inst, const int32_t* row_rank,
+                     const int64_t* msg_bytes, int64_t row_bytes, const rails_sched_t* sched,
+                     const int64_t* rail_base, void* const* rail_ptr, const int64_t* rail_cap,
+                     void* stream) {
+  int rc = check_topo(topo);
+  if (rc || (rc = check_shard(topo, sh))) return rc;
+  if (g0 < 0 || ng < 1 || g0 + ng > topo->N)
+    return fail(RAILS_EINVAL, "GPU range [%d, %d) outside [0, %d)", g0, g0 + ng, topo->N);
+  if (T < 1 || k < 1 || k > 32 || n_inst < 1) return fail(RAILS_EINVAL, "bad T, k or n_inst");
+  if (row_bytes < 16 || row_bytes % 16 || row_bytes > (1LL << 30))
+    return fail(RAILS_EINVAL, "row_bytes=%lld must be a positive multiple of 16",
+                (long long)row_bytes);
+  if (topo->chunk_bytes % 16)
+    return fail(RAILS_EINVAL, "pack needs chunk_bytes %% 16 == 0 (16-byte vector copies)");
+  if (!x || !topk_inst || !inst_to_gpu || !row_rank || !msg_bytes || !sched ||
+      !sched->full_base || !sched->rem_rail || !sched->rem_off || !rail_base || !rail_ptr ||
+      !rail_cap)
+    return fail(RAILS_EINVAL, "NULL argument");
+  if (!al(x, 16)) return fail(RAILS_EINVAL, "x must be 16-byte aligned");
+  for (int j = 0; j < topo->N; ++j) {
+    if (rail_cap[j] < 0 || (rail_cap[j] > 0 && (!rail_ptr[j] || !al(rail_ptr[j], 16))))
+      return fail(RAILS_EINVAL, "rail %d: pointer NULL/misaligned or negative capacity", j);
+  }
+  LaunchCtx c;
+  if ((rc = ctx(stream, &c))) return rc;
+  return cuda_rc(launch_pack_owner(c, sh->U, sh->nd, sh->d0, topo->M, topo->N, g0, ng, T, k,
+                                   topo->chunk_bytes, x, topk_inst, inst_to_gpu, n_inst,
+                                   row_rank, msg_bytes, row_bytes, *sched, rail_base, rail_ptr,
+                                   rail_cap),
+                 "rails_pack_owner launch");
+}
+
+int rails_enable_peer_access(int32_t peer_device) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_rc(e, "cudaGetDevice");
+  if (peer_device == dev) return RAILS_OK;
+  int can = 0;
+  e = cudaDeviceCanAccessPeer(&can, dev, peer_device);
+  if (e != cudaSuccess) return cuda_rc(e, "cudaDeviceCanAccessPeer");
+  if (!can) return fail(RAILS_ECUDA, "device %d cannot access device %d", dev, peer_device);
+  e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return RAILS_OK;
+  }
+  return cuda_rc(e, "cudaDeviceEnablePeerAccess");
 }
 
 }  // extern "C"

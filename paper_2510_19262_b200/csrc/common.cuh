@@ -143,6 +143,12 @@ __device__ __forceinline__ void st_stream(uint4* p, const uint4& v) {
                : "memory");
 }
 
+__device__ __forceinline__ void st_cs(uint4* p, const uint4& v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
 }  // namespace rails
 
 // ---------------------------------------------------------------- host launchers
@@ -154,8 +160,8 @@ struct LaunchCtx {
   int num_sms;
 };
 
-cudaError_t launch_histogram(const LaunchCtx&, int U, int nd, int d0, int M, int N, int T,
-                             int k, const int32_t* topk, const int32_t* lut, int n_inst,
+cudaError_t launch_histogram(const LaunchCtx&, int U, int nd, int d0, int M, int N, int ngs,
+                             int T, int k, const int32_t* topk, const int32_t* lut, int n_inst,
                              long long row_bytes, int32_t* counts, int64_t* msg,
                              int32_t* rank);
 
@@ -182,6 +188,16 @@ cudaError_t launch_pack(const LaunchCtx&, int U, int nd, int d0, int M, int N, i
                         int n_inst, const int32_t* rank, const int64_t* msg,
                         long long row_bytes, const rails_sched_t& s, const int64_t* rail_base,
                         void* out, long long out_cap, int impl);
+
+cudaError_t launch_pack_owner(const LaunchCtx&, int U, int nd, int d0, int M, int N, int g0,
+                              int ng, int T, int k, long long C, const void* x,
+                              const int32_t* topk, const int32_t* lut, int n_inst,
+                              const int32_t* rank, const int64_t* msg, long long row_bytes,
+                              const rails_sched_t& s, const int64_t* rail_base,
+                              void* const* rail_ptr, const int64_t* rail_cap);
+cudaError_t launch_rail_offsets_owner(const LaunchCtx&, long long ublk, int N,
+                                      const int64_t* send_load, int64_t* rail_base,
+                                      int64_t* rail_total);
 
 void count_launch(int n);
 }  // namespace rails

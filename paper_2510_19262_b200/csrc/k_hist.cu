@@ -24,13 +24,13 @@ namespace rails {
 template <int W, int UNR, int HB>
 __global__ void __launch_bounds__(W * 32)
     k_hist_rank(const int32_t* __restrict__ topk, const int32_t* __restrict__ lut, int n_inst,
-                int M, int N, int d0, int nd, int T, int k, long long RB,
+                int M, int N, int ngs, int d0, int nd, int T, int k, long long RB,
                 int32_t* __restrict__ counts, int64_t* __restrict__ msg,
                 int32_t* __restrict__ rank, int* err) {
   extern __shared__ int32_t cnt[];  // [W][G]
   const int G = M * N;
-  const long long cta = blockIdx.x;  // ((u*nd) + dl)*N + g
-  const long long ul = cta / N;
+  const long long cta = blockIdx.x;  // ((u*nd) + dl)*ngs + gl
+  const long long ul = cta / ngs;
   const int d = d0 + (int)(ul % nd);
   const long long ne = (long long)T * k;
   const int32_t* __restrict__ src = topk + cta * ne;
@@ -130,63 +130,61 @@ __global__ void __launch_bounds__(W * 32)
 // counts and bytes are written once at the end.
 constexpr int HW_WARPS = 4;
 
-template <int UNR>
+template <int UNR, bool RANK>
 __global__ void __launch_bounds__(HW_WARPS * 32)
     k_hist_w1(const int32_t* __restrict__ topk, const int32_t* __restrict__ lut, int n_inst,
-              int M, int N, int d0, int nd, int T, int k, long long RB, long long nsegs,
-              int32_t* __restrict__ counts, int64_t* __restrict__ msg,
+              int M, int N, int ngs, int d0, int nd, int T, int k, long long RB,
+              long long nsegs, int32_t* __restrict__ counts, int64_t* __restrict__ msg,
               int32_t* __restrict__ rank, int* err) {
   extern __shared__ __align__(16) uint16_t sm3[];
   const int G = M * N;
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long sg = (long long)blockIdx.x * HW_WARPS + wid;  // ((u*nd)+dl)*N + g
-  uint16_t* cnt = sm3 + wid * G;  // running counts (< 2^16: T*k <= 65535)
-  uint8_t* tg = (uint8_t*)(sm3 + HW_WARPS * G) + wid * G;
+  const long long sg = (long long)blockIdx.x * HW_WARPS + wid;  // ((u*nd)+dl)*ngs + gl
+  uint16_t* const cnt = sm3 + wid * G;  // running counts (< 2^16: T*k <= 65535)
+  uint8_t* const tg = (uint8_t*)(sm3 + HW_WARPS * G) + wid * G;
   if (sg >= nsegs) return;
-  const long long ul = sg / N;
+  const long long ul = sg / ngs;
   const int d = d0 + (int)(ul % nd);
   const int ne = T * k;
-  const int32_t* __restrict__ src = topk + sg * (long long)ne;
-  int32_t* __restrict__ dst = rank ? rank + sg * (long long)ne : nullptr;
+  const int32_t* __restrict__ src = topk + sg * (long long)ne + lane;
+  int32_t* __restrict__ dst = RANK ? rank + sg * (long long)ne + lane : nullptr;
   for (int i = lane; i < G; i += 32) cnt[i] = 0;
+  const unsigned lt = lanemask_lt();
+  bool bad = false;
   __syncwarp();
   for (int base = 0; base < ne; base += 32 * UNR) {
     int hv[UNR];
 #pragma unroll
-    for (int j = 0; j < UNR; ++j) {
-      const int e = base + j * 32 + lane;
-      hv[j] = (e < ne) ? __ldg(src + e) : -1;
-    }
+    for (int j = 0; j < UNR; ++j)
+      hv[j] = (base + j * 32 + lane < ne) ? __ldg(src + base + j * 32) : -1;
 #pragma unroll
     for (int j = 0; j < UNR; ++j) {
-      const int e = base + j * 32 + lane;
+      const bool in = base + j * 32 + lane < ne;
       int h = -1;
-      const int inst = hv[j];
-      if (inst >= 0 && inst < n_inst) {
-        h = __ldg(lut + inst);
-        if (h < 0 || h >= G) h = -1;
-      }
-      if (e < ne && h < 0) flag_error(err, ERR_RANGE);
-      const bool valid = h >= 0;
+      if ((unsigned)hv[j] < (unsigned)n_inst) h = __ldg(lut + hv[j]);
+      const bool valid = (unsigned)h < (unsigned)G;
+      bad |= in && !valid;
+      // equal destinations inside the group: tag write / read-back
+      // (a winner that already sees a loser's mark is correctly a duplicate too)
       if (valid) tg[h] = (uint8_t)lane;
       __syncwarp();
-      bool dup = valid && tg[h] != lane;  // lost the write: an equal key exists
-      __syncwarp();
-      if (dup) tg[h] = (uint8_t)(32 | lane);  // mark it for the winner
+      bool dup = valid && tg[h] != lane;
+      if (dup) tg[h] = (uint8_t)(32 | lane);
       __syncwarp();
       if (valid && !dup) dup = tg[h] != lane;
       const unsigned dmask = __ballot_sync(FULL, dup);
-      unsigned peers = valid ? (1u << lane) : 0u;
-      if (dup) peers = __match_any_sync(dmask, h);
-      int r = -1;
-      if (valid) r = cnt[h] + __popc(peers & lanemask_lt());
+      unsigned peers = 1u << lane;
+      if (dmask) {
+        if (dup) peers = __match_any_sync(dmask, h);
+      }
+      const int c = valid ? cnt[h] : 0;
       __syncwarp();
-      if (valid && lane == __ffs(peers) - 1) cnt[h] = (uint16_t)(cnt[h] + __popc(peers));
-      __syncwarp();
-      if (dst && e < ne) dst[e] = r;
+      if (valid && (peers & lt) == 0) cnt[h] = (uint16_t)(c + __popc(peers));
+      if (RANK && in) dst[base + j * 32] = valid ? c + __popc(peers & lt) : -1;
+      // the next group reads cnt only after its own two tag syncs
     }
   }
-  __syncwarp();
+  if (__any_sync(FULL, bad) && lane == 0) flag_error(err, ERR_RANGE);
   for (int h = lane; h < G; h += 32) {
     const int c = cnt[h];
     counts[sg * G + h] = c;
@@ -208,7 +206,7 @@ constexpr int HIST2_MAX_NE = 16384;
 template <int W, int UNR>
 __global__ void __launch_bounds__(W * 32)
     k_hist_rank2(const int32_t* __restrict__ topk, const int32_t* __restrict__ lut, int n_inst,
-                 int M, int N, int d0, int nd, int T, int k, long long RB,
+                 int M, int N, int ngs, int d0, int nd, int T, int k, long long RB,
                  int32_t* __restrict__ counts, int64_t* __restrict__ msg,
                  int32_t* __restrict__ rank, int* err) {
   extern __shared__ __align__(16) int32_t sm2[];
@@ -216,7 +214,7 @@ __global__ void __launch_bounds__(W * 32)
   int32_t* cnt = sm2;                                   // [W][G]
   uint32_t* pk = (uint32_t*)(cnt + W * G);              // [ne]
   const long long cta = blockIdx.x;
-  const long long ul = cta / N;
+  const long long ul = cta / ngs;
   const int d = d0 + (int)(ul % nd);
   const int ne = T * k;
   uint8_t* tag = (uint8_t*)(pk + ne);                   // [W][G]
@@ -296,7 +294,8 @@ __global__ void __launch_bounds__(W * 32)
 }
 
 template <int W, int HB>
-static cudaError_t launch_wh(const LaunchCtx& c, long long grid, int M, int N, int d0, int nd,
+static cudaError_t launch_wh(const LaunchCtx& c, long long grid, int M, int N, int ngs, int d0,
+                             int nd,
                              int T, int k, const int32_t* topk, const int32_t* lut, int n_inst,
                              long long RB, int32_t* counts, int64_t* msg, int32_t* rank) {
   size_t smem = (size_t)W * M * N * sizeof(int32_t);
@@ -304,15 +303,16 @@ static cudaError_t launch_wh(const LaunchCtx& c, long long grid, int M, int N, i
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<(unsigned)grid, W * 32, smem, c.stream>>>(topk, lut, n_inst, M, N, d0, nd, T, k, RB,
-                                                    counts, msg, rank, c.err);
+  kern<<<(unsigned)grid, W * 32, smem, c.stream>>>(topk, lut, n_inst, M, N, ngs, d0, nd, T, k,
+                                                    RB, counts, msg, rank, c.err);
   count_launch(1);
   return cudaGetLastError();
 }
 
 // key width (bits of the largest bin index) as a template parameter
 template <int W>
-static cudaError_t launch_w(const LaunchCtx& c, long long grid, int M, int N, int d0, int nd,
+static cudaError_t launch_w(const LaunchCtx& c, long long grid, int M, int N, int ngs, int d0,
+                            int nd,
                             int T, int k, const int32_t* topk, const int32_t* lut, int n_inst,
                             long long RB, int32_t* counts, int64_t* msg, int32_t* rank) {
   int hb = 0;
@@ -320,7 +320,7 @@ static cudaError_t launch_w(const LaunchCtx& c, long long grid, int M, int N, in
   switch (hb) {
 #define RAILS_HB(B)                                                                         \
   case B:                                                                                   \
-    return launch_wh<W, B>(c, grid, M, N, d0, nd, T, k, topk, lut, n_inst, RB, counts, msg, \
+    return launch_wh<W, B>(c, grid, M, N, ngs, d0, nd, T, k, topk, lut, n_inst, RB, counts, msg, \
                            rank);
     RAILS_HB(1) RAILS_HB(2) RAILS_HB(3) RAILS_HB(4) RAILS_HB(5) RAILS_HB(6) RAILS_HB(7)
     RAILS_HB(8) RAILS_HB(9) RAILS_HB(10) RAILS_HB(11) RAILS_HB(12) RAILS_HB(13) RAILS_HB(14)
@@ -331,11 +331,11 @@ static cudaError_t launch_w(const LaunchCtx& c, long long grid, int M, int N, in
   }
 }
 
-cudaError_t launch_histogram(const LaunchCtx& c, int U, int nd, int d0, int M, int N, int T,
-                             int k, const int32_t* topk, const int32_t* lut, int n_inst,
+cudaError_t launch_histogram(const LaunchCtx& c, int U, int nd, int d0, int M, int N, int ngs,
+                             int T, int k, const int32_t* topk, const int32_t* lut, int n_inst,
                              long long row_bytes, int32_t* counts, int64_t* msg,
                              int32_t* rank) {
-  const long long grid = (long long)U * nd * N;
+  const long long grid = (long long)U * nd * ngs;
   const long long G = (long long)M * N;
   const char* hv = getenv("RAILS_HIST_IMPL");
   const long long ne = (long long)T * k;
@@ -345,12 +345,12 @@ cudaError_t launch_histogram(const LaunchCtx& c, int U, int nd, int d0, int M, i
   if (!(hv && (hv[0] == '1' || hv[0] == '2')) && G <= 12288 && ne <= 65535 &&
       (many || (hv && hv[0] == '3'))) {
     const size_t smem = (size_t)HW_WARPS * G * 3;
-    auto kern = k_hist_w1<8>;
+    auto kern = rank ? k_hist_w1<8, true> : k_hist_w1<8, false>;
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     kern<<<(unsigned)((grid + HW_WARPS - 1) / HW_WARPS), HW_WARPS * 32, smem, c.stream>>>(
-        topk, lut, n_inst, M, N, d0, nd, T, k, row_bytes, grid, counts, msg, rank, c.err);
+        topk, lut, n_inst, M, N, ngs, d0, nd, T, k, row_bytes, grid, counts, msg, rank, c.err);
     count_launch(1);
     return cudaGetLastError();
   }
@@ -366,7 +366,7 @@ cudaError_t launch_histogram(const LaunchCtx& c, int U, int nd, int d0, int M, i
     auto kern = k_hist_rank2<WW, 8>;                                                        \
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     if (e != cudaSuccess) return e;                                                         \
-    kern<<<(unsigned)grid, WW * 32, smem, c.stream>>>(topk, lut, n_inst, M, N, d0, nd, T, k, \
+    kern<<<(unsigned)grid, WW * 32, smem, c.stream>>>(topk, lut, n_inst, M, N, ngs, d0, nd, T, k, \
                                                       row_bytes, counts, msg, rank, c.err); \
     count_launch(1);                                                                        \
     return cudaGetLastError();                                                              \
@@ -380,15 +380,15 @@ cudaError_t launch_histogram(const LaunchCtx& c, int U, int nd, int d0, int M, i
   }
   // Warps per CTA: as many private sub-histograms as fit in 64 KiB (>= 1).
   if (G * 8 * 4 <= 65536)
-    return launch_w<8>(c, grid, M, N, d0, nd, T, k, topk, lut, n_inst, row_bytes, counts, msg,
+    return launch_w<8>(c, grid, M, N, ngs, d0, nd, T, k, topk, lut, n_inst, row_bytes, counts, msg,
                        rank);
   if (G * 4 * 4 <= 65536)
-    return launch_w<4>(c, grid, M, N, d0, nd, T, k, topk, lut, n_inst, row_bytes, counts, msg,
+    return launch_w<4>(c, grid, M, N, ngs, d0, nd, T, k, topk, lut, n_inst, row_bytes, counts, msg,
                        rank);
   if (G * 2 * 4 <= 98304)
-    return launch_w<2>(c, grid, M, N, d0, nd, T, k, topk, lut, n_inst, row_bytes, counts, msg,
+    return launch_w<2>(c, grid, M, N, ngs, d0, nd, T, k, topk, lut, n_inst, row_bytes, counts, msg,
                        rank);
-  return launch_w<1>(c, grid, M, N, d0, nd, T, k, topk, lut, n_inst, row_bytes, counts, msg,
+  return launch_w<1>(c, grid, M, N, ngs, d0, nd, T, k, topk, lut, n_inst, row_bytes, counts, msg,
                      rank);
 }
 

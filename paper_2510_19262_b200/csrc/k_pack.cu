@@ -17,6 +17,8 @@
 // loads are in flight, then broadcast by shuffle.
 //   MULTI = false: C >= RB, a row copy spans at most two chunks.
 //   MULTI = true : C <  RB, the chunk of every 16-byte vector is computed.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace rails {
@@ -46,7 +48,7 @@ __device__ __forceinline__ long long chunk_addr(long long c, long long fb, long 
   return rr >= 0 ? rbase[rr] + ro : -(1LL << 62);
 }
 
-template <int VPL, bool MULTI>
+template <int VPL, bool MULTI, bool CS = false>
 __global__ void __launch_bounds__(PACK_THREADS)
     k_pack(int U, int nd, int d0, int M, int N, int T, int k, long long C, int cshift,
            const uint4* __restrict__ x, const int32_t* __restrict__ topk,
@@ -132,10 +134,14 @@ __global__ void __launch_bounds__(PACK_THREADS)
             if (vi < nvec) {
               const long long o = (long long)vi << 4;
               const long long a = (o < B0) ? D0 + o : D1 + (o - B0);
-              if (a >= 0 && a + 16 <= out_cap)
-                st_stream((uint4*)(out + a), v[i]);
-              else
+              if (a >= 0 && a + 16 <= out_cap) {
+                if (CS)
+                  st_cs((uint4*)(out + a), v[i]);
+                else
+                  st_stream((uint4*)(out + a), v[i]);
+              } else {
                 flag_error(err, ERR_NOSPC);
+              }
             }
           }
         } else {
@@ -175,7 +181,8 @@ static cudaError_t launch_v(const LaunchCtx& c, int U, int nd, int d0, int M, in
                             const int32_t* lut, int n_inst, const int32_t* rank,
                             const int64_t* msg, long long RB, const rails_sched_t& s,
                             const int64_t* rail_base, void* out, long long out_cap) {
-  auto kern = k_pack<VPL, MULTI>;
+  const char* st = getenv("RAILS_PACK_ST");
+  auto kern = (st && st[0] == '1') ? k_pack<VPL, MULTI, true> : k_pack<VPL, MULTI, false>;
   int per_sm = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PACK_THREADS, 0);
   if (e != cudaSuccess) return e;

@@ -80,6 +80,14 @@ def lib():
         L.rails_rail_offsets.argtypes = [PT, PS, P, P, P, P]
         L.rails_pack.argtypes = [PT, PS, i32, i32, P, P, P, i32, P, P, i64,
                                  ctypes.POINTER(_Sched), P, P, i64, P]
+        L.rails_histogram_gpus.argtypes = [PT, PS, i32, i32, i32, i32, P, P, i32, i64, P, P, P, P]
+        L.rails_rail_offsets_owner.argtypes = [PT, PS, P, P, P, P]
+        L.rails_pack_owner.argtypes = [PT, PS, i32, i32, i32, i32, P, P, P, i32, P, P, i64,
+                                       ctypes.POINTER(_Sched), P, P, P, P]
+        L.rails_enable_peer_access.argtypes = [i32]
+        for n in ("rails_histogram_gpus", "rails_rail_offsets_owner", "rails_pack_owner",
+                  "rails_enable_peer_access"):
+            getattr(L, n).restype = ctypes.c_int
         L.rails_check.argtypes = [P]
         L.rails_last_error.restype = ctypes.c_char_p
         L.rails_launch_count.argtypes = [i32]
@@ -302,6 +310,65 @@ def pack(tp: Topo, sh: Shard, T: int, k: int, x: torch.Tensor, topk: torch.Tenso
                          _ptr(msg, torch.int64, "msg"), row_bytes, ctypes.byref(cs),
                          _ptr(rail_base, torch.int64, "rail_base"), _ptr(out, None, "out"),
                          out.numel() * out.element_size(), _stream(stream)))
+
+
+# ---------------------------------------------------------------- NEXT f2 (rail owner)
+def histogram_gpus(tp: Topo, sh: Shard, g0: int, topk: torch.Tensor, lut: torch.Tensor,
+                   row_bytes: int, out=None, stream=None):
+    """topk int32 [U][nd][ng][T][k] of source GPUs g0..g0+ng-1."""
+    U, nd, ng, T, k = topk.shape
+    G = tp.M * tp.N
+    dev = topk.device
+    if out is None:
+        out = (torch.empty((U, nd, ng, G), dtype=torch.int32, device=dev),
+               torch.empty((U, nd, ng, G), dtype=torch.int64, device=dev),
+               torch.empty((U, nd, ng, T, k), dtype=torch.int32, device=dev))
+    counts, msg, rank = out
+    _ok(lib().rails_histogram_gpus(ctypes.byref(tp), ctypes.byref(sh), g0, ng, T, k,
+                                   _ptr(topk, torch.int32, "topk"), _ptr(lut, torch.int32, "lut"),
+                                   lut.numel(), row_bytes, _ptr(counts, torch.int32, "counts"),
+                                   _ptr(msg, torch.int64, "msg"), _ptr(rank, torch.int32, "rank"),
+                                   _stream(stream)))
+    return counts, msg, rank
+
+
+def rail_offsets_owner(tp: Topo, sh: Shard, send_load: torch.Tensor, rail_base=None,
+                       rail_total=None, stream=None):
+    if rail_base is None:
+        rail_base = torch.empty_like(send_load)
+    if rail_total is None:
+        rail_total = torch.empty(tp.N, dtype=torch.int64, device=send_load.device)
+    _ok(lib().rails_rail_offsets_owner(ctypes.byref(tp), ctypes.byref(sh),
+                                       _ptr(send_load, torch.int64, "send_load"),
+                                       _ptr(rail_base, torch.int64, "rail_base"),
+                                       _ptr(rail_total, torch.int64, "rail_total"),
+                                       _stream(stream)))
+    return rail_base, rail_total
+
+
+def pack_owner(tp: Topo, sh: Shard, g0: int, T: int, k: int, x: torch.Tensor,
+               topk: torch.Tensor, lut: torch.Tensor, rank: torch.Tensor, msg_node: torch.Tensor,
+               row_bytes: int, sched: Schedule, rail_base: torch.Tensor, rail_ptrs, rail_caps,
+               stream=None):
+    """rail_ptrs / rail_caps: python lists of N ints (device pointers, peer-mapped for
+    rails owned by other GPUs) and capacities."""
+    ng = topk.shape[2]
+    N = tp.N
+    ptrs = (ctypes.c_void_p * N)(*[ctypes.c_void_p(int(p)) for p in rail_ptrs])
+    caps = (ctypes.c_int64 * N)(*[int(c) for c in rail_caps])
+    cs = sched.c()
+    _ok(lib().rails_pack_owner(ctypes.byref(tp), ctypes.byref(sh), g0, ng, T, k, _ptr(x, None, "x"),
+                               _ptr(topk, torch.int32, "topk"), _ptr(lut, torch.int32, "lut"),
+                               lut.numel(), _ptr(rank, torch.int32, "rank"),
+                               _ptr(msg_node, torch.int64, "msg"), row_bytes, ctypes.byref(cs),
+                               _ptr(rail_base, torch.int64, "rail_base"),
+                               ctypes.cast(ptrs, ctypes.c_void_p), ctypes.cast(caps, ctypes.c_void_p),
+                               _stream(stream)))
+
+
+def enable_peer_access(peer_device: int):
+    """Let kernels on the current device load/store memory of `peer_device`."""
+    _ok(lib().rails_enable_peer_access(peer_device))
 
 
 # ---------------------------------------------------------------- misc

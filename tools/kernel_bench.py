@@ -70,8 +70,10 @@ def bench_pack(res):
     total = int(pipe.total.item())
     algo = M * N * T * RB + total
     ref = None
-    for impl in ("1", "2"):
-        os.environ["RAILS_PACK_IMPL"] = impl
+    for impl in ("1", "2", "1cs"):
+        os.environ["RAILS_PACK_IMPL"] = impl[0]
+        if impl == "1cs":
+            os.environ["RAILS_PACK_ST"] = "1"
         pipe.out.zero_()
         t = timeit(lambda: rails.pack(pipe.tp, pipe.sh, T, k, x, topk, lut, pipe.rank, pipe.msg, RB,
                                       pipe.sched, pipe.rail_base, pipe.out), flush=False)
@@ -85,6 +87,7 @@ def bench_pack(res):
         res[f"pack_impl{impl}"] = dict(t, gbs=gbs, frac=gbs / PEAK, bytes=algo, same_as_impl1=same)
         del h
     os.environ.pop("RAILS_PACK_IMPL", None)
+    os.environ.pop("RAILS_PACK_ST", None)
     # context only (NOT the roofline denominator): the same 1-read : 2-write byte
     # mix as the pack, done by a plain torch broadcast copy of every 8 KiB row into
     # two adjacent slots (second read of a row hits L2)
