@@ -225,6 +225,33 @@ def d1_uniform(M: int, N: int, V: int) -> np.ndarray:
     return np.repeat(D[:, None, :], N, axis=1).copy()
 
 
+def d1_sparse_topk(M: int, N: int, V: int, sparsity: float, K: int, seed: int, u: int) -> np.ndarray:
+    """Table 1 "Sparse": floor(sparsity*M) seeded
+    destination domains receive nothing; every source GPU picks K distinct active
+    domains other than its own (seeded) and splits V equally over their N*K GPUs
+    (floor, remainder to the first chosen GPU).  int64 [M][N][G]."""
+    G = M * N
+    sigma = unit_seed(seed, u)
+    order = _perm(sigma, M)
+    n_off = int(np.floor(sparsity * M))
+    active = np.ones(M, bool)
+    active[order[:n_off]] = False
+    D = np.zeros((M, N, G), np.int64)
+    for d in range(M):
+        cand = np.nonzero(active & (np.arange(M) != d))[0]
+        if len(cand) < K:
+            raise ValueError("fewer active destination domains than K")
+        for g in range(N):
+            keys = mix64_np((cand.astype(np.uint64) * np.uint64(1000003)
+                             + np.uint64((d * N + g) * 7919)) ^ np.uint64(sigma))
+            pick = cand[np.argsort(keys, kind="stable")[:K]]
+            dst = np.sort(np.concatenate([np.arange(f * N, (f + 1) * N) for f in pick]))
+            each = V // len(dst)
+            D[d, g, dst] = each
+            D[d, g, dst[0]] += V - each * len(dst)
+    return D
+
+
 def d1_units(cfg: dict, seed: int, u0: int, U: int) -> np.ndarray:
     """Stack of D^(1) matrices int64 [U][M][N][G] for units u0..u0+U-1."""
     M, N, V = cfg["M"], cfg["N"], cfg["V"]
@@ -234,6 +261,37 @@ def d1_units(cfg: dict, seed: int, u0: int, U: int) -> np.ndarray:
             out[i] = d1_receiver_skew(M, N, V, cfg["zipf_s"], seed, u0 + i)
         elif cfg.get("skew") == "sender":
             out[i] = d1_sender_skew(M, N, V, cfg["zipf_s"], seed, u0 + i)
+        elif cfg.get("skew") == "sparse":
+            out[i] = d1_sparse_topk(M, N, V, cfg["sparsity"], cfg.get("K", 2), seed, u0 + i)
         else:
             out[i] = d1_uniform(M, N, V)
     return out
+
+
+# ---------------------------------------------------------------- NEXT f1 inputs
+def expert_outputs(shape, seed: int, u: int, device="cpu") -> torch.Tensor:
+    """Finite bf16 expert-output rows as int16 bit patterns, `shape` = [..., H]:
+    sign random, exponent 2^-8 .. 2^2, random 7-bit mantissa (no NaN/Inf, so the
+    fp32 weighted sums are comparable bit for bit)."""
+    sigma = unit_seed(seed ^ 0xE0E0E0, u)
+    n = 1
+    for s in shape:
+        n *= s
+    idx = torch.arange(n, dtype=torch.int64, device=device)
+    z = mix64_t(idx ^ _s64(sigma))
+    sign = z & 1
+    ex = 119 + (_srl(z, 1) % 11)
+    mant = _srl(z, 8) & 0x7F
+    bits = (sign << 15) | (ex << 7) | mant
+    return (bits - ((bits >> 15) << 16)).to(torch.int16).view(*shape)
+
+
+def gate_weights(shape, seed: int, u: int, device="cpu") -> torch.Tensor:
+    """Top-k gate weights in [0, 1), exactly representable in fp32 (24-bit grid)."""
+    sigma = unit_seed(seed ^ 0x6A7E, u)
+    n = 1
+    for s in shape:
+        n *= s
+    idx = torch.arange(n, dtype=torch.int64, device=device)
+    z = _srl(mix64_t(idx ^ _s64(sigma)), 40)
+    return (z.to(torch.float64) / float(1 << 24)).to(torch.float32).view(*shape)

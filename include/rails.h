@@ -218,6 +218,50 @@ int rails_pack(const rails_topo_t* topo, const rails_shard_t* shard, int32_t T,
                const int64_t* msg_bytes, int64_t row_bytes, const rails_sched_t* sched,
                const int64_t* rail_base, void* out, int64_t out_cap, void* stream);
 
+/* ------------------------------------------------------------------ NEXT f1 */
+/* Combine all-to-all (Alg. 1 step 4): expert outputs go back from
+ * expert GPU h = f*N+m to the token's GPU a = d*N+g as a SECOND all-to-all round
+ * with its own LoadState.  Readings R#28-R#31.
+ *
+ * rails_transpose_traffic: combine traffic msg_t[u][f][m][a] = msg[u][a/N][a%N][f*N+m]
+ *   for every node (msg, msg_t: int64 [U][M][N][G]; R#28).  The combine schedule and
+ *   evaluation are then rails_lpt_schedule / rails_eval on msg_t, unchanged. */
+int rails_transpose_traffic(const rails_topo_t* topo, int32_t U, const int64_t* msg,
+                            int64_t* msg_t, void* stream);
+
+/* Expert-output buffer layout (R#29): GPU b holds the rows it received in dispatch,
+ * message by message in ascending source GPU a, each in dispatch rank order.
+ * counts: dispatch counts int32 [U][M][N][G] (all nodes); in_off int64 [U][G][G]:
+ * in_off[u][b][a] = first row of message a in b's buffer; rows_in int64 [U][G]. */
+int rails_recv_offsets(const rails_topo_t* topo, int32_t U, const int32_t* counts,
+                       int64_t* in_off, int64_t* rows_in, void* stream);
+
+/* Combine pack of the shard's SENDER nodes f (R#30): message (m, a) = rows
+ * in_off[u][f*N+m][a] .. of y (bytes [U][nd][N][rows_cap][row_bytes]), chunked by
+ * the combine schedule (msg_comb [U][nd][N][G], sched) into out at
+ * rail_base[u][dl][j] + off (as rails_pack).  Intra-node messages are skipped. */
+int rails_pack_combine(const rails_topo_t* topo, const rails_shard_t* shard, int64_t row_bytes,
+                       int64_t rows_cap, const void* y, const int64_t* in_off,
+                       const int64_t* rows_in, const int64_t* msg_comb,
+                       const rails_sched_t* sched, const int64_t* rail_base, void* out,
+                       int64_t out_cap, void* stream);
+
+/* Unpack + top-k weighted combine on the shard's RECEIVER nodes d (R#31):
+ *   out[u][dl][g][t][e] = sum_{s<k} w[t][s] * row(t,s)[e],  e < row_bytes/2 (bf16)
+ * accumulated in fp32 in slot order, every product and sum rounded (no FMA).
+ * row(t,s): expert h = inst_to_gpu[topk[t][s]] on node f; rank rho = row_rank[t][s];
+ * f == d: y row in_off[u][h][a] + rho of GPU h (never railed); f != d: message
+ * bytes [rho*RB, (rho+1)*RB) of combine message (h -> a), read from comb_out with
+ * node f's combine schedule (msg_comb_all/sched_all/rail_base_all cover ALL M
+ * sender nodes: [U][M][N][G] / [U][M][N]).  w: float [U][nd][N][T][k];
+ * out: float [U][nd][N][T][row_bytes/2]. */
+int rails_unpack_combine(const rails_topo_t* topo, const rails_shard_t* shard, int32_t T,
+                         int32_t k, const int32_t* topk_inst, const int32_t* inst_to_gpu,
+                         int32_t n_inst, const int32_t* row_rank, const float* w, const void* y,
+                         int64_t rows_cap, const int64_t* in_off, const int64_t* msg_comb_all,
+                         const rails_sched_t* sched_all, const int64_t* rail_base_all,
+                         const void* comb_out, float* out, int64_t row_bytes, void* stream);
+
 /* ------------------------------------------------------------------ NEXT f2 */
 /* Rail-owner variant (one multi-GPU box = one RailS node): NIC j hangs off GPU j
  * (P:184), so rail j's send buffer lives in GPU j's HBM and traffic of GPU g on

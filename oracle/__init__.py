@@ -231,3 +231,98 @@ def run_unit_routing(M, N, T, k, row_bytes, C, R2, ecmp_seed, topk_unit, lut):
         counts[d], msg[d], rank[d] = histogram_node(M, N, d, T, k, topk_unit[d], lut, row_bytes)
     scheds, ev = run_unit_matrix(M, N, C, R2, ecmp_seed, msg)
     return dict(counts=counts, msg=msg, rank=rank, scheds=scheds, eval=ev)
+
+
+# ------------------------------------------------------------------ NEXT f1 (combine)
+def _sig_f1(L):
+    P = ctypes.c_void_p
+    i32, i64 = ctypes.c_int32, ctypes.c_int64
+    L.orc_transpose.restype = None
+    L.orc_transpose.argtypes = [i32, i32, P, P]
+    L.orc_recv_offsets.restype = None
+    L.orc_recv_offsets.argtypes = [i64, P, P]
+    L.orc_pack_combine_node.restype = ctypes.c_int
+    L.orc_pack_combine_node.argtypes = [i32, i32, i32, i64, i64, P, P, P, i64, P, P, P, P, P, P,
+                                        P, P, i64]
+    L.orc_unpack_combine.restype = ctypes.c_int
+    L.orc_unpack_combine.argtypes = [i32, i32, i32, i32, i32, i32, i64, i64, P, P, P, P, P, P,
+                                     P, P, P, P, P, P]
+
+
+def transpose(M, N, msg_unit):
+    """Combine traffic of one unit (R#28): [M][N][G] -> [M][N][G]."""
+    L = lib(); _sig_f1(L)
+    msg_unit = _c(msg_unit, np.int64)
+    out = np.zeros_like(msg_unit)
+    L.orc_transpose(M, N, _p(msg_unit), _p(out))
+    return out
+
+
+def recv_offsets(rows_in):
+    """Exclusive prefix of one receiving GPU's incoming row counts (R#29)."""
+    L = lib(); _sig_f1(L)
+    rows_in = _c(rows_in, np.int64)
+    out = np.zeros_like(rows_in)
+    L.orc_recv_offsets(len(rows_in), _p(rows_in), _p(out))
+    return out
+
+
+def pack_combine_node(M, N, f, RB, C, y_node, in_off_node, msgc_node, sched, rail_base, out_cap):
+    """Combine pack of sender node f (R#30).  y_node: list of N uint8 arrays [rows][RB];
+    in_off_node: [N][G] (rows of GPU f*N+m); msgc_node: [N][G] combine bytes."""
+    L = lib(); _sig_f1(L)
+    ys = [_c(v, np.uint8) for v in y_node]
+    yp = (ctypes.c_void_p * N)(*[v.ctypes.data for v in ys])
+    in_off_node, msgc_node = _c(in_off_node, np.int64), _c(msgc_node, np.int64)
+    ch = sched["chunks"]
+    rail_base = _c(rail_base, np.int64)
+    out = np.zeros(int(out_cap), np.uint8)
+    rc = L.orc_pack_combine_node(M, N, f, RB, C, ctypes.cast(yp, ctypes.c_void_p), _p(in_off_node),
+                                 _p(msgc_node), len(ch["size"]), _p(ch["g"]), _p(ch["h"]),
+                                 _p(ch["c"]), _p(ch["size"]), _p(_c(sched["rail"], np.int32)),
+                                 _p(_c(sched["off"], np.int64)), _p(rail_base), _p(out), out_cap)
+    if rc != 0:
+        raise RuntimeError(f"oracle combine pack failed rc={rc}")
+    return out
+
+
+def first_chunk_table(N, G, sched):
+    """Index (emission order) of chunk 0 of every message of a node's chunk list."""
+    ch = sched["chunks"]
+    first = np.full((N, G), -1, np.int64)
+    sel = ch["c"] == 0
+    first[ch["g"][sel], ch["h"][sel]] = np.nonzero(sel)[0]
+    return first
+
+
+def unpack_combine(M, N, d, g, T, k, RB, C, topk_g, lut, rank_g, w_g, y_node_d, in_off_node_d,
+                   rails_bytes, rail_bases, firsts, scheds):
+    """Top-k weighted combine for GPU (d,g) by definition (R#31); float32 [T][RB/2].
+    rails_bytes[f]: node f's combine rail buffer block; rail_bases[f]: [N] offsets
+    of its rails; firsts[f]/scheds[f]: node f's combine chunk list lookup."""
+    L = lib(); _sig_f1(L)
+    H = RB // 2
+    out = np.zeros((T, H), np.float32)
+    topk_g, lut, rank_g = _c(topk_g, np.int32), _c(lut, np.int32), _c(rank_g, np.int32)
+    w_g = _c(w_g, np.float32)
+    yd = [_c(v, np.uint8) for v in y_node_d]
+    yp = (ctypes.c_void_p * N)(*[v.ctypes.data for v in yd])
+    in_off_node_d = _c(in_off_node_d, np.int64)
+    keep = []
+
+    def arr(lst, dtype):
+        a = [_c(v, dtype) for v in lst]
+        keep.append(a)
+        return (ctypes.c_void_p * len(a))(*[v.ctypes.data for v in a])
+    rp = arr(rails_bytes, np.uint8)
+    rbp = arr(rail_bases, np.int64)
+    fp = arr(firsts, np.int64)
+    railp = arr([s["rail"] for s in scheds], np.int32)
+    offp = arr([s["off"] for s in scheds], np.int64)
+    cv = lambda x: ctypes.cast(x, ctypes.c_void_p)  # noqa: E731
+    rc = L.orc_unpack_combine(M, N, d, g, T, k, RB, C, _p(topk_g), _p(lut), _p(rank_g), _p(w_g),
+                              cv(yp), _p(in_off_node_d), cv(rp), cv(rbp), cv(fp), cv(railp),
+                              cv(offp), _p(out))
+    if rc != 0:
+        raise RuntimeError(f"oracle unpack failed rc={rc}")
+    return out

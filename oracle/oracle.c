@@ -363,3 +363,120 @@ done:
     free(fill);
     return rc;
 }
+
+/* ================================================================ NEXT f1: combine */
+/* Combine all-to-all (Alg. 1 step 4): the expert outputs of every
+ * dispatched row travel back from expert GPU h = f*N+m to the token's GPU (d,g);
+ * it is a separate all-to-all round with its own LoadState (R#6).
+ *
+ * orc_transpose: combine traffic D_c[f][m][d*N+g] = D_d[d][g][f*N+m] (R#28). */
+void orc_transpose(int32_t M, int32_t N, const int64_t *disp, int64_t *comb) {
+    int64_t G = (int64_t)M * N;
+    for (int64_t a = 0; a < G; a++)          /* a = d*N+g: dispatch source GPU */
+        for (int64_t b = 0; b < G; b++)      /* b = f*N+m: dispatch destination */
+            comb[b * G + a] = disp[a * G + b];
+}
+
+/* Expert-output buffer of GPU (f,m) (R#29): the rows it received in dispatch,
+ * message by message in ascending source GPU a = d*N+g, each message's rows in
+ * their dispatch order (rank rho).  rows_in[a] = dispatch counts[a][f*N+m]
+ * (intra-node sources included: those rows came over NVLink).  Returns the
+ * first row of message a in y: in_off[a] = sum_{a' < a} rows_in[a']. */
+void orc_recv_offsets(int64_t G, const int64_t *rows_in, int64_t *in_off) {
+    int64_t run = 0;
+    for (int64_t a = 0; a < G; a++) { in_off[a] = run; run += rows_in[a]; }
+}
+
+/* Combine pack of sender node f by definition (R#29-R#30): combine message
+ * (m, a) = rows [in_off_m[a], in_off_m[a] + cnt) of y_m, i.e. the bytes of the
+ * expert outputs in dispatch order; chunk c of it (from the combine round's LPT
+ * schedule, chunk list ch_* in emission order) is copied to
+ * out + rail_base[rail] + off.  Intra-node messages (a on node f) are not sent.
+ * y: [N] pointers to [rows][RB]; in_off: [N][G]; msgc: combine bytes [N][G]. */
+int orc_pack_combine_node(int32_t M, int32_t N, int32_t f, int64_t RB, int64_t C,
+                          const uint8_t *const *y, const int64_t *in_off,
+                          const int64_t *msgc, int64_t F, const int32_t *ch_g,
+                          const int32_t *ch_h, const int64_t *ch_c, const int64_t *ch_size,
+                          const int32_t *ch_rail, const int64_t *ch_off,
+                          const int64_t *rail_base, uint8_t *out, int64_t out_cap) {
+    int64_t G = (int64_t)M * N;
+    (void)f;
+    for (int64_t i = 0; i < F; i++) {
+        int32_t m = ch_g[i];
+        int64_t a = ch_h[i];
+        const uint8_t *stream = y[m] + in_off[(int64_t)m * G + a] * RB;
+        int64_t dst = rail_base[ch_rail[i]] + ch_off[i];
+        if (msgc[(int64_t)m * G + a] <= 0) return ORC_ERANGE;
+        if (dst < 0 || dst + ch_size[i] > out_cap) return ORC_ERANGE;
+        memcpy(out + dst, stream + ch_c[i] * C, (size_t)ch_size[i]);
+    }
+    return ORC_OK;
+}
+
+static float bf16_to_float(uint16_t b) {
+    uint32_t u = (uint32_t)b << 16;
+    float x;
+    memcpy(&x, &u, 4);
+    return x;
+}
+
+/* Unpack + top-k weighted combine on GPU (d,g) (Alg. 1 step 5 input; R#31):
+ *   out[t][e] = sum_{s=0..k-1} w[t][s] * row(t,s)[e]      (e < H = RB/2 bf16 values)
+ * accumulated in fp32 in the order s = 0..k-1 (each product and sum rounded to
+ * fp32, no FMA).  row(t,s) is the expert output of slot (t,s): message
+ * (h -> (d,g)) of the combine round, h = lut[topk[t][s]], at message row rho =
+ * rank[t][s] (the dispatch rank).  If h is on node d the row never crossed a rail
+ * and is read from y of GPU h (row in_off[h][d*N+g] + rho); otherwise from the
+ * combine rail buffers of node f = h/N: chunk c = floor(rho*RB / C) ... located
+ * through the chunk list of node f (first chunk of each message: first[m][a]).
+ * rails_f: [M] pointers to node f's combine rail buffer block (rail_base applied
+ * by the caller through rb[f][j]); ch_rail/ch_off/first: per node f arrays.
+ * Returns ORC_ERANGE if a row is not found. */
+int orc_unpack_combine(int32_t M, int32_t N, int32_t d, int32_t g, int32_t T, int32_t k,
+                       int64_t RB, int64_t C, const int32_t *topk, const int32_t *lut,
+                       const int32_t *rank, const float *w, const uint8_t *const *y_node_d,
+                       const int64_t *in_off_node_d, const uint8_t *const *rails_f,
+                       const int64_t *const *rb_f, const int64_t *const *first_f,
+                       const int32_t *const *rail_f, const int64_t *const *off_f,
+                       float *out) {
+    int64_t G = (int64_t)M * N;
+    int64_t H = RB / 2;
+    int64_t a = (int64_t)d * N + g;
+    uint8_t *row = (uint8_t *)malloc((size_t)RB);
+    if (!row) return ORC_ENOMEM;
+    for (int32_t t = 0; t < T; t++) {
+        for (int64_t e = 0; e < H; e++) out[(int64_t)t * H + e] = 0.0f;
+        for (int32_t s = 0; s < k; s++) {
+            int64_t h = lut[topk[(int64_t)t * k + s]];
+            int64_t rho = rank[(int64_t)t * k + s];
+            int64_t fdst = h / N, m = h % N;
+            if (fdst == d) {
+                const uint8_t *src = y_node_d[m] + (in_off_node_d[m * G + a] + rho) * RB;
+                memcpy(row, src, (size_t)RB);
+            } else {
+                /* gather the row piece by piece from node f's combine chunks */
+                int64_t p = rho * RB, got = 0;
+                while (got < RB) {
+                    int64_t c = (p + got) / C;
+                    int64_t in_c = (p + got) - c * C;
+                    int64_t idx = first_f[fdst][m * G + a] + c;
+                    int64_t len = C - in_c;
+                    if (len > RB - got) len = RB - got;
+                    int32_t j = rail_f[fdst][idx];
+                    const uint8_t *src = rails_f[fdst] + rb_f[fdst][j] + off_f[fdst][idx] + in_c;
+                    memcpy(row + got, src, (size_t)len);
+                    got += len;
+                }
+            }
+            float wt = w[(int64_t)t * k + s];
+            for (int64_t e = 0; e < H; e++) {
+                uint16_t b;
+                memcpy(&b, row + 2 * e, 2);
+                float prod = wt * bf16_to_float(b);
+                out[(int64_t)t * H + e] = out[(int64_t)t * H + e] + prod;
+            }
+        }
+    }
+    free(row);
+    return ORC_OK;
+}

@@ -335,6 +335,75 @@ int rails_pack_owner(const rails_topo_t* topo, const rails_shard_t* sh, int32_t 
                  "rails_pack_owner launch");
 }
 
+int rails_transpose_traffic(const rails_topo_t* topo, int32_t U, const int64_t* msg,
+                            int64_t* msg_t, void* stream) {
+  int rc = check_topo(topo);
+  if (rc) return rc;
+  if (U < 1 || !msg || !msg_t || msg == msg_t) return fail(RAILS_EINVAL, "bad argument");
+  LaunchCtx c;
+  if ((rc = ctx(stream, &c))) return rc;
+  return cuda_rc(launch_transpose(c, U, (long long)topo->M * topo->N, msg, msg_t),
+                 "rails_transpose_traffic launch");
+}
+
+int rails_recv_offsets(const rails_topo_t* topo, int32_t U, const int32_t* counts,
+                       int64_t* in_off, int64_t* rows_in, void* stream) {
+  int rc = check_topo(topo);
+  if (rc) return rc;
+  if (U < 1 || !counts || !in_off || !rows_in) return fail(RAILS_EINVAL, "bad argument");
+  LaunchCtx c;
+  if ((rc = ctx(stream, &c))) return rc;
+  return cuda_rc(launch_recv_offsets(c, U, (long long)topo->M * topo->N, counts, in_off, rows_in),
+                 "rails_recv_offsets launch");
+}
+
+int rails_pack_combine(const rails_topo_t* topo, const rails_shard_t* sh, int64_t row_bytes,
+                       int64_t rows_cap, const void* y, const int64_t* in_off,
+                       const int64_t* rows_in, const int64_t* msg_comb,
+                       const rails_sched_t* sched, const int64_t* rail_base, void* out,
+                       int64_t out_cap, void* stream) {
+  int rc = check_topo(topo);
+  if (rc || (rc = check_shard(topo, sh))) return rc;
+  if (row_bytes < 16 || row_bytes % 16 || topo->chunk_bytes % 16 || rows_cap < 0)
+    return fail(RAILS_EINVAL, "row_bytes and chunk_bytes must be multiples of 16");
+  if (!y || !in_off || !rows_in || !msg_comb || !sched || !sched->full_base || !sched->rem_rail ||
+      !sched->rem_off || !rail_base || (!out && out_cap > 0))
+    return fail(RAILS_EINVAL, "NULL argument");
+  if (!al(y, 16) || (out && !al(out, 16))) return fail(RAILS_EINVAL, "y/out must be 16-byte aligned");
+  LaunchCtx c;
+  if ((rc = ctx(stream, &c))) return rc;
+  return cuda_rc(launch_pack_combine(c, sh->U, sh->nd, sh->d0, topo->M, topo->N, rows_cap,
+                                     topo->chunk_bytes, y, in_off, rows_in, msg_comb, *sched,
+                                     rail_base, out, out_cap, row_bytes),
+                 "rails_pack_combine launch");
+}
+
+int rails_unpack_combine(const rails_topo_t* topo, const rails_shard_t* sh, int32_t T, int32_t k,
+                         const int32_t* topk_inst, const int32_t* inst_to_gpu, int32_t n_inst,
+                         const int32_t* row_rank, const float* w, const void* y,
+                         int64_t rows_cap, const int64_t* in_off, const int64_t* msg_comb_all,
+                         const rails_sched_t* sched_all, const int64_t* rail_base_all,
+                         const void* comb_out, float* out, int64_t row_bytes, void* stream) {
+  int rc = check_topo(topo);
+  if (rc || (rc = check_shard(topo, sh))) return rc;
+  if (T < 1 || k < 1 || k > 32 || n_inst < 1) return fail(RAILS_EINVAL, "bad T, k or n_inst");
+  if (row_bytes < 16 || row_bytes % 16 || topo->chunk_bytes % 16 || rows_cap < 0)
+    return fail(RAILS_EINVAL, "row_bytes and chunk_bytes must be multiples of 16");
+  if (!topk_inst || !inst_to_gpu || !row_rank || !w || !y || !in_off || !msg_comb_all ||
+      !sched_all || !sched_all->full_base || !sched_all->rem_rail || !sched_all->rem_off ||
+      !rail_base_all || !comb_out || !out)
+    return fail(RAILS_EINVAL, "NULL argument");
+  if (!al(y, 16) || !al(comb_out, 16) || !al(out, 16))
+    return fail(RAILS_EINVAL, "y/comb_out/out must be 16-byte aligned");
+  LaunchCtx c;
+  if ((rc = ctx(stream, &c))) return rc;
+  return cuda_rc(launch_unpack_combine(c, sh->U, sh->nd, sh->d0, topo->M, topo->N, T, k,
+                                       topo->chunk_bytes, topk_inst, inst_to_gpu, n_inst,
+                                       row_rank, w, y, rows_cap, in_off, msg_comb_all, *sched_all,
+                                       rail_base_all, comb_out, out, row_bytes),
+                 "rails_unpack_combine launch");
+}
+
 int rails_enable_peer_access(int32_t peer_device) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);

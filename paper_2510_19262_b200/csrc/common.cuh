@@ -199,5 +199,22 @@ cudaError_t launch_rail_offsets_owner(const LaunchCtx&, long long ublk, int N,
                                       const int64_t* send_load, int64_t* rail_base,
                                       int64_t* rail_total);
 
+cudaError_t launch_transpose(const LaunchCtx&, int U, long long G, const int64_t* src,
+                             int64_t* dst);
+cudaError_t launch_recv_offsets(const LaunchCtx&, int U, long long G, const int32_t* counts,
+                                int64_t* in_off, int64_t* rows_in);
+cudaError_t launch_pack_combine(const LaunchCtx&, int U, int nd, int d0, int M, int N,
+                                long long Rcap, long long C, const void* y,
+                                const int64_t* in_off, const int64_t* rows_in,
+                                const int64_t* msgc, const rails_sched_t& s,
+                                const int64_t* rail_base, void* out, long long out_cap,
+                                long long RB);
+cudaError_t launch_unpack_combine(const LaunchCtx&, int U, int nd, int d0, int M, int N, int T,
+                                  int k, long long C, const int32_t* topk, const int32_t* lut,
+                                  int n_inst, const int32_t* rank, const float* w, const void* y,
+                                  long long Rcap, const int64_t* in_off, const int64_t* msgc,
+                                  const rails_sched_t& s, const int64_t* rail_base_c,
+                                  const void* comb_out, float* out, long long RB);
+
 void count_launch(int n);
 }  // namespace rails

@@ -84,6 +84,15 @@ def lib():
         L.rails_rail_offsets_owner.argtypes = [PT, PS, P, P, P, P]
         L.rails_pack_owner.argtypes = [PT, PS, i32, i32, i32, i32, P, P, P, i32, P, P, i64,
                                        ctypes.POINTER(_Sched), P, P, P, P]
+        L.rails_transpose_traffic.argtypes = [PT, i32, P, P, P]
+        L.rails_recv_offsets.argtypes = [PT, i32, P, P, P, P]
+        L.rails_pack_combine.argtypes = [PT, PS, i64, i64, P, P, P, P, ctypes.POINTER(_Sched), P,
+                                         P, i64, P]
+        L.rails_unpack_combine.argtypes = [PT, PS, i32, i32, P, P, i32, P, P, P, i64, P, P,
+                                           ctypes.POINTER(_Sched), P, P, P, i64, P]
+        for n in ("rails_transpose_traffic", "rails_recv_offsets", "rails_pack_combine",
+                  "rails_unpack_combine"):
+            getattr(L, n).restype = ctypes.c_int
         L.rails_enable_peer_access.argtypes = [i32]
         for n in ("rails_histogram_gpus", "rails_rail_offsets_owner", "rails_pack_owner",
                   "rails_enable_peer_access"):
@@ -310,6 +319,65 @@ def pack(tp: Topo, sh: Shard, T: int, k: int, x: torch.Tensor, topk: torch.Tenso
                          _ptr(msg, torch.int64, "msg"), row_bytes, ctypes.byref(cs),
                          _ptr(rail_base, torch.int64, "rail_base"), _ptr(out, None, "out"),
                          out.numel() * out.element_size(), _stream(stream)))
+
+
+# ---------------------------------------------------------------- NEXT f1 (combine)
+def transpose_traffic(tp: Topo, msg: torch.Tensor, out=None, stream=None):
+    """Dispatch traffic [U][M][N][G] -> combine traffic (same shape, transposed GPUs)."""
+    if out is None:
+        out = torch.empty_like(msg)
+    _ok(lib().rails_transpose_traffic(ctypes.byref(tp), msg.shape[0], _ptr(msg, torch.int64, "msg"),
+                                      _ptr(out, torch.int64, "out"), _stream(stream)))
+    return out
+
+
+def recv_offsets(tp: Topo, counts: torch.Tensor, in_off=None, rows_in=None, stream=None):
+    """Dispatch counts [U][M][N][G] -> in_off [U][G][G], rows_in [U][G]."""
+    U = counts.shape[0]
+    G = tp.M * tp.N
+    if in_off is None:
+        in_off = torch.empty((U, G, G), dtype=torch.int64, device=counts.device)
+    if rows_in is None:
+        rows_in = torch.empty((U, G), dtype=torch.int64, device=counts.device)
+    _ok(lib().rails_recv_offsets(ctypes.byref(tp), U, _ptr(counts, torch.int32, "counts"),
+                                 _ptr(in_off, torch.int64, "in_off"),
+                                 _ptr(rows_in, torch.int64, "rows_in"), _stream(stream)))
+    return in_off, rows_in
+
+
+def pack_combine(tp: Topo, sh: Shard, row_bytes: int, y: torch.Tensor, in_off: torch.Tensor,
+                 rows_in: torch.Tensor, msg_comb: torch.Tensor, sched: Schedule,
+                 rail_base: torch.Tensor, out: torch.Tensor, stream=None):
+    """y: bytes [U][nd][N][rows_cap][row_bytes] (any dtype view)."""
+    rows_cap = y.shape[3]
+    cs = sched.c()
+    _ok(lib().rails_pack_combine(ctypes.byref(tp), ctypes.byref(sh), row_bytes, rows_cap,
+                                 _ptr(y, None, "y"), _ptr(in_off, torch.int64, "in_off"),
+                                 _ptr(rows_in, torch.int64, "rows_in"),
+                                 _ptr(msg_comb, torch.int64, "msg_comb"), ctypes.byref(cs),
+                                 _ptr(rail_base, torch.int64, "rail_base"), _ptr(out, None, "out"),
+                                 out.numel() * out.element_size(), _stream(stream)))
+
+
+def unpack_combine(tp: Topo, sh: Shard, T: int, k: int, topk: torch.Tensor, lut: torch.Tensor,
+                   rank: torch.Tensor, w: torch.Tensor, y: torch.Tensor, in_off: torch.Tensor,
+                   msg_comb_all: torch.Tensor, sched_all: Schedule, rail_base_all: torch.Tensor,
+                   comb_out: torch.Tensor, row_bytes: int, out=None, stream=None):
+    """-> float32 [U][nd][N][T][row_bytes/2]: top-k weighted expert outputs per token."""
+    U, nd, N = sh.U, sh.nd, tp.N
+    if out is None:
+        out = torch.empty((U, nd, N, T, row_bytes // 2), dtype=torch.float32, device=topk.device)
+    cs = sched_all.c()
+    _ok(lib().rails_unpack_combine(ctypes.byref(tp), ctypes.byref(sh), T, k,
+                                   _ptr(topk, torch.int32, "topk"), _ptr(lut, torch.int32, "lut"),
+                                   lut.numel(), _ptr(rank, torch.int32, "rank"),
+                                   _ptr(w, torch.float32, "w"), _ptr(y, None, "y"), y.shape[3],
+                                   _ptr(in_off, torch.int64, "in_off"),
+                                   _ptr(msg_comb_all, torch.int64, "msg_comb"), ctypes.byref(cs),
+                                   _ptr(rail_base_all, torch.int64, "rail_base"),
+                                   _ptr(comb_out, None, "comb_out"),
+                                   _ptr(out, torch.float32, "out"), row_bytes, _stream(stream)))
+    return out
 
 
 # ---------------------------------------------------------------- NEXT f2 (rail owner)

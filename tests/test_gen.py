@@ -80,3 +80,20 @@ def test_receiver_skew_is_skewed():
     D = gen.d1_receiver_skew(16, 8, 256 << 20, 1.2, 1, 0)
     col = D.sum(axis=(0, 1))
     assert col.max() > 20 * np.median(col)
+
+
+def test_sparse_topk_recipe():
+    # S:162-170 / S:209: floor(s*M) domains silent; K active domains per sender;
+    # per-sender volume preserved for every sparsity
+    M, N, V = 10, 4, 10 ** 6 + 7
+    for s in (0.0, 0.2, 0.4, 0.6):
+        D = gen.d1_sparse_topk(M, N, V, s, 2, 3, 0)
+        assert (D.sum(axis=2) == V).all()
+        col = D.reshape(M, N, M, N).sum(axis=(0, 1, 3))
+        assert (col == 0).sum() == int(np.floor(s * M))
+        for d in range(M):
+            assert (D[d, :, d * N:(d + 1) * N] == 0).all()
+            for g in range(N):
+                doms = set(np.nonzero(D[d, g])[0] // N)
+                assert len(doms) == 2
+    assert np.array_equal(gen.d1_sparse_topk(M, N, V, 0.6, 2, 3, 0), gen.d1_sparse_topk(M, N, V, 0.6, 2, 3, 0))
