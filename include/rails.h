@@ -299,6 +299,18 @@ int rails_pack_owner(const rails_topo_t* topo, const rails_shard_t* shard, int32
                      const int64_t* rail_base, void* const* rail_ptr, const int64_t* rail_cap,
                      void* stream);
 
+/* Inter-process rail buffers for rails_pack_owner (one process per GPU): the
+ * owner allocates with rails_ipc_alloc (device memory of the current device, 256-B
+ * aligned, plus a 64-byte cudaIpcMemHandle_t written to `handle`), ships the
+ * handle to the other processes of the box, and each of them maps it with
+ * rails_ipc_open while ITS OWN device is current (peer access enabled lazily), so
+ * its kernels can store into the owner's HBM over NVLink.  rails_ipc_close unmaps
+ * an opened buffer; rails_ipc_free releases an owned one. */
+int rails_ipc_alloc(int64_t bytes, void** dptr, void* handle);
+int rails_ipc_open(const void* handle, void** dptr);
+int rails_ipc_close(void* dptr);
+int rails_ipc_free(void* dptr);
+
 /* Enable direct loads/stores from kernels on the current device to memory of
  * `peer_device` (cudaDeviceEnablePeerAccess; "already enabled" is not an error).
  * RAILS_ECUDA if the devices cannot reach each other. */

@@ -404,6 +404,43 @@ int rails_unpack_combine(const rails_topo_t* topo, const rails_shard_t* sh, int3
                  "rails_unpack_combine launch");
 }
 
+int rails_ipc_alloc(int64_t bytes, void** dptr, void* handle) {
+  if (bytes < 1 || !dptr || !handle) return fail(RAILS_EINVAL, "bad argument");
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, (size_t)bytes);
+  if (e != cudaSuccess) return cuda_rc(e, "cudaMalloc");
+  cudaIpcMemHandle_t h;
+  e = cudaIpcGetMemHandle(&h, p);
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    return cuda_rc(e, "cudaIpcGetMemHandle");
+  }
+  memcpy(handle, &h, sizeof(h));
+  *dptr = p;
+  return RAILS_OK;
+}
+
+int rails_ipc_open(const void* handle, void** dptr) {
+  if (!handle || !dptr) return fail(RAILS_EINVAL, "bad argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  void* p = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return cuda_rc(e, "cudaIpcOpenMemHandle");
+  *dptr = p;
+  return RAILS_OK;
+}
+
+int rails_ipc_close(void* dptr) {
+  if (!dptr) return fail(RAILS_EINVAL, "NULL pointer");
+  return cuda_rc(cudaIpcCloseMemHandle(dptr), "cudaIpcCloseMemHandle");
+}
+
+int rails_ipc_free(void* dptr) {
+  if (!dptr) return fail(RAILS_EINVAL, "NULL pointer");
+  return cuda_rc(cudaFree(dptr), "cudaFree");
+}
+
 int rails_enable_peer_access(int32_t peer_device) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);

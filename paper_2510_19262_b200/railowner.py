@@ -10,7 +10,8 @@ rail j's send buffer lives in GPU j's HBM.  One step:
   4. rails_rail_offsets_owner + rails_pack_owner: each chunk piece is stored
      straight into the owner's buffer through a peer-mapped pointer   (kernel)
   5. a one-element NCCL all-reduce orders every rank's pack before any consumer.
-Peer mapping uses CUDA IPC through torch's tensor-sharing reductions (plumbing).
+Peer mapping: CUDA IPC handles exported/imported by librails (rails_ipc_*), each
+rank mapping the peers' buffers under its own device.
 """
 from __future__ import annotations
 
@@ -30,7 +31,6 @@ class RailOwnerNode:
     def __init__(self, M: int, N: int, T: int, k: int, row_bytes: int, chunk_bytes: int, U: int,
                  d: int, n_inst: int, group=None, R2: float = 5.0e10):
         import torch.distributed as dist
-        from torch.multiprocessing.reductions import reduce_tensor
 
         self.dist = dist
         self.group = group
@@ -61,25 +61,35 @@ class RailOwnerNode:
         # T*k*RB + C (all N GPUs' rows spread over N rails, chunks <= C)
         self.cap = U * (T * k * row_bytes + chunk_bytes)
         self.cap = (self.cap + 255) // 256 * 256
-        self.buf = torch.empty(self.ng * self.cap, dtype=torch.uint8, device=dev)
+        # own rail buffers in this GPU's HBM, exported by CUDA IPC; the other ranks
+        # map them under their own device so their pack kernels store over NVLink
+        self.own_ptr, handle, self.buf = rails.ipc_alloc(self.ng * self.cap)
         objs = [None] * self.P
-        dist.all_gather_object(objs, reduce_tensor(self.buf), group=group)
-        peers = []
-        devs = []
-        for q, (fn, args) in enumerate(objs):
+        dist.all_gather_object(objs, (handle, dev.index), group=group)
+        _enable_peer_access(dev.index, [o[1] for o in objs])
+        bases = []
+        self.opened = []
+        for q, (h, _) in enumerate(objs):
             if q == self.p:
-                peers.append(self.buf)
-                devs.append(dev.index)
+                bases.append(self.own_ptr)
             else:
-                t = fn(*args)
-                peers.append(t)
-                devs.append(t.device.index)
-        _enable_peer_access(dev.index, devs)
-        torch.cuda.set_device(dev)
-        self.peers = peers
-        self.rail_ptrs = [peers[j // self.ng].data_ptr() + (j % self.ng) * self.cap
-                          for j in range(N)]
+                ptr = rails.ipc_open(h)
+                self.opened.append(ptr)
+                bases.append(ptr)
+        self.rail_ptrs = [bases[j // self.ng] + (j % self.ng) * self.cap for j in range(N)]
         self.rail_caps = [self.cap] * N
+        dist.barrier(group=group)
+
+    def close(self):
+        """Unmap the peers' buffers, then free this rank's own (collective)."""
+        torch.cuda.synchronize()
+        self.dist.barrier(group=self.group)
+        for ptr in self.opened:
+            rails.ipc_close(ptr)
+        self.opened = []
+        self.dist.barrier(group=self.group)
+        rails.ipc_free(self.own_ptr)
+        self.own_ptr = None
 
     def own_rail(self, j: int) -> torch.Tensor:
         """This rank's buffer of rail j (must be owned here)."""

@@ -93,6 +93,12 @@ def lib():
         for n in ("rails_transpose_traffic", "rails_recv_offsets", "rails_pack_combine",
                   "rails_unpack_combine"):
             getattr(L, n).restype = ctypes.c_int
+        L.rails_ipc_alloc.argtypes = [i64, ctypes.POINTER(ctypes.c_void_p), P]
+        L.rails_ipc_open.argtypes = [P, ctypes.POINTER(ctypes.c_void_p)]
+        L.rails_ipc_close.argtypes = [P]
+        L.rails_ipc_free.argtypes = [P]
+        for n in ("rails_ipc_alloc", "rails_ipc_open", "rails_ipc_close", "rails_ipc_free"):
+            getattr(L, n).restype = ctypes.c_int
         L.rails_enable_peer_access.argtypes = [i32]
         for n in ("rails_histogram_gpus", "rails_rail_offsets_owner", "rails_pack_owner",
                   "rails_enable_peer_access"):
@@ -432,6 +438,39 @@ def pack_owner(tp: Topo, sh: Shard, g0: int, T: int, k: int, x: torch.Tensor,
                                _ptr(rail_base, torch.int64, "rail_base"),
                                ctypes.cast(ptrs, ctypes.c_void_p), ctypes.cast(caps, ctypes.c_void_p),
                                _stream(stream)))
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of raw device bytes (for torch.as_tensor)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                         "data": (int(ptr), False), "version": 3}
+
+
+def ipc_alloc(nbytes: int):
+    """Owner side: (device pointer, 64-byte handle, uint8 tensor view)."""
+    p = ctypes.c_void_p()
+    h = ctypes.create_string_buffer(64)
+    _ok(lib().rails_ipc_alloc(nbytes, ctypes.byref(p), h))
+    view = torch.as_tensor(_CudaArray(p.value, nbytes), device="cuda")
+    return p.value, bytes(h.raw), view
+
+
+def ipc_open(handle: bytes) -> int:
+    """Map another process's rail buffer for kernels of the current device."""
+    p = ctypes.c_void_p()
+    h = ctypes.create_string_buffer(handle, 64)
+    _ok(lib().rails_ipc_open(h, ctypes.byref(p)))
+    return p.value
+
+
+def ipc_close(ptr: int):
+    _ok(lib().rails_ipc_close(ctypes.c_void_p(ptr)))
+
+
+def ipc_free(ptr: int):
+    _ok(lib().rails_ipc_free(ctypes.c_void_p(ptr)))
 
 
 def enable_peer_access(peer_device: int):

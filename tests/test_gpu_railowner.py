@@ -27,6 +27,15 @@ def _port():
 
 
 def _worker(rank, world, port, cfg, q):
+    import traceback
+    try:
+        _worker_body(rank, world, port, cfg, q)
+    except BaseException:
+        q.put((rank, ["EXC " + traceback.format_exc()]))
+        raise
+
+
+def _worker_body(rank, world, port, cfg, q):
     import torch.distributed as dist
 
     import oracle
@@ -69,6 +78,7 @@ def _worker(rank, world, port, cfg, q):
             if not np.array_equal(got, want[base[j]:base[j] + L[j]]):
                 errors.append(f"u{u} rail{j}")
     q.put((rank, errors))
+    node.close()
     dist.barrier()
     dist.destroy_process_group()
 
@@ -88,9 +98,23 @@ def test_railowner_pack_matches_oracle(cfg):
     procs = [ctx.Process(target=_worker, args=(r, world, port, cfg, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = dict(q.get(timeout=600) for _ in range(world))
+    import queue
+    import time
+    res = {}
+    t_end = time.time() + 600
+    while len(res) < world and time.time() < t_end:
+        try:
+            r, errs = q.get(timeout=5)
+            res[r] = errs
+            if any(e.startswith("EXC") for e in errs):
+                break
+        except queue.Empty:
+            if any(p.exitcode not in (None, 0) for p in procs):
+                break
     for p in procs:
-        p.join(timeout=120)
-        assert p.exitcode == 0
+        p.join(timeout=30)
+        if p.is_alive():
+            p.kill()
     for r, errs in res.items():
         assert not errs, (r, errs)
+    assert len(res) == world, f"workers: exit codes {[p.exitcode for p in procs]}"

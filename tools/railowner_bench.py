@@ -99,6 +99,7 @@ def main():
            "nodes_per_s": U / (step_ms / 1e3)}
     if rank == 0:
         print(json.dumps(out), flush=True)
+    node.close()
     dist.barrier()
     dist.destroy_process_group()
 
