@@ -186,11 +186,24 @@ def run_reference(args, rank, world):
             "config": {"workload": args.workload}, "gpu_launches": 0,
             "cpu_baseline": dict(info, value=v),
             "e2e": {"value": v, "unit": "nodes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ---------------------------------------------------------------- GPU arm
+_JSON_OUT = None
+
+
+def emit(obj):
+    """The one JSON line on the original stdout (everything else goes to stderr)."""
+    _JSON_OUT.write(json.dumps(obj) + "\n")
+    _JSON_OUT.flush()
+
+
 def main():
+    global _JSON_OUT
+    # NCCL and CUDA libraries may print banners on fd 1: keep stdout for the JSON line
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     args = parse()
     rank, world, local = dist_env()
     if args.impl == "reference":
@@ -343,7 +356,7 @@ def main():
     if world == 1 and not args.no_cpu:
         out["cpu_baseline"] = oracle_sample(args.workload)
     if rank == 0:
-        print(json.dumps(out), flush=True)
+        emit(out)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()

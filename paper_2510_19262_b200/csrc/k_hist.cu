@@ -158,10 +158,12 @@ __global__ void __launch_bounds__(HW_WARPS * 32)
     for (int j = 0; j < UNR; ++j)
       hv[j] = (base + j * 32 + lane < ne) ? __ldg(src + base + j * 32) : -1;
 #pragma unroll
+    for (int j = 0; j < UNR; ++j)  // all LUT lookups of the batch in flight together
+      hv[j] = ((unsigned)hv[j] < (unsigned)n_inst) ? __ldg(lut + hv[j]) : -1;
+#pragma unroll
     for (int j = 0; j < UNR; ++j) {
       const bool in = base + j * 32 + lane < ne;
-      int h = -1;
-      if ((unsigned)hv[j] < (unsigned)n_inst) h = __ldg(lut + hv[j]);
+      const int h = hv[j];
       const bool valid = (unsigned)h < (unsigned)G;
       bad |= in && !valid;
       // equal destinations inside the group: tag write / read-back
@@ -172,10 +174,14 @@ __global__ void __launch_bounds__(HW_WARPS * 32)
       if (dup) tg[h] = (uint8_t)(32 | lane);
       __syncwarp();
       if (valid && !dup) dup = tg[h] != lane;
-      const unsigned dmask = __ballot_sync(FULL, dup);
+      // equal keys among the (few) duplicated lanes: warp-uniform loop over them
+      unsigned dm = __ballot_sync(FULL, dup);
       unsigned peers = 1u << lane;
-      if (dmask) {
-        if (dup) peers = __match_any_sync(dmask, h);
+      while (dm) {
+        const int b = __ffs(dm) - 1;
+        dm &= dm - 1;
+        const int hb = __shfl_sync(FULL, h, b);
+        if (dup && hb == h) peers |= 1u << b;
       }
       const int c = valid ? cnt[h] : 0;
       __syncwarp();

@@ -64,10 +64,22 @@ def test_two_rank_sharded_pipeline_matches_single():
              for r in range(2)]
     for p in procs:
         p.start()
-    got = dict(q.get(timeout=300) for _ in range(2))
+    import queue
+    import time
+    got = {}
+    t_end = time.time() + 300
+    while len(got) < 2 and time.time() < t_end:
+        try:
+            r, res = q.get(timeout=5)
+            got[r] = res
+        except queue.Empty:
+            if any(p.exitcode not in (None, 0) for p in procs):
+                break
     for p in procs:
-        p.join(timeout=120)
-        assert p.exitcode == 0
+        p.join(timeout=60)
+        if p.is_alive():
+            p.kill()
+    assert len(got) == 2, f"workers failed: exit codes {[p.exitcode for p in procs]}"
     dev = "cuda:0"
     seed = 77
     topk = torch.stack([gen.routing(M, N, T, k, E, seed, u, device=dev) for u in range(U)])
