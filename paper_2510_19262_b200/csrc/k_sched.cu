@@ -46,20 +46,35 @@ __device__ void radix_pass(const KeyT* kin, const IdxT* iin, KeyT* kout, IdxT* i
   }
   __syncthreads();
   // digit totals -> exclusive digit bases -> per-warp starting positions
-  // (threads 0..255 = warps 0..7, one digit each)
-  int tot = 0, inc = 0;
-  if (threadIdx.x < 256) {
-    for (int w = 0; w < W; ++w) tot += hist[w * 256 + threadIdx.x];
-    inc = warp_incl_scan(tot);
-    if (lane == 31) sc[wid] = inc;
+  // digit totals (any block size), exclusive scan of the 256 totals by warp 0
+  // (8 digits per lane), then per-warp starting positions per digit.
+  // sc: >= 256 ints of shared scratch.
+  for (int b = threadIdx.x; b < 256; b += blockDim.x) {
+    int tot = 0;
+    for (int w = 0; w < W; ++w) tot += hist[w * 256 + b];
+    sc[b] = tot;
   }
   __syncthreads();
-  if (threadIdx.x < 256) {
-    int run = inc - tot;
-    for (int w = 0; w < wid; ++w) run += sc[w];
+  if (wid == 0) {
+    int v[8], s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      v[i] = sc[lane * 8 + i];
+      s += v[i];
+    }
+    int run = warp_incl_scan(s) - s;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      sc[lane * 8 + i] = run;
+      run += v[i];
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < 256; b += blockDim.x) {
+    int run = sc[b];
     for (int w = 0; w < W; ++w) {
-      int c = hist[w * 256 + threadIdx.x];
-      hist[w * 256 + threadIdx.x] = run;
+      const int c = hist[w * 256 + b];
+      hist[w * 256 + b] = run;
       run += c;
     }
   }
@@ -129,8 +144,8 @@ __device__ __forceinline__ T block_reduce_and(T v, T* s) {
 constexpr int SORT_THREADS = 512;
 constexpr int SORT_SMEM_ITEMS = 16384;  // items per CTA kept in shared memory
 
-template <typename IdxT>
-__global__ void __launch_bounds__(SORT_THREADS)
+template <typename IdxT, int THREADS>
+__global__ void __launch_bounds__(THREADS)
     k_chunk_sort(const int64_t* __restrict__ msg, long long NG, int N, int d0, int nd,
                  long long C, int cshift, int nbits, int64_t* __restrict__ full_base, int8_t* __restrict__ rem_rail,
                  int64_t* __restrict__ rem_off, int64_t* __restrict__ n_full_out,
@@ -139,8 +154,8 @@ __global__ void __launch_bounds__(SORT_THREADS)
                  int* err) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ long long scan_scratch[33];
-  __shared__ int hist[(SORT_THREADS / 32) * 256];
-  __shared__ int sc[32];
+  __shared__ int hist[(THREADS / 32) * 256];
+  __shared__ int sc[256];
   __shared__ uint32_t red32[32];
 
   const long long seg = blockIdx.x;
@@ -163,7 +178,7 @@ __global__ void __launch_bounds__(SORT_THREADS)
   long long carry_full = 0;
   int carry_rem = 0;
   uint32_t kor = 0, kand = 0xffffffffu;
-  for (long long t0 = 0; t0 < NG; t0 += SORT_THREADS) {
+  for (long long t0 = 0; t0 < NG; t0 += THREADS) {
     const long long m = t0 + threadIdx.x;
     long long B = 0;
     if (m < NG) {
@@ -208,7 +223,7 @@ __global__ void __launch_bounds__(SORT_THREADS)
   const int which = radix_sort<uint32_t, IdxT>(kA, iA, kB, iB, n, kor, kand, nbits, hist, sc);
   const uint32_t* ks = which ? kB : kA;
   const IdxT* is = which ? iB : iA;
-  for (int i = threadIdx.x; i < n; i += SORT_THREADS) {
+  for (int i = threadIdx.x; i < n; i += THREADS) {
     ws_w[seg * NG + i] = (uint32_t)(C - 1 - (long long)ks[i]);
     ws_m[seg * NG + i] = (uint32_t)is[i];
   }
@@ -545,14 +560,16 @@ cudaError_t launch_schedule(const LaunchCtx& c, int U, int nd, int d0, int M, in
   cudaError_t e;
   if (NG <= SORT_SMEM_ITEMS) {
     const size_t smem = (size_t)NG * (8 + 2 * sizeof(uint16_t));
-    auto kern = k_chunk_sort<uint16_t>;
+    // small segments: 128-thread CTAs, many resident per SM; large: 512 threads
+    const bool small = NG <= 2048;
+    auto kern = small ? k_chunk_sort<uint16_t, 128> : k_chunk_sort<uint16_t, SORT_THREADS>;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<(unsigned)nseg, SORT_THREADS, smem, c.stream>>>(
+    kern<<<(unsigned)nseg, small ? 128 : SORT_THREADS, smem, c.stream>>>(
         msg, NG, N, d0, nd, C, cshift, nbits, s.full_base, s.rem_rail, s.rem_off, s.n_full, s.n_rem, ws_w,
         ws_m, nullptr, 1, c.err);
   } else {
-    k_chunk_sort<uint32_t><<<(unsigned)nseg, SORT_THREADS, 0, c.stream>>>(
+    k_chunk_sort<uint32_t, SORT_THREADS><<<(unsigned)nseg, SORT_THREADS, 0, c.stream>>>(
         msg, NG, N, d0, nd, C, cshift, nbits, s.full_base, s.rem_rail, s.rem_off, s.n_full, s.n_rem, ws_w,
         ws_m, scratch, 0, c.err);
   }
@@ -605,7 +622,7 @@ __global__ void __launch_bounds__(SORT_THREADS)
              int32_t* __restrict__ rail, int64_t* __restrict__ off, int64_t* __restrict__ load,
              uint64_t* kA, uint64_t* kB, uint32_t* iA, uint32_t* iB, int* err) {
   __shared__ int hist[(SORT_THREADS / 32) * 256];
-  __shared__ int sc[32];
+  __shared__ int sc[256];
   __shared__ uint64_t red64[32];
   const int s = blockIdx.x;
   const long long b0 = seg_off[s], b1 = seg_off[s + 1];
