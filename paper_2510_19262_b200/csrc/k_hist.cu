@@ -136,19 +136,19 @@ __global__ void __launch_bounds__(HW_WARPS * 32)
               int M, int N, int ngs, int d0, int nd, int T, int k, long long RB,
               long long nsegs, int32_t* __restrict__ counts, int64_t* __restrict__ msg,
               int32_t* __restrict__ rank, int* err) {
-  extern __shared__ __align__(16) uint16_t sm3[];
+  // one 32-bit word per bin: bits 0..23 running count, bits 24..31 tag (lane id)
+  extern __shared__ __align__(16) uint32_t sw1[];
   const int G = M * N;
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long sg = (long long)blockIdx.x * HW_WARPS + wid;  // ((u*nd)+dl)*ngs + gl
-  uint16_t* const cnt = sm3 + wid * G;  // running counts (< 2^16: T*k <= 65535)
-  uint8_t* const tg = (uint8_t*)(sm3 + HW_WARPS * G) + wid * G;
+  uint32_t* const bin = sw1 + wid * G;
   if (sg >= nsegs) return;
   const long long ul = sg / ngs;
   const int d = d0 + (int)(ul % nd);
   const int ne = T * k;
   const int32_t* __restrict__ src = topk + sg * (long long)ne + lane;
   int32_t* __restrict__ dst = RANK ? rank + sg * (long long)ne + lane : nullptr;
-  for (int i = lane; i < G; i += 32) cnt[i] = 0;
+  for (int i = lane; i < G; i += 32) bin[i] = 0;
   const unsigned lt = lanemask_lt();
   bool bad = false;
   __syncwarp();
@@ -166,33 +166,31 @@ __global__ void __launch_bounds__(HW_WARPS * 32)
       const int h = hv[j];
       const bool valid = (unsigned)h < (unsigned)G;
       bad |= in && !valid;
-      // equal destinations inside the group: tag write / read-back
-      // (a winner that already sees a loser's mark is correctly a duplicate too)
-      if (valid) tg[h] = (uint8_t)lane;
+      // 1. tag write: for equal keys one lane's id survives
+      if (valid) ((uint8_t*)(bin + h))[3] = (uint8_t)lane;
       __syncwarp();
-      bool dup = valid && tg[h] != lane;
-      if (dup) tg[h] = (uint8_t)(32 | lane);
-      __syncwarp();
-      if (valid && !dup) dup = tg[h] != lane;
-      // equal keys among the (few) duplicated lanes: warp-uniform loop over them
-      unsigned dm = __ballot_sync(FULL, dup);
-      unsigned peers = 1u << lane;
-      while (dm) {
-        const int b = __ffs(dm) - 1;
-        dm &= dm - 1;
-        const int hb = __shfl_sync(FULL, h, b);
-        if (dup && hb == h) peers |= 1u << b;
+      // 2. one read gives the surviving tag and the running count
+      const uint32_t word = valid ? bin[h] : 0u;
+      const int t = (int)(word >> 24);
+      const int c = (int)(word & 0xffffffu);
+      const bool loser = valid && t != lane;
+      // 3. peers: a loser knows the winner (its tag); every lane scans the losers
+      unsigned peers = (1u << lane) | (loser ? (1u << t) : 0u);
+      unsigned lm = __ballot_sync(FULL, loser);
+      while (lm) {
+        const int b = __ffs(lm) - 1;
+        lm &= lm - 1;
+        if (__shfl_sync(FULL, h, b) == h) peers |= 1u << b;
       }
-      const int c = valid ? cnt[h] : 0;
-      __syncwarp();
-      if (valid && (peers & lt) == 0) cnt[h] = (uint16_t)(c + __popc(peers));
       if (RANK && in) dst[base + j * 32] = valid ? c + __popc(peers & lt) : -1;
-      // the next group reads cnt only after its own two tag syncs
+      // 4. the lowest lane of each key advances the count
+      if (valid && (peers & lt) == 0) bin[h] = (uint32_t)(c + __popc(peers));
+      __syncwarp();
     }
   }
   if (__any_sync(FULL, bad) && lane == 0) flag_error(err, ERR_RANGE);
   for (int h = lane; h < G; h += 32) {
-    const int c = cnt[h];
+    const int c = (int)(bin[h] & 0xffffffu);
     counts[sg * G + h] = c;
     msg[sg * G + h] = (h / N == d) ? 0LL : (long long)c * RB;
   }
@@ -350,7 +348,7 @@ cudaError_t launch_histogram(const LaunchCtx& c, int U, int nd, int d0, int M, i
   const bool many = grid >= (long long)c.num_sms * 16;
   if (!(hv && (hv[0] == '1' || hv[0] == '2')) && G <= 12288 && ne <= 65535 &&
       (many || (hv && hv[0] == '3'))) {
-    const size_t smem = (size_t)HW_WARPS * G * 3;
+    const size_t smem = (size_t)HW_WARPS * G * 4;
     auto kern = rank ? k_hist_w1<8, true> : k_hist_w1<8, false>;
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
