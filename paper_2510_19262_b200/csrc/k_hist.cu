@@ -122,12 +122,15 @@ __global__ void __launch_bounds__(W * 32)
 // owns one (unit, node, source GPU): it walks
 // the T*k routing entries once, in order, 32 at a time, with a private running
 // count per bin in shared memory, so rank = running count + equal destinations
-// among lower lanes and no cross-warp scan or second pass is needed.  Equal
-// destinations inside a group are found with a tag write/read-back (each lane
-// writes its lane id at tag[h]; a lane that reads another id, or whose id was
-// overwritten by a loser's mark, has a duplicate) and match.any runs only over
-// those lanes.  Ranks are stored as they are produced (coalesced 128 B per group);
-// counts and bytes are written once at the end.
+// among lower lanes and no cross-warp scan or second pass is needed.  Each bin is
+// one 32-bit shared word (running count | tag byte).  Equal destinations inside a
+// group: every lane writes its lane id into the tag byte of its bin; one 32-bit
+// read then returns both the surviving tag and the count; a lane that reads
+// another id (a "loser") knows the winner's lane, and the winner learns its
+// losers by a warp-uniform loop over the (rarely non-empty) loser ballot.  Three
+// shared accesses per 32 entries (tag store, word load, leader's count store).
+// Ranks are stored as they are produced (coalesced 128 B per group); counts and
+// bytes are written once at the end.
 constexpr int HW_WARPS = 4;
 
 template <int UNR, bool RANK>

@@ -491,21 +491,23 @@ __global__ void __launch_bounds__(128)
   }
   constexpr int PF = 8;
   int i = 0;
+  // batches of 8 as two 16-byte loads per array (chain lists start 16-B aligned:
+  // N*G is a multiple of 4 for even N)
+  auto ld8 = [](const uint32_t* p, uint32_t (&o)[PF]) {
+    const uint4 a = __ldg((const uint4*)p), b = __ldg((const uint4*)p + 1);
+    o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w;
+    o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
+  };
   uint32_t wv[PF], mv[PF];
   if (PF <= nr) {
-#pragma unroll
-    for (int p = 0; p < PF; ++p) {
-      wv[p] = __ldg(sw + p);
-      mv[p] = __ldg(sm + p);
-    }
+    ld8(sw, wv);
+    ld8(sm, mv);
   }
   for (; i + PF <= nr; i += PF) {
     uint32_t wn[PF], mn[PF];  // next batch in flight while this one is assigned
-    const bool more = i + 2 * PF <= nr;
-#pragma unroll
-    for (int p = 0; p < PF; ++p) {
-      wn[p] = more ? __ldg(sw + i + PF + p) : 0u;
-      mn[p] = more ? __ldg(sm + i + PF + p) : 0u;
+    if (i + 2 * PF <= nr) {
+      ld8(sw + i + PF, wn);
+      ld8(sm + i + PF, mn);
     }
 #pragma unroll
     for (int p = 0; p < PF; ++p) {
