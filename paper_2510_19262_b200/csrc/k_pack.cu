@@ -206,7 +206,13 @@ static cudaError_t launch_m(const LaunchCtx& c, int U, int nd, int d0, int M, in
                             const int64_t* msg, long long RB, const rails_sched_t& s,
                             const int64_t* rail_base, void* out, long long out_cap) {
   const long long nvec = RB >> 4;
-  const long long vpl = (nvec + 31) / 32;
+  long long vpl = (nvec + 31) / 32;
+  // tuning knob: RAILS_PACK_VPL caps the 16-byte vectors held per lane (the row is
+  // then copied in windows; fewer registers, more resident warps)
+  if (const char* ev = getenv("RAILS_PACK_VPL")) {
+    const long long cap = atoll(ev);
+    if (cap >= 1 && cap < vpl) vpl = cap;
+  }
 #define RAILS_PACK_CASE(V)                                                                  \
   if (vpl <= V)                                                                             \
     return launch_v<V, MULTI>(c, U, nd, d0, M, N, T, k, C, cshift, x, topk, lut, n_inst, rank, \

@@ -147,8 +147,8 @@ constexpr int SORT_SMEM_ITEMS = 16384;  // items per CTA kept in shared memory
 template <typename IdxT, int THREADS>
 __global__ void __launch_bounds__(THREADS)
     k_chunk_sort(const int64_t* __restrict__ msg, long long NG, int N, int d0, int nd,
-                 long long C, int cshift, int nbits, int64_t* __restrict__ full_base, int8_t* __restrict__ rem_rail,
-                 int64_t* __restrict__ rem_off, int64_t* __restrict__ n_full_out,
+                 long long C, int cshift, int nbits, int64_t* __restrict__ full_base,
+                 int32_t* __restrict__ ws_inv, int64_t* __restrict__ n_full_out,
                  int32_t* __restrict__ n_rem_out, uint32_t* __restrict__ ws_w,
                  uint32_t* __restrict__ ws_m, uint8_t* __restrict__ ws_scratch, int use_smem,
                  int* err) {
@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(THREADS)
     if (m < NG) {
       B = mg[m];
       // negative bytes, or bytes to a GPU of the source node (R#2), are invalid
-      if (B < 0 || (B != 0 && (m % G) / N == d)) {
+      if (B < 0 || (B != 0 && (int)((unsigned)m % (unsigned)G) / N == d)) {
         flag_error(err, ERR_RANGE);
         B = 0;
       }
@@ -205,8 +205,7 @@ __global__ void __launch_bounds__(THREADS)
         kor |= key;
         kand &= key;
       } else {
-        rem_rail[seg * NG + m] = -1;
-        rem_off[seg * NG + m] = 0;
+        ws_inv[seg * NG + m] = -1;  // no remainder chunk
       }
     }
     carry_full += tot >> 16;
@@ -226,17 +225,25 @@ __global__ void __launch_bounds__(THREADS)
   for (int i = threadIdx.x; i < n; i += THREADS) {
     ws_w[seg * NG + i] = (uint32_t)(C - 1 - (long long)ks[i]);
     ws_m[seg * NG + i] = (uint32_t)is[i];
+    ws_inv[seg * NG + is[i]] = i;  // sorted position of message is[i]'s remainder
   }
 }
 
 // ---------------------------------------------------------------- a4 chain
 constexpr int CHAIN_WARPS = 4;
 
+// Chain results are written in SORTED order (sequential per chain: full sectors,
+// no read-modify-write), packed as rail << 56 | offset; k_expand_rem then writes
+// rem_rail / rem_off per message, coalesced, through the sort's inverse permutation.
+constexpr long long OFF_MASK = (1LL << 56) - 1;
+__device__ __forceinline__ uint64_t pack_res(unsigned rail, long long off) {
+  return ((uint64_t)rail << 56) | ((uint64_t)off & (uint64_t)OFF_MASK);
+}
+
 __global__ void __launch_bounds__(CHAIN_WARPS * 32)
     k_lpt_chain(long long nseg, int N, long long C, long long NG,
                 const int64_t* __restrict__ n_full, const int32_t* __restrict__ n_rem,
-                const uint32_t* __restrict__ ws_w, const uint32_t* __restrict__ ws_m,
-                int8_t* __restrict__ rem_rail, int64_t* __restrict__ rem_off,
+                const uint32_t* __restrict__ ws_w, uint64_t* __restrict__ ws_res,
                 int64_t* __restrict__ send_load, int* err) {
   const int lane = threadIdx.x & 31;
   const long long seg = (long long)blockIdx.x * CHAIN_WARPS + (threadIdx.x >> 5);
@@ -246,32 +253,25 @@ __global__ void __launch_bounds__(CHAIN_WARPS * 32)
   const int r = (int)(nf - q * N);
   const int nr = n_rem[seg];
   const uint32_t* __restrict__ sw = ws_w + seg * NG;
-  const uint32_t* __restrict__ sm = ws_m + seg * NG;
-  int8_t* __restrict__ rr = rem_rail + seg * NG;
-  int64_t* __restrict__ ro = rem_off + seg * NG;
+  uint64_t* __restrict__ res = ws_res + seg * NG;
 
   if (C < (1LL << 26)) {
     // Fast path: relative loads, single redux.sync per step.
     long long base = C * q;  // current minimum load (full-chunk closed form)
     uint32_t rel = (lane < r) ? (uint32_t)C : 0u;
     for (int i0 = 0; i0 < nr; i0 += 32) {
-      uint32_t wv = 0, mv = 0;
-      if (i0 + lane < nr) {
-        wv = sw[i0 + lane];
-        mv = sm[i0 + lane];
-      }
+      uint32_t wv = 0;
+      if (i0 + lane < nr) wv = sw[i0 + lane];
       const int cnt = min(32, nr - i0);
       for (int b = 0; b < cnt; ++b) {
         const uint32_t wb = __shfl_sync(FULL, wv, b);
-        const uint32_t mb = __shfl_sync(FULL, mv, b);
         const uint32_t key = (lane < N) ? ((rel << 5) | (uint32_t)lane) : 0xffffffffu;
         const uint32_t kmin = __reduce_min_sync(FULL, key);
         const int j = (int)(kmin & 31u);
         const uint32_t mrel = kmin >> 5;
         if (lane == j) {
           rel += wb;
-          rr[mb] = (int8_t)j;
-          ro[mb] = base + mrel;
+          res[i0 + b] = pack_res((unsigned)j, base + mrel);
         }
         rel -= mrel;
         base += mrel;
@@ -282,15 +282,11 @@ __global__ void __launch_bounds__(CHAIN_WARPS * 32)
     // General path: 64-bit loads, butterfly argmin over (load, lane).
     long long L = (lane < N) ? C * (q + (lane < r ? 1 : 0)) : LLONG_MAX;
     for (int i0 = 0; i0 < nr; i0 += 32) {
-      uint32_t wv = 0, mv = 0;
-      if (i0 + lane < nr) {
-        wv = sw[i0 + lane];
-        mv = sm[i0 + lane];
-      }
+      uint32_t wv = 0;
+      if (i0 + lane < nr) wv = sw[i0 + lane];
       const int cnt = min(32, nr - i0);
       for (int b = 0; b < cnt; ++b) {
         const uint32_t wb = __shfl_sync(FULL, wv, b);
-        const uint32_t mb = __shfl_sync(FULL, mv, b);
         long long v = L;
         int ix = lane;
 #pragma unroll
@@ -303,8 +299,7 @@ __global__ void __launch_bounds__(CHAIN_WARPS * 32)
           }
         }
         if (lane == ix) {
-          rr[mb] = (int8_t)ix;
-          ro[mb] = v;
+          res[i0 + b] = pack_res((unsigned)ix, v);
           L += wb;
         }
       }
@@ -322,13 +317,11 @@ __global__ void __launch_bounds__(CHAIN_WARPS * 32)
 // rail keys (rel << 5) | rail; the chunk of size w goes to K[0]'s rail (argmin,
 // lowest rail on ties) at offset base + rel, and K[0] + (w << 5) is merged back.
 template <int NT>
-__device__ __forceinline__ void lpt_step(uint32_t (&K)[NT], uint32_t w, uint32_t m,
-                                         long long base, int8_t* __restrict__ rr,
-                                         int64_t* __restrict__ ro) {
+__device__ __forceinline__ void lpt_step(uint32_t (&K)[NT], uint32_t w, uint64_t* __restrict__ res_i,
+                                         long long base) {
   const uint32_t head = K[0];
   const uint32_t x = head + (w << 5);
-  rr[m] = (int8_t)(head & 31u);
-  ro[m] = base + (long long)(head >> 5);
+  *res_i = pack_res(head & 31u, base + (long long)(head >> 5));
   bool cprev = true;
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
@@ -350,6 +343,31 @@ __device__ __forceinline__ void lpt_rebase(uint32_t (&K)[NT], long long& base) {
   }
 }
 
+// Eight consecutive sorted items.  Exact fast path for a run of equal sizes w: if
+// every rail is within w of the minimum (spread < w), LPT deals the next NT items
+// of size w one per rail in the current (load, rail) order -- after k of them the
+// assigned rails sit at >= min + w > every unassigned rail -- and the sorted order
+// is unchanged afterwards, all loads having grown by w.  So 8 equal items (8 a
+// multiple of NT) go to K[p mod NT] at rel + (p div NT)*w and base += (8/NT)*w,
+// with no compare network.  Otherwise: eight network steps.
+template <int NT>
+__device__ __forceinline__ void lpt_group8(uint32_t (&K)[NT], const uint32_t (&w8)[8],
+                                           uint64_t* __restrict__ out, long long& base) {
+  const uint32_t w = w8[0];
+  const uint32_t spread = (K[NT - 1] >> 5) - (K[0] >> 5);
+  if ((8 % NT) == 0 && w8[7] == w && spread < w) {
+#pragma unroll
+    for (int p = 0; p < 8; ++p)
+      out[p] = pack_res(K[p % NT] & 31u,
+                        base + (long long)(K[p % NT] >> 5) + (long long)(p / NT) * w);
+    base += (long long)(8 / NT) * w;
+  } else {
+#pragma unroll
+    for (int p = 0; p < 8; ++p) lpt_step<NT>(K, w8[p], out + p, base);
+  }
+  lpt_rebase<NT>(K, base);
+}
+
 // Few long chains (C3: 64, C5: 256): one chain per warp.  All 32 lanes stream the
 // sorted remainder list through a double-buffered shared-memory stage with
 // coalesced loads, one batch ahead; lane 0 runs the register compare network,
@@ -361,9 +379,8 @@ template <int NT>
 __global__ void __launch_bounds__(WS_WARPS * 32)
     k_lpt_wstage(long long nseg, long long C, long long NG, const int64_t* __restrict__ n_full,
                  const int32_t* __restrict__ n_rem, const uint32_t* __restrict__ ws_w,
-                 const uint32_t* __restrict__ ws_m, int8_t* __restrict__ rem_rail,
-                 int64_t* __restrict__ rem_off, int64_t* __restrict__ send_load) {
-  __shared__ uint32_t sW[WS_WARPS][2][WS_BATCH], sM[WS_WARPS][2][WS_BATCH];
+                 uint64_t* __restrict__ ws_res, int64_t* __restrict__ send_load) {
+  __shared__ uint32_t sW[WS_WARPS][2][WS_BATCH];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const long long seg = (long long)blockIdx.x * WS_WARPS + wid;
   if (seg >= nseg) return;
@@ -372,9 +389,7 @@ __global__ void __launch_bounds__(WS_WARPS * 32)
   const int r = (int)(nf - q * NT);
   const int nr = n_rem[seg];
   const uint32_t* __restrict__ gw = ws_w + seg * NG;
-  const uint32_t* __restrict__ gm = ws_m + seg * NG;
-  int8_t* __restrict__ rr = rem_rail + seg * NG;
-  int64_t* __restrict__ ro = rem_off + seg * NG;
+  uint64_t* __restrict__ res = ws_res + seg * NG;
   long long base = C * q;
   uint32_t K[NT];
 #pragma unroll
@@ -383,60 +398,44 @@ __global__ void __launch_bounds__(WS_WARPS * 32)
     K[i] = (((i < NT - r) ? 0u : (uint32_t)C) << 5) | (uint32_t)rail;
   }
   constexpr int PL = WS_BATCH / 32;
-  uint32_t pw[PL], pm[PL];
+  uint32_t pw[PL];
 #pragma unroll
   for (int p = 0; p < PL; ++p) {
     const int i = p * 32 + lane;
     pw[p] = i < nr ? gw[i] : 0u;
-    pm[p] = i < nr ? gm[i] : 0u;
   }
   int cur = 0;
   for (int b0 = 0; b0 < nr; b0 += WS_BATCH) {
 #pragma unroll
-    for (int p = 0; p < PL; ++p) {
-      sW[wid][cur][p * 32 + lane] = pw[p];
-      sM[wid][cur][p * 32 + lane] = pm[p];
-    }
+    for (int p = 0; p < PL; ++p) sW[wid][cur][p * 32 + lane] = pw[p];
     __syncwarp();
     const int nb = b0 + WS_BATCH;  // prefetch the next batch while lane 0 works
 #pragma unroll
     for (int p = 0; p < PL; ++p) {
       const int i = nb + p * 32 + lane;
       pw[p] = i < nr ? gw[i] : 0u;
-      pm[p] = i < nr ? gm[i] : 0u;
     }
     if (lane == 0) {
       const int cnt = min(WS_BATCH, nr - b0);
       const uint32_t* w_ = sW[wid][cur];
-      const uint32_t* m_ = sM[wid][cur];
+      uint64_t* rb = res + b0;
       // groups of 8 items held in registers, the next group loaded before the
       // current one is assigned (global stores would otherwise order the loads)
       constexpr int GB = 8;
-      uint32_t cw[GB], cm[GB];
+      uint32_t cw[GB];
 #pragma unroll
-      for (int p = 0; p < GB; ++p) {
-        cw[p] = w_[p];
-        cm[p] = m_[p];
-      }
+      for (int p = 0; p < GB; ++p) cw[p] = w_[p];
       int i = 0;
       for (; i + GB <= cnt; i += GB) {
-        uint32_t nw[GB], nm[GB];
+        uint32_t nw[GB];
 #pragma unroll
-        for (int p = 0; p < GB; ++p) {
-          nw[p] = w_[(i + GB + p) & (WS_BATCH - 1)];
-          nm[p] = m_[(i + GB + p) & (WS_BATCH - 1)];
-        }
+        for (int p = 0; p < GB; ++p) nw[p] = w_[(i + GB + p) & (WS_BATCH - 1)];
+        lpt_group8<NT>(K, cw, rb + i, base);
 #pragma unroll
-        for (int p = 0; p < GB; ++p) lpt_step<NT>(K, cw[p], cm[p], base, rr, ro);
-        lpt_rebase<NT>(K, base);
-#pragma unroll
-        for (int p = 0; p < GB; ++p) {
-          cw[p] = nw[p];
-          cm[p] = nm[p];
-        }
+        for (int p = 0; p < GB; ++p) cw[p] = nw[p];
       }
       for (; i < cnt; ++i) {
-        lpt_step<NT>(K, w_[i], m_[i], base, rr, ro);
+        lpt_step<NT>(K, w_[i], rb + i, base);
         lpt_rebase<NT>(K, base);
       }
     }
@@ -464,8 +463,7 @@ template <int NT>
 __global__ void __launch_bounds__(128)
     k_lpt_thread(long long nseg, int cpw, long long C, long long NG,
                  const int64_t* __restrict__ n_full, const int32_t* __restrict__ n_rem,
-                 const uint32_t* __restrict__ ws_w, const uint32_t* __restrict__ ws_m,
-                 int8_t* __restrict__ rem_rail, int64_t* __restrict__ rem_off,
+                 const uint32_t* __restrict__ ws_w, uint64_t* __restrict__ ws_res,
                  int64_t* __restrict__ send_load) {
   const int lane = threadIdx.x & 31;
   const long long gw = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -476,9 +474,7 @@ __global__ void __launch_bounds__(128)
   const int r = (int)(nf - q * NT);
   const int nr = n_rem[seg];
   const uint32_t* __restrict__ sw = ws_w + seg * NG;
-  const uint32_t* __restrict__ sm = ws_m + seg * NG;
-  int8_t* __restrict__ rr = rem_rail + seg * NG;
-  int64_t* __restrict__ ro = rem_off + seg * NG;
+  uint64_t* __restrict__ res = ws_res + seg * NG;
   // full-chunk closed form: rails 0..r-1 hold C*(q+1), the rest C*q.  Sorted by
   // (load, rail): rails r..NT-1 (rel 0) first, then rails 0..r-1 (rel C).
   long long base = C * q;
@@ -498,30 +494,17 @@ __global__ void __launch_bounds__(128)
     o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w;
     o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
   };
-  uint32_t wv[PF], mv[PF];
-  if (PF <= nr) {
-    ld8(sw, wv);
-    ld8(sm, mv);
-  }
+  uint32_t wv[PF];
+  if (PF <= nr) ld8(sw, wv);
   for (; i + PF <= nr; i += PF) {
-    uint32_t wn[PF], mn[PF];  // next batch in flight while this one is assigned
-    if (i + 2 * PF <= nr) {
-      ld8(sw + i + PF, wn);
-      ld8(sm + i + PF, mn);
-    }
+    uint32_t wn[PF];  // next batch in flight while this one is assigned
+    if (i + 2 * PF <= nr) ld8(sw + i + PF, wn);
+    lpt_group8<NT>(K, wv, res + i, base);
 #pragma unroll
-    for (int p = 0; p < PF; ++p) {
-      lpt_step<NT>(K, wv[p], mv[p], base, rr, ro);
-      lpt_rebase<NT>(K, base);
-    }
-#pragma unroll
-    for (int p = 0; p < PF; ++p) {
-      wv[p] = wn[p];
-      mv[p] = mn[p];
-    }
+    for (int p = 0; p < PF; ++p) wv[p] = wn[p];
   }
   for (; i < nr; ++i) {
-    lpt_step<NT>(K, __ldg(sw + i), __ldg(sm + i), base, rr, ro);
+    lpt_step<NT>(K, __ldg(sw + i), res + i, base);
     lpt_rebase<NT>(K, base);
   }
 #pragma unroll
@@ -541,11 +524,35 @@ static int ceil_log2(long long x) {  // bits needed for values 0..x-1
   return b;
 }
 
+// Expand the sorted-order chain results into per-message rem_rail / rem_off,
+// coalesced: message m of segment seg has a remainder iff ws_inv[m] >= 0 (the
+// sorted position written by k_chunk_sort).
+__global__ void __launch_bounds__(256)
+    k_expand_rem(long long NG, const int32_t* __restrict__ ws_inv,
+                 const uint64_t* __restrict__ ws_res, int8_t* __restrict__ rem_rail,
+                 int64_t* __restrict__ rem_off) {
+  const long long seg = blockIdx.y;
+  const long long m = (long long)blockIdx.x * 256 + threadIdx.x;
+  if (m >= NG) return;
+  const int pos = ws_inv[seg * NG + m];
+  int8_t r = -1;
+  long long o = 0;
+  if (pos >= 0) {
+    const uint64_t v = ws_res[seg * NG + pos];
+    r = (int8_t)(v >> 56);
+    o = (long long)(v & (uint64_t)OFF_MASK);
+  }
+  rem_rail[seg * NG + m] = r;
+  rem_off[seg * NG + m] = o;
+}
+
+// workspace: [256 B header][ws_res u64 (nseg*NG)][ws_w u32][ws_m u32][ws_inv i32]
+//            [sort spill scratch when N*G > SORT_SMEM_ITEMS]
 size_t schedule_workspace_bytes(int U, int nd, long long NG) {
   const long long nseg = (long long)U * nd;
-  size_t sorted = (size_t)nseg * NG * 8;  // ws_w + ws_m
+  size_t lists = (size_t)nseg * NG * (8 + 4 + 4 + 4);
   size_t scratch = (NG <= SORT_SMEM_ITEMS) ? 0 : (size_t)nseg * (NG * (8 + 2 * 4) + 64);
-  return 256 + sorted + scratch;
+  return 256 + lists + scratch;
 }
 
 cudaError_t launch_schedule(const LaunchCtx& c, int U, int nd, int d0, int M, int N, long long C,
@@ -556,9 +563,11 @@ cudaError_t launch_schedule(const LaunchCtx& c, int U, int nd, int d0, int M, in
   if ((C & (C - 1)) == 0) cshift = ceil_log2(C);
   const int nbits = ceil_log2(C > 1 ? C - 1 : 1) + 1;
   uint8_t* w8 = (uint8_t*)ws;
-  uint32_t* ws_w = (uint32_t*)(w8 + 256);
+  uint64_t* ws_res = (uint64_t*)(w8 + 256);
+  uint32_t* ws_w = (uint32_t*)(ws_res + nseg * NG);
   uint32_t* ws_m = ws_w + nseg * NG;
-  uint8_t* scratch = (uint8_t*)(ws_m + nseg * NG);
+  int32_t* ws_inv = (int32_t*)(ws_m + nseg * NG);
+  uint8_t* scratch = (uint8_t*)(ws_inv + nseg * NG);
   cudaError_t e;
   if (NG <= SORT_SMEM_ITEMS) {
     const size_t smem = (size_t)NG * (8 + 2 * sizeof(uint16_t));
@@ -568,12 +577,12 @@ cudaError_t launch_schedule(const LaunchCtx& c, int U, int nd, int d0, int M, in
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     kern<<<(unsigned)nseg, small ? 128 : SORT_THREADS, smem, c.stream>>>(
-        msg, NG, N, d0, nd, C, cshift, nbits, s.full_base, s.rem_rail, s.rem_off, s.n_full, s.n_rem, ws_w,
-        ws_m, nullptr, 1, c.err);
+        msg, NG, N, d0, nd, C, cshift, nbits, s.full_base, ws_inv, s.n_full, s.n_rem, ws_w, ws_m,
+        nullptr, 1, c.err);
   } else {
     k_chunk_sort<uint32_t, SORT_THREADS><<<(unsigned)nseg, SORT_THREADS, 0, c.stream>>>(
-        msg, NG, N, d0, nd, C, cshift, nbits, s.full_base, s.rem_rail, s.rem_off, s.n_full, s.n_rem, ws_w,
-        ws_m, scratch, 0, c.err);
+        msg, NG, N, d0, nd, C, cshift, nbits, s.full_base, ws_inv, s.n_full, s.n_rem, ws_w, ws_m,
+        scratch, 0, c.err);
   }
   count_launch(1);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -583,8 +592,7 @@ cudaError_t launch_schedule(const LaunchCtx& c, int U, int nd, int d0, int M, in
 #define RAILS_WS_CHAIN(NT)                                                                  \
   if (N == NT)                                                                              \
     k_lpt_wstage<NT><<<wgrid, WS_WARPS * 32, 0, c.stream>>>(nseg, C, NG, s.n_full, s.n_rem, \
-                                                           ws_w, ws_m, s.rem_rail, s.rem_off, \
-                                                           s.send_load);
+                                                           ws_w, ws_res, s.send_load);
     RAILS_WS_CHAIN(2)
     RAILS_WS_CHAIN(4)
     RAILS_WS_CHAIN(8)
@@ -599,8 +607,7 @@ cudaError_t launch_schedule(const LaunchCtx& c, int U, int nd, int d0, int M, in
 #define RAILS_THREAD_CHAIN(NT)                                                            \
   if (N == NT)                                                                            \
     k_lpt_thread<NT><<<tgrid, 128, 0, c.stream>>>(nseg, (int)cpw, C, NG, s.n_full, s.n_rem, \
-                                                  ws_w, ws_m, s.rem_rail, s.rem_off,      \
-                                                  s.send_load);
+                                                  ws_w, ws_res, s.send_load);
     RAILS_THREAD_CHAIN(2)
     RAILS_THREAD_CHAIN(4)
     RAILS_THREAD_CHAIN(8)
@@ -609,9 +616,12 @@ cudaError_t launch_schedule(const LaunchCtx& c, int U, int nd, int d0, int M, in
   } else {
     const unsigned grid = (unsigned)((nseg + CHAIN_WARPS - 1) / CHAIN_WARPS);
     k_lpt_chain<<<grid, CHAIN_WARPS * 32, 0, c.stream>>>(nseg, N, C, NG, s.n_full, s.n_rem, ws_w,
-                                                         ws_m, s.rem_rail, s.rem_off,
-                                                         s.send_load, c.err);
+                                                         ws_res, s.send_load, c.err);
   }
+  count_launch(1);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  k_expand_rem<<<dim3((unsigned)((NG + 255) / 256), (unsigned)nseg), 256, 0, c.stream>>>(
+      NG, ws_inv, ws_res, s.rem_rail, s.rem_off);
   count_launch(1);
   return cudaGetLastError();
 }

@@ -90,6 +90,9 @@ def test_histogram_range_error_flagged():
     (3, 4, 96, 1, 0, 3, 0.8, 10, 32),                # many equal sizes (ties)
     (2, 1, 4096, 3, 0, 2, 1.0, 100000, 1),           # N = 1
     (300, 8, 4096, 1, 0, 2, 0.9, 50000, 1),          # NG = 19200 > smem: global-scratch sort
+    (6, 8, 1 << 24, 1, 0, 6, 0.8, 1 << 26, 1),       # 2^23 <= C < 2^26: warp relative-key chain
+    (5, 16, 65536, 2, 0, 5, 0.6, 400000, 1),         # N = 16 register-network chain
+    (40, 2, 8192, 30, 0, 40, 0.7, 100000, 1),        # N = 2, 1200 chains (thread chains)
 ])
 def test_schedule_parity(M, N, C, U, d0, nd, p, hi, mult):
     rng = np.random.default_rng(M * 1000 + N * 10 + U)

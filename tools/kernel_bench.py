@@ -70,10 +70,14 @@ def bench_pack(res):
     total = int(pipe.total.item())
     algo = M * N * T * RB + total
     ref = None
-    for impl in ("1", "2", "1cs"):
+    for impl in ("1", "2", "1cs", "1v8", "1v4"):
         os.environ["RAILS_PACK_IMPL"] = impl[0]
+        os.environ.pop("RAILS_PACK_ST", None)
+        os.environ.pop("RAILS_PACK_VPL", None)
         if impl == "1cs":
             os.environ["RAILS_PACK_ST"] = "1"
+        if impl.startswith("1v"):
+            os.environ["RAILS_PACK_VPL"] = impl[2:]
         pipe.out.zero_()
         t = timeit(lambda: rails.pack(pipe.tp, pipe.sh, T, k, x, topk, lut, pipe.rank, pipe.msg, RB,
                                       pipe.sched, pipe.rail_base, pipe.out), flush=False)
@@ -88,6 +92,7 @@ def bench_pack(res):
         del h
     os.environ.pop("RAILS_PACK_IMPL", None)
     os.environ.pop("RAILS_PACK_ST", None)
+    os.environ.pop("RAILS_PACK_VPL", None)
     # context only (NOT the roofline denominator): the same 1-read : 2-write byte
     # mix as the pack, done by a plain torch broadcast copy of every 8 KiB row into
     # two adjacent slots (second read of a row hits L2)
