@@ -199,107 +199,6 @@ __global__ void __launch_bounds__(HW_WARPS * 32)
   }
 }
 
-// ---------------------------------------------------------------- single-read variant
-// Same contract.  One read of the routing: for each 32-entry group of its segment
-// a warp finds equal destinations with a shared-memory tag write/read-back (every
-// lane writes its lane id to tag[h]; a lane that reads back another id, or whose
-// id was overwritten-marked by a loser, has a duplicate) and runs match.any only
-// over the duplicated lanes -- typically none or two, so its cost (which grows
-// with the number of distinct values) stays small.  local rank = warp running
-// count + peers below; (h, local) is packed into shared memory.  After the
-// cross-warp scan, a coalesced pass writes rank = warp base + local.
-constexpr int HIST2_MAX_NE = 16384;
-
-template <int W, int UNR>
-__global__ void __launch_bounds__(W * 32)
-    k_hist_rank2(const int32_t* __restrict__ topk, const int32_t* __restrict__ lut, int n_inst,
-                 int M, int N, int ngs, int d0, int nd, int T, int k, long long RB,
-                 int32_t* __restrict__ counts, int64_t* __restrict__ msg,
-                 int32_t* __restrict__ rank, int* err) {
-  extern __shared__ __align__(16) int32_t sm2[];
-  const int G = M * N;
-  int32_t* cnt = sm2;                                   // [W][G]
-  uint32_t* pk = (uint32_t*)(cnt + W * G);              // [ne]
-  const long long cta = blockIdx.x;
-  const long long ul = cta / ngs;
-  const int d = d0 + (int)(ul % nd);
-  const int ne = T * k;
-  uint8_t* tag = (uint8_t*)(pk + ne);                   // [W][G]
-  const int32_t* __restrict__ src = topk + cta * (long long)ne;
-  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  for (int i = threadIdx.x; i < W * G; i += W * 32) cnt[i] = 0;
-  __syncthreads();
-  const int seg = (((ne + W - 1) / W) + 31) & ~31;
-  const int beg = wid * seg;
-  const int end = min(ne, beg + seg);
-  int32_t* my = cnt + wid * G;
-  uint8_t* tg = tag + wid * G;
-
-  for (int base = beg; base < end; base += 32 * UNR) {
-    int hv[UNR];
-#pragma unroll
-    for (int j = 0; j < UNR; ++j) {
-      const int e = base + j * 32 + lane;
-      hv[j] = (e < end) ? __ldg(src + e) : -1;
-    }
-#pragma unroll
-    for (int j = 0; j < UNR; ++j) {
-      const int e = base + j * 32 + lane;
-      int h = -1;
-      if (e < end) {
-        const int inst = hv[j];
-        if (inst >= 0 && inst < n_inst) {
-          h = __ldg(lut + inst);
-          if (h < 0 || h >= G) h = -1;
-        }
-        if (h < 0) flag_error(err, ERR_RANGE);
-      }
-      const bool valid = h >= 0;
-      if (valid) tg[h] = (uint8_t)lane;
-      __syncwarp();
-      bool dup = false;
-      if (valid) {
-        dup = tg[h] != lane;  // lost the write: someone else has the same h
-      }
-      __syncwarp();
-      if (dup) tg[h] = (uint8_t)(32 | lane);  // tell the winner
-      __syncwarp();
-      if (valid && !dup) dup = tg[h] != lane;
-      const unsigned dmask = __ballot_sync(FULL, dup);
-      unsigned peers = valid ? (1u << lane) : 0u;
-      if (dup) peers = __match_any_sync(dmask, h);
-      int r = 0;
-      if (valid) r = my[h] + __popc(peers & lanemask_lt());
-      __syncwarp();
-      if (valid && lane == __ffs(peers) - 1) my[h] += __popc(peers);
-      __syncwarp();
-      if (e < end) pk[e] = valid ? (((uint32_t)h << 16) | (uint32_t)r) : 0xffffffffu;
-    }
-  }
-  __syncthreads();
-  for (int h = threadIdx.x; h < G; h += W * 32) {
-    int run = 0;
-#pragma unroll
-    for (int w = 0; w < W; ++w) {
-      const int c = cnt[w * G + h];
-      cnt[w * G + h] = run;
-      run += c;
-    }
-    counts[cta * G + h] = run;
-    msg[cta * G + h] = (h / N == d) ? 0LL : (long long)run * RB;
-  }
-  if (rank == nullptr) return;
-  __syncthreads();
-  int32_t* __restrict__ dst = rank + cta * (long long)ne;
-  for (int e = threadIdx.x; e < ne; e += W * 32) {
-    const uint32_t v = pk[e];
-    int r = -1;
-    if (v != 0xffffffffu) r = cnt[(e / seg) * G + (int)(v >> 16)] + (int)(v & 0xffffu);
-    dst[e] = r;
-  }
-}
-
 template <int W, int HB>
 static cudaError_t launch_wh(const LaunchCtx& c, long long grid, int M, int N, int ngs, int d0,
                              int nd,
@@ -360,30 +259,6 @@ cudaError_t launch_histogram(const LaunchCtx& c, int U, int nd, int d0, int M, i
         topk, lut, n_inst, M, N, ngs, d0, nd, T, k, row_bytes, grid, counts, msg, rank, c.err);
     count_launch(1);
     return cudaGetLastError();
-  }
-  if (hv && hv[0] == '2' && ne <= HIST2_MAX_NE && G <= 65535) {
-    // single-read variant: W warps, smem = W*G*4 (counts) + ne*4 (packed) + W*G (tags)
-    int W = 8;
-    while (W > 1 && (size_t)W * G * 5 + ne * 4 > 160 * 1024) W >>= 1;
-    const size_t smem = (size_t)W * G * 4 + (size_t)ne * 4 + (size_t)W * G;
-    if (smem <= 200 * 1024) {
-      cudaError_t e;
-#define RAILS_H2(WW)                                                                        \
-  if (W == WW) {                                                                            \
-    auto kern = k_hist_rank2<WW, 8>;                                                        \
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    if (e != cudaSuccess) return e;                                                         \
-    kern<<<(unsigned)grid, WW * 32, smem, c.stream>>>(topk, lut, n_inst, M, N, ngs, d0, nd, T, k, \
-                                                      row_bytes, counts, msg, rank, c.err); \
-    count_launch(1);                                                                        \
-    return cudaGetLastError();                                                              \
-  }
-      RAILS_H2(8)
-      RAILS_H2(4)
-      RAILS_H2(2)
-      RAILS_H2(1)
-#undef RAILS_H2
-    }
   }
   // Warps per CTA: as many private sub-histograms as fit in 64 KiB (>= 1).
   if (G * 8 * 4 <= 65536)
