@@ -277,13 +277,18 @@ def expert_outputs(shape, seed: int, u: int, device="cpu") -> torch.Tensor:
     n = 1
     for s in shape:
         n *= s
-    idx = torch.arange(n, dtype=torch.int64, device=device)
-    z = mix64_t(idx ^ _s64(sigma))
-    sign = z & 1
-    ex = 119 + (_srl(z, 1) % 11)
-    mant = _srl(z, 8) & 0x7F
-    bits = (sign << 15) | (ex << 7) | mant
-    return (bits - ((bits >> 15) << 16)).to(torch.int16).view(*shape)
+    out = torch.empty(n, dtype=torch.int16, device=device)
+    step = 1 << 26  # bounded int64 temporaries
+    for a in range(0, n, step):
+        b = min(n, a + step)
+        idx = torch.arange(a, b, dtype=torch.int64, device=device)
+        z = mix64_t(idx ^ _s64(sigma))
+        sign = z & 1
+        ex = 119 + (_srl(z, 1) % 11)
+        mant = _srl(z, 8) & 0x7F
+        bits = (sign << 15) | (ex << 7) | mant
+        out[a:b] = (bits - ((bits >> 15) << 16)).to(torch.int16)
+    return out.view(*shape)
 
 
 def gate_weights(shape, seed: int, u: int, device="cpu") -> torch.Tensor:
