@@ -144,7 +144,9 @@ __device__ __forceinline__ T block_reduce_and(T v, T* s) {
 constexpr int SORT_THREADS = 512;
 constexpr int SORT_SMEM_ITEMS = 16384;  // items per CTA kept in shared memory
 
-template <typename IdxT, int THREADS>
+// KeyT: uint16_t when every key C-1-size fits 16 bits (C <= 65536), else uint32_t;
+// IdxT: uint16_t message index when N*G <= 65536.  Smaller items -> more CTAs per SM.
+template <typename KeyT, typename IdxT, int THREADS>
 __global__ void __launch_bounds__(THREADS)
     k_chunk_sort(const int64_t* __restrict__ msg, long long NG, int N, int d0, int nd,
                  long long C, int cshift, int nbits, int64_t* __restrict__ full_base,
@@ -164,12 +166,12 @@ __global__ void __launch_bounds__(THREADS)
   const long long G = NG / N;
   const int d = d0 + (int)(seg % nd);
 
-  uint32_t *kA, *kB;
+  KeyT *kA, *kB;
   IdxT *iA, *iB;
   {
     const long long cap = NG;
     uint8_t* base = use_smem ? smem : (ws_scratch + seg * (cap * (8 + 2 * sizeof(IdxT)) + 64));
-    kA = (uint32_t*)base;
+    kA = (KeyT*)base;
     kB = kA + cap;
     iA = (IdxT*)(kB + cap);
     iB = iA + cap;
@@ -177,7 +179,7 @@ __global__ void __launch_bounds__(THREADS)
 
   long long carry_full = 0;
   int carry_rem = 0;
-  uint32_t kor = 0, kand = 0xffffffffu;
+  KeyT kor = 0, kand = (KeyT)~(KeyT)0;
   for (long long t0 = 0; t0 < NG; t0 += THREADS) {
     const long long m = t0 + threadIdx.x;
     long long B = 0;
@@ -199,7 +201,7 @@ __global__ void __launch_bounds__(THREADS)
       full_base[seg * NG + m] = carry_full + (ex >> 16);
       if (fl) {
         const int pos = carry_rem + (int)(ex & 0xffff);
-        const uint32_t key = (uint32_t)(C - 1 - rem);
+        const KeyT key = (KeyT)(C - 1 - rem);
         kA[pos] = key;
         iA[pos] = (IdxT)m;
         kor |= key;
@@ -211,16 +213,16 @@ __global__ void __launch_bounds__(THREADS)
     carry_full += tot >> 16;
     carry_rem += (int)(tot & 0xffff);
   }
-  kor = block_reduce_or(kor, red32);
-  kand = block_reduce_and(kand, red32);
+  kor = (KeyT)block_reduce_or((uint32_t)kor, red32);
+  kand = (KeyT)block_reduce_and((uint32_t)kand, red32);
   if (threadIdx.x == 0) {
     n_full_out[seg] = carry_full;
     n_rem_out[seg] = carry_rem;
   }
   __syncthreads();
   const int n = carry_rem;
-  const int which = radix_sort<uint32_t, IdxT>(kA, iA, kB, iB, n, kor, kand, nbits, hist, sc);
-  const uint32_t* ks = which ? kB : kA;
+  const int which = radix_sort<KeyT, IdxT>(kA, iA, kB, iB, n, kor, kand, nbits, hist, sc);
+  const KeyT* ks = which ? kB : kA;
   const IdxT* is = which ? iB : iA;
   for (int i = threadIdx.x; i < n; i += THREADS) {
     ws_w[seg * NG + i] = (uint32_t)(C - 1 - (long long)ks[i]);
@@ -570,17 +572,29 @@ cudaError_t launch_schedule(const LaunchCtx& c, int U, int nd, int d0, int M, in
   uint8_t* scratch = (uint8_t*)(ws_inv + nseg * NG);
   cudaError_t e;
   if (NG <= SORT_SMEM_ITEMS) {
-    const size_t smem = (size_t)NG * (8 + 2 * sizeof(uint16_t));
-    // small segments: 128-thread CTAs, many resident per SM; large: 512 threads
-    const bool small = NG <= 2048;
-    auto kern = small ? k_chunk_sort<uint16_t, 128> : k_chunk_sort<uint16_t, SORT_THREADS>;
+    // CTA size by segment size (128 / 256 / 512 threads) and 16-bit keys when
+    // C <= 65536, so that several CTAs fit per SM (shared memory per item: 2 keys
+    // + 2 indices).
+    const bool k16 = C <= 65536;
+    const size_t smem = (size_t)NG * (2 * (k16 ? 2 : 4) + 2 * sizeof(uint16_t));
+    const int thr = NG <= 2048 ? 128 : (NG <= 8192 ? 256 : SORT_THREADS);
+    void (*kern)(const int64_t*, long long, int, int, int, long long, int, int, int64_t*,
+                 int32_t*, int64_t*, int32_t*, uint32_t*, uint32_t*, uint8_t*, int, int*);
+    if (k16)
+      kern = thr == 128 ? k_chunk_sort<uint16_t, uint16_t, 128>
+           : thr == 256 ? k_chunk_sort<uint16_t, uint16_t, 256>
+                        : k_chunk_sort<uint16_t, uint16_t, SORT_THREADS>;
+    else
+      kern = thr == 128 ? k_chunk_sort<uint32_t, uint16_t, 128>
+           : thr == 256 ? k_chunk_sort<uint32_t, uint16_t, 256>
+                        : k_chunk_sort<uint32_t, uint16_t, SORT_THREADS>;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<(unsigned)nseg, small ? 128 : SORT_THREADS, smem, c.stream>>>(
+    kern<<<(unsigned)nseg, thr, smem, c.stream>>>(
         msg, NG, N, d0, nd, C, cshift, nbits, s.full_base, ws_inv, s.n_full, s.n_rem, ws_w, ws_m,
         nullptr, 1, c.err);
   } else {
-    k_chunk_sort<uint32_t, SORT_THREADS><<<(unsigned)nseg, SORT_THREADS, 0, c.stream>>>(
+    k_chunk_sort<uint32_t, uint32_t, SORT_THREADS><<<(unsigned)nseg, SORT_THREADS, 0, c.stream>>>(
         msg, NG, N, d0, nd, C, cshift, nbits, s.full_base, ws_inv, s.n_full, s.n_rem, ws_w, ws_m,
         scratch, 0, c.err);
   }
