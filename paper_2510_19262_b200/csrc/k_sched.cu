@@ -352,6 +352,49 @@ __device__ __forceinline__ void lpt_rebase(uint32_t (&K)[NT], long long& base) {
 // is unchanged afterwards, all loads having grown by w.  So 8 equal items (8 a
 // multiple of NT) go to K[p mod NT] at rel + (p div NT)*w and base += (8/NT)*w,
 // with no compare network.  Otherwise: eight network steps.
+__device__ __forceinline__ void cas_u32(uint32_t& a, uint32_t& b) {
+  const uint32_t lo = min(a, b), hi = max(a, b);
+  a = lo;
+  b = hi;
+}
+
+// NT = 8, 8 equal items, w <= spread < 2w.  The picks are the 8 smallest slots
+// (value, rail) among every rail's next slots rel + t*w; a rail's third slot is at
+// >= min + 2w > max, so the 8 smallest lie in {K_i} U {K_i + w}: a bitonic
+// half-cleaner (K ascending against K + w descending) selects them, an 8-wide
+// bitonic merge orders them.  K_i was taken iff K_i < K_{7-i} + w, and K_i + w iff
+// K_i + w < K_{7-i}; the new keys K_i + (takes)*w are re-sorted (Batcher, 19 CAS).
+__device__ __forceinline__ void lpt_merge8(uint32_t (&K)[8], uint32_t w,
+                                           uint64_t* __restrict__ out, long long base) {
+  const uint32_t W = w << 5;
+  uint32_t L[8];
+  int c[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t a = K[i], b = K[7 - i] + W;
+    L[i] = min(a, b);
+    c[i] = (a < b) ? 1 : 0;  // K_i taken
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) c[i] += (K[i] + W < K[7 - i]) ? 1 : 0;  // K_i + w taken
+  // L is bitonic: merge 8
+#pragma unroll
+  for (int i = 0; i < 4; ++i) cas_u32(L[i], L[i + 4]);
+  cas_u32(L[0], L[2]); cas_u32(L[1], L[3]); cas_u32(L[4], L[6]); cas_u32(L[5], L[7]);
+  cas_u32(L[0], L[1]); cas_u32(L[2], L[3]); cas_u32(L[4], L[5]); cas_u32(L[6], L[7]);
+#pragma unroll
+  for (int p = 0; p < 8; ++p) out[p] = pack_res(L[p] & 31u, base + (long long)(L[p] >> 5));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) K[i] += (uint32_t)c[i] * W;
+  // Batcher odd-even merge sort of 8
+  cas_u32(K[0], K[1]); cas_u32(K[2], K[3]); cas_u32(K[4], K[5]); cas_u32(K[6], K[7]);
+  cas_u32(K[0], K[2]); cas_u32(K[1], K[3]); cas_u32(K[4], K[6]); cas_u32(K[5], K[7]);
+  cas_u32(K[1], K[2]); cas_u32(K[5], K[6]);
+  cas_u32(K[0], K[4]); cas_u32(K[1], K[5]); cas_u32(K[2], K[6]); cas_u32(K[3], K[7]);
+  cas_u32(K[2], K[4]); cas_u32(K[3], K[5]);
+  cas_u32(K[1], K[2]); cas_u32(K[3], K[4]); cas_u32(K[5], K[6]);
+}
+
 template <int NT>
 __device__ __forceinline__ void lpt_group8(uint32_t (&K)[NT], const uint32_t (&w8)[8],
                                            uint64_t* __restrict__ out, long long& base) {
@@ -363,6 +406,8 @@ __device__ __forceinline__ void lpt_group8(uint32_t (&K)[NT], const uint32_t (&w
       out[p] = pack_res(K[p % NT] & 31u,
                         base + (long long)(K[p % NT] >> 5) + (long long)(p / NT) * w);
     base += (long long)(8 / NT) * w;
+  } else if (NT == 8 && w8[7] == w && spread < 2 * w) {
+    lpt_merge8(reinterpret_cast<uint32_t(&)[8]>(K), w, out, base);
   } else {
 #pragma unroll
     for (int p = 0; p < 8; ++p) lpt_step<NT>(K, w8[p], out + p, base);

@@ -56,3 +56,26 @@ def test_equal_run_cyclic_when_spread_below_w():
                 hits += 1
             p += N
     assert hits > 100
+
+
+def test_equal_run_merge_when_spread_below_2w():
+    # N = 8, 8 equal items, spread < 2w: the picks are the 8 smallest (load, rail)
+    # slots among {L_j, L_j + w} (lpt_merge8), checked against plain Alg. 2
+    rng = np.random.default_rng(3)
+    hits = 0
+    for _ in range(1500):
+        N = 8
+        big = list(rng.integers(60, 500, size=int(rng.integers(0, 25))))
+        wr = int(rng.integers(5, 60))
+        w = np.array(sorted(big, reverse=True) + [wr] * 8, np.int64)
+        order, rail, off, load = oracle.lpt(w, N)
+        before = _replay_loads(w, N, order, rail)
+        Lb = before[len(big)]
+        if not (Lb.max() - Lb.min() < 2 * wr):
+            continue
+        cand = sorted([(int(Lb[j]), j) for j in range(N)] + [(int(Lb[j]) + wr, j) for j in range(N)])
+        picks = cand[:8]
+        got = [(int(off[order[len(big) + t]]), int(rail[order[len(big) + t]])) for t in range(8)]
+        assert got == picks
+        hits += 1
+    assert hits > 100
