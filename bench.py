@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-ring", action="store_true",
+                    help="force the pinned-ring staging of the payload (testing)")
     ap.add_argument("--nd", type=int, default=None,
                     help="nodes per rank override (profiling runs only; not a bench line)")
     return ap.parse_args()
@@ -311,6 +313,12 @@ def main():
     quality = {"T_lpt_over_Tstar": float((fin["T"] / fin["T_star"]).max()),
                "T_ecmp_over_Tstar": float((fin["T_e"] / fin["T_star"]).max()),
                "busbw_lpt_over_ecmp": float((fin["busbw"] / fin["busbw_e"]).min())}
+    # per-node send makespan over the mean rail load (an upper bound on makespan/OPT,
+    # since OPT >= ceil(sum/N)); report-side arithmetic on the kernels' S
+    S = pipe.ev.S.double()
+    tot = S.sum(-1)
+    mk = torch.where(tot > 0, S.amax(-1) / torch.ceil(tot / N).clamp(min=1), torch.ones_like(tot))
+    quality["node_makespan_over_mean_max"] = float(mk.max())
     if cfg["kind"] == "routing":
         tokens = U * nd * N * T
         pack_bytes = tokens * RB + int(pipe.total.item())  # read each row once + write copies
@@ -371,7 +379,8 @@ def e2e(args, cfg, pipe, rails, stream, dist, world, env):
         topk, x, lut = env["topk"], env["x"], env["lut"]
         need = topk.numel() * 4 + x.numel() * 8
         local_ranks = int(os.environ.get("LOCAL_WORLD_SIZE", world))
-        full_copy = psutil.virtual_memory().available > 2.0 * need * local_ranks
+        full_copy = (psutil.virtual_memory().available > 2.0 * need * local_ranks
+                     and not args.e2e_ring)
         h_topk = torch.empty(topk.shape, dtype=topk.dtype, pin_memory=True)
         h_topk.copy_(topk)
         xs = x.view(-1, x.shape[-2], x.shape[-1])  # [U*nd*N][T][W]: one GPU's rows per slice

@@ -319,11 +319,10 @@ __global__ void __launch_bounds__(CHAIN_WARPS * 32)
 // rail keys (rel << 5) | rail; the chunk of size w goes to K[0]'s rail (argmin,
 // lowest rail on ties) at offset base + rel, and K[0] + (w << 5) is merged back.
 template <int NT>
-__device__ __forceinline__ void lpt_step(uint32_t (&K)[NT], uint32_t w, uint64_t* __restrict__ res_i,
-                                         long long base) {
+__device__ __forceinline__ uint64_t lpt_step_v(uint32_t (&K)[NT], uint32_t w, long long base) {
   const uint32_t head = K[0];
   const uint32_t x = head + (w << 5);
-  *res_i = pack_res(head & 31u, base + (long long)(head >> 5));
+  const uint64_t res = pack_res(head & 31u, base + (long long)(head >> 5));
   bool cprev = true;
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
@@ -333,6 +332,20 @@ __device__ __forceinline__ void lpt_step(uint32_t (&K)[NT], uint32_t w, uint64_t
     K[j] = c ? a : (cprev ? x : b);
     cprev = c;
   }
+  return res;
+}
+
+template <int NT>
+__device__ __forceinline__ void lpt_step(uint32_t (&K)[NT], uint32_t w, uint64_t* __restrict__ res_i,
+                                         long long base) {
+  *res_i = lpt_step_v<NT>(K, w, base);
+}
+
+// eight packed results -> four 16-byte stores (out is 64-byte aligned)
+__device__ __forceinline__ void store8(uint64_t* __restrict__ out, const uint64_t (&r)[8]) {
+  ulonglong2* o = reinterpret_cast<ulonglong2*>(out);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) o[q] = make_ulonglong2(r[2 * q], r[2 * q + 1]);
 }
 
 template <int NT>
@@ -400,18 +413,20 @@ __device__ __forceinline__ void lpt_group8(uint32_t (&K)[NT], const uint32_t (&w
                                            uint64_t* __restrict__ out, long long& base) {
   const uint32_t w = w8[0];
   const uint32_t spread = (K[NT - 1] >> 5) - (K[0] >> 5);
+  uint64_t r[8];
   if ((8 % NT) == 0 && w8[7] == w && spread < w) {
 #pragma unroll
     for (int p = 0; p < 8; ++p)
-      out[p] = pack_res(K[p % NT] & 31u,
-                        base + (long long)(K[p % NT] >> 5) + (long long)(p / NT) * w);
+      r[p] = pack_res(K[p % NT] & 31u,
+                      base + (long long)(K[p % NT] >> 5) + (long long)(p / NT) * w);
     base += (long long)(8 / NT) * w;
   } else if (NT == 8 && w8[7] == w && spread < 2 * w) {
-    lpt_merge8(reinterpret_cast<uint32_t(&)[8]>(K), w, out, base);
+    lpt_merge8(reinterpret_cast<uint32_t(&)[8]>(K), w, r, base);
   } else {
 #pragma unroll
-    for (int p = 0; p < 8; ++p) lpt_step<NT>(K, w8[p], out + p, base);
+    for (int p = 0; p < 8; ++p) r[p] = lpt_step_v<NT>(K, w8[p], base);
   }
+  store8(out, r);
   lpt_rebase<NT>(K, base);
 }
 
