@@ -359,10 +359,11 @@ __device__ __forceinline__ void lpt_rebase(uint32_t (&K)[NT], long long& base) {
 }
 
 // Eight consecutive sorted items.  Exact fast path for a run of equal sizes w: if
-// every rail is within w of the minimum (spread < w), LPT deals the next NT items
-// of size w one per rail in the current (load, rail) order -- after k of them the
-// assigned rails sit at >= min + w > every unassigned rail -- and the sorted order
-// is unchanged afterwards, all loads having grown by w.  So 8 equal items (8 a
+// the largest key is below the smallest key plus w, compared as (load, rail) keys
+// (K[NT-1] - K[0] < w << 5), LPT deals the next NT items of size w one per rail in
+// the current (load, rail) order -- after k of them the assigned rails sit at keys
+// K_i + (w << 5) > K[NT-1] >= every unassigned key -- and the sorted order is
+// unchanged afterwards, all loads having grown by w.  So 8 equal items (8 a
 // multiple of NT) go to K[p mod NT] at rel + (p div NT)*w and base += (8/NT)*w,
 // with no compare network.  Otherwise: eight network steps.
 __device__ __forceinline__ void cas_u32(uint32_t& a, uint32_t& b) {
@@ -371,9 +372,10 @@ __device__ __forceinline__ void cas_u32(uint32_t& a, uint32_t& b) {
   b = hi;
 }
 
-// NT = 8, 8 equal items, w <= spread < 2w.  The picks are the 8 smallest slots
-// (value, rail) among every rail's next slots rel + t*w; a rail's third slot is at
-// >= min + 2w > max, so the 8 smallest lie in {K_i} U {K_i + w}: a bitonic
+// NT = 8, 8 equal items, key spread K[7] - K[0] < 2w << 5.  The picks are the 8
+// smallest slots (value, rail) among every rail's next slots rel + t*w; a rail's
+// third slot is at key >= K[0] + 2(w << 5) > K[7], so the 8 smallest lie in
+// {K_i} U {K_i + w}: a bitonic
 // half-cleaner (K ascending against K + w descending) selects them, an 8-wide
 // bitonic merge orders them.  K_i was taken iff K_i < K_{7-i} + w, and K_i + w iff
 // K_i + w < K_{7-i}; the new keys K_i + (takes)*w are re-sorted (Batcher, 19 CAS).
@@ -408,32 +410,69 @@ __device__ __forceinline__ void lpt_merge8(uint32_t (&K)[8], uint32_t w,
   cas_u32(K[1], K[2]); cas_u32(K[3], K[4]); cas_u32(K[5], K[6]);
 }
 
+// Keys stay below 2^32: rel < 2^23 after a rebase, spread < 2w < 2^24 on the fast
+// paths, at most 8 network steps between rebases (C < 2^23).
 template <int NT>
-__device__ __forceinline__ void lpt_group8(uint32_t (&K)[NT], const uint32_t (&w8)[8],
-                                           uint64_t* __restrict__ out, long long& base) {
+__device__ __forceinline__ void lpt_group8_v(uint32_t (&K)[NT], const uint32_t (&w8)[8],
+                                             uint64_t (&r)[8], long long& base) {
   const uint32_t w = w8[0];
-  const uint32_t spread = (K[NT - 1] >> 5) - (K[0] >> 5);
-  uint64_t r[8];
-  if ((8 % NT) == 0 && w8[7] == w && spread < w) {
+  const uint32_t kspread = K[NT - 1] - K[0];
+  if ((8 % NT) == 0 && w8[7] == w && kspread < (w << 5)) {
 #pragma unroll
     for (int p = 0; p < 8; ++p)
       r[p] = pack_res(K[p % NT] & 31u,
                       base + (long long)(K[p % NT] >> 5) + (long long)(p / NT) * w);
     base += (long long)(8 / NT) * w;
-  } else if (NT == 8 && w8[7] == w && spread < 2 * w) {
+  } else if (NT == 8 && w8[7] == w && kspread < (w << 6)) {
     lpt_merge8(reinterpret_cast<uint32_t(&)[8]>(K), w, r, base);
   } else {
 #pragma unroll
     for (int p = 0; p < 8; ++p) r[p] = lpt_step_v<NT>(K, w8[p], base);
   }
+  lpt_rebase<NT>(K, base);
+}
+
+template <int NT>
+__device__ __forceinline__ void lpt_group8(uint32_t (&K)[NT], const uint32_t (&w8)[8],
+                                           uint64_t* __restrict__ out, long long& base) {
+  uint64_t r[8];
+  lpt_group8_v<NT>(K, w8, r, base);
   store8(out, r);
+}
+
+// A whole run of n equal sizes w once K[NT-1] - K[0] < w << 5 (the cyclic case
+// above, repeated): item t of the run goes to K[t mod NT] at rel + (t div NT)*w,
+// so the warp writes the run in parallel, lane l taking t = l, l + 32, ... (NT
+// divides 32, so t mod NT = l mod NT).  Afterwards rail K_i carries
+// q = n div NT more items, plus one for i < n mod NT: the sorted keys become
+// K[rr..NT-1] + q*w, K[0..rr-1] + (q+1)*w (still sorted, spread still < w).
+template <int NT>
+__device__ __forceinline__ void lpt_run_cyclic(uint32_t (&K)[NT], uint32_t w, int n, int lane,
+                                               uint64_t* __restrict__ out, long long& base) {
+  uint32_t kl = K[0];
+#pragma unroll
+  for (int j = 1; j < NT; ++j)
+    if ((lane % NT) == j) kl = K[j];
+  const long long lb = base + (long long)(kl >> 5);
+  for (int t = lane; t < n; t += 32) out[t] = pack_res(kl & 31u, lb + (long long)(t / NT) * w);
+  base += (long long)(n / NT) * w;
+  const uint32_t W = w << 5;
+  for (int s = n % NT; s > 0; --s) {
+    const uint32_t h = K[0] + W;
+#pragma unroll
+    for (int j = 0; j < NT - 1; ++j) K[j] = K[j + 1];
+    K[NT - 1] = h;
+  }
   lpt_rebase<NT>(K, base);
 }
 
 // Few long chains (C3: 64, C5: 256): one chain per warp.  All 32 lanes stream the
 // sorted remainder list through a double-buffered shared-memory stage with
-// coalesced loads, one batch ahead; lane 0 runs the register compare network,
-// so the serial chain never waits on global memory.
+// coalesced loads, one batch ahead, and all run the same (warp-uniform) register
+// state.  A run of >= 32 equal sizes -- routing traffic has only C / row_bytes
+// distinct remainder sizes -- is assigned by single network steps until the
+// cyclic condition holds, then written by the whole warp (lpt_run_cyclic); other
+// items go eight at a time through lpt_group8_v with lane 0 storing.
 constexpr int WS_WARPS = 4;
 constexpr int WS_BATCH = 256;
 
@@ -468,37 +507,103 @@ __global__ void __launch_bounds__(WS_WARPS * 32)
   }
   int cur = 0;
   for (int b0 = 0; b0 < nr; b0 += WS_BATCH) {
+    uint32_t cw[PL];
 #pragma unroll
-    for (int p = 0; p < PL; ++p) sW[wid][cur][p * 32 + lane] = pw[p];
+    for (int p = 0; p < PL; ++p) {
+      sW[wid][cur][p * 32 + lane] = pw[p];
+      cw[p] = pw[p];
+    }
     __syncwarp();
-    const int nb = b0 + WS_BATCH;  // prefetch the next batch while lane 0 works
+    const int nb = b0 + WS_BATCH;  // prefetch the next batch while this one is assigned
 #pragma unroll
     for (int p = 0; p < PL; ++p) {
       const int i = nb + p * 32 + lane;
       pw[p] = i < nr ? gw[i] : 0u;
     }
-    if (lane == 0) {
-      const int cnt = min(WS_BATCH, nr - b0);
-      const uint32_t* w_ = sW[wid][cur];
-      uint64_t* rb = res + b0;
-      // groups of 8 items held in registers, the next group loaded before the
-      // current one is assigned (global stores would otherwise order the loads)
-      constexpr int GB = 8;
-      uint32_t cw[GB];
+    const int cnt = min(WS_BATCH, nr - b0);
+    const uint32_t* w_ = sW[wid][cur];
+    uint64_t* rb = res + b0;
+    // the next group's sizes (and the size 31 ahead, the run test) are read from
+    // shared memory before the current group is assigned
+    uint32_t w8[8], w31;
+    auto load8 = [&](int at) {
 #pragma unroll
-      for (int p = 0; p < GB; ++p) cw[p] = w_[p];
-      int i = 0;
-      for (; i + GB <= cnt; i += GB) {
-        uint32_t nw[GB];
+      for (int p = 0; p < 8; ++p) w8[p] = w_[(at + p) & (WS_BATCH - 1)];
+      w31 = w_[(at + 31) & (WS_BATCH - 1)];
+    };
+    int i = 0;
+    load8(0);
+    while (i < cnt) {
+      const uint32_t w = w8[0];
+      if (i + 32 <= cnt && w31 == w) {
+        // run [i, e) of equal sizes inside this batch (the list is sorted, so the
+        // equal entries at or after i are contiguous)
+        int e = i;
 #pragma unroll
-        for (int p = 0; p < GB; ++p) nw[p] = w_[(i + GB + p) & (WS_BATCH - 1)];
-        lpt_group8<NT>(K, cw, rb + i, base);
+        for (int p = 0; p < PL; ++p) {
+          const int j = p * 32 + lane;
+          e += __popc(__ballot_sync(0xffffffffu, j >= i && j < cnt && cw[p] == w));
+        }
+        while (i < e && K[NT - 1] - K[0] >= (w << 5)) {
+          const uint64_t r = lpt_step_v<NT>(K, w, base);
+          if (lane == 0) rb[i] = r;
+          lpt_rebase<NT>(K, base);
+          ++i;
+        }
+        if (i < e) lpt_run_cyclic<NT>(K, w, e - i, lane, rb + i, base);
+        i = e;
+        load8(i);
+      } else if ((8 % NT) == 0 && (i & 7) == 0 && i + 8 <= cnt && w8[7] == w &&
+                 K[NT - 1] - K[0] < (w << 5)) {
+        // window of up to 32 aligned groups, lane l taking group i + 8l: while
+        // every group is 8 equal sizes w_l with K[NT-1] - K[0] < w_l << 5, each is
+        // dealt cyclically, K is unchanged and base grows by (8/NT)*w_l, so the
+        // groups' bases are an exclusive scan of those increments
+        const int at = i + 8 * lane;
+        uint32_t a = 0, b = 0;
+        if (at + 8 <= cnt) {
+          a = w_[at];
+          b = w_[at + 7];
+        }
+        const bool ok = at + 8 <= cnt && a == b && K[NT - 1] - K[0] < (a << 5);
+        const unsigned bad = __ballot_sync(0xffffffffu, !ok);
+        const int nok = bad ? __ffs(bad) - 1 : 32;  // >= 1: lane 0's group passed above
+        const uint32_t inc = lane < nok ? (uint32_t)(8 / NT) * a : 0u;
+        uint32_t ex = inc;
 #pragma unroll
-        for (int p = 0; p < GB; ++p) cw[p] = nw[p];
-      }
-      for (; i < cnt; ++i) {
-        lpt_step<NT>(K, w_[i], rb + i, base);
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t t = __shfl_up_sync(0xffffffffu, ex, o);
+          if (lane >= o) ex += t;
+        }
+        const uint32_t tot = __shfl_sync(0xffffffffu, ex, 31);
+        ex -= inc;
+        if (lane < nok) {
+          uint64_t r[8];
+          const long long bl = base + (long long)ex;
+#pragma unroll
+          for (int p = 0; p < 8; ++p)
+            r[p] = pack_res(K[p % NT] & 31u,
+                            bl + (long long)(K[p % NT] >> 5) + (long long)(p / NT) * a);
+          store8(rb + at, r);
+        }
+        base += (long long)tot;
+        i += 8 * nok;
+        load8(i);
+      } else if (i + 8 <= cnt && (i & 7) == 0) {
+        uint32_t g8[8];
+        uint64_t r[8];
+#pragma unroll
+        for (int p = 0; p < 8; ++p) g8[p] = w8[p];
+        load8(i + 8);
+        lpt_group8_v<NT>(K, g8, r, base);
+        if (lane == 0) store8(rb + i, r);
+        i += 8;
+      } else {
+        const uint64_t r = lpt_step_v<NT>(K, w, base);
+        if (lane == 0) rb[i] = r;
         lpt_rebase<NT>(K, base);
+        ++i;
+        load8(i);
       }
     }
     __syncwarp();

@@ -105,6 +105,40 @@ def test_schedule_parity(M, N, C, U, d0, nd, p, hi, mult):
             compare_schedule(s, u, dl, oracle.schedule_node(msg[u, dl], C), f"u{u} d{dl}")
 
 
+@pytest.mark.parametrize("M,N,U,RB,C,outliers", [
+    (64, 8, 1, 12288, 32768, 0),     # C4 rows: 7 remainder sizes, runs span batches
+    (64, 8, 1, 8192, 32768, 6),      # C3 rows: 3 sizes, a few odd sizes break runs
+    (40, 4, 2, 12288, 32768, 3),     # N = 4
+    (30, 16, 1, 4096, 65536, 2),     # N = 16 (no 8-item cyclic group, run path only)
+    (50, 2, 1, 3000, 32768, 4),      # N = 2, 11 sizes
+    (40, 8, 32, 12288, 32768, 2),    # 1280 chains: thread-per-chain kernel
+    (64, 8, 1, 0, 4096, 0),          # RB = 0: size depends on the destination only,
+    (64, 4, 1, 0, 65536, 3),         # so aligned groups of N equal sizes (C5-like)
+    (64, 2, 1, 0, 1 << 20, 0),       # -> the warp-scan window path
+])
+def test_schedule_parity_equal_runs(M, N, U, RB, C, outliers):
+    # routing-like traffic (row multiples) makes long runs of equal remainder sizes:
+    # the cyclic run path (lpt_run_cyclic) and its single-step transients
+    rng = np.random.default_rng(M * 7 + N + U)
+    G = M * N
+    if RB:
+        msg = rng.integers(0, 40, size=(U, M, N, G)).astype(np.int64) * RB
+        msg *= rng.random((U, M, N, G)) < 0.9
+    else:
+        col = rng.integers(1, 1 << 24, size=(U, M, 1, G)).astype(np.int64)
+        msg = np.repeat(col, N, axis=2)
+        RB = 1
+    for _ in range(outliers * U * M):
+        u, d, g, h = (int(rng.integers(0, x)) for x in (U, M, N, G))
+        msg[u, d, g, h] = int(rng.integers(1, 40 * RB))
+    for d in range(M):
+        msg[:, d, :, d * N:(d + 1) * N] = 0
+    s = rails.lpt_schedule(rails.topo(M, N, C), rails.shard(U, 0, M), torch.from_numpy(msg).to(DEV))
+    for u in range(U):
+        for d in range(M):
+            compare_schedule(s, u, d, oracle.schedule_node(msg[u, d], C), f"u{u} d{d}")
+
+
 def test_schedule_general_path_large_chunks():
     # C >= 2^26 uses the 64-bit argmin chain
     rng = np.random.default_rng(5)
