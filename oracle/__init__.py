@@ -326,3 +326,34 @@ def unpack_combine(M, N, d, g, T, k, RB, C, topk_g, lut, rank_g, w_g, y_node_d, 
     if rc != 0:
         raise RuntimeError(f"oracle unpack failed rc={rc}")
     return out
+
+
+# ------------------------------------------------------------------ NEXT f2 (QP map)
+def qp_map(order, rail, N, qps_per_rail):
+    """Alg. 2 step 4 (R#34): per-rail round-robin QP index of every chunk,
+    visiting chunks in assignment order (order from lpt())."""
+    L = lib()
+    L.orc_qp_map.restype = ctypes.c_int
+    L.orc_qp_map.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
+                             ctypes.c_int64, ctypes.c_void_p]
+    order = _c(order, np.int64)
+    rail = _c(rail, np.int32)
+    qp = np.zeros(len(order), np.int64)
+    rc = L.orc_qp_map(len(order), N, _p(order), _p(rail), qps_per_rail, _p(qp))
+    if rc != 0:
+        raise ValueError(f"oracle qp_map rc={rc}")
+    return qp
+
+
+def rem_qp_node(msg_node, C, qps_per_rail, sched=None):
+    """QP index of each message's remainder chunk, -1 if none: int64 [N][G]."""
+    msg_node = _c(msg_node, np.int64)
+    N, G = msg_node.shape
+    s = schedule_node(msg_node, C) if sched is None else sched
+    qp = qp_map(s["order"], s["rail"], N, qps_per_rail)
+    ch = s["chunks"]
+    out = np.full((N, G), -1, np.int64)
+    for i in range(len(ch["size"])):
+        if ch["size"][i] < C:
+            out[ch["g"][i], ch["h"][i]] = qp[i]
+    return out, qp

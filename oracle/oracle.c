@@ -30,6 +30,8 @@
  *   orc_pack_node       rail buffers by definition (R#18-R#20): message byte
  *                       stream = concatenation of rows in (t,s) order, chunk c of
  *                       message (g,h) copied to rail[j] + offset.
+ *   orc_qp_map          NEXT f2: Alg. 2 step 4 round-robin QP index
+ *                       per rail in assignment order (R#34).
  *
  * Parity pins live in tests/test_oracle_pins.py (worked examples from the paper /
  * SPEC, closed forms, invariants and brute force).  The ECMP hash is this build's
@@ -478,5 +480,29 @@ int orc_unpack_combine(int32_t M, int32_t N, int32_t d, int32_t g, int32_t T, in
         }
     }
     free(row);
+    return ORC_OK;
+}
+
+/* ================================================================ NEXT f2: QP map */
+/* Alg. 2 step 4: "For each assignment (w_i, j*): select port p from
+ * NIC j* by round-robin; map (j*, p) to a QP in NIC's QP set; bind w_i to the
+ * chosen QP."  Reading R#34: one counter per rail, reset with the
+ * LoadState at the start of the all-to-all round; the assignments are
+ * visited in Step-3 order, and the chunk gets the rail's counter modulo
+ * qps_per_rail, then the counter advances.
+ *   order[p] = index of the p-th assigned chunk (orc_lpt), rail[i] = its rail;
+ *   qp[i] = QP index of chunk i in [0, qps_per_rail). */
+int orc_qp_map(int64_t F, int32_t N, const int64_t *order, const int32_t *rail,
+               int64_t qps_per_rail, int64_t *qp) {
+    if (qps_per_rail < 1) return ORC_ERANGE;
+    int64_t *next = (int64_t *)calloc((size_t)N, sizeof(int64_t));
+    if (!next) return ORC_ENOMEM;
+    for (int64_t p = 0; p < F; p++) {
+        int64_t i = order[p];
+        int32_t j = rail[i];
+        qp[i] = next[j] % qps_per_rail;
+        next[j] += 1;
+    }
+    free(next);
     return ORC_OK;
 }

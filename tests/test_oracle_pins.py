@@ -439,3 +439,42 @@ def test_pack_unpack_roundtrip():
         for key, parts in rebuilt.items():
             assert b"".join(parts[c] for c in sorted(parts)) == streams[key]
         assert sum(len(v) for v in streams.values()) == int(load.sum()) == int(msg.sum())
+
+
+# ------------------------------------------------------------------ NEXT f2: QP map
+@pytest.mark.parametrize("ex", GOLD["qp_map"])
+def test_qp_map_worked_examples(ex):
+    # Alg. 2 step 4, SPEC S:304-312 examples and a hand-derived case
+    order, rail, off, load = oracle.lpt(np.array(ex["sizes"], np.int64), ex["N"])
+    qp = oracle.qp_map(order, rail, ex["N"], ex["qps_per_rail"])
+    assert [int(qp[i]) for i in order] == ex["qp_in_assignment_order"]
+
+
+def test_qp_map_matches_rail_offset_order():
+    # independent of the visiting order: on one rail, offsets grow with assignment
+    # order (sizes > 0), so the k-th chunk of rail j by OFFSET has QP k mod Q;
+    # full chunk i (emission order) is the floor(i/N)-th chunk of rail i mod N
+    rng = np.random.default_rng(34)
+    for _ in range(60):
+        N = int(rng.integers(1, 9))
+        M = int(rng.integers(2, 5))
+        C = int(rng.choice([64, 100, 4096]))
+        Q = int(rng.choice([1, 2, 3, 64]))
+        msg = rng.integers(0, 5 * C, size=(N, M * N)) * (rng.random((N, M * N)) < 0.8)
+        msg[:, :N] = 0
+        s = oracle.schedule_node(msg.astype(np.int64), C)
+        qp = oracle.qp_map(s["order"], s["rail"], N, Q)
+        for j in range(N):
+            on_j = np.nonzero(s["rail"] == j)[0]
+            by_off = on_j[np.argsort(s["off"][on_j], kind="stable")]
+            assert np.all(np.diff(s["off"][by_off]) > 0)
+            assert [int(qp[i]) for i in by_off] == [k % Q for k in range(len(by_off))]
+        full = np.nonzero(s["chunks"]["size"] == C)[0]
+        for i_em, i in enumerate(full):  # chunks are in emission order
+            assert s["rail"][i] == i_em % N and qp[i] == (i_em // N) % Q
+
+
+def test_qp_map_rejects_zero_qps():
+    order, rail, off, load = oracle.lpt(np.array([3, 2], np.int64), 1)
+    with pytest.raises(ValueError):
+        oracle.qp_map(order, rail, 1, 0)
