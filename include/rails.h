@@ -127,6 +127,22 @@ int rails_lpt_schedule(const rails_topo_t* topo, const rails_shard_t* shard,
                        const int64_t* msg_bytes, const rails_sched_t* out,
                        void* workspace, size_t workspace_bytes, void* stream);
 
+/* NEXT f2 -- QP map (Alg. 2 step 4: "select port p from NIC j* by
+ * round-robin; map (j*, p) to a QP"; R#34).  Same as rails_lpt_schedule (same
+ * outputs, same workspace) plus the QP index of every remainder chunk: per rail,
+ * chunks take QP indices round-robin over qps_per_rail in assignment (Step 3)
+ * order, one counter per rail and (unit, node) round.  Because full chunks are
+ * assigned first and in emission order, the i-th full chunk of a node
+ * (i = full_base[g][h] + c) is the floor(i/N)-th chunk of rail i mod N and gets
+ * QP floor(i/N) mod qps_per_rail (closed form, not stored).
+ *   qps_per_rail  >= 1 (ports x QPs per port; the paper uses up to 256);
+ *   rem_qp        int32 [U][nd][N][G]  QP of the message's remainder chunk, -1 if
+ *                 none.  Errors: RAILS_EINVAL for qps_per_rail < 1 or NULL rem_qp. */
+int rails_lpt_schedule_qp(const rails_topo_t* topo, const rails_shard_t* shard,
+                          const int64_t* msg_bytes, const rails_sched_t* out,
+                          int32_t qps_per_rail, int32_t* rem_qp,
+                          void* workspace, size_t workspace_bytes, void* stream);
+
 /* Generic atomic-flow LPT ("small application-layer messages" P:603):
  * n_seg independent flow sets, set s = flows seg_off[s] .. seg_off[s+1]-1
  * (seg_off: device int64 [n_seg+1], non-decreasing, seg_off[0] = 0, last = F).

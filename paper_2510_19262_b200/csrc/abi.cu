@@ -157,9 +157,9 @@ int rails_schedule_workspace(const rails_topo_t* topo, const rails_shard_t* sh, 
   return RAILS_OK;
 }
 
-int rails_lpt_schedule(const rails_topo_t* topo, const rails_shard_t* sh,
-                       const int64_t* msg_bytes, const rails_sched_t* out, void* ws,
-                       size_t ws_bytes, void* stream) {
+static int schedule_impl(const rails_topo_t* topo, const rails_shard_t* sh,
+                         const int64_t* msg_bytes, const rails_sched_t* out, void* ws,
+                         size_t ws_bytes, int32_t* rem_qp, int32_t qps, void* stream) {
   int rc = check_topo(topo);
   if (rc || (rc = check_shard(topo, sh))) return rc;
   if (!msg_bytes || !out || !out->full_base || !out->rem_rail || !out->rem_off ||
@@ -172,8 +172,23 @@ int rails_lpt_schedule(const rails_topo_t* topo, const rails_shard_t* sh,
   LaunchCtx c;
   if ((rc = ctx(stream, &c))) return rc;
   return cuda_rc(launch_schedule(c, sh->U, sh->nd, sh->d0, topo->M, topo->N, topo->chunk_bytes,
-                                 msg_bytes, *out, ws),
+                                 msg_bytes, *out, ws, rem_qp, qps),
                  "rails_lpt_schedule launch");
+}
+
+int rails_lpt_schedule(const rails_topo_t* topo, const rails_shard_t* sh,
+                       const int64_t* msg_bytes, const rails_sched_t* out, void* ws,
+                       size_t ws_bytes, void* stream) {
+  return schedule_impl(topo, sh, msg_bytes, out, ws, ws_bytes, nullptr, 0, stream);
+}
+
+int rails_lpt_schedule_qp(const rails_topo_t* topo, const rails_shard_t* sh,
+                          const int64_t* msg_bytes, const rails_sched_t* out,
+                          int32_t qps_per_rail, int32_t* rem_qp, void* ws, size_t ws_bytes,
+                          void* stream) {
+  if (qps_per_rail < 1) return fail(RAILS_EINVAL, "qps_per_rail %d < 1", (int)qps_per_rail);
+  if (!rem_qp) return fail(RAILS_EINVAL, "rem_qp is NULL");
+  return schedule_impl(topo, sh, msg_bytes, out, ws, ws_bytes, rem_qp, qps_per_rail, stream);
 }
 
 int rails_assign_workspace(int32_t n_seg, int64_t F, size_t* bytes) {

@@ -167,7 +167,8 @@ cudaError_t launch_histogram(const LaunchCtx&, int U, int nd, int d0, int M, int
 
 size_t schedule_workspace_bytes(int U, int nd, long long NG);
 cudaError_t launch_schedule(const LaunchCtx&, int U, int nd, int d0, int M, int N, long long C,
-                            const int64_t* msg, const rails_sched_t& s, void* ws);
+                            const int64_t* msg, const rails_sched_t& s, void* ws,
+                            int32_t* rem_qp, int qps_per_rail);
 
 size_t assign_workspace_bytes(int n_seg, long long F);
 cudaError_t launch_assign(const LaunchCtx&, int N, int n_seg, const int64_t* seg_off,

@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(THREADS)
                  long long C, int cshift, int nbits, int64_t* __restrict__ full_base,
                  int32_t* __restrict__ ws_inv, int64_t* __restrict__ n_full_out,
                  int32_t* __restrict__ n_rem_out, uint32_t* __restrict__ ws_w,
-                 uint32_t* __restrict__ ws_m, uint8_t* __restrict__ ws_scratch, int use_smem,
+                 uint8_t* __restrict__ ws_scratch, int use_smem,
                  int* err) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ long long scan_scratch[33];
@@ -226,7 +226,6 @@ __global__ void __launch_bounds__(THREADS)
   const IdxT* is = which ? iB : iA;
   for (int i = threadIdx.x; i < n; i += THREADS) {
     ws_w[seg * NG + i] = (uint32_t)(C - 1 - (long long)ks[i]);
-    ws_m[seg * NG + i] = (uint32_t)is[i];
     ws_inv[seg * NG + is[i]] = i;  // sorted position of message is[i]'s remainder
   }
 }
@@ -697,23 +696,84 @@ static int ceil_log2(long long x) {  // bits needed for values 0..x-1
 __global__ void __launch_bounds__(256)
     k_expand_rem(long long NG, const int32_t* __restrict__ ws_inv,
                  const uint64_t* __restrict__ ws_res, int8_t* __restrict__ rem_rail,
-                 int64_t* __restrict__ rem_off) {
+                 int64_t* __restrict__ rem_off, const uint32_t* __restrict__ ws_qp,
+                 int32_t* __restrict__ rem_qp) {
   const long long seg = blockIdx.y;
   const long long m = (long long)blockIdx.x * 256 + threadIdx.x;
   if (m >= NG) return;
   const int pos = ws_inv[seg * NG + m];
   int8_t r = -1;
   long long o = 0;
+  int32_t q = -1;
   if (pos >= 0) {
     const uint64_t v = ws_res[seg * NG + pos];
     r = (int8_t)(v >> 56);
     o = (long long)(v & (uint64_t)OFF_MASK);
+    if (rem_qp) q = (int32_t)ws_qp[seg * NG + pos];
   }
   rem_rail[seg * NG + m] = r;
   rem_off[seg * NG + m] = o;
+  if (rem_qp) rem_qp[seg * NG + m] = q;
 }
 
-// workspace: [256 B header][ws_res u64 (nseg*NG)][ws_w u32][ws_m u32][ws_inv i32]
+// NEXT f2, Alg. 2 step 4 (R#34): per-rail round-robin QP index in
+// assignment order.  The chain results are already in sorted (= assignment)
+// order, so the QP of the p-th remainder is (full chunks on its rail + remainders
+// on its rail before p) mod Q, full chunks being assigned first (i mod N).  One
+// CTA per (unit, node); warp w owns a contiguous slice of the sorted list.
+// Pass 1 counts each slice's items per rail; thread j < N turns the counts into
+// per-warp starting counters (exclusive over warps, plus rail j's full chunks);
+// pass 2 ranks each 32-item batch by rail with a ballot multi-split (5 ballots,
+// rails < 32) and advances the warp's counters from the group leaders.
+constexpr int QP_WARPS = 8;
+
+__global__ void __launch_bounds__(QP_WARPS * 32)
+    k_qp_rank(int N, int Q, long long NG, const int64_t* __restrict__ n_full,
+              const int32_t* __restrict__ n_rem, const uint64_t* __restrict__ ws_res,
+              uint32_t* __restrict__ ws_qp) {
+  __shared__ unsigned cnt[QP_WARPS][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long seg = blockIdx.x;
+  const long long nf = n_full[seg];
+  const int nr = n_rem[seg];
+  const uint64_t* __restrict__ res = ws_res + seg * NG;
+  uint32_t* __restrict__ out = ws_qp + seg * NG;
+  const int per = (((nr + QP_WARPS - 1) / QP_WARPS) + 31) & ~31;
+  const int beg = wid * per, end = min(nr, beg + per);
+  const unsigned lt = lanemask_lt();
+  cnt[wid][lane] = 0;
+  __syncwarp();
+  for (int p0 = beg; p0 < end; p0 += 32) {  // pass 1: per-rail counts of the slice
+    const int p = p0 + lane;
+    const unsigned r = p < end ? (unsigned)(res[p] >> 56) : 0u;
+    const unsigned peers = warp_match_nb<5>(r, p < end);
+    if (p < end && (peers & lt) == 0) cnt[wid][r] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  const unsigned q = (unsigned)Q;
+  if (threadIdx.x < 32) {  // counters are kept modulo Q from here on (32-bit math)
+    const int j = threadIdx.x;
+    unsigned run = (unsigned)((nf / N + ((long long)j < nf % N ? 1 : 0)) % Q);
+    for (int w = 0; w < QP_WARPS; ++w) {
+      const unsigned c = cnt[w][j] % q;
+      cnt[w][j] = run;
+      run = (run + c) % q;
+    }
+  }
+  __syncthreads();
+  for (int p0 = beg; p0 < end; p0 += 32) {  // pass 2: QP = counter + rank, mod Q
+    const int p = p0 + lane;
+    const unsigned r = p < end ? (unsigned)(res[p] >> 56) : 0u;
+    const unsigned peers = warp_match_nb<5>(r, p < end);
+    if (p < end) out[p] = (cnt[wid][r] + __popc(peers & lt)) % q;
+    __syncwarp();
+    if (p < end && (peers & lt) == 0) cnt[wid][r] = (cnt[wid][r] + __popc(peers)) % q;
+    __syncwarp();
+  }
+}
+
+// workspace: [256 B header][ws_res u64 (nseg*NG)][ws_w u32][ws_qp u32][ws_inv i32]
 //            [sort spill scratch when N*G > SORT_SMEM_ITEMS]
 size_t schedule_workspace_bytes(int U, int nd, long long NG) {
   const long long nseg = (long long)U * nd;
@@ -723,7 +783,8 @@ size_t schedule_workspace_bytes(int U, int nd, long long NG) {
 }
 
 cudaError_t launch_schedule(const LaunchCtx& c, int U, int nd, int d0, int M, int N, long long C,
-                            const int64_t* msg, const rails_sched_t& s, void* ws) {
+                            const int64_t* msg, const rails_sched_t& s, void* ws,
+                            int32_t* rem_qp, int qps_per_rail) {
   const long long nseg = (long long)U * nd;
   const long long NG = (long long)N * M * N;
   int cshift = -1;
@@ -732,8 +793,8 @@ cudaError_t launch_schedule(const LaunchCtx& c, int U, int nd, int d0, int M, in
   uint8_t* w8 = (uint8_t*)ws;
   uint64_t* ws_res = (uint64_t*)(w8 + 256);
   uint32_t* ws_w = (uint32_t*)(ws_res + nseg * NG);
-  uint32_t* ws_m = ws_w + nseg * NG;
-  int32_t* ws_inv = (int32_t*)(ws_m + nseg * NG);
+  uint32_t* ws_qp = ws_w + nseg * NG;
+  int32_t* ws_inv = (int32_t*)(ws_qp + nseg * NG);
   uint8_t* scratch = (uint8_t*)(ws_inv + nseg * NG);
   cudaError_t e;
   if (NG <= SORT_SMEM_ITEMS) {
@@ -744,7 +805,7 @@ cudaError_t launch_schedule(const LaunchCtx& c, int U, int nd, int d0, int M, in
     const size_t smem = (size_t)NG * (2 * (k16 ? 2 : 4) + 2 * sizeof(uint16_t));
     const int thr = NG <= 2048 ? 128 : (NG <= 8192 ? 256 : SORT_THREADS);
     void (*kern)(const int64_t*, long long, int, int, int, long long, int, int, int64_t*,
-                 int32_t*, int64_t*, int32_t*, uint32_t*, uint32_t*, uint8_t*, int, int*);
+                 int32_t*, int64_t*, int32_t*, uint32_t*, uint8_t*, int, int*);
     if (k16)
       kern = thr == 128 ? k_chunk_sort<uint16_t, uint16_t, 128>
            : thr == 256 ? k_chunk_sort<uint16_t, uint16_t, 256>
@@ -756,11 +817,11 @@ cudaError_t launch_schedule(const LaunchCtx& c, int U, int nd, int d0, int M, in
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     kern<<<(unsigned)nseg, thr, smem, c.stream>>>(
-        msg, NG, N, d0, nd, C, cshift, nbits, s.full_base, ws_inv, s.n_full, s.n_rem, ws_w, ws_m,
+        msg, NG, N, d0, nd, C, cshift, nbits, s.full_base, ws_inv, s.n_full, s.n_rem, ws_w,
         nullptr, 1, c.err);
   } else {
     k_chunk_sort<uint32_t, uint32_t, SORT_THREADS><<<(unsigned)nseg, SORT_THREADS, 0, c.stream>>>(
-        msg, NG, N, d0, nd, C, cshift, nbits, s.full_base, ws_inv, s.n_full, s.n_rem, ws_w, ws_m,
+        msg, NG, N, d0, nd, C, cshift, nbits, s.full_base, ws_inv, s.n_full, s.n_rem, ws_w,
         scratch, 0, c.err);
   }
   count_launch(1);
@@ -799,8 +860,14 @@ cudaError_t launch_schedule(const LaunchCtx& c, int U, int nd, int d0, int M, in
   }
   count_launch(1);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (rem_qp) {
+    k_qp_rank<<<(unsigned)nseg, QP_WARPS * 32, 0, c.stream>>>(N, qps_per_rail, NG, s.n_full,
+                                                              s.n_rem, ws_res, ws_qp);
+    count_launch(1);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
   k_expand_rem<<<dim3((unsigned)((NG + 255) / 256), (unsigned)nseg), 256, 0, c.stream>>>(
-      NG, ws_inv, ws_res, s.rem_rail, s.rem_off);
+      NG, ws_inv, ws_res, s.rem_rail, s.rem_off, rem_qp ? ws_qp : nullptr, rem_qp);
   count_launch(1);
   return cudaGetLastError();
 }

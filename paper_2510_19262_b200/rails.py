@@ -73,6 +73,8 @@ def lib():
         L.rails_histogram.argtypes = [PT, PS, i32, i32, P, P, i32, i64, P, P, P, P]
         L.rails_schedule_workspace.argtypes = [PT, PS, ctypes.POINTER(sz)]
         L.rails_lpt_schedule.argtypes = [PT, PS, P, ctypes.POINTER(_Sched), P, sz, P]
+        L.rails_lpt_schedule_qp.argtypes = [PT, PS, P, ctypes.POINTER(_Sched), i32, P, P, sz, P]
+        L.rails_lpt_schedule_qp.restype = ctypes.c_int
         L.rails_assign_workspace.argtypes = [i32, i64, ctypes.POINTER(sz)]
         L.rails_lpt_assign.argtypes = [i32, i32, P, i64, P, P, P, P, P, sz, P]
         L.rails_eval.argtypes = [PT, PS, P, ctypes.POINTER(_Sched), ctypes.POINTER(_Eval), P]
@@ -217,6 +219,25 @@ def lpt_schedule(tp: Topo, sh: Shard, msg: torch.Tensor, out: Schedule | None = 
                                  ctypes.byref(cs), _ptr(workspace, torch.uint8, "workspace"),
                                  workspace.numel(), _stream(stream)))
     return out
+
+
+def lpt_schedule_qp(tp: Topo, sh: Shard, msg: torch.Tensor, qps_per_rail: int,
+                    out: Schedule | None = None, rem_qp: torch.Tensor | None = None,
+                    workspace: torch.Tensor | None = None, stream=None):
+    """rails_lpt_schedule_qp (NEXT f2): the schedule plus rem_qp int32 [U][nd][N][G]."""
+    if out is None:
+        out = Schedule.empty(tp, sh, msg.device)
+    if rem_qp is None:
+        rem_qp = torch.empty(out.rem_rail.shape, dtype=torch.int32, device=msg.device)
+    if workspace is None:
+        workspace = torch.empty(schedule_workspace(tp, sh), dtype=torch.uint8, device=msg.device)
+    cs = out.c()
+    _ok(lib().rails_lpt_schedule_qp(ctypes.byref(tp), ctypes.byref(sh),
+                                    _ptr(msg, torch.int64, "msg"), ctypes.byref(cs),
+                                    int(qps_per_rail), _ptr(rem_qp, torch.int32, "rem_qp"),
+                                    _ptr(workspace, torch.uint8, "workspace"), workspace.numel(),
+                                    _stream(stream)))
+    return out, rem_qp
 
 
 def lpt_assign(N: int, seg_off: torch.Tensor, w: torch.Tensor, stream=None):

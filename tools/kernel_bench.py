@@ -108,6 +108,9 @@ def bench_pack(res):
     # schedule-side kernels of the same C3 unit
     res["c3_schedule"] = timeit(lambda: rails.lpt_schedule(pipe.tp, pipe.sh, pipe.msg, out=pipe.sched,
                                                            workspace=pipe.ws))
+    qp = torch.empty(pipe.sched.rem_rail.shape, dtype=torch.int32, device=DEV)
+    res["c3_schedule_qp64"] = timeit(lambda: rails.lpt_schedule_qp(
+        pipe.tp, pipe.sh, pipe.msg, 64, out=pipe.sched, rem_qp=qp, workspace=pipe.ws))
     res["c3_histogram"] = timeit(lambda: rails.histogram(pipe.tp, pipe.sh, topk, lut, RB,
                                                          out=(pipe.counts, pipe.msg, pipe.rank)))
     res["c3_eval"] = timeit(lambda: rails.eval(pipe.tp, pipe.sh, pipe.msg, pipe.sched, out=pipe.ev))
@@ -138,6 +141,9 @@ def bench_hist_c4(res):
     pipe = MatrixPipeline(M, N, cfg["C"], U, 0, M, DEV)
     res["c4_schedule"] = timeit(lambda: rails.lpt_schedule(pipe.tp, pipe.sh, msg, out=pipe.sched,
                                                            workspace=pipe.ws))
+    qp = torch.empty(pipe.sched.rem_rail.shape, dtype=torch.int32, device=DEV)
+    res["c4_schedule_qp64"] = timeit(lambda: rails.lpt_schedule_qp(
+        pipe.tp, pipe.sh, msg, 64, out=pipe.sched, rem_qp=qp, workspace=pipe.ws))
     res["c4_eval"] = timeit(lambda: rails.eval(pipe.tp, pipe.sh, msg, pipe.sched, out=pipe.ev))
     del topk, out, msg, pipe
     torch.cuda.empty_cache()
