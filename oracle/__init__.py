@@ -18,16 +18,18 @@ import subprocess
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SRC = os.path.join(_HERE, "oracle.c")
+_SRCS = [os.path.join(_HERE, "oracle.c"), os.path.join(_HERE, "flowsim.c")]
 _LIB = os.path.join(_HERE, "liboracle.so")
 
 
 def build(force: bool = False) -> str:
     """Compile liboracle.so with gcc (no FP contraction: R#25)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    stale = not os.path.exists(_LIB) or any(
+        os.path.getmtime(_LIB) < os.path.getmtime(s) for s in _SRCS)
+    if force or stale:
         subprocess.check_call(
             ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fPIC", "-shared",
-             "-o", _LIB, _SRC])
+             "-o", _LIB] + _SRCS + ["-lm"])
     return _LIB
 
 
@@ -357,3 +359,60 @@ def rem_qp_node(msg_node, C, qps_per_rail, sched=None):
         if ch["size"][i] < C:
             out[ch["g"][i], ch["h"][i]] = qp[i]
     return out, qp
+
+
+# ------------------------------------------------------------------ NEXT f4 (flowsim)
+FS_POLICIES = {"lpt": 0, "uniform": 1, "ecmp": 2, "reps": 3, "minrtt": 4}
+FS_STATS = ("T", "total", "busbw", "cct_mean", "cct_p80", "cct_p95", "cct_p99",
+            "max_pair_frac", "events", "flows")
+
+
+def fs_nlinks(M, N, S):
+    L = lib()
+    L.orc_fs_nlinks.restype = ctypes.c_int64
+    L.orc_fs_nlinks.argtypes = [ctypes.c_int32] * 3
+    return int(L.orc_fs_nlinks(M, N, S))
+
+
+def max_min(paths, w, cap):
+    """Progressive-filling max-min rates (R#37) of subflows with link lists
+    `paths` (each <= 4 links), share-weights `w`, link capacities `cap`."""
+    L = lib()
+    P = ctypes.c_void_p
+    L.orc_max_min.restype = ctypes.c_int
+    L.orc_max_min.argtypes = [ctypes.c_int64, P, P, P, ctypes.c_int64, P, P]
+    n = len(paths)
+    nl = np.array([len(p) for p in paths], np.int32)
+    links = np.full((max(n, 1), 4), -1, np.int64)
+    for i, p in enumerate(paths):
+        links[i, :len(p)] = p
+    w = _c(w, np.float64)
+    cap = _c(cap, np.float64)
+    rate = np.zeros(n, np.float64)
+    rc = L.orc_max_min(n, _p(nl), _p(links), _p(w), len(cap), _p(cap), _p(rate))
+    assert rc == 0
+    return rate
+
+
+def flowsim(M, N, S, R1, R2, Rs, C, policy, msg_unit, seed=None):
+    """One all-to-all round through the fluid simulator (R#35-R#39).
+    msg_unit int64 [M][N][G].  Returns dict(msg_cct [M][N][G], link_bytes [L],
+    and the FS_STATS scalars)."""
+    L = lib()
+    P = ctypes.c_void_p
+    i32, i64, dbl = ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+    L.orc_flowsim.restype = ctypes.c_int
+    L.orc_flowsim.argtypes = [i32, i32, i32, dbl, dbl, dbl, i64, ctypes.c_uint64, i32, P, P, P, P]
+    pol = FS_POLICIES[policy] if isinstance(policy, str) else int(policy)
+    msg_unit = _c(msg_unit, np.int64)
+    G = M * N
+    cct = np.zeros((M, N, G), np.float64)
+    lb = np.zeros(fs_nlinks(M, N, S), np.float64)
+    st = np.zeros(10, np.float64)
+    rc = L.orc_flowsim(M, N, S, R1, R2, Rs, C, DEFAULT_ECMP_SEED if seed is None else seed, pol,
+                       _p(msg_unit), _p(cct), _p(lb), _p(st))
+    if rc != 0:
+        raise ValueError(f"oracle flowsim rc={rc}")
+    out = dict(msg_cct=cct, link_bytes=lb)
+    out.update({k: float(v) for k, v in zip(FS_STATS, st)})
+    return out
