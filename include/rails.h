@@ -332,6 +332,61 @@ int rails_ipc_free(void* dptr);
  * RAILS_ECUDA if the devices cannot reach each other. */
 int rails_enable_peer_access(int32_t peer_device);
 
+/* ------------------------------------------------------------------ NEXT f4 */
+/* Fluid (flow-level) simulation of one all-to-all round per simulation (SPEC
+ * flowsim S:464-537 in place of the paper's Mininet testbed), with the
+ * paper's comparison policies and its metrics (CCT avg/p80/p95/p99,
+ * BusBw).  Readings R#35-R#39.
+ *
+ * Fabric (R#35): topo gives M, N, R2 (NIC<->leaf rate), chunk_bytes C and the
+ * ECMP seed; the fabric adds S spines, the intra-domain GPU<->NIC rate R1 (> R2)
+ * and the leaf<->spine rate Rs.  Directed links, in this order:
+ *   GPU_UP[M][N][N] (g -> NIC n, R1), NIC_UP[M][N] (R2), LEAF_SPINE[N][S] (Rs),
+ *   SPINE_LEAF[S][N] (Rs), NIC_DOWN[M][N] (R2), GPU_DOWN[M][N][N] (NIC n -> m, R1);
+ *   L = 2MN^2 + 2MN + 2NS.
+ * Policies (R#36): LPT chunks of the node's LPT schedule on rail paths; UNIFORM
+ * N flows of B/N per message (Theorem 3's P* = 1/N); ECMP whole message on one
+ * hashed spine path; REPS whole message split evenly over every spine path;
+ * MINRTT LPT-sized chunks each on the least backlogged spine path at t = 0.
+ * Rates are max-min fair (progressive filling, R#37); a flow completes at the
+ * event where its remaining / rate reaches the step (R#38). */
+enum {
+    RAILS_POL_LPT = 0,
+    RAILS_POL_UNIFORM = 1,
+    RAILS_POL_ECMP = 2,
+    RAILS_POL_REPS = 3,
+    RAILS_POL_MINRTT = 4
+};
+#define RAILS_FS_NSTATS 10
+typedef struct {
+    int32_t S;    /* spines, >= 1 (default N) */
+    double R1;    /* intra-domain GPU<->NIC rate, B/s, > R2 (default 8*R2) */
+    double Rs;    /* leaf<->spine rate, B/s, > 0 (default M*R2/S) */
+} rails_fabric_t;
+
+/* Flows and subflows each simulation makes: totals int64 [n_sim][2] (device).
+ *   policy int32 [n_sim] (device), msg int64 [n_sim][M][N][G] (device, >= 0, zero
+ *   for intra-node pairs).  Use the maxima to size the workspace. */
+int rails_flowsim_plan(const rails_topo_t* topo, const rails_fabric_t* fabric, int32_t n_sim,
+                       const int32_t* policy, const int64_t* msg, int64_t* totals,
+                       void* stream);
+int rails_flowsim_workspace(const rails_topo_t* topo, const rails_fabric_t* fabric,
+                            int32_t n_sim, int64_t max_flows, int64_t max_subflows,
+                            size_t* workspace_bytes);
+/* Run n_sim simulations, one CTA each.  Outputs (device):
+ *   msg_cct    double [n_sim][M][N][G]  completion time (s) of each message, 0 if none;
+ *   link_bytes double [n_sim][L]        bytes carried per directed link;
+ *   stats      double [n_sim][RAILS_FS_NSTATS]  T, total bytes, busbw = total / T,
+ *              CCT mean, p80, p95, p99 (nearest rank over messages with bytes),
+ *              max over events of the largest domain-pair rate / (N*R2) (Theorem 1),
+ *              events, flows.
+ * A simulation whose flows exceed max_flows / max_subflows sets RAILS_ENOSPC and
+ * leaves its outputs unwritten. */
+int rails_flowsim(const rails_topo_t* topo, const rails_fabric_t* fabric, int32_t n_sim,
+                  const int32_t* policy, const int64_t* msg, int64_t max_flows,
+                  int64_t max_subflows, void* workspace, size_t workspace_bytes,
+                  double* msg_cct, double* link_bytes, double* stats, void* stream);
+
 /* ------------------------------------------------------------------ misc */
 /* Synchronise `stream`, then return (and clear) the first device-side error
  * recorded since the last check: RAILS_OK, RAILS_ERANGE, RAILS_ENOSPC or

@@ -456,6 +456,62 @@ int rails_ipc_free(void* dptr) {
   return cuda_rc(cudaFree(dptr), "cudaFree");
 }
 
+static int check_fabric(const rails_topo_t* topo, const rails_fabric_t* fb) {
+  if (!fb) return fail(RAILS_EINVAL, "fabric is NULL");
+  if (fb->S < 1 || fb->S > 32) return fail(RAILS_EINVAL, "spines S=%d not in 1..32", (int)fb->S);
+  if (!(fb->R1 > topo->R2)) return fail(RAILS_EINVAL, "R1 must exceed R2 (P:333)");
+  if (!(fb->Rs > 0.0)) return fail(RAILS_EINVAL, "Rs must be > 0");
+  const long long L = 2LL * topo->M * topo->N * topo->N + 2LL * topo->M * topo->N +
+                      2LL * topo->N * fb->S;
+  if (L > (1 << 20) || (long long)topo->M * topo->N * topo->M * topo->N > (1LL << 30))
+    return fail(RAILS_ENOSPC, "fabric too large for the simulator");
+  const size_t smem = flowsim_smem_bytes(*topo, *fb);
+  if (smem > 200 * 1024) return fail(RAILS_ENOSPC, "L=%lld links exceed shared memory", L);
+  return RAILS_OK;
+}
+
+int rails_flowsim_plan(const rails_topo_t* topo, const rails_fabric_t* fb, int32_t n_sim,
+                       const int32_t* policy, const int64_t* msg, int64_t* totals,
+                       void* stream) {
+  int rc = check_topo(topo);
+  if (rc || (rc = check_fabric(topo, fb))) return rc;
+  if (n_sim < 1 || !policy || !msg || !totals) return fail(RAILS_EINVAL, "bad arguments");
+  LaunchCtx c;
+  if ((rc = ctx(stream, &c))) return rc;
+  return cuda_rc(launch_flowsim_plan(c, *topo, *fb, n_sim, policy, msg, totals),
+                 "rails_flowsim_plan launch");
+}
+
+int rails_flowsim_workspace(const rails_topo_t* topo, const rails_fabric_t* fb, int32_t n_sim,
+                            int64_t max_flows, int64_t max_subflows, size_t* bytes) {
+  int rc = check_topo(topo);
+  if (rc || (rc = check_fabric(topo, fb))) return rc;
+  if (n_sim < 1 || max_flows < 0 || max_subflows < 0 || !bytes)
+    return fail(RAILS_EINVAL, "bad arguments");
+  if (max_flows > (1LL << 28) || max_subflows > (1LL << 28))
+    return fail(RAILS_ENOSPC, "too many flows per simulation");
+  *bytes = flowsim_workspace_bytes(*topo, *fb, n_sim, max_flows, max_subflows);
+  return RAILS_OK;
+}
+
+int rails_flowsim(const rails_topo_t* topo, const rails_fabric_t* fb, int32_t n_sim,
+                  const int32_t* policy, const int64_t* msg, int64_t max_flows,
+                  int64_t max_subflows, void* ws, size_t ws_bytes, double* msg_cct,
+                  double* link_bytes, double* stats, void* stream) {
+  size_t need = 0;
+  int rc = rails_flowsim_workspace(topo, fb, n_sim, max_flows, max_subflows, &need);
+  if (rc) return rc;
+  if (!policy || !msg || !ws || !msg_cct || !link_bytes || !stats)
+    return fail(RAILS_EINVAL, "NULL argument");
+  if (!al(ws, 256)) return fail(RAILS_EINVAL, "workspace must be 256-byte aligned");
+  if (ws_bytes < need) return fail(RAILS_ENOSPC, "workspace %zu < %zu bytes", ws_bytes, need);
+  LaunchCtx c;
+  if ((rc = ctx(stream, &c))) return rc;
+  return cuda_rc(launch_flowsim(c, *topo, *fb, n_sim, policy, msg, max_flows, max_subflows, ws,
+                                msg_cct, link_bytes, stats),
+                 "rails_flowsim launch");
+}
+
 int rails_enable_peer_access(int32_t peer_device) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);

@@ -217,5 +217,16 @@ cudaError_t launch_unpack_combine(const LaunchCtx&, int U, int nd, int d0, int M
                                   const rails_sched_t& s, const int64_t* rail_base_c,
                                   const void* comb_out, float* out, long long RB);
 
+size_t flowsim_workspace_bytes(const rails_topo_t& tp, const rails_fabric_t& fb, int n_sim,
+                               long long capF, long long capS);
+size_t flowsim_smem_bytes(const rails_topo_t& tp, const rails_fabric_t& fb);
+cudaError_t launch_flowsim_plan(const LaunchCtx&, const rails_topo_t& tp,
+                                const rails_fabric_t& fb, int n_sim, const int32_t* policy,
+                                const int64_t* msg, int64_t* totals);
+cudaError_t launch_flowsim(const LaunchCtx&, const rails_topo_t& tp, const rails_fabric_t& fb,
+                           int n_sim, const int32_t* policy, const int64_t* msg, long long capF,
+                           long long capS, void* ws, double* msg_cct, double* link_bytes,
+                           double* stats);
+
 void count_launch(int n);
 }  // namespace rails

@@ -37,6 +37,10 @@ class Topo(ctypes.Structure):
                 ("R2", ctypes.c_double), ("R1", ctypes.c_double), ("ecmp_seed", ctypes.c_uint64)]
 
 
+class Fabric(ctypes.Structure):
+    _fields_ = [("S", ctypes.c_int32), ("R1", ctypes.c_double), ("Rs", ctypes.c_double)]
+
+
 class Shard(ctypes.Structure):
     _fields_ = [("U", ctypes.c_int32), ("d0", ctypes.c_int32), ("nd", ctypes.c_int32)]
 
@@ -75,6 +79,13 @@ def lib():
         L.rails_lpt_schedule.argtypes = [PT, PS, P, ctypes.POINTER(_Sched), P, sz, P]
         L.rails_lpt_schedule_qp.argtypes = [PT, PS, P, ctypes.POINTER(_Sched), i32, P, P, sz, P]
         L.rails_lpt_schedule_qp.restype = ctypes.c_int
+        PF = ctypes.POINTER(Fabric)
+        L.rails_flowsim_plan.argtypes = [PT, PF, i32, P, P, P, P]
+        L.rails_flowsim_plan.restype = ctypes.c_int
+        L.rails_flowsim_workspace.argtypes = [PT, PF, i32, i64, i64, ctypes.POINTER(sz)]
+        L.rails_flowsim_workspace.restype = ctypes.c_int
+        L.rails_flowsim.argtypes = [PT, PF, i32, P, P, i64, i64, P, sz, P, P, P, P]
+        L.rails_flowsim.restype = ctypes.c_int
         L.rails_assign_workspace.argtypes = [i32, i64, ctypes.POINTER(sz)]
         L.rails_lpt_assign.argtypes = [i32, i32, P, i64, P, P, P, P, P, sz, P]
         L.rails_eval.argtypes = [PT, PS, P, ctypes.POINTER(_Sched), ctypes.POINTER(_Eval), P]
@@ -511,3 +522,46 @@ def launch_count(reset: bool = False) -> int:
 
 def version() -> int:
     return int(lib().rails_version())
+
+
+# ---------------------------------------------------------------- NEXT f4 (flowsim)
+FS_POLICIES = {"lpt": 0, "uniform": 1, "ecmp": 2, "reps": 3, "minrtt": 4}
+FS_STATS = ("T", "total", "busbw", "cct_mean", "cct_p80", "cct_p95", "cct_p99",
+            "max_pair_frac", "events", "flows")
+
+
+def fabric(M: int, N: int, R2: float, S: int | None = None, R1: float | None = None,
+           Rs: float | None = None) -> Fabric:
+    """Defaults of R#35: S = N spines, R1 = 8*R2, Rs = M*R2/S."""
+    S = N if S is None else S
+    return Fabric(S, 8.0 * R2 if R1 is None else R1, M * R2 / S if Rs is None else Rs)
+
+
+def fs_nlinks(M: int, N: int, S: int) -> int:
+    return 2 * M * N * N + 2 * M * N + 2 * N * S
+
+
+def flowsim(tp: Topo, fb: Fabric, policy: torch.Tensor, msg: torch.Tensor, stream=None):
+    """rails_flowsim_plan + rails_flowsim: policy int32 [n_sim], msg int64
+    [n_sim][M][N][G] (device).  Returns (msg_cct, link_bytes, stats) device tensors.
+    The plan's flow totals are read back to size the workspace (one sync)."""
+    n_sim = policy.numel()
+    dev = msg.device
+    tot = torch.empty((n_sim, 2), dtype=torch.int64, device=dev)
+    _ok(lib().rails_flowsim_plan(ctypes.byref(tp), ctypes.byref(fb), n_sim,
+                                 _ptr(policy, torch.int32, "policy"), _ptr(msg, torch.int64, "msg"),
+                                 _ptr(tot), _stream(stream)))
+    mx = tot.max(dim=0).values.cpu()
+    capF, capS = max(int(mx[0]), 1), max(int(mx[1]), 1)
+    n = ctypes.c_size_t(0)
+    _ok(lib().rails_flowsim_workspace(ctypes.byref(tp), ctypes.byref(fb), n_sim, capF, capS,
+                                      ctypes.byref(n)))
+    ws = torch.empty(int(n.value), dtype=torch.uint8, device=dev)
+    G = tp.M * tp.N
+    cct = torch.empty((n_sim, tp.M, tp.N, G), dtype=torch.float64, device=dev)
+    lb = torch.empty((n_sim, fs_nlinks(tp.M, tp.N, fb.S)), dtype=torch.float64, device=dev)
+    st = torch.empty((n_sim, len(FS_STATS)), dtype=torch.float64, device=dev)
+    _ok(lib().rails_flowsim(ctypes.byref(tp), ctypes.byref(fb), n_sim, _ptr(policy), _ptr(msg),
+                            capF, capS, _ptr(ws), ws.numel(), _ptr(cct), _ptr(lb), _ptr(st),
+                            _stream(stream)))
+    return cct, lb, st
