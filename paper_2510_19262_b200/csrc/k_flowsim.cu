@@ -544,13 +544,22 @@ __global__ void __launch_bounds__(FS_THREADS)
       used[l] = 0.0;
     }
     __syncthreads();
+    double xu = 0.0;  // x*/S of the previous iteration, for its pending dnew
     for (int it = 0;; ++it) {
       if (it > t.L + 1) {
         if (threadIdx.x == 0) flag_error(err, ERR_RANGE);
         break;
       }
+      // the last iteration's newly frozen weight leaves wsum and joins used at its
+      // x* (each link is owned by one thread here and in the listing below)
       double lmin = fs_inf();
       for (int l = threadIdx.x; l < t.L; l += FS_THREADS) {
+        const unsigned dn = dnew[l];
+        if (dn != 0) {
+          wsum[l] -= dn;
+          used[l] = __dadd_rn(used[l], __dmul_rn((double)dn, xu));
+          dnew[l] = 0;
+        }
         if (wsum[l] == 0) continue;
         const double r = fmax(__dsub_rn(l_cap(t, l), used[l]), 0.0);
         lmin = fmin(lmin, __ddiv_rn(__dmul_rn(Sd, r), (double)wsum[l]));
@@ -558,6 +567,7 @@ __global__ void __launch_bounds__(FS_THREADS)
       if (threadIdx.x == 0) nb = 0;
       const double xs = block_min_d(lmin, dscr);
       if (!(xs < fs_inf())) break;  // every active subflow frozen
+      xu = __ddiv_rn(xs, Sd);
       const double thr = __dmul_rn(xs, 1.0 + 1e-12);
       for (int l = threadIdx.x; l < t.L; l += FS_THREADS) {
         if (wsum[l] == 0) continue;
@@ -568,17 +578,29 @@ __global__ void __launch_bounds__(FS_THREADS)
       // the listed links' subflow lists, flattened over the whole CTA (a hot
       // receiver's link can carry thousands of subflows)
       const int nbl = nb;
-      long long carry = 0;
-      for (int b0 = 0; b0 < nbl; b0 += FS_THREADS) {
-        const int b = b0 + threadIdx.x;
-        const long long len = b < nbl ? w.loff[blist[b] + 1] - w.loff[blist[b]] : 0;
-        long long tot;
-        const long long ex = block_excl_scan(len, lscan, &tot);
-        if (b < nbl) bpre[b] = (int)(carry + ex);
-        carry += tot;
+      int ntot;
+      if (nbl <= 32) {  // usual case: one warp scans the list lengths
+        if (threadIdx.x < 32) {
+          const int len = threadIdx.x < nbl ? w.loff[blist[threadIdx.x] + 1] - w.loff[blist[threadIdx.x]] : 0;
+          const int inc = warp_incl_scan(len);
+          if (threadIdx.x < nbl) bpre[threadIdx.x] = inc - len;
+          if (threadIdx.x == 31) lscan[32] = inc;
+        }
+        __syncthreads();
+        ntot = (int)lscan[32];
+      } else {
+        long long carry = 0;
+        for (int b0 = 0; b0 < nbl; b0 += FS_THREADS) {
+          const int b = b0 + threadIdx.x;
+          const long long len = b < nbl ? w.loff[blist[b] + 1] - w.loff[blist[b]] : 0;
+          long long tot;
+          const long long ex = block_excl_scan(len, lscan, &tot);
+          if (b < nbl) bpre[b] = (int)(carry + ex);
+          carry += tot;
+        }
+        __syncthreads();
+        ntot = (int)carry;
       }
-      __syncthreads();
-      const int ntot = (int)carry;
       for (int x = threadIdx.x; x < ntot; x += FS_THREADS) {
         int lo_ = 0, hi_ = nbl - 1;  // last b with bpre[b] <= x
         while (lo_ < hi_) {
@@ -594,16 +616,6 @@ __global__ void __launch_bounds__(FS_THREADS)
         const int nl = w.snl[s];
         for (int a = 0; a < nl; ++a)
           atomicAdd(&dnew[w.slink[(long long)s * FS_MAXL + a]], (unsigned)w.swi[s]);
-      }
-      __syncthreads();
-      // the newly frozen weight of each link leaves wsum and joins used at x*
-      const double xu = __ddiv_rn(xs, Sd);
-      for (int l = threadIdx.x; l < t.L; l += FS_THREADS) {
-        const unsigned dn = dnew[l];
-        if (dn == 0) continue;
-        wsum[l] -= dn;
-        used[l] = __dadd_rn(used[l], __dmul_rn((double)dn, xu));
-        dnew[l] = 0;
       }
       __syncthreads();
     }
