@@ -347,7 +347,10 @@ int rails_enable_peer_access(int32_t peer_device);
  * Policies (R#36): LPT chunks of the node's LPT schedule on rail paths; UNIFORM
  * N flows of B/N per message (Theorem 3's P* = 1/N); ECMP whole message on one
  * hashed spine path; REPS whole message split evenly over every spine path;
- * MINRTT LPT-sized chunks each on the least backlogged spine path at t = 0.
+ * MINRTT LPT-sized chunks each on the least backlogged spine path at t = 0;
+ * PLB as ECMP, re-hashing the spine of a flow whose rate a spine link set, at a
+ * completion event (not at two consecutive events).  Unknown policy values set
+ * RAILS_ERANGE and give no flows.
  * Rates are max-min fair (progressive filling, R#37); a flow completes at the
  * event where its remaining / rate reaches the step (R#38). */
 enum {
@@ -355,7 +358,8 @@ enum {
     RAILS_POL_UNIFORM = 1,
     RAILS_POL_ECMP = 2,
     RAILS_POL_REPS = 3,
-    RAILS_POL_MINRTT = 4
+    RAILS_POL_MINRTT = 4,
+    RAILS_POL_PLB = 5
 };
 #define RAILS_FS_NSTATS 10
 typedef struct {

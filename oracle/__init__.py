@@ -362,7 +362,7 @@ def rem_qp_node(msg_node, C, qps_per_rail, sched=None):
 
 
 # ------------------------------------------------------------------ NEXT f4 (flowsim)
-FS_POLICIES = {"lpt": 0, "uniform": 1, "ecmp": 2, "reps": 3, "minrtt": 4}
+FS_POLICIES = {"lpt": 0, "uniform": 1, "ecmp": 2, "reps": 3, "minrtt": 4, "plb": 5}
 FS_STATS = ("T", "total", "busbw", "cct_mean", "cct_p80", "cct_p95", "cct_p99",
             "max_pair_frac", "events", "flows")
 

@@ -35,7 +35,12 @@
  *     4 MINRTT   the LPT chunks, each on the spine path (fixed source NIC g)
  *                minimising max over its links of backlog/capacity at decision
  *                time (t = 0, chunks in (d, g, h, c) order), lowest spine
- *                on ties; backlog += chunk bytes on the chosen links.
+ *                on ties; backlog += chunk bytes on the chosen links;
+ *     5 PLB      as ECMP, but at every completion event a flow whose rate was set
+ *                by a congested spine link (a LEAF_SPINE / SPINE_LEAF bottleneck)
+ *                re-hashes its spine: attempt a -> spine hash with seed + a*phi,
+ *                at most every other event ("switch paths during idle
+ *                periods"; R#36).
  *
  *   Max-min rates (R#37): progressive filling over subflows with
  *   share-weights: level x* = min over links of (cap - frozen rates) / (sum of
@@ -134,6 +139,7 @@ static int spine_path(const fs_topo *t, int k, int g, int f, int m, int j, int64
 /* ---------------------------------------------------------------- flows */
 typedef struct {
     int64_t nflow, nsub;
+    uint8_t *init;    /* [nsub] active at t = 0 (PLB's spare spine paths are not) */
     double *bytes;    /* [nflow] */
     int64_t *msg;     /* [nflow] message index d*N*G + g*G + h */
     int64_t *sub0;    /* [nflow+1] first subflow */
@@ -143,7 +149,8 @@ typedef struct {
 } fs_flows;
 
 static void fs_free(fs_flows *F) {
-    free(F->bytes); free(F->msg); free(F->sub0); free(F->w); free(F->nl); free(F->links);
+    free(F->init); free(F->bytes); free(F->msg); free(F->sub0); free(F->w); free(F->nl);
+    free(F->links);
     memset(F, 0, sizeof(*F));
 }
 
@@ -156,7 +163,8 @@ static int fs_alloc(fs_flows *F, int64_t nflow, int64_t nsub) {
     F->w = (double *)calloc((size_t)(nsub + 1), sizeof(double));
     F->nl = (int32_t *)calloc((size_t)(nsub + 1), sizeof(int32_t));
     F->links = (int64_t *)calloc((size_t)(nsub + 1) * FS_MAXL, sizeof(int64_t));
-    if (!F->bytes || !F->msg || !F->sub0 || !F->w || !F->nl || !F->links) return FS_ENOMEM;
+    F->init = (uint8_t *)calloc((size_t)(nsub + 1), 1);
+    if (!F->init || !F->bytes || !F->msg || !F->sub0 || !F->w || !F->nl || !F->links) return FS_ENOMEM;
     return FS_OK;
 }
 
@@ -169,6 +177,7 @@ static void add_flow(fs_flows *F, double bytes, int64_t msg) {
 }
 static int64_t *add_sub(fs_flows *F, double w) {
     F->w[F->nsub] = w;
+    F->init[F->nsub] = 1;
     F->nsub++;
     F->sub0[F->nflow] = F->nsub;
     return F->links + (F->nsub - 1) * FS_MAXL;
@@ -260,6 +269,16 @@ static int build_flows(const fs_topo *t, int64_t C, uint64_t seed, int policy,
                         add_flow(F, (double)B, mi);
                         int64_t *p = add_sub(F, 1.0);
                         F->nl[F->nsub - 1] = spine_path(t, d, g, f, m, j, p);
+                    } else if (policy == 5) {
+                        /* PLB: every spine path is a candidate; the ECMP one starts */
+                        add_flow(F, (double)B, mi);
+                        const int j0 = orc_ecmp_rail(seed, (int64_t)d * N + g, h, S);
+                        const int nj = (g == m) ? 1 : S;
+                        for (int j = 0; j < nj; j++) {
+                            int64_t *p = add_sub(F, 1.0);
+                            F->nl[F->nsub - 1] = spine_path(t, d, g, f, m, j, p);
+                            F->init[F->nsub - 1] = (uint8_t)(nj == 1 || j == j0);
+                        }
                     } else {
                         add_flow(F, (double)B, mi);
                         const int nj = (g == m) ? 1 : S;
@@ -277,9 +296,12 @@ static int build_flows(const fs_topo *t, int64_t C, uint64_t seed, int policy,
 
 /* ---------------------------------------------------------------- max-min */
 /* Progressive filling (R#37) over the subflows with act[s] != 0.  rate[s] out. */
+/* shit[s] (may be NULL): some bottleneck link of s's freezing step lies in the
+ * spine layer [ls0, ls1) -- PLB's congestion signal. */
 static void max_min(int64_t nsub, const int32_t *nl, const int64_t *links, const double *w,
                     const uint8_t *act, int64_t L, const double *cap, double *rate,
-                    double *sumw, double *used, uint8_t *frozen, uint8_t *bott) {
+                    double *sumw, double *used, uint8_t *frozen, uint8_t *bott,
+                    uint8_t *shit, int64_t ls0, int64_t ls1) {
     for (int64_t s = 0; s < nsub; s++) {
         frozen[s] = 0;
         rate[s] = 0.0;
@@ -314,11 +336,16 @@ static void max_min(int64_t nsub, const int32_t *nl, const int64_t *links, const
         }
         for (int64_t s = 0; s < nsub; s++) {
             if (!act[s] || frozen[s]) continue;
-            int hit = 0;
-            for (int a = 0; a < nl[s]; a++) hit |= bott[links[s * FS_MAXL + a]];
+            int hit = 0, sp = 0;
+            for (int a = 0; a < nl[s]; a++) {
+                const int64_t l = links[s * FS_MAXL + a];
+                hit |= bott[l];
+                sp |= bott[l] && l >= ls0 && l < ls1;
+            }
             if (hit) {
                 rate[s] = w[s] * xs;
                 frozen[s] = 1;
+                if (shit) shit[s] = (uint8_t)sp;
             }
         }
     }
@@ -334,7 +361,7 @@ int orc_max_min(int64_t nsub, const int32_t *nl, const int64_t *links, const dou
     uint8_t *act = (uint8_t *)malloc((size_t)nsub + 1);
     if (!sumw || !used || !frozen || !bott || !act) return FS_ENOMEM;
     memset(act, 1, (size_t)nsub + 1);
-    max_min(nsub, nl, links, w, act, L, cap, rate, sumw, used, frozen, bott);
+    max_min(nsub, nl, links, w, act, L, cap, rate, sumw, used, frozen, bott, NULL, 0, 0);
     free(sumw); free(used); free(frozen); free(bott); free(act);
     return FS_OK;
 }
@@ -354,7 +381,7 @@ int orc_flowsim(int32_t M, int32_t N, int32_t S, double R1, double R2, double Rs
                 uint64_t seed, int32_t policy, const int64_t *msg, double *msg_cct,
                 double *link_bytes, double *stats) {
     if (M < 2 || N < 1 || S < 1 || !(R1 > R2) || !(R2 > 0.0) || !(Rs > 0.0) || C < 1 ||
-        policy < 0 || policy > 4)
+        policy < 0 || policy > 5)
         return FS_EINVAL;
     fs_topo t = {M, N, S, R1, R2, Rs};
     const int64_t G = (int64_t)M * N, L = orc_fs_nlinks(M, N, S);
@@ -374,8 +401,12 @@ int orc_flowsim(int32_t M, int32_t N, int32_t S, double R1, double R2, double Rs
     double *frate = (double *)calloc((size_t)nf + 1, sizeof(double));
     double *done = (double *)calloc((size_t)nf + 1, sizeof(double));
     double *pair = (double *)calloc((size_t)M * M, sizeof(double));
+    uint8_t *fact = (uint8_t *)calloc((size_t)nf + 1, 1);
+    uint8_t *shit = (uint8_t *)calloc((size_t)ns + 1, 1);
+    int64_t *att = (int64_t *)calloc((size_t)nf + 1, sizeof(int64_t));
+    int64_t *last = (int64_t *)malloc(sizeof(int64_t) * (size_t)(nf + 1));
     if (!cap || !sumw || !used || !bott || !rate || !frozen || !act || !rem || !frate || !done ||
-        !pair) {
+        !pair || !fact || !shit || !att || !last) {
         fs_free(&F);
         return FS_ENOMEM;
     }
@@ -383,16 +414,19 @@ int orc_flowsim(int32_t M, int32_t N, int32_t S, double R1, double R2, double Rs
     int64_t active = 0;
     for (int64_t i = 0; i < nf; i++) {
         rem[i] = F.bytes[i];
-        for (int64_t s = F.sub0[i]; s < F.sub0[i + 1]; s++) act[s] = 1;
+        fact[i] = 1;
+        last[i] = -2;
+        for (int64_t s = F.sub0[i]; s < F.sub0[i + 1]; s++) act[s] = F.init[s];
         active++;
     }
     double tnow = 0.0, maxpair = 0.0;
     int64_t events = 0;
     while (active > 0) {
-        max_min(ns, F.nl, F.links, F.w, act, L, cap, rate, sumw, used, frozen, bott);
+        max_min(ns, F.nl, F.links, F.w, act, L, cap, rate, sumw, used, frozen, bott, shit,
+                L_leaf_spine(&t, 0, 0), L_nic_down(&t, 0, 0));
         double dt = INFINITY;
         for (int64_t i = 0; i < nf; i++) {
-            if (!act[F.sub0[i]]) continue;
+            if (!fact[i]) continue;
             double r = 0.0;
             for (int64_t s = F.sub0[i]; s < F.sub0[i + 1]; s++) r += rate[s];
             frate[i] = r;
@@ -402,7 +436,7 @@ int orc_flowsim(int32_t M, int32_t N, int32_t S, double R1, double R2, double Rs
         /* Theorem 1 ceiling: aggregate rate between two domains <= N*R2 */
         memset(pair, 0, sizeof(double) * (size_t)M * M);
         for (int64_t i = 0; i < nf; i++) {
-            if (!act[F.sub0[i]]) continue;
+            if (!fact[i]) continue;
             const int64_t mi = F.msg[i];
             const int d = (int)(mi / (N * G)), f = (int)((mi % G) / N);
             pair[(int64_t)d * M + f] += frate[i];
@@ -410,9 +444,8 @@ int orc_flowsim(int32_t M, int32_t N, int32_t S, double R1, double R2, double Rs
         for (int64_t q = 0; q < (int64_t)M * M; q++)
             if (pair[q] / ((double)N * R2) > maxpair) maxpair = pair[q] / ((double)N * R2);
         tnow = tnow + dt;
-        events++;
         for (int64_t i = 0; i < nf; i++) {
-            if (!act[F.sub0[i]]) continue;
+            if (!fact[i]) continue;
             for (int64_t s = F.sub0[i]; s < F.sub0[i + 1]; s++) {
                 const double b = rate[s] * dt;
                 for (int a = 0; a < F.nl[s]; a++) link_bytes[F.links[s * FS_MAXL + a]] += b;
@@ -427,10 +460,31 @@ int orc_flowsim(int32_t M, int32_t N, int32_t S, double R1, double R2, double Rs
                     for (int a = 0; a < F.nl[s]; a++) link_bytes[F.links[s * FS_MAXL + a]] += b;
                 }
                 done[i] = tnow;
+                fact[i] = 0;
                 for (int64_t s = F.sub0[i]; s < F.sub0[i + 1]; s++) act[s] = 0;
                 active--;
             }
         }
+        /* PLB (R#36): a flow held back by a spine bottleneck re-hashes its spine,
+         * not at two consecutive events */
+        if (policy == 5) {
+            for (int64_t i = 0; i < nf; i++) {
+                if (!fact[i] || F.sub0[i + 1] - F.sub0[i] < 2 || last[i] == events - 1) continue;
+                int64_t cur = F.sub0[i];
+                while (!act[cur]) cur++;
+                if (!shit[cur]) continue;
+                const int64_t mi = F.msg[i];
+                const int64_t src = mi / G, dst = mi % G;
+                att[i]++;
+                const int j = orc_ecmp_rail(seed + (uint64_t)att[i] * 0x9E3779B97F4A7C15ULL, src,
+                                            dst, S);
+                last[i] = events;
+                if (F.sub0[i] + j == cur) continue;
+                act[cur] = 0;
+                act[F.sub0[i] + j] = 1;
+            }
+        }
+        events++;
     }
     /* per message completion = its last flow (R#39) */
     for (int64_t q = 0; q < (int64_t)M * N * G; q++) msg_cct[q] = 0.0;
@@ -468,7 +522,7 @@ int orc_flowsim(int32_t M, int32_t N, int32_t S, double R1, double R2, double Rs
     stats[9] = (double)nf;
     free(cs);
     free(cap); free(sumw); free(used); free(bott); free(rate); free(frozen); free(act);
-    free(rem); free(frate); free(done); free(pair);
+    free(rem); free(frate); free(done); free(pair); free(fact); free(shit); free(att); free(last);
     fs_free(&F);
     return FS_OK;
 }

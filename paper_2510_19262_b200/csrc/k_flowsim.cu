@@ -114,12 +114,17 @@ struct FsWs {
   uint32_t* ciB;
   double* simstat;   // [4] max pair fraction, events, flows, subflows
   unsigned long long* pair;  // [M*M] per-event domain-pair rate, fixed point
+  uint8_t* sinit;    // [capS] active at t = 0 (PLB's spare spine paths are not)
+  uint8_t* shit;     // [capS] frozen by a spine-layer bottleneck (PLB signal)
+  int* fcur;         // [capF] PLB: the flow's active subflow
+  int* fatt;         // [capF] PLB: re-hash attempts
+  int* flast;        // [capF] PLB: event of the last re-hash
 };
 
 static inline size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct FsLayout {
-  size_t o[32];
+  size_t o[40];
   size_t stride;
 };
 
@@ -130,7 +135,8 @@ static FsLayout fs_layout(long long Q, int L, long long capF, long long capS) {
       (size_t)capS * 16, (size_t)capS * 16, (size_t)capS * 16, (size_t)capS * 16,
       (size_t)(L + 1) * 4, (size_t)capS * 16, (size_t)capF * 8, (size_t)capF * 8,
       (size_t)capF * 8, (size_t)capF, (size_t)capS * 8, (size_t)capS * 4, (size_t)capS,
-      (size_t)capS * 4, (size_t)Q * 8, (size_t)Q * 8, (size_t)Q * 4, (size_t)Q * 4, 64, (size_t)Q * 8};
+      (size_t)capS * 4, (size_t)Q * 8, (size_t)Q * 8, (size_t)Q * 4, (size_t)Q * 4, 64, (size_t)Q * 8, (size_t)capS, (size_t)capS,
+      (size_t)capF * 4, (size_t)capF * 4, (size_t)capF * 4};
   FsLayout lo;
   size_t off = 0;
   const int n = (int)(sizeof(sz) / sizeof(sz[0]));
@@ -172,11 +178,16 @@ __device__ __forceinline__ FsWs fs_ws(uint8_t* base, const size_t* o) {
   w.ciB = (uint32_t*)(base + o[25]);
   w.simstat = (double*)(base + o[26]);
   w.pair = (unsigned long long*)(base + o[27]);
+  w.sinit = base + o[28];
+  w.shit = base + o[29];
+  w.fcur = (int*)(base + o[30]);
+  w.fatt = (int*)(base + o[31]);
+  w.flast = (int*)(base + o[32]);
   return w;
 }
 
 struct FsOffsets {
-  size_t o[32];
+  size_t o[40];
 };
 
 __device__ __forceinline__ double fs_inf() { return __longlong_as_double(0x7ff0000000000000LL); }
@@ -254,7 +265,7 @@ __device__ __forceinline__ void msg_counts(const FsTopo& t, int pol, long long q
     case RAILS_POL_ECMP:
       nf = ns = 1;
       break;
-    default:  // REPS
+    default:  // REPS, PLB
       nf = 1;
       ns = (g == m) ? 1 : t.S;
   }
@@ -265,13 +276,22 @@ __device__ __forceinline__ void msg_counts(const FsTopo& t, int pol, long long q
 __global__ void __launch_bounds__(FS_THREADS)
     k_fs_count(FsTopo t, const int32_t* __restrict__ policy, const int64_t* __restrict__ msg,
                uint8_t* ws, FsOffsets lo, size_t stride, int64_t* __restrict__ totals,
-               int plan) {
+               int plan, int* err) {
   __shared__ long long scr[33];
   const long long sim = blockIdx.x;
   const int pol = policy[sim];
   const int64_t* __restrict__ ms = msg + sim * t.Q;
   FsWs w = fs_ws(ws + sim * stride, lo.o);
   long long cf = 0, cs = 0;
+  if (pol < RAILS_POL_LPT || pol > RAILS_POL_PLB) {  // unknown policy: no flows
+    if (threadIdx.x == 0) {
+      flag_error(err, ERR_RANGE);
+      if (plan) totals[2 * sim] = totals[2 * sim + 1] = 0;
+    }
+    if (!plan)
+      for (long long q = threadIdx.x; q <= t.Q; q += FS_THREADS) w.foff[q] = w.soff[q] = 0;
+    return;
+  }
   for (long long q0 = 0; q0 < t.Q; q0 += FS_THREADS) {
     const long long q = q0 + threadIdx.x;
     long long nf = 0, ns = 0;
@@ -328,6 +348,7 @@ __global__ void __launch_bounds__(FS_THREADS)
         w.fsub0[i] = (int)s;
         w.sw[s] = 1.0;
         w.swi[s] = t.S;
+        w.sinit[s] = 1;
         if (pol == RAILS_POL_LPT) {
           const int rail = c < nfull ? (int)((fb + c) % t.N) : (int)rem_rail[sim * t.Q + q];
           w.snl[s] = rail_path(t, d, g, f, m, rail, w.slink + s * FS_MAXL);
@@ -342,6 +363,7 @@ __global__ void __launch_bounds__(FS_THREADS)
         w.fsub0[fo + n] = (int)(so + n);
         w.sw[so + n] = 1.0;
         w.swi[so + n] = t.S;
+        w.sinit[so + n] = 1;
         w.snl[so + n] = rail_path(t, d, g, f, m, n, w.slink + (so + n) * FS_MAXL);
       }
     } else if (pol == RAILS_POL_ECMP) {
@@ -351,7 +373,24 @@ __global__ void __launch_bounds__(FS_THREADS)
       w.fsub0[fo] = (int)so;
       w.sw[so] = 1.0;
       w.swi[so] = t.S;
+      w.sinit[so] = 1;
       w.snl[so] = spine_path(t, d, g, f, m, j, w.slink + so * FS_MAXL);
+    } else if (pol == RAILS_POL_PLB) {
+      // every spine path is a candidate subflow; the ECMP-hashed one starts
+      const int nj = (g == m) ? 1 : t.S;
+      const int j0 = ecmp_rail(t.seed, (long long)d * t.N + g, h, t.S);
+      w.fbytes[fo] = (double)B;
+      w.fmsg[fo] = (int)q;
+      w.fsub0[fo] = (int)so;
+      w.fcur[fo] = (int)so + (nj == 1 ? 0 : j0);
+      w.fatt[fo] = 0;
+      w.flast[fo] = -2;
+      for (int j = 0; j < nj; ++j) {
+        w.sw[so + j] = 1.0;
+        w.swi[so + j] = t.S;
+        w.sinit[so + j] = (uint8_t)(nj == 1 || j == j0);
+        w.snl[so + j] = spine_path(t, d, g, f, m, j, w.slink + (so + j) * FS_MAXL);
+      }
     } else {  // REPS
       const int nj = (g == m) ? 1 : t.S;
       w.fbytes[fo] = (double)B;
@@ -360,6 +399,7 @@ __global__ void __launch_bounds__(FS_THREADS)
       for (int j = 0; j < nj; ++j) {
         w.sw[so + j] = __ddiv_rn(1.0, (double)nj);
         w.swi[so + j] = t.S / nj;
+        w.sinit[so + j] = 1;
         w.snl[so + j] = spine_path(t, d, g, f, m, j, w.slink + (so + j) * FS_MAXL);
       }
     }
@@ -491,8 +531,9 @@ __global__ void __launch_bounds__(512)
 // subflow-links), not O(iterations * subflows).  Link bytes grow by used*dt.
 
 __global__ void __launch_bounds__(FS_THREADS)
-    k_fs_sim(FsTopo t, uint8_t* ws, FsOffsets lo, size_t stride, long long capF, long long capS,
-             double* __restrict__ link_bytes, int* err) {
+    k_fs_sim(FsTopo t, const int32_t* __restrict__ policy, uint8_t* ws, FsOffsets lo,
+             size_t stride, long long capF, long long capS, double* __restrict__ link_bytes,
+             int* err) {
   extern __shared__ __align__(16) uint8_t fs_smem[];
   double* used = (double*)fs_smem;                                  // [L]
   double* lb = used + t.L;                                           // [L]
@@ -501,6 +542,7 @@ __global__ void __launch_bounds__(FS_THREADS)
   unsigned* dnew = wbase + t.L;                                      // [L]
   int* blist = (int*)(dnew + t.L);                                   // [L]
   int* bpre = blist + t.L;                                           // [L]
+  uint8_t* isb = (uint8_t*)(bpre + t.L);                             // [L] listed now
   __shared__ double dscr[32];
   __shared__ long long lscr[32];
   __shared__ long long lscan[33];
@@ -522,9 +564,12 @@ __global__ void __launch_bounds__(FS_THREADS)
     w.fact[i] = 1;
   }
   __syncthreads();
+  const bool plb = policy[sim] == RAILS_POL_PLB;
+  const int ls0 = l_leaf_spine(t, 0, 0), ls1 = l_nic_down(t, 0, 0);  // spine layer
   for (int s = threadIdx.x; s < nsub; s += FS_THREADS) {
-    w.sact[s] = 1;
+    w.sact[s] = w.sinit[s];
     w.fep[s] = -1;
+    if (!w.sinit[s]) continue;
     const int nl = w.snl[s];
     for (int a = 0; a < nl; ++a) atomicAdd(&wbase[w.slink[(long long)s * FS_MAXL + a]], w.swi[s]);
   }
@@ -560,6 +605,7 @@ __global__ void __launch_bounds__(FS_THREADS)
           used[l] = __dadd_rn(used[l], __dmul_rn((double)dn, xu));
           dnew[l] = 0;
         }
+        isb[l] = 0;
         if (wsum[l] == 0) continue;
         const double r = fmax(__dsub_rn(l_cap(t, l), used[l]), 0.0);
         lmin = fmin(lmin, __ddiv_rn(__dmul_rn(Sd, r), (double)wsum[l]));
@@ -572,7 +618,10 @@ __global__ void __launch_bounds__(FS_THREADS)
       for (int l = threadIdx.x; l < t.L; l += FS_THREADS) {
         if (wsum[l] == 0) continue;
         const double r = fmax(__dsub_rn(l_cap(t, l), used[l]), 0.0);
-        if (__ddiv_rn(__dmul_rn(Sd, r), (double)wsum[l]) <= thr) blist[atomicAdd(&nb, 1)] = l;
+        if (__ddiv_rn(__dmul_rn(Sd, r), (double)wsum[l]) <= thr) {
+          blist[atomicAdd(&nb, 1)] = l;
+          isb[l] = 1;
+        }
       }
       __syncthreads();
       // the listed links' subflow lists, flattened over the whole CTA (a hot
@@ -614,8 +663,13 @@ __global__ void __launch_bounds__(FS_THREADS)
         if (atomicMax(&w.fep[s], events) >= events) continue;  // claimed elsewhere
         w.rate[s] = __dmul_rn(w.sw[s], xs);
         const int nl = w.snl[s];
-        for (int a = 0; a < nl; ++a)
-          atomicAdd(&dnew[w.slink[(long long)s * FS_MAXL + a]], (unsigned)w.swi[s]);
+        bool sp = false;
+        for (int a = 0; a < nl; ++a) {
+          const int l2 = w.slink[(long long)s * FS_MAXL + a];
+          atomicAdd(&dnew[l2], (unsigned)w.swi[s]);
+          sp |= isb[l2] && l2 >= ls0 && l2 < ls1;
+        }
+        w.shit[s] = sp;
       }
       __syncthreads();
     }
@@ -626,7 +680,8 @@ __global__ void __launch_bounds__(FS_THREADS)
     for (int i = threadIdx.x; i < nflow; i += FS_THREADS) {
       if (!w.fact[i]) continue;
       double r = 0.0;
-      for (int s = w.fsub0[i]; s < w.fsub0[i + 1]; ++s) r = __dadd_rn(r, w.rate[s]);
+      for (int s = w.fsub0[i]; s < w.fsub0[i + 1]; ++s)
+        if (w.sact[s]) r = __dadd_rn(r, w.rate[s]);
       w.frate[i] = r;
       dmin = fmin(dmin, __ddiv_rn(w.rem[i], r));
       const int q = w.fmsg[i];
@@ -655,10 +710,31 @@ __global__ void __launch_bounds__(FS_THREADS)
         w.fact[i] = 0;
         ++ndone;
         for (int s = w.fsub0[i]; s < w.fsub0[i + 1]; ++s) {
+          if (!w.sact[s]) continue;
           w.sact[s] = 0;
           const int nl = w.snl[s];
           for (int a = 0; a < nl; ++a)
             atomicSub(&wbase[w.slink[(long long)s * FS_MAXL + a]], (unsigned)w.swi[s]);
+        }
+      } else if (plb && w.fsub0[i + 1] - w.fsub0[i] > 1 && w.flast[i] != events - 1) {
+        // PLB (R#36): a flow held back by a spine bottleneck re-hashes its spine
+        const int cur = w.fcur[i];
+        if (w.shit[cur]) {
+          const int q = w.fmsg[i];
+          const int att = ++w.fatt[i];
+          const int j = ecmp_rail(t.seed + (uint64_t)att * 0x9E3779B97F4A7C15ull, q / t.G,
+                                  q % t.G, t.S);
+          w.flast[i] = events;
+          const int nxt = w.fsub0[i] + j;
+          if (nxt != cur) {
+            w.sact[cur] = 0;
+            w.sact[nxt] = 1;
+            w.fcur[i] = nxt;
+            for (int a = 0; a < w.snl[cur]; ++a)
+              atomicSub(&wbase[w.slink[(long long)cur * FS_MAXL + a]], (unsigned)w.swi[cur]);
+            for (int a = 0; a < w.snl[nxt]; ++a)
+              atomicAdd(&wbase[w.slink[(long long)nxt * FS_MAXL + a]], (unsigned)w.swi[nxt]);
+          }
         }
       }
     }
@@ -784,7 +860,7 @@ size_t flowsim_workspace_bytes(const rails_topo_t& tp, const rails_fabric_t& fb,
 
 size_t flowsim_smem_bytes(const rails_topo_t& tp, const rails_fabric_t& fb) {
   const FsTopo t = fs_topo(tp, fb);
-  return (size_t)t.L * (8 + 8 + 4 + 4 + 4 + 4 + 4) + 16;
+  return (size_t)t.L * (8 + 8 + 4 + 4 + 4 + 4 + 4 + 1) + 16;
 }
 
 cudaError_t launch_flowsim_plan(const LaunchCtx& c, const rails_topo_t& tp,
@@ -792,7 +868,8 @@ cudaError_t launch_flowsim_plan(const LaunchCtx& c, const rails_topo_t& tp,
                                 const int64_t* msg, int64_t* totals) {
   const FsTopo t = fs_topo(tp, fb);
   FsOffsets o{};
-  k_fs_count<<<n_sim, FS_THREADS, 0, c.stream>>>(t, policy, msg, nullptr, o, 0, totals, 1);
+  k_fs_count<<<n_sim, FS_THREADS, 0, c.stream>>>(t, policy, msg, nullptr, o, 0, totals, 1,
+                                                 c.err);
   count_launch(1);
   return cudaGetLastError();
 }
@@ -804,7 +881,7 @@ cudaError_t launch_flowsim(const LaunchCtx& c, const rails_topo_t& tp, const rai
   const FsTopo t = fs_topo(tp, fb);
   const FsLayout lay = fs_layout(t.Q, t.L, capF, capS);
   FsOffsets o;
-  for (int i = 0; i < 32; ++i) o.o[i] = lay.o[i];
+  for (int i = 0; i < 40; ++i) o.o[i] = lay.o[i];
   uint8_t* base = (uint8_t*)ws_ + 256;
   uint8_t* sims = base;
   uint8_t* schw = sims + lay.stride * (size_t)n_sim;
@@ -827,7 +904,8 @@ cudaError_t launch_flowsim(const LaunchCtx& c, const rails_topo_t& tp, const rai
   if ((e = launch_schedule(c, n_sim, tp.M, 0, tp.M, tp.N, tp.chunk_bytes, msg, s, schw,
                            nullptr, 0)) != cudaSuccess)
     return e;
-  k_fs_count<<<n_sim, FS_THREADS, 0, c.stream>>>(t, policy, msg, sims, o, lay.stride, nullptr, 0);
+  k_fs_count<<<n_sim, FS_THREADS, 0, c.stream>>>(t, policy, msg, sims, o, lay.stride, nullptr, 0,
+                                                 c.err);
   k_fs_build<<<n_sim, FS_THREADS, 0, c.stream>>>(t, policy, msg, s.full_base, s.rem_rail, sims,
                                                  o, lay.stride, capF, capS, c.err);
   const size_t bsm = (size_t)t.L * 8;
@@ -846,7 +924,7 @@ cudaError_t launch_flowsim(const LaunchCtx& c, const rails_topo_t& tp, const rai
                                   (int)ssm)) != cudaSuccess)
       return e;
   }
-  k_fs_sim<<<n_sim, FS_THREADS, ssm, c.stream>>>(t, sims, o, lay.stride, capF, capS,
+  k_fs_sim<<<n_sim, FS_THREADS, ssm, c.stream>>>(t, policy, sims, o, lay.stride, capF, capS,
                                                  link_bytes, c.err);
   k_fs_finish<<<n_sim, FS_THREADS, 0, c.stream>>>(t, msg, sims, o, lay.stride, capF, capS,
                                                   msg_cct, stats);

@@ -525,7 +525,7 @@ def version() -> int:
 
 
 # ---------------------------------------------------------------- NEXT f4 (flowsim)
-FS_POLICIES = {"lpt": 0, "uniform": 1, "ecmp": 2, "reps": 3, "minrtt": 4}
+FS_POLICIES = {"lpt": 0, "uniform": 1, "ecmp": 2, "reps": 3, "minrtt": 4, "plb": 5}
 FS_STATS = ("T", "total", "busbw", "cct_mean", "cct_p80", "cct_p95", "cct_p99",
             "max_pair_frac", "events", "flows")
 

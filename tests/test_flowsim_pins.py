@@ -185,3 +185,34 @@ def test_receiver_skew_rails_beats_fixed_nic_policies():
     lpt = _sim(M, N, msg, "lpt", C=65536)
     for pol in ("ecmp", "reps", "minrtt"):
         assert _sim(M, N, msg, pol, C=65536)["T"] > 1.5 * lpt["T"]
+
+
+def test_plb_equals_ecmp_without_spine_congestion():
+    # R#36: PLB only repaths flows whose rate a spine link set; with spines far
+    # faster than the NICs that never happens and PLB is ECMP, event for event
+    rng = np.random.default_rng(21)
+    M, N = 4, 4
+    msg = _rand_msg(rng, M, N, 3_000_000)
+    kw = dict(S=N, R1=8 * R2, R2=R2, Rs=100 * R2)
+    e = oracle.flowsim(M, N, kw["S"], kw["R1"], R2, kw["Rs"], 65536, "ecmp", msg)
+    p = oracle.flowsim(M, N, kw["S"], kw["R1"], R2, kw["Rs"], 65536, "plb", msg)
+    assert np.array_equal(e["msg_cct"], p["msg_cct"])
+    assert e["events"] == p["events"]
+
+
+def test_plb_repaths_under_spine_congestion():
+    # oversubscribed spines (Rs = R2/4): ECMP's hashed spine links are the
+    # bottlenecks, PLB moves flows off them at completion events -- its spine
+    # link loads differ from ECMP's, the bytes conserved and T still >= T*
+    rng = np.random.default_rng(22)
+    M, N = 4, 4
+    msg = _rand_msg(rng, M, N, 3_000_000)
+    Rs = R2 / 4
+    e = oracle.flowsim(M, N, N, 8 * R2, R2, Rs, 65536, "ecmp", msg)
+    p = oracle.flowsim(M, N, N, 8 * R2, R2, Rs, 65536, "plb", msg)
+    ids = _link_ids(M, N, N)
+    sp = slice(ids["leaf_spine"], ids["nic_down"])
+    assert not np.allclose(e["link_bytes"][sp], p["link_bytes"][sp])
+    tot = float(msg.sum())
+    assert p["link_bytes"][ids["nic_up"]:ids["leaf_spine"]].sum() == pytest.approx(tot, rel=1e-9)
+    assert p["T"] >= msg.sum(axis=(1, 2)).max() / (N * R2) * (1 - 1e-9)

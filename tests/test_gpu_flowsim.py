@@ -20,7 +20,7 @@ if torch.cuda.is_available():
 DEV = "cuda:0"
 R2 = 100e9 / 8
 TOL = 1e-6
-POLS = ["lpt", "uniform", "ecmp", "reps", "minrtt"]
+POLS = ["lpt", "uniform", "ecmp", "reps", "minrtt", "plb"]
 
 
 @pytest.fixture(autouse=True)
@@ -60,18 +60,19 @@ def _close(a, b, what):
     assert err.max(initial=0) <= TOL, f"{what}: max rel err {err.max():g}"
 
 
-@pytest.mark.parametrize("M,N,S,C,kind", [
-    (3, 2, 2, 65536, "rand"),
-    (4, 4, 4, 65536, "rand"),
-    (4, 4, 4, 1 << 20, "uniform"),
-    (4, 4, 2, 262144, "recv"),      # fewer spines than rails
-    (5, 3, 3, 131072, "sender"),    # N not a power of two
-    (6, 4, 4, 1 << 20, "sparse"),
+@pytest.mark.parametrize("M,N,S,C,kind,rs", [
+    (3, 2, 2, 65536, "rand", None),
+    (4, 4, 4, 65536, "rand", None),
+    (4, 4, 4, 65536, "rand", 0.25),      # oversubscribed spines: PLB repaths
+    (4, 4, 4, 1 << 20, "uniform", None),
+    (4, 4, 2, 262144, "recv", None),     # fewer spines than rails
+    (5, 3, 3, 131072, "sender", 0.5),    # N not a power of two
+    (6, 4, 4, 1 << 20, "sparse", None),
 ])
-def test_flowsim_parity(M, N, S, C, kind):
+def test_flowsim_parity(M, N, S, C, kind, rs):
     msg = _workload(kind, M, N, M * 10 + N)
     tp = rails.topo(M, N, C, R2=R2)
-    fb = rails.fabric(M, N, R2, S=S)
+    fb = rails.fabric(M, N, R2, S=S, Rs=None if rs is None else rs * R2)
     pol = torch.tensor([rails.FS_POLICIES[p] for p in POLS], dtype=torch.int32, device=DEV)
     msgs = torch.from_numpy(np.stack([msg] * len(POLS))).to(DEV)
     cct, lb, st = rails.flowsim(tp, fb, pol, msgs)
@@ -97,8 +98,8 @@ def test_flowsim_spec_single_flow():
     msg[0, 0, 1] = 64_000_000
     tp = rails.topo(M, N, 1 << 30, R2=R2)
     fb = rails.fabric(M, N, R2)
-    pol = torch.arange(5, dtype=torch.int32, device=DEV)
-    cct, lb, st = rails.flowsim(tp, fb, pol, torch.from_numpy(np.stack([msg] * 5)).to(DEV))
+    pol = torch.arange(6, dtype=torch.int32, device=DEV)
+    cct, lb, st = rails.flowsim(tp, fb, pol, torch.from_numpy(np.stack([msg] * 6)).to(DEV))
     assert np.allclose(st[:, 0].cpu().numpy(), 5.12e-3, rtol=1e-12)
 
 
@@ -114,3 +115,16 @@ def test_flowsim_batch_independent():
     mix = rails.flowsim(tp, fb, pol.repeat(2), torch.from_numpy(
         np.stack([b, b, b, a, a, a])).to(DEV))[2]
     assert torch.equal(one, mix[3:])  # deterministic, bit for bit
+
+
+def test_flowsim_bad_policy_flagged():
+    M, N = 2, 1
+    msg = np.zeros((1, M, N, M * N), np.int64)
+    msg[0, 0, 0, 1] = 1000
+    tp = rails.topo(M, N, 4096, R2=R2)
+    fb = rails.fabric(M, N, R2)
+    pol = torch.tensor([9], dtype=torch.int32, device=DEV)
+    rails.flowsim(tp, fb, pol, torch.from_numpy(msg).to(DEV))
+    with pytest.raises(rails.RailsError) as ei:
+        rails.check()
+    assert ei.value.code == rails.RAILS_ERANGE

@@ -26,7 +26,7 @@ import gen  # noqa: E402
 from paper_2510_19262_b200 import rails  # noqa: E402
 
 DEV = "cuda:0"
-POLS = ["lpt", "uniform", "ecmp", "reps", "minrtt"]
+POLS = ["lpt", "uniform", "ecmp", "reps", "minrtt", "plb"]
 
 
 def family_msg(fam, M, N, V, seed, u):
@@ -51,6 +51,7 @@ def main():
                                           "sender,receiver")
     ap.add_argument("--iters", type=int, default=2)
     ap.add_argument("--oracle", type=int, default=5, help="oracle sample: simulations timed")
+    ap.add_argument("--rs", type=float, default=None, help="leaf-spine rate / R2 (default M/S)")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     M, N, C = a.M, a.N, a.C
@@ -67,7 +68,7 @@ def main():
                 pols.append(rails.FS_POLICIES[p])
                 keys.append((fam, u, p))
     tp = rails.topo(M, N, C, R2=R2)
-    fb = rails.fabric(M, N, R2, S=S)
+    fb = rails.fabric(M, N, R2, S=S, Rs=None if a.rs is None else a.rs * R2)
     msg_t = torch.from_numpy(np.stack(msgs)).to(DEV)
     pol_t = torch.tensor(pols, dtype=torch.int32, device=DEV)
     rails.flowsim(tp, fb, pol_t, msg_t)  # warm-up (also sizes the workspace)
@@ -85,7 +86,8 @@ def main():
     ms = min(ts)
     n_sim = len(keys)
     ev = float(st[:, 8].sum())
-    res = {"M": M, "N": N, "S": S, "V": a.V, "C": C, "units": a.units, "families": fams,
+    res = {"M": M, "N": N, "S": S, "Rs_over_R2": fb.Rs / R2, "V": a.V, "C": C, "units": a.units,
+           "families": fams,
            "n_sim": n_sim, "batch_ms": ms, "sims_per_s": n_sim / (ms / 1e3),
            "events": ev, "events_per_s": ev / (ms / 1e3),
            "flows": float(st[:, 9].sum()), "max_sim_events": float(st[:, 8].max())}
