@@ -64,37 +64,52 @@ __global__ void __launch_bounds__(THREADS)
     iB = iA + cap;
   }
 
+  // Pass over the messages in tiles of THREADS * IPT, each thread owning IPT
+  // consecutive messages: its loads are all in flight at once and one block scan
+  // per tile gives the running (full chunks, remainders) prefix.
+  constexpr int IPT = 8;
   long long carry_full = 0;
   int carry_rem = 0;
   KeyT kor = 0, kand = (KeyT)~(KeyT)0;
-  for (long long t0 = 0; t0 < NG; t0 += THREADS) {
-    const long long m = t0 + threadIdx.x;
-    long long B = 0;
-    if (m < NG) {
-      B = mg[m];
+  for (long long t0 = 0; t0 < NG; t0 += (long long)THREADS * IPT) {
+    const long long m0 = t0 + (long long)threadIdx.x * IPT;
+    long long B[IPT];
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) B[j] = m0 + j < NG ? mg[m0 + j] : 0;
+    long long snf = 0;
+    int srem = 0;
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+      const long long m = m0 + j;
       // negative bytes, or bytes to a GPU of the source node (R#2), are invalid
-      if (B < 0 || (B != 0 && (int)((unsigned)m % (unsigned)G) / N == d)) {
+      if (B[j] < 0 || (B[j] != 0 && (int)((unsigned)m % (unsigned)G) / N == d)) {
         flag_error(err, ERR_RANGE);
-        B = 0;
+        B[j] = 0;
       }
+      const long long nf = cd.div(B[j]);
+      if (nf >= (1LL << 40)) flag_error(err, ERR_OVERFLOW);
+      snf += nf;
+      srem += (B[j] - nf * C) > 0;
     }
-    const long long nf = cd.div(B);
-    const long long rem = B - nf * C;
-    const int fl = rem > 0;
-    if (nf >= (1LL << 40)) flag_error(err, ERR_OVERFLOW);
     long long tot;
-    const long long ex = block_excl_scan((nf << 16) | fl, scan_scratch, &tot);
-    if (m < NG) {
-      full_base[seg * NG + m] = carry_full + (ex >> 16);
-      if (fl) {
-        const int pos = carry_rem + (int)(ex & 0xffff);
+    const long long ex = block_excl_scan((snf << 16) | srem, scan_scratch, &tot);
+    long long fb = carry_full + (ex >> 16);
+    int pos = carry_rem + (int)(ex & 0xffff);
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+      const long long m = m0 + j;
+      if (m >= NG) break;
+      const long long nf = cd.div(B[j]);
+      const long long rem = B[j] - nf * C;
+      full_base[seg * NG + m] = fb;
+      fb += nf;
+      if (rem > 0) {
         const KeyT key = (KeyT)(C - 1 - rem);
         kA[pos] = key;
         iA[pos] = (IdxT)m;
         kor |= key;
         kand &= key;
-      } else {
-        ws_inv[seg * NG + m] = -1;  // no remainder chunk
+        ++pos;
       }
     }
     carry_full += tot >> 16;
@@ -111,10 +126,19 @@ __global__ void __launch_bounds__(THREADS)
   const int which = radix_sort<KeyT, IdxT>(kA, iA, kB, iB, n, kor, kand, nbits, hist, sc);
   const KeyT* ks = which ? kB : kA;
   const IdxT* is = which ? iB : iA;
+  // inverse permutation in the free index buffer, then written out coalesced
+  // (message m -> sorted position of its remainder, -1 if none)
+  IdxT* inv = which ? iA : iB;
+  constexpr IdxT NONE = (IdxT)~(IdxT)0;
+  for (long long m = threadIdx.x; m < NG; m += THREADS) inv[m] = NONE;
+  __syncthreads();
   for (int i = threadIdx.x; i < n; i += THREADS) {
     ws_w[seg * NG + i] = (uint32_t)(C - 1 - (long long)ks[i]);
-    ws_inv[seg * NG + is[i]] = i;  // sorted position of message is[i]'s remainder
+    inv[is[i]] = (IdxT)i;
   }
+  __syncthreads();
+  for (long long m = threadIdx.x; m < NG; m += THREADS)
+    ws_inv[seg * NG + m] = inv[m] == NONE ? -1 : (int32_t)inv[m];
 }
 
 // ---------------------------------------------------------------- a4 chain
@@ -566,9 +590,11 @@ __global__ void __launch_bounds__(128)
 
 // LPT chain implementation: 0 = thread-per-chain when N allows (default),
 // 1 = warp-per-chain (RAILS_CHAIN_IMPL=1, kept as the reference path).
+// RAILS_CHAIN_IMPL: 1 = generic warp chain, 2 = warp-staged (the default),
+// 3 = thread-per-chain (measurement overrides)
 static int chain_impl() {
   const char* e = getenv("RAILS_CHAIN_IMPL");
-  return (e && e[0] == '1') ? 1 : 0;
+  return (e && e[0] >= '1' && e[0] <= '3') ? e[0] - '0' : 0;
 }
 
 static int ceil_log2(long long x) {  // bits needed for values 0..x-1
@@ -713,8 +739,12 @@ cudaError_t launch_schedule(const LaunchCtx& c, int U, int nd, int d0, int M, in
   }
   count_launch(1);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  if (C < (1LL << 23) && chain_impl() == 0 && (N == 2 || N == 4 || N == 8 || N == 16) &&
-      nseg <= (long long)c.num_sms * 8) {
+  const int ci = chain_impl();
+  const bool nt_ok = C < (1LL << 23) && (N == 2 || N == 4 || N == 8 || N == 16);
+  // warp-staged chains by default: measured faster than thread-per-chain for few
+  // long chains (C3, C5) and for many (C2: 16 000, C4: 4 096), since runs of
+  // equal sizes are written by whole warps and the list staging hides latency
+  if (nt_ok && (ci == 0 || ci == 2)) {
     const unsigned wgrid = (unsigned)((nseg + WS_WARPS - 1) / WS_WARPS);
 #define RAILS_WS_CHAIN(NT)                                                                  \
   if (N == NT)                                                                              \
@@ -725,7 +755,7 @@ cudaError_t launch_schedule(const LaunchCtx& c, int U, int nd, int d0, int M, in
     RAILS_WS_CHAIN(8)
     RAILS_WS_CHAIN(16)
 #undef RAILS_WS_CHAIN
-  } else if (C < (1LL << 23) && chain_impl() == 0 && (N == 2 || N == 4 || N == 8 || N == 16)) {
+  } else if (nt_ok && ci != 1) {
     // chains per warp: fill ~8 warps per SM before packing lanes (LSU sharing)
     long long cpw = nseg / ((long long)c.num_sms * 8);
     cpw = cpw < 1 ? 1 : (cpw > 32 ? 32 : cpw);

@@ -440,3 +440,18 @@ def test_determinism_repeat():
 
 def test_report_max_float_error():
     print(f"max relative float error observed vs oracle: {MAX_ERR['v']:.3g}")
+
+
+@pytest.mark.parametrize("impl", ["1", "3"])
+def test_schedule_parity_alternate_chain_kernels(impl, monkeypatch):
+    # the generic warp chain (1) and the thread-per-chain kernel (3) stay
+    # selectable (RAILS_CHAIN_IMPL) and exact
+    monkeypatch.setenv("RAILS_CHAIN_IMPL", impl)
+    rng = np.random.default_rng(77)
+    for (M, N, C, U, mult) in [(40, 8, 32768, 4, 12288), (5, 4, 65536, 2, 1), (30, 2, 4096, 3, 100)]:
+        msg = random_msg(rng, U, M, N, p=0.8, hi=40, mult=mult) if mult > 1 else \
+            random_msg(rng, U, M, N, p=0.8, hi=400000)
+        s = rails.lpt_schedule(rails.topo(M, N, C), rails.shard(U, 0, M), torch.from_numpy(msg).to(DEV))
+        for u in range(U):
+            for d in range(M):
+                compare_schedule(s, u, d, oracle.schedule_node(msg[u, d], C), f"impl{impl} u{u} d{d}")
