@@ -171,8 +171,9 @@ __device__ __forceinline__ void divmod_n(long long a, int N, long long& q, int& 
   }
 }
 
+template <int NT>  // NT = N when it is a power of two <= 32 (divisions by shifts), else 0
 __global__ void __launch_bounds__(EV2_THREADS)
-    k_eval_node2(int M, int N, int nd, int d0, long long C, int cshift, uint64_t seed, int FT,
+    k_eval_node2(int M, int N_rt, int nd, int d0, long long C, int cshift, uint64_t seed, int FT,
                  const int64_t* __restrict__ msg, const int64_t* __restrict__ full_base,
                  const int8_t* __restrict__ rem_rail, const int64_t* __restrict__ n_full,
                  int64_t* __restrict__ S, int64_t* __restrict__ S_e, double* __restrict__ mse,
@@ -180,6 +181,7 @@ __global__ void __launch_bounds__(EV2_THREADS)
                  int64_t* __restrict__ red_max, long long rsl) {
   extern __shared__ __align__(16) uint8_t ev_smem[];
   __shared__ unsigned long long sS[32], sSe[32];
+  const int N = NT ? NT : N_rt;
   const long long seg = blockIdx.x;
   const long long u = seg / nd;
   const int d = d0 + (int)(seg % nd);
@@ -200,7 +202,8 @@ __global__ void __launch_bounds__(EV2_THREADS)
   uint32_t* sRem = (uint32_t*)(sB + TM);               // [TM]
   int8_t* sRr = (int8_t*)(sRem + TM);                  // [TM]
   int8_t* sE = sRr + TM;                               // [TM]
-  long long* sQ = (long long*)(((uintptr_t)(sE + TM) + 15) & ~(uintptr_t)15);  // [N][FT+1]
+  // (offsets from ev_smem, not integer casts, so the compiler keeps shared loads)
+  long long* sQ = (long long*)(ev_smem + ((size_t)TM * 14 + 15) / 16 * 16);  // [N][FT+1]
   int* sR = (int*)(sQ + N * (FT + 1));                 // [N][FT+1]
   __shared__ unsigned long long sCol[64];
 
@@ -208,6 +211,9 @@ __global__ void __launch_bounds__(EV2_THREADS)
     sS[threadIdx.x] = 0;
     sSe[threadIdx.x] = 0;
   }
+  const bool pow2 = NT != 0;
+  unsigned long long accS = 0, accSe = 0;
+  __shared__ unsigned long long sAcc[2][EV2_THREADS];
   for (int f0 = 0; f0 < M; f0 += FT) {
     const int ft = min(FT, M - f0);
     const int tm = N * ft * N;
@@ -247,12 +253,17 @@ __global__ void __launch_bounds__(EV2_THREADS)
       sR[g * (FT + 1) + fl] = r;
     }
     __syncthreads();
-    // stage 2: thread per (fl, j)
-    for (int t = threadIdx.x; t < ft * N; t += EV2_THREADS) {
+    // stage 2: thread per (fl, j).  N a power of two: j = t mod N is the same for a
+    // thread in every tile, so S / S_e accumulate in registers and the column sum
+    // of fl is a shuffle reduction over its N consecutive lanes (64-bit shared
+    // atomics are CAS loops on this GPU); other N use shared atomics.
+    for (int t0 = 0; t0 < ft * N; t0 += EV2_THREADS) {
+      const int t = t0 + threadIdx.x;
+      const bool act = t < ft * N;
       const int fl = t / N, j = t - (t / N) * N;
       const int f = f0 + fl;
       long long full = 0, Rv = 0, Rev = 0;
-      if (f != d) {
+      if (act && f != d) {
         for (int g = 0; g < N; ++g) {
           const long long qa = sQ[g * (FT + 1) + fl], qb = sQ[g * (FT + 1) + fl + 1];
           const int ra = sR[g * (FT + 1) + fl], rb = sR[g * (FT + 1) + fl + 1];
@@ -265,19 +276,39 @@ __global__ void __launch_bounds__(EV2_THREADS)
         }
         Rv += full * C;
       }
-      if (Rv) {
-        atomicAdd(R + (long long)f * N + j, (unsigned long long)Rv);
-        atomicAdd(&sS[j], (unsigned long long)Rv);
-        atomicAdd(&sCol[fl], (unsigned long long)Rv);
-      }
-      if (Rev) {
-        atomicAdd(Re + (long long)f * N + j, (unsigned long long)Rev);
-        atomicAdd(&sSe[j], (unsigned long long)Rev);
+      if (Rv) atomicAdd(R + (long long)f * N + j, (unsigned long long)Rv);
+      if (Rev) atomicAdd(Re + (long long)f * N + j, (unsigned long long)Rev);
+      if (pow2) {
+        accS += (unsigned long long)Rv;
+        accSe += (unsigned long long)Rev;
+        unsigned long long v = (unsigned long long)Rv;
+        for (int o = 1; o < N; o <<= 1) v += __shfl_xor_sync(FULL, v, o);
+        if (act && j == 0) sCol[fl] = v;
+      } else {
+        if (Rv) {
+          atomicAdd(&sS[j], (unsigned long long)Rv);
+          atomicAdd(&sCol[fl], (unsigned long long)Rv);
+        }
+        if (Rev) atomicAdd(&sSe[j], (unsigned long long)Rev);
       }
     }
     __syncthreads();
     for (int fl = threadIdx.x; fl < ft; fl += EV2_THREADS)
       if (sCol[fl]) atomicAdd(col + f0 + fl, sCol[fl]);
+  }
+  if (pow2) {  // per-rail totals of the register partials (thread t holds rail t mod N)
+    sAcc[0][threadIdx.x] = accS;
+    sAcc[1][threadIdx.x] = accSe;
+    __syncthreads();
+    if (threadIdx.x < N) {
+      unsigned long long a = 0, b = 0;
+      for (int t = threadIdx.x; t < EV2_THREADS; t += N) {
+        a += sAcc[0][t];
+        b += sAcc[1][t];
+      }
+      sS[threadIdx.x] = a;
+      sSe[threadIdx.x] = b;
+    }
   }
   __syncthreads();
   if (threadIdx.x >= 32) return;
@@ -402,10 +433,14 @@ cudaError_t launch_eval(const LaunchCtx& c, int U, int nd, int d0, int M, int N,
     const int FT = (EV2_THREADS / N) < 64 ? (EV2_THREADS / N) : 64;
     const size_t tm = (size_t)N * FT * N;
     const size_t smem = tm * (8 + 4 + 1 + 1) + 16 + (size_t)N * (FT + 1) * (8 + 4);
-    err = cudaFuncSetAttribute(k_eval_node2, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem);
+    void (*kern)(int, int, int, int, long long, int, uint64_t, int, const int64_t*,
+                 const int64_t*, const int8_t*, const int64_t*, int64_t*, int64_t*, double*,
+                 double*, int64_t*, int64_t*, long long) =
+        N == 2 ? k_eval_node2<2> : N == 4 ? k_eval_node2<4> : N == 8 ? k_eval_node2<8>
+        : N == 16 ? k_eval_node2<16> : N == 32 ? k_eval_node2<32> : k_eval_node2<0>;
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
-    k_eval_node2<<<(unsigned)((long long)U * nd), EV2_THREADS, smem, c.stream>>>(
+    kern<<<(unsigned)((long long)U * nd), EV2_THREADS, smem, c.stream>>>(
         M, N, nd, d0, C, pow2_shift(C), seed, FT, msg, s.full_base, s.rem_rail, s.n_full, e.S,
         e.S_e, e.mse, e.nmse, e.red_sum, e.red_max, rsl);
   }
