@@ -250,7 +250,9 @@ def main():
             gen.payload(M, N, T, RB, seed, u, d0, nd, device=dev, out=x[u])
         pipe = RoutingPipeline(M, N, T, k, RB, C, U, d0, nd, lut.numel(), dev)
 
-        def step(ev_p0, ev_p1):
+        def step(ev_p0, ev_p1, ev_s0=None):
+            if ev_s0 is not None:
+                ev_s0.record(stream)
             pipe.schedule_part(topk, lut)
             pipe.finalize_part(reduce if dist is not None else None)
             rails.rail_offsets(pipe.tp, pipe.sh, pipe.sched.send_load, pipe.rail_base, pipe.total)
@@ -262,7 +264,9 @@ def main():
         msg = torch.from_numpy(gen.d1_units(cfg, seed, 0, U)[:, d0:d0 + nd].copy()).to(dev)
         pipe = MatrixPipeline(M, N, C, U, d0, nd, dev)
 
-        def step(ev_p0, ev_p1):
+        def step(ev_p0, ev_p1, ev_s0=None):
+            if ev_s0 is not None:
+                ev_s0.record(stream)
             ev_p0.record(stream)
             pipe.step(msg, reduce if dist is not None else None)
             ev_p1.record(stream)
@@ -277,6 +281,7 @@ def main():
     # timed region
     # per-step events around the dominant kernel (k_pack), on its launch stream
     kev = [evpair() for _ in range(args.steps)]
+    sev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
@@ -286,7 +291,7 @@ def main():
         t_all1 = torch.cuda.Event(enable_timing=True)
         t_all0.record(stream)
         for i in range(args.steps):
-            step(*kev[i])
+            step(*kev[i], sev[i])
         t_all1.record(stream)
         torch.cuda.synchronize()
     launches = rails.launch_count(reset=True)
@@ -295,6 +300,12 @@ def main():
     total_ms = t_all0.elapsed_time(t_all1)
     kern_avg_ms = sum(a.elapsed_time(b) for a, b in kev) / len(kev)
     pack_avg_ms = kern_avg_ms
+    # schedule part of the step (K1-K5 + the a6 NCCL reduction + rail offsets; the
+    # SURVEY d.1 "LPT-scheduled nodes/s", pack excluded)
+    if cfg["kind"] == "routing":
+        sched_avg_ms = sum(sev[i].elapsed_time(kev[i][0]) for i in range(args.steps)) / args.steps
+    else:
+        sched_avg_ms = kern_avg_ms
     rails.check()
 
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -309,6 +320,13 @@ def main():
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
            "data": "synthetic"}
+    ts = torch.tensor([sched_avg_ms], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(ts, op=dist.ReduceOp.MAX)
+    out["schedule_only"] = {"value": nodes / (float(ts.item()) / 1000.0), "unit": "nodes/s",
+                            "ms_per_step": float(ts.item()),
+                            "what": "histogram + chunk/sort + LPT + eval + NCCL reduction + "
+                                    "rail offsets per step, pack excluded (SURVEY 8(d) d.1)"}
     fin = {kk: vv.cpu() for kk, vv in pipe.final.items()}
     quality = {"T_lpt_over_Tstar": float((fin["T"] / fin["T_star"]).max()),
                "T_ecmp_over_Tstar": float((fin["T_e"] / fin["T_star"]).max()),
