@@ -161,6 +161,11 @@ __device__ __forceinline__ void bf16x8_fma(float* acc, const uint4& v, float w) 
   }
 }
 
+// KS = k known at compile time (1 or 2): the window issues every slot's loads
+// before the first multiply-add (the slots' rows are independent gathers), with
+// the per-slot metadata broadcast once per token.  KS = 0: any k, slot by slot.
+// The fp32 sum is formed in slot order either way (R#31).
+template <int KS>
 __global__ void __launch_bounds__(UP_THREADS)
     k_unpack_combine(int U, int nd, int d0, int M, int N, int T, int k, long long C, int cshift,
                      const int32_t* __restrict__ topk, const int32_t* __restrict__ lut,
@@ -226,6 +231,72 @@ __global__ void __launch_bounds__(UP_THREADS)
       }
     }
     float* dst = out + tok * (RB >> 1);
+    if constexpr (KS > 0) {
+      constexpr int VW = KS == 1 ? 4 : 2;
+      int okv[KS], inv_[KS], bsv[KS];
+      float wsv[KS];
+      long long Av[KS], Bv[KS], P0v[KS], MIv[KS], NFv[KS], FBv[KS];
+#pragma unroll
+      for (int sl = 0; sl < KS; ++sl) {
+        okv[sl] = __shfl_sync(FULL, ok, sl);
+        wsv[sl] = __shfl_sync(FULL, w, sl);
+        inv_[sl] = __shfl_sync(FULL, intra, sl);
+        Av[sl] = __shfl_sync(FULL, srcA, sl);
+        Bv[sl] = __shfl_sync(FULL, srcB, sl);
+        bsv[sl] = __shfl_sync(FULL, bsplit, sl);
+        P0v[sl] = __shfl_sync(FULL, p0, sl);
+        MIv[sl] = __shfl_sync(FULL, mi, sl);
+        NFv[sl] = __shfl_sync(FULL, nfull, sl);
+        FBv[sl] = __shfl_sync(FULL, fblk, sl);
+      }
+      for (int w0 = 0; w0 < nvec; w0 += VW * 32) {
+        uint4 v[KS][VW];
+#pragma unroll
+        for (int sl = 0; sl < KS; ++sl) {
+#pragma unroll
+          for (int i = 0; i < VW; ++i) {
+            const int vi = w0 + i * 32 + lane;
+            v[sl][i] = make_uint4(0, 0, 0, 0);
+            if (okv[sl] && vi < nvec) {
+              const long long o = (long long)vi << 4;
+              if (inv_[sl]) {
+                v[sl][i] = ld_stream((const uint4*)((const uint8_t*)y + Av[sl] + o));
+              } else {
+                long long addr;
+                if (o < bsv[sl]) addr = Av[sl] + o;
+                else if (C >= RB) addr = Bv[sl] + (o - bsv[sl]);
+                else addr = msg_byte_addr(P0v[sl] + o, MIv[sl], NFv[sl], s, N, C, cd,
+                                          rail_base_c + FBv[sl] * N);
+                v[sl][i] = ld_stream((const uint4*)(comb_out + addr));
+              }
+            }
+          }
+        }
+        float acc[VW * 8];
+#pragma unroll
+        for (int q = 0; q < VW * 8; ++q) acc[q] = 0.f;
+#pragma unroll
+        for (int sl = 0; sl < KS; ++sl) {
+          if (!okv[sl]) continue;
+#pragma unroll
+          for (int i = 0; i < VW; ++i) bf16x8_fma(acc + 8 * i, v[sl][i], wsv[sl]);
+        }
+#pragma unroll
+        for (int i = 0; i < VW; ++i) {
+          const int vi = w0 + i * 32 + lane;
+          if (vi < nvec) {
+            float4* p = (float4*)(dst + (long long)vi * 8);
+            st_cs((uint4*)p, make_uint4(__float_as_uint(acc[8 * i]), __float_as_uint(acc[8 * i + 1]),
+                                        __float_as_uint(acc[8 * i + 2]),
+                                        __float_as_uint(acc[8 * i + 3])));
+            st_cs((uint4*)p + 1,
+                  make_uint4(__float_as_uint(acc[8 * i + 4]), __float_as_uint(acc[8 * i + 5]),
+                             __float_as_uint(acc[8 * i + 6]), __float_as_uint(acc[8 * i + 7])));
+          }
+        }
+      }
+      continue;
+    }
     for (int w0 = 0; w0 < nvec; w0 += UP_VW * 32) {
       float acc[UP_VW * 8];
 #pragma unroll
@@ -340,8 +411,12 @@ cudaError_t launch_unpack_combine(const LaunchCtx& c, int U, int nd, int d0, int
                                   const rails_sched_t& s, const int64_t* rail_base_c,
                                   const void* comb_out, float* out, long long RB) {
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_unpack_combine,
-                                                                UP_THREADS, 0);
+  void (*kern)(int, int, int, int, int, int, int, long long, int, const int32_t*,
+               const int32_t*, int, const int32_t*, const float*, const uint4*, long long,
+               const int64_t*, const int64_t*, CSched, const int64_t*, const uint8_t*, float*,
+               long long, int*) =
+      k == 1 ? k_unpack_combine<1> : k == 2 ? k_unpack_combine<2> : k_unpack_combine<0>;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, UP_THREADS, 0);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   const long long toks = (long long)U * nd * N * T;
@@ -350,7 +425,7 @@ cudaError_t launch_unpack_combine(const LaunchCtx& c, int U, int nd, int d0, int
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
   CSched cs{s.full_base, s.rem_rail, s.rem_off};
-  k_unpack_combine<<<(unsigned)grid, UP_THREADS, 0, c.stream>>>(
+  kern<<<(unsigned)grid, UP_THREADS, 0, c.stream>>>(
       U, nd, d0, M, N, T, k, C, cshift_of(C), topk, lut, n_inst, rank, w, (const uint4*)y, Rcap,
       in_off, msgc, cs, rail_base_c, (const uint8_t*)comb_out, out, RB, c.err);
   count_launch(1);

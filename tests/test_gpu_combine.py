@@ -31,6 +31,8 @@ def _need_cuda():
     (4, 4, 200, 2, 8, 256, 1024, 2),     # C >= RB
     (3, 2, 150, 3, 6, 512, 192, 1),      # C < RB, C not a power of two
     (5, 4, 64, 2, 8, 4096, 32768, 1),    # 4 KiB rows, 32 KiB chunks
+    (3, 2, 150, 2, 6, 512, 192, 1),      # k = 2 (two-slot kernel) with C < RB
+    (4, 4, 100, 1, 8, 1024, 4096, 2),    # k = 1 (one-slot kernel)
 ])
 def test_combine_round_and_unpack(M, N, T, k, E, RB, C, U):
     G = M * N
