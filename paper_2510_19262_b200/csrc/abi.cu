@@ -86,10 +86,11 @@ static int check_shard(const rails_topo_t* t, const rails_shard_t* s) {
 
 static bool al(const void* p, size_t a) { return ((uintptr_t)p % a) == 0; }
 
-// Pack implementation: RAILS_PACK_IMPL=1 (LDG/STG) or 2 (TMA bulk); default below.
+// Pack implementation: RAILS_PACK_IMPL=1 (LDG/STG), 2 (TMA bulk), 3 (TMA bulk with
+// batched metadata); default below.
 static int pack_impl() {
   const char* e = getenv("RAILS_PACK_IMPL");
-  if (e && (e[0] == '1' || e[0] == '2')) return e[0] - '0';
+  if (e && e[0] >= '1' && e[0] <= '3') return e[0] - '0';
   return 1;
 }
 }  // namespace rails

@@ -419,6 +419,159 @@ __global__ void __launch_bounds__(TMA_WARPS * 32)
   if (lane == 0) bulk_wait_all();
 }
 
+// ---------------------------------------------------------------- TMA pipeline v2
+// C >= RB only (a row copy spans at most two chunks).  As k_pack_tma, but the
+// slot metadata -- a chain of dependent loads (routing -> LUT -> message tables
+// -> rail base) -- is computed for 32 rows at once, one row per lane, into a
+// per-warp shared table, so its latency is paid once per 32 rows instead of once
+// per row on the issuing path.  W warps per CTA, S row stages per warp, loads D
+// rows ahead.
+constexpr int TMA2_MAXK = 4;
+struct TmaMeta2 {
+  long long dst0, dst1;  // output address of row byte 0 / of chunk c0+1
+  int b0, ok;            // row bytes in chunk c0; remote and valid
+};
+
+template <int S, int D, int W>
+__global__ void __launch_bounds__(W * 32)
+    k_pack_tma2(int U, int nd, int d0, int M, int N, int T, int k, long long C, int cshift,
+                const uint8_t* __restrict__ x, const int32_t* __restrict__ topk,
+                const int32_t* __restrict__ lut, int n_inst, const int32_t* __restrict__ rank,
+                const int64_t* __restrict__ msg, long long RB,
+                const int64_t* __restrict__ full_base, const int8_t* __restrict__ rem_rail,
+                const int64_t* __restrict__ rem_off, const int64_t* __restrict__ rail_base,
+                uint8_t* __restrict__ out, long long out_cap, int* err) {
+  static_assert(D >= 1 && D < S, "prefetch distance");
+  extern __shared__ __align__(128) uint8_t sbuf[];
+  __shared__ __align__(8) uint64_t bars[W][S];
+  __shared__ TmaMeta2 meta[W][32][TMA2_MAXK];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long nwarps = (long long)gridDim.x * W;
+  const long long rows = (long long)U * nd * N * T;
+  const long long G = (long long)M * N;
+  const ChunkDiv cd{C, cshift};
+  uint8_t* buf = sbuf + (size_t)wid * S * RB;
+  uint64_t* bar = bars[wid];
+  const long long row0 = (long long)blockIdx.x * W + wid;
+  if (lane == 0) {
+    for (int q = 0; q < S; ++q) mbar_init(&bar[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  // metadata of this warp's rows j0 .. j0+31 (lane l: row j0 + l)
+  auto make_meta32 = [&](long long j0) {
+    const long long row = row0 + (j0 + lane) * nwarps;
+    for (int sl = 0; sl < k; ++sl) {
+      TmaMeta2 m{0, 0, 0, 0};
+      if (row < rows) {
+        const long long ug = row / T;
+        const long long ul = ug / N;
+        const int d = d0 + (int)(ul % nd);
+        const int64_t* __restrict__ rbase = rail_base + ul * N;
+        const long long e = row * k + sl;
+        const int inst = __ldg(topk + e);
+        int h = (inst >= 0 && inst < n_inst) ? __ldg(lut + inst) : -1;
+        if (h < 0 || h >= G) {
+          flag_error(err, ERR_RANGE);
+          h = -1;
+        }
+        if (h >= 0 && h / N != d) {
+          const long long mi = ug * G + h;
+          const long long B = msg[mi];
+          const int rk = rank[e];
+          const long long p0 = (long long)rk * RB;
+          if (rk < 0 || p0 + RB > B) {
+            flag_error(err, ERR_RANGE);
+          } else {
+            const long long fb = full_base[mi], nfull = cd.div(B);
+            const int rr = rem_rail[mi];
+            const long long ro = rem_off[mi];
+            const long long c0 = cd.div(p0);
+            m.dst0 = chunk_addr(c0, fb, nfull, rr, ro, N, C, rbase) + (p0 - c0 * C);
+            const long long b0 = (c0 + 1) * C - p0;
+            m.b0 = (int)(b0 < RB ? b0 : RB);
+            if (m.b0 < RB) m.dst1 = chunk_addr(c0 + 1, fb, nfull, rr, ro, N, C, rbase);
+            m.ok = 1;
+          }
+        }
+      }
+      meta[wid][lane][sl] = m;
+    }
+  };
+  // prologue: loads of rows 0..D-1 of this warp
+  if (lane == 0) {
+    for (int j = 0; j < D; ++j) {
+      const long long row = row0 + (long long)j * nwarps;
+      if (row >= rows) break;
+      mbar_expect_tx(&bar[j], (uint32_t)RB);
+      bulk_load(buf + (size_t)j * RB, x + row * RB, (uint32_t)RB, &bar[j]);
+    }
+  }
+  long long j = 0;
+  for (long long row = row0; row < rows; row += nwarps, ++j) {
+    if ((j & 31) == 0) {
+      __syncwarp();
+      make_meta32(j);
+      __syncwarp();
+    }
+    if (lane == 0) {
+      const long long rn = row + (long long)D * nwarps;
+      const int stn = (int)((j + D) % S);
+      if (rn < rows) {
+        bulk_wait_read<S - D - 1>();  // stage stn's previous stores have read it
+        mbar_expect_tx(&bar[stn], (uint32_t)RB);
+        bulk_load(buf + (size_t)stn * RB, x + rn * RB, (uint32_t)RB, &bar[stn]);
+      }
+      const int st = (int)(j % S);
+      mbar_wait(&bar[st], (uint32_t)((j / S) & 1));
+      const uint8_t* src = buf + (size_t)st * RB;
+      for (int sl = 0; sl < k; ++sl) {
+        const TmaMeta2 m = meta[wid][j & 31][sl];
+        if (!m.ok) continue;
+        if (m.dst0 >= 0 && m.dst0 + m.b0 <= out_cap)
+          bulk_store(out + m.dst0, src, (uint32_t)m.b0);
+        else
+          flag_error(err, ERR_NOSPC);
+        if (m.b0 < RB) {
+          if (m.dst1 >= 0 && m.dst1 + (RB - m.b0) <= out_cap)
+            bulk_store(out + m.dst1, src + m.b0, (uint32_t)(RB - m.b0));
+          else
+            flag_error(err, ERR_NOSPC);
+        }
+      }
+      bulk_commit();
+    }
+  }
+  if (lane == 0) bulk_wait_all();
+}
+
+template <int S, int D, int W>
+static cudaError_t launch_tma2(const LaunchCtx& c, int U, int nd, int d0, int M, int N, int T,
+                               int k, long long C, int cshift, const void* x,
+                               const int32_t* topk, const int32_t* lut, int n_inst,
+                               const int32_t* rank, const int64_t* msg, long long RB,
+                               const rails_sched_t& s, const int64_t* rail_base, void* out,
+                               long long out_cap) {
+  auto kern = k_pack_tma2<S, D, W>;
+  const size_t smem = (size_t)W * S * RB;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const long long rows = (long long)U * nd * N * T;
+  long long grid = (long long)c.num_sms * per_sm;
+  const long long need = (rows + W - 1) / W;
+  if (grid > need) grid = need;
+  if (grid < 1) grid = 1;
+  kern<<<(unsigned)grid, W * 32, smem, c.stream>>>(
+      U, nd, d0, M, N, T, k, C, cshift, (const uint8_t*)x, topk, lut, n_inst, rank, msg, RB,
+      s.full_base, s.rem_rail, s.rem_off, rail_base, (uint8_t*)out, out_cap, c.err);
+  count_launch(1);
+  return cudaGetLastError();
+}
+
 template <int S, int D, bool MULTI>
 static cudaError_t launch_tma_sd(const LaunchCtx& c, int U, int nd, int d0, int M, int N, int T,
                                  int k, long long C, int cshift, const void* x,
@@ -480,6 +633,26 @@ cudaError_t launch_pack(const LaunchCtx& c, int U, int nd, int d0, int M, int N,
   if ((C & (C - 1)) == 0) {
     cshift = 0;
     while ((1LL << cshift) < C) ++cshift;
+  }
+  // impl 3: TMA pipeline v2 (batched metadata), RAILS_PACK_TMA = "S,D,W" selects
+  // the stage / distance / warps shape among the compiled ones
+  if (impl == 3 && k <= TMA2_MAXK && C >= row_bytes && row_bytes <= 8 * 1024) {
+    const char* sh = getenv("RAILS_PACK_TMA");
+    const int v = sh ? atoi(sh) : 0;
+#define RAILS_TMA2(SS, DD, WW)                                                               \
+  if (v == SS * 100 + DD * 10 + WW || (v == 0 && SS == 4 && DD == 3 && WW == 6))            \
+    return launch_tma2<SS, DD, WW>(c, U, nd, d0, M, N, T, k, C, cshift, x, topk, lut, n_inst, \
+                                   rank, msg, row_bytes, s, rail_base, out, out_cap);
+    if (row_bytes * 4 * 6 <= 200 * 1024) {
+      RAILS_TMA2(4, 3, 6)
+      RAILS_TMA2(3, 2, 8)
+      RAILS_TMA2(6, 4, 4)
+      RAILS_TMA2(4, 2, 6)
+      RAILS_TMA2(2, 1, 8)
+    }
+#undef RAILS_TMA2
+    return launch_tma2<2, 1, 4>(c, U, nd, d0, M, N, T, k, C, cshift, x, topk, lut, n_inst, rank,
+                                msg, row_bytes, s, rail_base, out, out_cap);
   }
   // impl 2: TMA bulk-copy pipeline (rows up to 48 KiB, k <= 8); 1: LDG/STG registers
   if (impl == 2 && k <= TMA_MAXK && row_bytes <= 48 * 1024) {

@@ -70,14 +70,18 @@ def bench_pack(res):
     total = int(pipe.total.item())
     algo = M * N * T * RB + total
     ref = None
-    for impl in ("1", "2", "1cs", "1v8", "1v4"):
+    variants = os.environ.get("KB_PACK_VARIANTS", "1,2,1cs,1v8,1v4,3s436,3s328,3s644,3s426,3s218")
+    for impl in variants.split(","):
         os.environ["RAILS_PACK_IMPL"] = impl[0]
         os.environ.pop("RAILS_PACK_ST", None)
         os.environ.pop("RAILS_PACK_VPL", None)
+        os.environ.pop("RAILS_PACK_TMA", None)
         if impl == "1cs":
             os.environ["RAILS_PACK_ST"] = "1"
         if impl.startswith("1v"):
             os.environ["RAILS_PACK_VPL"] = impl[2:]
+        if impl.startswith("3s"):
+            os.environ["RAILS_PACK_TMA"] = impl[2:]
         pipe.out.zero_()
         t = timeit(lambda: rails.pack(pipe.tp, pipe.sh, T, k, x, topk, lut, pipe.rank, pipe.msg, RB,
                                       pipe.sched, pipe.rail_base, pipe.out), flush=False)
@@ -93,6 +97,7 @@ def bench_pack(res):
     os.environ.pop("RAILS_PACK_IMPL", None)
     os.environ.pop("RAILS_PACK_ST", None)
     os.environ.pop("RAILS_PACK_VPL", None)
+    os.environ.pop("RAILS_PACK_TMA", None)
     # context only (NOT the roofline denominator): the same 1-read : 2-write byte
     # mix as the pack, done by a plain torch broadcast copy of every 8 KiB row into
     # two adjacent slots (second read of a row hits L2)
@@ -167,6 +172,24 @@ def bench_matrix(res, name, C=None, U=None):
                            "Te_over_Tstar": float((fin["T_e"] / fin["T_star"]).max())}
 
 
+def bench_bw(res):
+    """Context for the pack's roofline: torch's own streaming kernels on 8 GiB
+    buffers -- write-only (fill), read-only (sum) and 1:1 copy -- so the 1 read :
+    2 write mix of the pack can be set against pure read / write bandwidth."""
+    n = 8 << 30
+    a = torch.empty(n // 4, dtype=torch.float32, device=DEV)
+    b = torch.empty(n // 4, dtype=torch.float32, device=DEV)
+    a.fill_(1.0)
+    t = timeit(lambda: a.fill_(2.0), iters=5)
+    res["bw_write_fill"] = dict(t, gbs=n / (t["median_ms"] / 1e3) / 1e9)
+    t = timeit(lambda: a.sum(), iters=5)
+    res["bw_read_sum"] = dict(t, gbs=n / (t["median_ms"] / 1e3) / 1e9)
+    t = timeit(lambda: b.copy_(a), iters=5)
+    res["bw_copy"] = dict(t, gbs=2 * n / (t["median_ms"] / 1e3) / 1e9)
+    del a, b
+    torch.cuda.empty_cache()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
@@ -174,6 +197,8 @@ def main():
     a = ap.parse_args()
     res = {"device": torch.cuda.get_device_name(0), "peak_gbs": PEAK}
     only = a.only.split(",")
+    if "bw" in only:
+        bench_bw(res)
     if "pack" in only:
         bench_pack(res)
     if "hist" in only:
