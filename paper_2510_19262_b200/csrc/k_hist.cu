@@ -144,39 +144,49 @@ __global__ void __launch_bounds__(HW_WARPS * 32)
   const int G = M * N;
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long sg = (long long)blockIdx.x * HW_WARPS + wid;  // ((u*nd)+dl)*ngs + gl
-  uint32_t* const bin = sw1 + wid * G;
+  uint32_t* const bin = sw1 + wid * (G + 1);  // bin G: sink for invalid ids
   if (sg >= nsegs) return;
   const long long ul = sg / ngs;
   const int d = d0 + (int)(ul % nd);
   const int ne = T * k;
   const int32_t* __restrict__ src = topk + sg * (long long)ne + lane;
   int32_t* __restrict__ dst = RANK ? rank + sg * (long long)ne + lane : nullptr;
-  for (int i = lane; i < G; i += 32) bin[i] = 0;
+  for (int i = lane; i <= G; i += 32) bin[i] = 0;
   const unsigned lt = lanemask_lt();
   bool bad = false;
   __syncwarp();
+  // routing ids of the next batch are loaded while this batch is ranked (software
+  // pipelining: the HBM latency of the stream overlaps the shared-memory work)
+  int nx[UNR];
+#pragma unroll
+  for (int j = 0; j < UNR; ++j) nx[j] = (j * 32 + lane < ne) ? __ldg(src + j * 32) : -1;
   for (int base = 0; base < ne; base += 32 * UNR) {
     int hv[UNR];
 #pragma unroll
+    for (int j = 0; j < UNR; ++j) hv[j] = nx[j];
+    const int nb = base + 32 * UNR;
+#pragma unroll
     for (int j = 0; j < UNR; ++j)
-      hv[j] = (base + j * 32 + lane < ne) ? __ldg(src + base + j * 32) : -1;
+      nx[j] = (nb + j * 32 + lane < ne) ? __ldg(src + nb + j * 32) : -1;
 #pragma unroll
     for (int j = 0; j < UNR; ++j)  // all LUT lookups of the batch in flight together
       hv[j] = ((unsigned)hv[j] < (unsigned)n_inst) ? __ldg(lut + hv[j]) : -1;
 #pragma unroll
     for (int j = 0; j < UNR; ++j) {
       const bool in = base + j * 32 + lane < ne;
-      const int h = hv[j];
-      const bool valid = (unsigned)h < (unsigned)G;
+      // invalid ids (and the tail's idle lanes) all go to the sink bin G, so every
+      // lane runs the same branch-free sequence
+      const bool valid = (unsigned)hv[j] < (unsigned)G;
+      const int h = valid ? hv[j] : G;
       bad |= in && !valid;
       // 1. tag write: for equal keys one lane's id survives
-      if (valid) ((uint8_t*)(bin + h))[3] = (uint8_t)lane;
+      ((uint8_t*)(bin + h))[3] = (uint8_t)lane;
       __syncwarp();
       // 2. one read gives the surviving tag and the running count
-      const uint32_t word = valid ? bin[h] : 0u;
+      const uint32_t word = bin[h];
       const int t = (int)(word >> 24);
       const int c = (int)(word & 0xffffffu);
-      const bool loser = valid && t != lane;
+      const bool loser = t != lane;
       // 3. peers: a loser knows the winner (its tag); every lane scans the losers
       unsigned peers = (1u << lane) | (loser ? (1u << t) : 0u);
       unsigned lm = __ballot_sync(FULL, loser);
@@ -187,7 +197,7 @@ __global__ void __launch_bounds__(HW_WARPS * 32)
       }
       if (RANK && in) dst[base + j * 32] = valid ? c + __popc(peers & lt) : -1;
       // 4. the lowest lane of each key advances the count
-      if (valid && (peers & lt) == 0) bin[h] = (uint32_t)(c + __popc(peers));
+      if ((peers & lt) == 0) bin[h] = (uint32_t)((c + __popc(peers)) & 0xffffffu);
       __syncwarp();
     }
   }
@@ -250,7 +260,7 @@ cudaError_t launch_histogram(const LaunchCtx& c, int U, int nd, int d0, int M, i
   const bool many = grid >= (long long)c.num_sms * 16;
   if (!(hv && (hv[0] == '1' || hv[0] == '2')) && G <= 12288 && ne <= 65535 &&
       (many || (hv && hv[0] == '3'))) {
-    const size_t smem = (size_t)HW_WARPS * G * 4;
+    const size_t smem = (size_t)HW_WARPS * (G + 1) * 4;
     auto kern = rank ? k_hist_w1<8, true> : k_hist_w1<8, false>;
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
