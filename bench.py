@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c3", choices=["c3", "c2", "c1", "c4"])
+    ap.add_argument("--reduce", default="peer", choices=["peer", "nccl"],
+                    help="a6 at N > 1: fused finalize over NVLink peer memory, or NCCL")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -271,6 +273,13 @@ def main():
             pipe.step(msg, reduce if dist is not None else None)
             ev_p1.record(stream)
 
+    peer = None
+    if dist is not None and args.reduce == "peer":
+        # a6 + finalize in one kernel over NVLink peer memory
+        from paper_2510_19262_b200.dist import PeerFinalize
+        peer = PeerFinalize(pipe.tp, U, dev)
+        reduce = peer  # noqa: F811 -- the pipelines call reduce.finalize
+
     def evpair():
         return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
@@ -325,7 +334,7 @@ def main():
         dist.all_reduce(ts, op=dist.ReduceOp.MAX)
     out["schedule_only"] = {"value": nodes / (float(ts.item()) / 1000.0), "unit": "nodes/s",
                             "ms_per_step": float(ts.item()),
-                            "what": "histogram + chunk/sort + LPT + eval + NCCL reduction + "
+                            "what": "histogram + chunk/sort + LPT + eval + a6 reduction + "
                                     "rail offsets per step, pack excluded (SURVEY 8(d) d.1)"}
     fin = {kk: vv.cpu() for kk, vv in pipe.final.items()}
     quality = {"T_lpt_over_Tstar": float((fin["T"] / fin["T_star"]).max()),
@@ -353,6 +362,7 @@ def main():
                          "32 KiB chunks" if args.workload == "c3" else args.workload,
                          "units": U, "nodes_per_rank": nd * U, "M": M, "N": N, "T": T, "k": k,
                          "row_bytes": RB, "chunk_bytes": C, "parallelism": f"nodes{P}",
+                         "a6": (args.reduce if P > 1 else "none"),
                          "l2": "inputs larger than L2: 16 GiB payload + 31.5 GiB rail buffers "
                                "streamed per step per GPU"}
         traffic = None
@@ -370,7 +380,8 @@ def main():
                            "share_of_step": pack_avg_ms / (total_ms / args.steps)}
     else:
         out["config"] = {"workload": args.workload, "units": U, "nodes_per_rank": nd * U,
-                         "M": M, "N": N, "chunk_bytes": C, "parallelism": f"nodes{P}"}
+                         "M": M, "N": N, "chunk_bytes": C, "parallelism": f"nodes{P}",
+                         "a6": (args.reduce if P > 1 else "none")}
     out["quality"] = quality
     out["clocks"] = clk.summary()
     out["gpu_launches"] = int(launches)
@@ -383,6 +394,8 @@ def main():
         out["cpu_baseline"] = oracle_sample(args.workload)
     if rank == 0:
         emit(out)
+    if peer is not None:
+        peer.close()
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()

@@ -209,6 +209,29 @@ typedef struct {
 int rails_eval_finalize(const rails_topo_t* topo, int32_t U, const int64_t* red_sum,
                         const int64_t* red_max, const rails_final_t* out, void* stream);
 
+/* a6 fused with the finalize over NVLink peer memory (one process per GPU of a
+ * box): every rank pushes its partial red_sum / red_max of each unit into every
+ * rank's exchange buffer (remote stores through CUDA-IPC mappings), publishes a
+ * per-(unit, rank) flag with a system-scope release, waits for all ranks' flags,
+ * sums / maxes the partials (written back into red_sum / red_max, as an
+ * all-reduce would) and finalizes -- one kernel, no NCCL call.
+ *   buf[p]  rank p's exchange buffer as mapped in this process (own included),
+ *           rails_peer_buffer_bytes() bytes, zero-filled before the first call;
+ *   gen     call number: >= 1, equal on all ranks, +1 per call (flags compare to it).
+ * A rank that waits ~1 s for a peer sets RAILS_ECUDA-class error RAILS_ERANGE in the
+ * device flag and finalizes what it has (rails_check reports it). */
+#define RAILS_PEER_MAX 8
+typedef struct {
+    int32_t rank;
+    int32_t world;   /* 1 .. RAILS_PEER_MAX */
+    uint32_t gen;
+    void* buf[RAILS_PEER_MAX];
+} rails_peer_t;
+int rails_peer_buffer_bytes(const rails_topo_t* topo, int32_t U, int32_t world, size_t* bytes);
+int rails_eval_finalize_peer(const rails_topo_t* topo, int32_t U, int64_t* red_sum,
+                             int64_t* red_max, const rails_peer_t* peer,
+                             const rails_final_t* out, void* stream);
+
 /* ------------------------------------------------------------------ a7 */
 /* Rail buffer placement: rail_base int64 [U][nd][N] = exclusive prefix sum of
  * send_load in (u, dl, j) order, i.e. the byte offset of rail j of node d in one

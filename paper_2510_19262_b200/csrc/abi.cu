@@ -457,6 +457,35 @@ int rails_ipc_free(void* dptr) {
   return cuda_rc(cudaFree(dptr), "cudaFree");
 }
 
+int rails_peer_buffer_bytes(const rails_topo_t* topo, int32_t U, int32_t world, size_t* bytes) {
+  int rc = check_topo(topo);
+  if (rc) return rc;
+  if (U < 1 || world < 1 || world > RAILS_PEER_MAX || !bytes)
+    return fail(RAILS_EINVAL, "bad arguments");
+  *bytes = peer_buffer_bytes(U, world, RAILS_RED_SUM_LEN(topo->M, topo->N));
+  return RAILS_OK;
+}
+
+int rails_eval_finalize_peer(const rails_topo_t* topo, int32_t U, int64_t* red_sum,
+                             int64_t* red_max, const rails_peer_t* peer,
+                             const rails_final_t* out, void* stream) {
+  int rc = check_topo(topo);
+  if (rc) return rc;
+  if (U < 1 || !red_sum || !red_max || !peer || !out) return fail(RAILS_EINVAL, "NULL argument");
+  if (peer->world < 1 || peer->world > RAILS_PEER_MAX || peer->rank < 0 ||
+      peer->rank >= peer->world || peer->gen == 0)
+    return fail(RAILS_EINVAL, "bad peer descriptor (rank %d, world %d, gen %u)", (int)peer->rank,
+                (int)peer->world, (unsigned)peer->gen);
+  for (int p = 0; p < peer->world; ++p)
+    if (!peer->buf[p] || !al(peer->buf[p], 256))
+      return fail(RAILS_EINVAL, "peer buffer %d NULL or not 256-byte aligned", p);
+  LaunchCtx c;
+  if ((rc = ctx(stream, &c))) return rc;
+  return cuda_rc(launch_finalize_peer(c, U, topo->M, topo->N, topo->R2, red_sum, red_max, *peer,
+                                      *out),
+                 "rails_eval_finalize_peer launch");
+}
+
 static int check_fabric(const rails_topo_t* topo, const rails_fabric_t* fb) {
   if (!fb) return fail(RAILS_EINVAL, "fabric is NULL");
   if (fb->S < 1 || fb->S > 32) return fail(RAILS_EINVAL, "spines S=%d not in 1..32", (int)fb->S);

@@ -182,6 +182,11 @@ cudaError_t launch_finalize(const LaunchCtx&, int U, int M, int N, double R2,
                             const int64_t* red_sum, const int64_t* red_max,
                             const rails_final_t& f);
 
+size_t peer_buffer_bytes(int U, int world, long long rsl);
+cudaError_t launch_finalize_peer(const LaunchCtx&, int U, int M, int N, double R2,
+                                 int64_t* red_sum, int64_t* red_max, const rails_peer_t& peer,
+                                 const rails_final_t& f);
+
 cudaError_t launch_rail_offsets(const LaunchCtx&, long long n, const int64_t* send_load,
                                 int64_t* rail_base, int64_t* total);
 cudaError_t launch_pack(const LaunchCtx&, int U, int nd, int d0, int M, int N, int T, int k,

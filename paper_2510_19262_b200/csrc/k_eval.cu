@@ -341,6 +341,10 @@ __global__ void __launch_bounds__(EV2_THREADS)
   }
 }
 
+__device__ void finalize_unit(long long u, int N, double R2, long long mR, long long mRe,
+                              long long mc, long long rm0, long long rm1, long long rm2,
+                              long long total, long long total_e, const rails_final_t& out);
+
 __global__ void __launch_bounds__(256)
     k_eval_finalize(int M, int N, double R2, long long rsl, const int64_t* __restrict__ red_sum,
                     const int64_t* __restrict__ red_max, rails_final_t out) {
@@ -371,10 +375,17 @@ __global__ void __launch_bounds__(256)
     mc = max(mc, s3[2][w]);
   }
   const int64_t* rm = red_max + u * RAILS_RED_MAX_LEN;
-  const long long maxload = max((long long)rm[0], mR);
-  const long long maxload_e = max((long long)rm[1], mRe);
-  const long long rowmax = rm[2];
-  const long long total = rs[2 * MN + M], total_e = rs[2 * MN + M + 1];
+  finalize_unit(u, N, R2, mR, mRe, mc, rm[0], rm[1], rm[2], rs[2 * MN + M], rs[2 * MN + M + 1],
+                out);
+}
+
+// T, T*, busbw of unit u from the reduced maxima and totals (R#8, R#10, Thm 2/3).
+__device__ void finalize_unit(long long u, int N, double R2, long long mR, long long mRe,
+                              long long mc, long long rm0, long long rm1, long long rm2,
+                              long long total, long long total_e, const rails_final_t& out) {
+  const long long maxload = max(rm0, mR);
+  const long long maxload_e = max(rm1, mRe);
+  const long long rowmax = rm2;
   const double T = __ddiv_rn(__ll2double_rn(maxload), R2);
   const double T_e = __ddiv_rn(__ll2double_rn(maxload_e), R2);
   const long long lb = max(rowmax, mc);
@@ -389,6 +400,116 @@ __global__ void __launch_bounds__(256)
   if (out.T_star) out.T_star[u] = T_star;
   if (out.busbw) out.busbw[u] = total > 0 ? __ddiv_rn(__ll2double_rn(total), T) : 0.0;
   if (out.busbw_e) out.busbw_e[u] = total_e > 0 ? __ddiv_rn(__ll2double_rn(total_e), T_e) : 0.0;
+}
+
+// ---------------------------------------------------------------- a6 + finalize, peers
+struct PeerBufs {
+  uint8_t* p[RAILS_PEER_MAX];
+};
+
+__device__ __forceinline__ void st_release_sys(uint32_t* a, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* a) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+
+__host__ __device__ static inline size_t al256e(size_t x) { return (x + 255) & ~(size_t)255; }
+
+size_t peer_buffer_bytes(int U, int world, long long rsl) {
+  const long long rec = rsl + RAILS_RED_MAX_LEN;
+  return al256e((size_t)U * world * 4) + (size_t)world * U * rec * 8;
+}
+
+// One CTA per unit: push this rank's partials to every rank, release a flag per
+// (unit, rank), acquire every rank's flag, reduce the world's partials (in rank
+// order, so every rank computes identical sums) and finalize the unit.
+__global__ void __launch_bounds__(256)
+    k_finalize_peer(int M, int N, double R2, long long rsl, int U, int64_t* __restrict__ red_sum,
+                    int64_t* __restrict__ red_max, PeerBufs pb, int rank, int world,
+                    uint32_t gen, rails_final_t out, int* err) {
+  __shared__ long long s3[3][8];
+  __shared__ long long stot[2];
+  const long long u = blockIdx.x;
+  const long long rec = rsl + RAILS_RED_MAX_LEN;
+  const size_t slots_off = al256e((size_t)U * world * 4);
+  int64_t* rs = red_sum + u * rsl;
+  int64_t* rmx = red_max + u * RAILS_RED_MAX_LEN;
+  // 1. push (remote stores over NVLink for p != rank)
+  for (int p = 0; p < world; ++p) {
+    int64_t* dst = (int64_t*)(pb.p[p] + slots_off) + ((long long)rank * U + u) * rec;
+    for (long long i = threadIdx.x; i < rec; i += blockDim.x)
+      dst[i] = i < rsl ? rs[i] : rmx[i - rsl];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int p = 0; p < world; ++p)
+      st_release_sys((uint32_t*)pb.p[p] + u * world + rank, gen);
+  }
+  // 2. wait for every rank's partials of this unit
+  if (threadIdx.x < world) {
+    const uint32_t* f = (const uint32_t*)pb.p[rank] + u * world + threadIdx.x;
+    long long spins = 0;
+    while (ld_acquire_sys(f) != gen) {
+      __nanosleep(64);
+      if (++spins > (1LL << 24)) {
+        flag_error(err, ERR_RANGE);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  // 3. reduce in rank order (volatile loads: the data came from other GPUs)
+  const volatile int64_t* slots = (const volatile int64_t*)(pb.p[rank] + slots_off);
+  const long long MN = (long long)M * N;
+  long long mR = 0, mRe = 0, mc = 0;
+  for (long long i = threadIdx.x; i < rsl; i += blockDim.x) {
+    long long v = 0;
+    for (int p = 0; p < world; ++p) v += slots[((long long)p * U + u) * rec + i];
+    rs[i] = v;
+    if (i < MN) mR = max(mR, v);
+    else if (i < 2 * MN) mRe = max(mRe, v);
+    else if (i < 2 * MN + M) mc = max(mc, v);
+    else stot[i - 2 * MN - M] = v;
+  }
+  if (threadIdx.x < RAILS_RED_MAX_LEN) {
+    long long v = 0;
+    for (int p = 0; p < world; ++p)
+      v = max(v, (long long)slots[((long long)p * U + u) * rec + rsl + threadIdx.x]);
+    rmx[threadIdx.x] = v;
+  }
+  mR = warp_max(mR);
+  mRe = warp_max(mRe);
+  mc = warp_max(mc);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    s3[0][wid] = mR;
+    s3[1][wid] = mRe;
+    s3[2][wid] = mc;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+    mR = max(mR, s3[0][w]);
+    mRe = max(mRe, s3[1][w]);
+    mc = max(mc, s3[2][w]);
+  }
+  finalize_unit(u, N, R2, mR, mRe, mc, rmx[0], rmx[1], rmx[2], stot[0], stot[1], out);
+}
+
+cudaError_t launch_finalize_peer(const LaunchCtx& c, int U, int M, int N, double R2,
+                                 int64_t* red_sum, int64_t* red_max, const rails_peer_t& peer,
+                                 const rails_final_t& f) {
+  PeerBufs pb;
+  for (int p = 0; p < RAILS_PEER_MAX; ++p) pb.p[p] = (uint8_t*)(p < peer.world ? peer.buf[p] : nullptr);
+  k_finalize_peer<<<(unsigned)U, 256, 0, c.stream>>>(M, N, R2, RAILS_RED_SUM_LEN(M, N), U, red_sum,
+                                                     red_max, pb, peer.rank, peer.world, peer.gen,
+                                                     f, c.err);
+  count_launch(1);
+  return cudaGetLastError();
 }
 
 // Exclusive prefix of send_load in (u, dl, j) order -> rail_base; total bytes.

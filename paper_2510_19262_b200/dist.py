@@ -38,3 +38,64 @@ def make_reduce(group=None) -> Callable:
         dist.all_reduce(red_max, op=dist.ReduceOp.MAX, group=group)
 
     return reduce
+
+
+class PeerFinalize:
+    """a6 + finalize fused over NVLink peer memory (rails_eval_finalize_peer).
+
+    Collective setup: each rank allocates an exchange buffer exported by CUDA IPC,
+    the handles are all-gathered once (torch.distributed object collective), and
+    every rank maps the others' buffers.  Each call then runs ONE kernel per rank:
+    push partials to every rank, flag, wait, reduce, finalize -- no NCCL call in
+    the step.  Used as the `reduce` hook of the pipelines (they call .finalize)."""
+
+    def __init__(self, tp, U: int, device, group=None):
+        import torch
+        import torch.distributed as dist
+        from . import rails
+        self.dist, self.group, self.tp, self.U = dist, group, tp, U
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        if self.world > rails.PEER_MAX:
+            raise ValueError(f"peer finalize supports up to {rails.PEER_MAX} GPUs")
+        n = rails.peer_buffer_bytes(tp, U, self.world)
+        self.own_ptr, handle, view = rails.ipc_alloc(n)
+        view.zero_()
+        torch.cuda.synchronize(device)
+        objs = [None] * self.world
+        dist.all_gather_object(objs, (handle, torch.device(device).index), group=group)
+        for _, di in objs:
+            if di != torch.device(device).index:
+                rails.enable_peer_access(di)
+        self.opened = []
+        self.bufs = []
+        for q, (h, _) in enumerate(objs):
+            if q == self.rank:
+                self.bufs.append(self.own_ptr)
+            else:
+                ptr = rails.ipc_open(h)
+                self.opened.append(ptr)
+                self.bufs.append(ptr)
+        self.gen = 0
+        dist.barrier(group=group)
+
+    def finalize(self, red_sum, red_max, out, stream=None):
+        from . import rails
+        self.gen += 1
+        rails.eval_finalize_peer(self.tp, self.U, red_sum, red_max, self.rank, self.world,
+                                 self.gen, self.bufs, out=out, stream=stream)
+
+    def __call__(self, red_sum, red_max):  # pragma: no cover - use .finalize
+        raise RuntimeError("PeerFinalize reduces inside the finalize kernel; call .finalize")
+
+    def close(self):
+        import torch
+        from . import rails
+        torch.cuda.synchronize()
+        self.dist.barrier(group=self.group)
+        for ptr in self.opened:
+            rails.ipc_close(ptr)
+        self.opened = []
+        self.dist.barrier(group=self.group)
+        rails.ipc_free(self.own_ptr)
+        self.own_ptr = None

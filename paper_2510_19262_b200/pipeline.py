@@ -50,6 +50,9 @@ class RoutingPipeline:
         rails.eval(self.tp, self.sh, self.msg, self.sched, out=self.ev, stream=stream)
 
     def finalize_part(self, reduce: Callable | None = None, stream=None):
+        if reduce is not None and hasattr(reduce, "finalize"):  # fused a6 + finalize
+            reduce.finalize(self.ev.red_sum, self.ev.red_max, self.final, stream=stream)
+            return
         if reduce is not None:
             reduce(self.ev.red_sum, self.ev.red_max)
         rails.eval_finalize(self.tp, self.U, self.ev.red_sum, self.ev.red_max, out=self.final,
@@ -85,6 +88,9 @@ class MatrixPipeline:
     def step(self, msg: torch.Tensor, reduce: Callable | None = None, stream=None):
         rails.lpt_schedule(self.tp, self.sh, msg, out=self.sched, workspace=self.ws, stream=stream)
         rails.eval(self.tp, self.sh, msg, self.sched, out=self.ev, stream=stream)
+        if reduce is not None and hasattr(reduce, "finalize"):  # fused a6 + finalize
+            reduce.finalize(self.ev.red_sum, self.ev.red_max, self.final, stream=stream)
+            return
         if reduce is not None:
             reduce(self.ev.red_sum, self.ev.red_max)
         rails.eval_finalize(self.tp, self.U, self.ev.red_sum, self.ev.red_max, out=self.final,

@@ -62,6 +62,14 @@ class _Final(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in _FINAL_FIELDS]
 
 
+PEER_MAX = 8
+
+
+class Peer(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("gen", ctypes.c_uint32),
+                ("buf", ctypes.c_void_p * PEER_MAX)]
+
+
 _lib = None
 
 
@@ -90,6 +98,11 @@ def lib():
         L.rails_lpt_assign.argtypes = [i32, i32, P, i64, P, P, P, P, P, sz, P]
         L.rails_eval.argtypes = [PT, PS, P, ctypes.POINTER(_Sched), ctypes.POINTER(_Eval), P]
         L.rails_eval_finalize.argtypes = [PT, i32, P, P, ctypes.POINTER(_Final), P]
+        L.rails_peer_buffer_bytes.argtypes = [PT, i32, i32, ctypes.POINTER(sz)]
+        L.rails_peer_buffer_bytes.restype = ctypes.c_int
+        L.rails_eval_finalize_peer.argtypes = [PT, i32, P, P, ctypes.POINTER(Peer),
+                                               ctypes.POINTER(_Final), P]
+        L.rails_eval_finalize_peer.restype = ctypes.c_int
         L.rails_rail_offsets.argtypes = [PT, PS, P, P, P, P]
         L.rails_pack.argtypes = [PT, PS, i32, i32, P, P, P, i32, P, P, i64,
                                  ctypes.POINTER(_Sched), P, P, i64, P]
@@ -330,6 +343,28 @@ def eval_finalize(tp: Topo, U: int, red_sum: torch.Tensor, red_max: torch.Tensor
     _ok(lib().rails_eval_finalize(ctypes.byref(tp), U, _ptr(red_sum, torch.int64, "red_sum"),
                                   _ptr(red_max, torch.int64, "red_max"), ctypes.byref(cf),
                                   _stream(stream)))
+    return out
+
+
+def peer_buffer_bytes(tp: Topo, U: int, world: int) -> int:
+    n = ctypes.c_size_t(0)
+    _ok(lib().rails_peer_buffer_bytes(ctypes.byref(tp), U, world, ctypes.byref(n)))
+    return int(n.value)
+
+
+def eval_finalize_peer(tp: Topo, U: int, red_sum: torch.Tensor, red_max: torch.Tensor,
+                       rank: int, world: int, gen: int, bufs: list, out: dict | None = None,
+                       stream=None) -> dict:
+    """a6 + finalize in one kernel over NVLink peer memory (rails_eval_finalize_peer)."""
+    if out is None:
+        out = empty_final(U, red_sum.device)
+    cf = _Final(*[_ptr(out[n]) for n in _FINAL_FIELDS])
+    pr = Peer(rank, world, gen)
+    for i, b in enumerate(bufs):
+        pr.buf[i] = b
+    _ok(lib().rails_eval_finalize_peer(ctypes.byref(tp), U, _ptr(red_sum, torch.int64, "red_sum"),
+                                       _ptr(red_max, torch.int64, "red_max"), ctypes.byref(pr),
+                                       ctypes.byref(cf), _stream(stream)))
     return out
 
 
