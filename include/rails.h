@@ -338,6 +338,23 @@ int rails_pack_owner(const rails_topo_t* topo, const rails_shard_t* shard, int32
                      const int64_t* rail_base, void* const* rail_ptr, const int64_t* rail_cap,
                      void* stream);
 
+/* NVLink-native exchange of the rail-owner node (replaces NCCL in its step).
+ * Each rank owns an exchange buffer (rails_owner_exchange_layout bytes, zero-filled
+ * before first use, IPC-exported and mapped by every rank; rails_peer_t.buf[p] =
+ * rank p's buffer as mapped here; gen as for rails_eval_finalize_peer):
+ *   rails_gather_rows_peer: one kernel (one CTA per unit) stores this rank's
+ *     msg_bytes rows (msg_loc [U][1][ng][G], source GPUs g0..g0+ng-1) into every
+ *     rank's node-wide msg table at msg_offset ([U][1][N][G] int64), flags, and
+ *     returns when all ranks' rows are in this rank's table (the schedule input);
+ *   rails_peer_barrier: after rails_pack_owner, every rank's packed pieces are in
+ *     their owners' buffers when the barrier kernel of every rank has completed.
+ * A peer missing for ~1 s sets RAILS_ERANGE in the device flag. */
+int rails_owner_exchange_layout(const rails_topo_t* topo, int32_t U, int32_t world,
+                                size_t* bytes, size_t* msg_offset);
+int rails_gather_rows_peer(const rails_topo_t* topo, int32_t U, int32_t g0, int32_t ng,
+                           const int64_t* msg_loc, const rails_peer_t* peer, void* stream);
+int rails_peer_barrier(const rails_peer_t* peer, void* stream);
+
 /* Inter-process rail buffers for rails_pack_owner (one process per GPU): the
  * owner allocates with rails_ipc_alloc (device memory of the current device, 256-B
  * aligned, plus a 64-byte cudaIpcMemHandle_t written to `handle`), ships the

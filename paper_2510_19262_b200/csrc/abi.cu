@@ -457,6 +457,18 @@ int rails_ipc_free(void* dptr) {
   return cuda_rc(cudaFree(dptr), "cudaFree");
 }
 
+static int check_peer(const rails_peer_t* peer) {
+  if (!peer) return fail(RAILS_EINVAL, "peer is NULL");
+  if (peer->world < 1 || peer->world > RAILS_PEER_MAX || peer->rank < 0 ||
+      peer->rank >= peer->world || peer->gen == 0)
+    return fail(RAILS_EINVAL, "bad peer descriptor (rank %d, world %d, gen %u)", (int)peer->rank,
+                (int)peer->world, (unsigned)peer->gen);
+  for (int p = 0; p < peer->world; ++p)
+    if (!peer->buf[p] || !al(peer->buf[p], 256))
+      return fail(RAILS_EINVAL, "peer buffer %d NULL or not 256-byte aligned", p);
+  return RAILS_OK;
+}
+
 int rails_peer_buffer_bytes(const rails_topo_t* topo, int32_t U, int32_t world, size_t* bytes) {
   int rc = check_topo(topo);
   if (rc) return rc;
@@ -471,19 +483,45 @@ int rails_eval_finalize_peer(const rails_topo_t* topo, int32_t U, int64_t* red_s
                              const rails_final_t* out, void* stream) {
   int rc = check_topo(topo);
   if (rc) return rc;
-  if (U < 1 || !red_sum || !red_max || !peer || !out) return fail(RAILS_EINVAL, "NULL argument");
-  if (peer->world < 1 || peer->world > RAILS_PEER_MAX || peer->rank < 0 ||
-      peer->rank >= peer->world || peer->gen == 0)
-    return fail(RAILS_EINVAL, "bad peer descriptor (rank %d, world %d, gen %u)", (int)peer->rank,
-                (int)peer->world, (unsigned)peer->gen);
-  for (int p = 0; p < peer->world; ++p)
-    if (!peer->buf[p] || !al(peer->buf[p], 256))
-      return fail(RAILS_EINVAL, "peer buffer %d NULL or not 256-byte aligned", p);
+  if (U < 1 || !red_sum || !red_max || !out) return fail(RAILS_EINVAL, "NULL argument");
+  if ((rc = check_peer(peer))) return rc;
   LaunchCtx c;
   if ((rc = ctx(stream, &c))) return rc;
   return cuda_rc(launch_finalize_peer(c, U, topo->M, topo->N, topo->R2, red_sum, red_max, *peer,
                                       *out),
                  "rails_eval_finalize_peer launch");
+}
+
+int rails_owner_exchange_layout(const rails_topo_t* topo, int32_t U, int32_t world,
+                                size_t* bytes, size_t* msg_offset) {
+  int rc = check_topo(topo);
+  if (rc) return rc;
+  if (U < 1 || world < 1 || world > RAILS_PEER_MAX || !bytes || !msg_offset)
+    return fail(RAILS_EINVAL, "bad arguments");
+  size_t gf;
+  owner_exchange_layout(U, world, topo->N, (long long)topo->M * topo->N, bytes, &gf, msg_offset);
+  return RAILS_OK;
+}
+
+int rails_gather_rows_peer(const rails_topo_t* topo, int32_t U, int32_t g0, int32_t ng,
+                           const int64_t* msg_loc, const rails_peer_t* peer, void* stream) {
+  int rc = check_topo(topo);
+  if (rc || (rc = check_peer(peer))) return rc;
+  if (U < 1 || !msg_loc || g0 < 0 || ng < 1 || g0 + ng > topo->N)
+    return fail(RAILS_EINVAL, "bad arguments");
+  LaunchCtx c;
+  if ((rc = ctx(stream, &c))) return rc;
+  return cuda_rc(launch_gather_rows_peer(c, U, topo->N, (long long)topo->M * topo->N, g0, ng,
+                                         msg_loc, *peer),
+                 "rails_gather_rows_peer launch");
+}
+
+int rails_peer_barrier(const rails_peer_t* peer, void* stream) {
+  int rc = check_peer(peer);
+  if (rc) return rc;
+  LaunchCtx c;
+  if ((rc = ctx(stream, &c))) return rc;
+  return cuda_rc(launch_peer_barrier(c, *peer), "rails_peer_barrier launch");
 }
 
 static int check_fabric(const rails_topo_t* topo, const rails_fabric_t* fb) {

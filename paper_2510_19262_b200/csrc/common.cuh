@@ -183,6 +183,11 @@ cudaError_t launch_finalize(const LaunchCtx&, int U, int M, int N, double R2,
                             const rails_final_t& f);
 
 size_t peer_buffer_bytes(int U, int world, long long rsl);
+void owner_exchange_layout(int U, int world, long long N, long long G, size_t* bytes,
+                           size_t* gflag_off, size_t* msg_off);
+cudaError_t launch_gather_rows_peer(const LaunchCtx&, int U, int N, long long G, int g0, int ng,
+                                    const int64_t* msg_loc, const rails_peer_t& peer);
+cudaError_t launch_peer_barrier(const LaunchCtx&, const rails_peer_t& peer);
 cudaError_t launch_finalize_peer(const LaunchCtx&, int U, int M, int N, double R2,
                                  int64_t* red_sum, int64_t* red_max, const rails_peer_t& peer,
                                  const rails_final_t& f);

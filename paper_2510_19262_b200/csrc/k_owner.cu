@@ -178,6 +178,9 @@ __global__ void __launch_bounds__(OWN_THREADS)
       }
     }
   }
+  // this thread's stores into peers' HBM are performed system-wide before it
+  // exits, so a later rails_peer_barrier orders them for every rank
+  __threadfence_system();
 }
 
 // Per-rail placement inside the owner buffers: rail_base[u][dl][j] = bytes of rail j
@@ -269,6 +272,111 @@ cudaError_t launch_rail_offsets_owner(const LaunchCtx& c, long long ublk, int N,
                                       const int64_t* send_load, int64_t* rail_base,
                                       int64_t* rail_total) {
   k_rail_offsets_owner<<<1, 32, 0, c.stream>>>(ublk, N, send_load, rail_base, rail_total);
+  count_launch(1);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- peer exchange
+// Exchange buffer of a rail-owner rank (rails_owner_exchange_layout):
+//   [barrier flags: RAILS_PEER_MAX x u32, 256 B][gather flags: U x world x u32,
+//    256-aligned][msg_node: int64 [U][1][N][G]]
+__device__ __forceinline__ void st_rel_sys(uint32_t* a, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acq_sys(const uint32_t* a) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ bool wait_flag(const uint32_t* f, uint32_t gen, int* err) {
+  long long spins = 0;
+  while (ld_acq_sys(f) != gen) {
+    __nanosleep(64);
+    if (++spins > (1LL << 24)) {
+      flag_error(err, ERR_RANGE);
+      return false;
+    }
+  }
+  return true;
+}
+
+struct PeerBase {
+  uint8_t* p[RAILS_PEER_MAX];
+};
+
+static inline size_t al256o(size_t x) { return (x + 255) & ~(size_t)255; }
+
+void owner_exchange_layout(int U, int world, long long N, long long G, size_t* bytes,
+                           size_t* gflag_off, size_t* msg_off) {
+  *gflag_off = 256;
+  *msg_off = 256 + al256o((size_t)U * world * 4);
+  *bytes = *msg_off + (size_t)U * N * G * 8;
+}
+
+// One CTA per unit: this rank's message rows (source GPUs g0..g0+ng-1) go into
+// every rank's msg_node (NVLink stores), then a per-(unit, rank) flag; the CTA
+// returns when every rank's rows of the unit have arrived here.
+__global__ void __launch_bounds__(256)
+    k_gather_rows_peer(int U, int N, long long G, int g0, int ng,
+                       const int64_t* __restrict__ msg_loc, PeerBase pb, int rank, int world,
+                       uint32_t gen, size_t gflag_off, size_t msg_off, int* err) {
+  const long long u = blockIdx.x;
+  const long long n = (long long)ng * G;  // int64 per unit and rank
+  const int64_t* src = msg_loc + u * n;
+  for (int p = 0; p < world; ++p) {
+    int64_t* dst = (int64_t*)(pb.p[p] + msg_off) + (u * N + g0) * G;
+    if (((uintptr_t)dst & 15) == 0 && ((uintptr_t)src & 15) == 0) {
+      for (long long i = threadIdx.x; i < n / 2; i += blockDim.x)
+        ((int4*)dst)[i] = ((const int4*)src)[i];
+      if ((n & 1) && threadIdx.x == 0) dst[n - 1] = src[n - 1];
+    } else {
+      for (long long i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int p = 0; p < world; ++p)
+      st_rel_sys((uint32_t*)(pb.p[p] + gflag_off) + u * world + rank, gen);
+  }
+  if (threadIdx.x < world)
+    wait_flag((const uint32_t*)(pb.p[rank] + gflag_off) + u * world + threadIdx.x, gen, err);
+  __syncthreads();
+}
+
+// Every rank's earlier stream work (its stores included) precedes every rank's
+// later work: flag all ranks, wait for all ranks' flags.
+__global__ void k_peer_barrier(PeerBase pb, int rank, int world, uint32_t gen, int* err) {
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int p = 0; p < world; ++p) st_rel_sys((uint32_t*)pb.p[p] + rank, gen);
+  }
+  __syncwarp();
+  if (threadIdx.x < world) wait_flag((const uint32_t*)pb.p[rank] + threadIdx.x, gen, err);
+  __syncwarp();
+}
+
+static PeerBase peer_base(const rails_peer_t& peer) {
+  PeerBase pb;
+  for (int p = 0; p < RAILS_PEER_MAX; ++p)
+    pb.p[p] = (uint8_t*)(p < peer.world ? peer.buf[p] : nullptr);
+  return pb;
+}
+
+cudaError_t launch_gather_rows_peer(const LaunchCtx& c, int U, int N, long long G, int g0,
+                                    int ng, const int64_t* msg_loc, const rails_peer_t& peer) {
+  size_t bytes, gf, mo;
+  owner_exchange_layout(U, peer.world, N, G, &bytes, &gf, &mo);
+  k_gather_rows_peer<<<(unsigned)U, 256, 0, c.stream>>>(U, N, G, g0, ng, msg_loc,
+                                                        peer_base(peer), peer.rank, peer.world,
+                                                        peer.gen, gf, mo, c.err);
+  count_launch(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_peer_barrier(const LaunchCtx& c, const rails_peer_t& peer) {
+  k_peer_barrier<<<1, 32, 0, c.stream>>>(peer_base(peer), peer.rank, peer.world, peer.gen,
+                                         c.err);
   count_launch(1);
   return cudaGetLastError();
 }

@@ -5,11 +5,13 @@ Rank p (one process per GPU) holds source GPUs g0 = p*ng .. g0+ng-1 of the node
 (ng = N / P) and owns rails p*ng .. p*ng+ng-1: NIC j hangs off GPU j, so
 rail j's send buffer lives in GPU j's HBM.  One step:
   1. rails_histogram_gpus on the local rows                         (kernel)
-  2. all-gather of the node's msg_bytes rows over NCCL (N*G*8 B/unit) (collective)
+  2. rails_gather_rows_peer: the node's msg_bytes rows (N*G*8 B/unit) are stored
+     into every rank's node table over NVLink, flagged and awaited   (kernel)
   3. rails_lpt_schedule of the whole node, identical on every rank    (kernels)
   4. rails_rail_offsets_owner + rails_pack_owner: each chunk piece is stored
      straight into the owner's buffer through a peer-mapped pointer   (kernel)
-  5. a one-element NCCL all-reduce orders every rank's pack before any consumer.
+  5. rails_peer_barrier orders every rank's pack before any consumer (kernel).
+exchange="nccl" keeps the NCCL all-gather / all-reduce for steps 2 and 5.
 Peer mapping: CUDA IPC handles exported/imported by librails (rails_ipc_*), each
 rank mapping the peers' buffers under its own device.
 """
@@ -29,7 +31,7 @@ def _enable_peer_access(dev: int, peers):
 
 class RailOwnerNode:
     def __init__(self, M: int, N: int, T: int, k: int, row_bytes: int, chunk_bytes: int, U: int,
-                 d: int, n_inst: int, group=None, R2: float = 5.0e10):
+                 d: int, n_inst: int, group=None, R2: float = 5.0e10, exchange: str = "peer"):
         import torch.distributed as dist
 
         self.dist = dist
@@ -50,6 +52,9 @@ class RailOwnerNode:
         self.counts = torch.empty((U, 1, self.ng, G), dtype=torch.int32, device=dev)
         self.msg_loc = torch.empty((U, 1, self.ng, G), dtype=torch.int64, device=dev)
         self.rank_loc = torch.empty((U, 1, self.ng, T, k), dtype=torch.int32, device=dev)
+        self.exchange = exchange
+        if exchange not in ("peer", "nccl"):
+            raise ValueError("exchange must be 'peer' or 'nccl'")
         self.msg_node = torch.empty((U, 1, N, G), dtype=torch.int64, device=dev)
         self.sched = rails.Schedule.empty(self.tp, self.sh, dev)
         self.ws = torch.empty(rails.schedule_workspace(self.tp, self.sh), dtype=torch.uint8,
@@ -64,18 +69,31 @@ class RailOwnerNode:
         # own rail buffers in this GPU's HBM, exported by CUDA IPC; the other ranks
         # map them under their own device so their pack kernels store over NVLink
         self.own_ptr, handle, self.buf = rails.ipc_alloc(self.ng * self.cap)
+        # exchange buffer (flags + node-wide msg table) for the NVLink row gather
+        xb, moff = rails.owner_exchange_layout(self.tp, U, self.P)
+        self.xown, xhandle, xview = rails.ipc_alloc(xb)
+        xview.zero_()
+        torch.cuda.synchronize(dev)
+        if exchange == "peer":
+            self.msg_node = xview[moff:moff + U * N * G * 8].view(torch.int64).view(U, 1, N, G)
+        self.gen = 0
         objs = [None] * self.P
-        dist.all_gather_object(objs, (handle, dev.index), group=group)
+        dist.all_gather_object(objs, (handle, dev.index, xhandle), group=group)
         _enable_peer_access(dev.index, [o[1] for o in objs])
         bases = []
+        self.xbufs = []
         self.opened = []
-        for q, (h, _) in enumerate(objs):
+        for q, (h, _, xh) in enumerate(objs):
             if q == self.p:
                 bases.append(self.own_ptr)
+                self.xbufs.append(self.xown)
             else:
                 ptr = rails.ipc_open(h)
                 self.opened.append(ptr)
                 bases.append(ptr)
+                xp = rails.ipc_open(xh)
+                self.opened.append(xp)
+                self.xbufs.append(xp)
         self.rail_ptrs = [bases[j // self.ng] + (j % self.ng) * self.cap for j in range(N)]
         self.rail_caps = [self.cap] * N
         dist.barrier(group=group)
@@ -89,7 +107,9 @@ class RailOwnerNode:
         self.opened = []
         self.dist.barrier(group=self.group)
         rails.ipc_free(self.own_ptr)
+        rails.ipc_free(self.xown)
         self.own_ptr = None
+        self.xown = None
 
     def own_rail(self, j: int) -> torch.Tensor:
         """This rank's buffer of rail j (must be owned here)."""
@@ -100,9 +120,14 @@ class RailOwnerNode:
     def schedule_part(self, topk: torch.Tensor, lut: torch.Tensor):
         rails.histogram_gpus(self.tp, self.sh, self.g0, topk, lut, self.RB,
                              out=(self.counts, self.msg_loc, self.rank_loc))
-        for u in range(self.U):
-            self.dist.all_gather_into_tensor(self.msg_node[u, 0], self.msg_loc[u, 0],
-                                             group=self.group)
+        self.gen += 1
+        if self.exchange == "peer":
+            rails.gather_rows_peer(self.tp, self.U, self.g0, self.ng, self.msg_loc, self.p,
+                                   self.P, self.gen, self.xbufs)
+        else:
+            for u in range(self.U):
+                self.dist.all_gather_into_tensor(self.msg_node[u, 0], self.msg_loc[u, 0],
+                                                 group=self.group)
         rails.lpt_schedule(self.tp, self.sh, self.msg_node, out=self.sched, workspace=self.ws)
         rails.rail_offsets_owner(self.tp, self.sh, self.sched.send_load, self.rail_base,
                                  self.rail_total)
@@ -113,9 +138,12 @@ class RailOwnerNode:
                          self.rail_caps)
 
     def fence(self):
-        # every rank's pack precedes this all-reduce on its stream, so its
-        # completion anywhere orders all peer writes before later consumers
-        self.dist.all_reduce(self.flag, group=self.group)
+        # every rank's pack precedes this barrier on its stream, so its completion
+        # anywhere orders all peer writes before later consumers
+        if self.exchange == "peer":
+            rails.peer_barrier(self.p, self.P, self.gen, self.xbufs)
+        else:
+            self.dist.all_reduce(self.flag, group=self.group)
 
     def step(self, topk: torch.Tensor, lut: torch.Tensor, x: torch.Tensor):
         self.schedule_part(topk, lut)

@@ -103,6 +103,13 @@ def lib():
         L.rails_eval_finalize_peer.argtypes = [PT, i32, P, P, ctypes.POINTER(Peer),
                                                ctypes.POINTER(_Final), P]
         L.rails_eval_finalize_peer.restype = ctypes.c_int
+        L.rails_owner_exchange_layout.argtypes = [PT, i32, i32, ctypes.POINTER(sz),
+                                                  ctypes.POINTER(sz)]
+        L.rails_owner_exchange_layout.restype = ctypes.c_int
+        L.rails_gather_rows_peer.argtypes = [PT, i32, i32, i32, P, ctypes.POINTER(Peer), P]
+        L.rails_gather_rows_peer.restype = ctypes.c_int
+        L.rails_peer_barrier.argtypes = [ctypes.POINTER(Peer), P]
+        L.rails_peer_barrier.restype = ctypes.c_int
         L.rails_rail_offsets.argtypes = [PT, PS, P, P, P, P]
         L.rails_pack.argtypes = [PT, PS, i32, i32, P, P, P, i32, P, P, i64,
                                  ctypes.POINTER(_Sched), P, P, i64, P]
@@ -366,6 +373,32 @@ def eval_finalize_peer(tp: Topo, U: int, red_sum: torch.Tensor, red_max: torch.T
                                        _ptr(red_max, torch.int64, "red_max"), ctypes.byref(pr),
                                        ctypes.byref(cf), _stream(stream)))
     return out
+
+
+def _peer(rank: int, world: int, gen: int, bufs) -> Peer:
+    pr = Peer(rank, world, gen)
+    for i, b in enumerate(bufs):
+        pr.buf[i] = b
+    return pr
+
+
+def owner_exchange_layout(tp: Topo, U: int, world: int) -> tuple[int, int]:
+    """(bytes, msg_offset) of a rail-owner rank's exchange buffer."""
+    n, off = ctypes.c_size_t(0), ctypes.c_size_t(0)
+    _ok(lib().rails_owner_exchange_layout(ctypes.byref(tp), U, world, ctypes.byref(n),
+                                          ctypes.byref(off)))
+    return int(n.value), int(off.value)
+
+
+def gather_rows_peer(tp: Topo, U: int, g0: int, ng: int, msg_loc: torch.Tensor, rank: int,
+                     world: int, gen: int, bufs, stream=None):
+    _ok(lib().rails_gather_rows_peer(ctypes.byref(tp), U, g0, ng,
+                                     _ptr(msg_loc, torch.int64, "msg_loc"),
+                                     ctypes.byref(_peer(rank, world, gen, bufs)), _stream(stream)))
+
+
+def peer_barrier(rank: int, world: int, gen: int, bufs, stream=None):
+    _ok(lib().rails_peer_barrier(ctypes.byref(_peer(rank, world, gen, bufs)), _stream(stream)))
 
 
 # ---------------------------------------------------------------- a7

@@ -52,11 +52,15 @@ def _worker_body(rank, world, port, cfg, q):
     topk_all = torch.stack([gen.routing(M, N, T, k, E, seed, u, d, 1) for u in range(U)])
     x_all = torch.stack([gen.payload(M, N, T, RB, seed, u, d, 1) for u in range(U)])
     lut = gen.inst_lut(M, N, E)
-    node = RailOwnerNode(M, N, T, k, RB, C, U, d, lut.numel())
+    node = RailOwnerNode(M, N, T, k, RB, C, U, d, lut.numel(), exchange=cfg.get("ex", "peer"))
     g0, ng = node.g0, node.ng
     topk = topk_all[:, :, g0:g0 + ng].contiguous().to(dev)
     x = x_all[:, :, g0:g0 + ng].contiguous().to(dev)
     node.buf.zero_()
+    torch.cuda.synchronize()
+    dist.barrier()
+    node.step(topk, lut.to(dev), x)
+    node.buf.zero_()  # a second step re-gathers and re-packs (flags reused, gen 2)
     torch.cuda.synchronize()
     dist.barrier()
     node.step(topk, lut.to(dev), x)
@@ -86,6 +90,7 @@ def _worker_body(rank, world, port, cfg, q):
 @pytest.mark.parametrize("cfg", [
     dict(M=4, N=4, T=300, k=2, E=8, RB=1024, C=4096, U=2, d=1),   # 2-piece path
     dict(M=3, N=4, T=128, k=2, E=6, RB=2048, C=1024, U=1, d=2),   # C < RB multi-piece
+    dict(M=4, N=4, T=300, k=2, E=8, RB=1024, C=4096, U=2, d=1, ex="nccl"),  # NCCL exchange
 ])
 def test_railowner_pack_matches_oracle(cfg):
     ngpu = torch.cuda.device_count() if torch.cuda.is_available() else 0

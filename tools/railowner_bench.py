@@ -32,6 +32,7 @@ NVLINK_GBS = 770.0
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--units", type=int, default=8)
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"])
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     a = ap.parse_args()
@@ -46,7 +47,7 @@ def main():
     RB = cfg["H"] * 2
     U, d = a.units, 0
     seed = gen.config_seed(3)
-    node = RailOwnerNode(M, N, T, k, RB, C, U, d, M * E)
+    node = RailOwnerNode(M, N, T, k, RB, C, U, d, M * E, exchange=a.exchange)
     g0, ng = node.g0, node.ng
     topk = torch.stack([gen.routing(M, N, T, k, E, seed, u, d, 1, device=dev)
                         for u in range(U)])[:, :, g0:g0 + ng].contiguous()
@@ -89,7 +90,8 @@ def main():
     # chunk pieces land on rail j with probability ~1/N; owner = j // ng
     peer_frac = 1.0 - ng / N
     nv_bytes = wr_bytes * peer_frac
-    out = {"mode": "railowner", "n_gpus": world, "units_per_step": U, "N_rails": N,
+    out = {"mode": "railowner", "exchange": a.exchange, "n_gpus": world, "units_per_step": U,
+           "N_rails": N,
            "rails_per_gpu": ng, "step_ms": step_ms, "pack_ms": pack_ms,
            "pack_read_bytes_per_gpu": rd_bytes, "pack_write_bytes_per_gpu": wr_bytes,
            "nvlink_bytes_per_gpu_est": nv_bytes,
