@@ -33,7 +33,9 @@ constexpr int SORT_SMEM_ITEMS = 16384;  // items per CTA kept in shared memory
 
 // KeyT: uint16_t when every key C-1-size fits 16 bits (C <= 65536), else uint32_t;
 // IdxT: uint16_t message index when N*G <= 65536.  Smaller items -> more CTAs per SM.
-template <typename KeyT, typename IdxT, int THREADS>
+// SMEM: the segment's sort buffers are in shared memory (known at compile time, so
+// the radix passes use shared-memory instructions instead of generic ones).
+template <typename KeyT, typename IdxT, int THREADS, bool SMEM>
 __global__ void __launch_bounds__(THREADS)
     k_chunk_sort(const int64_t* __restrict__ msg, long long NG, int N, int d0, int nd,
                  long long C, int cshift, int nbits, int64_t* __restrict__ full_base,
@@ -57,7 +59,9 @@ __global__ void __launch_bounds__(THREADS)
   IdxT *iA, *iB;
   {
     const long long cap = NG;
-    uint8_t* base = use_smem ? smem : (ws_scratch + seg * (cap * (8 + 2 * sizeof(IdxT)) + 64));
+    uint8_t* base;
+    if constexpr (SMEM) base = smem;
+    else base = ws_scratch + seg * (cap * (8 + 2 * sizeof(IdxT)) + 64);
     kA = (KeyT*)base;
     kB = kA + cap;
     iA = (IdxT*)(kB + cap);
@@ -720,20 +724,20 @@ cudaError_t launch_schedule(const LaunchCtx& c, int U, int nd, int d0, int M, in
     void (*kern)(const int64_t*, long long, int, int, int, long long, int, int, int64_t*,
                  int32_t*, int64_t*, int32_t*, uint32_t*, uint8_t*, int, int*);
     if (k16)
-      kern = thr == 128 ? k_chunk_sort<uint16_t, uint16_t, 128>
-           : thr == 256 ? k_chunk_sort<uint16_t, uint16_t, 256>
-                        : k_chunk_sort<uint16_t, uint16_t, SORT_THREADS>;
+      kern = thr == 128 ? k_chunk_sort<uint16_t, uint16_t, 128, true>
+           : thr == 256 ? k_chunk_sort<uint16_t, uint16_t, 256, true>
+                        : k_chunk_sort<uint16_t, uint16_t, SORT_THREADS, true>;
     else
-      kern = thr == 128 ? k_chunk_sort<uint32_t, uint16_t, 128>
-           : thr == 256 ? k_chunk_sort<uint32_t, uint16_t, 256>
-                        : k_chunk_sort<uint32_t, uint16_t, SORT_THREADS>;
+      kern = thr == 128 ? k_chunk_sort<uint32_t, uint16_t, 128, true>
+           : thr == 256 ? k_chunk_sort<uint32_t, uint16_t, 256, true>
+                        : k_chunk_sort<uint32_t, uint16_t, SORT_THREADS, true>;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     kern<<<(unsigned)nseg, thr, smem, c.stream>>>(
         msg, NG, N, d0, nd, C, cshift, nbits, s.full_base, ws_inv, s.n_full, s.n_rem, ws_w,
         nullptr, 1, c.err);
   } else {
-    k_chunk_sort<uint32_t, uint32_t, SORT_THREADS><<<(unsigned)nseg, SORT_THREADS, 0, c.stream>>>(
+    k_chunk_sort<uint32_t, uint32_t, SORT_THREADS, false><<<(unsigned)nseg, SORT_THREADS, 0, c.stream>>>(
         msg, NG, N, d0, nd, C, cshift, nbits, s.full_base, ws_inv, s.n_full, s.n_rem, ws_w,
         scratch, 0, c.err);
   }
