@@ -533,8 +533,8 @@ static int check_fabric(const rails_topo_t* topo, const rails_fabric_t* fb) {
                       2LL * topo->N * fb->S;
   if (L > (1 << 20) || (long long)topo->M * topo->N * topo->M * topo->N > (1LL << 30))
     return fail(RAILS_ENOSPC, "fabric too large for the simulator");
-  const size_t smem = flowsim_smem_bytes(*topo, *fb);
-  if (smem > 200 * 1024) return fail(RAILS_ENOSPC, "L=%lld links exceed shared memory", L);
+  if (L * 8 > 200 * 1024)  // MinRTT's per-link backlog lives in shared memory
+    return fail(RAILS_ENOSPC, "L=%lld links exceed the simulator's shared memory", L);
   return RAILS_OK;
 }
 

@@ -17,6 +17,7 @@
 // that feed discrete decisions (__dmul_rn / __dadd_rn / __dsub_rn / __ddiv_rn).
 #include <cfloat>
 #include <climits>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "radix.cuh"
@@ -119,6 +120,7 @@ struct FsWs {
   int* fcur;         // [capF] PLB: the flow's active subflow
   int* fatt;         // [capF] PLB: re-hash attempts
   int* flast;        // [capF] PLB: event of the last re-hash
+  // o[33]: link state of k_fs_sim<true> (L * 40 bytes)
 };
 
 static inline size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -136,7 +138,7 @@ static FsLayout fs_layout(long long Q, int L, long long capF, long long capS) {
       (size_t)(L + 1) * 4, (size_t)capS * 16, (size_t)capF * 8, (size_t)capF * 8,
       (size_t)capF * 8, (size_t)capF, (size_t)capS * 8, (size_t)capS * 4, (size_t)capS,
       (size_t)capS * 4, (size_t)Q * 8, (size_t)Q * 8, (size_t)Q * 4, (size_t)Q * 4, 64, (size_t)Q * 8, (size_t)capS, (size_t)capS,
-      (size_t)capF * 4, (size_t)capF * 4, (size_t)capF * 4};
+      (size_t)capF * 4, (size_t)capF * 4, (size_t)capF * 4, (size_t)L * 40 + 64};
   FsLayout lo;
   size_t off = 0;
   const int n = (int)(sizeof(sz) / sizeof(sz[0]));
@@ -530,12 +532,18 @@ __global__ void __launch_bounds__(512)
 // listed at most once per event, so an event costs O(iterations * L +
 // subflow-links), not O(iterations * subflows).  Link bytes grow by used*dt.
 
+// GL: link state in the simulation's global workspace instead of shared memory
+// (fabrics whose L links do not fit, e.g. the paper's 128 domains x 8 rails).
+template <bool GL>
 __global__ void __launch_bounds__(FS_THREADS)
     k_fs_sim(FsTopo t, const int32_t* __restrict__ policy, uint8_t* ws, FsOffsets lo,
              size_t stride, long long capF, long long capS, double* __restrict__ link_bytes,
              int* err) {
   extern __shared__ __align__(16) uint8_t fs_smem[];
-  double* used = (double*)fs_smem;                                  // [L]
+  uint8_t* lbase;
+  if constexpr (GL) lbase = ws + blockIdx.x * stride + lo.o[33];
+  else lbase = fs_smem;
+  double* used = (double*)lbase;                                     // [L]
   double* lb = used + t.L;                                           // [L]
   unsigned* wsum = (unsigned*)(lb + t.L);                            // [L]
   unsigned* wbase = wsum + t.L;                                      // [L]
@@ -919,13 +927,19 @@ cudaError_t launch_flowsim(const LaunchCtx& c, const rails_topo_t& tp, const rai
   while ((1LL << nbits) <= t.L) ++nbits;
   k_fs_csr<<<n_sim, 512, 0, c.stream>>>(t, sims, o, lay.stride, nbits, capF, capS);
   const size_t ssm = flowsim_smem_bytes(tp, fb);
-  if (ssm > 48 * 1024) {
-    if ((e = cudaFuncSetAttribute(k_fs_sim, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)ssm)) != cudaSuccess)
-      return e;
+  const char* gv = getenv("RAILS_FS_GLOBAL");
+  if (ssm > 200 * 1024 || (gv && gv[0] == '1')) {
+    k_fs_sim<true><<<n_sim, FS_THREADS, 0, c.stream>>>(t, policy, sims, o, lay.stride, capF,
+                                                       capS, link_bytes, c.err);
+  } else {
+    if (ssm > 48 * 1024) {
+      if ((e = cudaFuncSetAttribute(k_fs_sim<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)ssm)) != cudaSuccess)
+        return e;
+    }
+    k_fs_sim<false><<<n_sim, FS_THREADS, ssm, c.stream>>>(t, policy, sims, o, lay.stride, capF,
+                                                          capS, link_bytes, c.err);
   }
-  k_fs_sim<<<n_sim, FS_THREADS, ssm, c.stream>>>(t, policy, sims, o, lay.stride, capF, capS,
-                                                 link_bytes, c.err);
   k_fs_finish<<<n_sim, FS_THREADS, 0, c.stream>>>(t, msg, sims, o, lay.stride, capF, capS,
                                                   msg_cct, stats);
   count_launch(6);

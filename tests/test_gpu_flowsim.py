@@ -128,3 +128,19 @@ def test_flowsim_bad_policy_flagged():
     with pytest.raises(rails.RailsError) as ei:
         rails.check()
     assert ei.value.code == rails.RAILS_ERANGE
+
+
+def test_flowsim_global_link_state_path(monkeypatch):
+    # fabrics too large for shared memory keep the link state in global memory
+    # (k_fs_sim<true>); forced here on a small case, same results as the oracle
+    monkeypatch.setenv("RAILS_FS_GLOBAL", "1")
+    M, N, S, C = 4, 4, 4, 65536
+    msg = _workload("recv", M, N, 5)
+    tp = rails.topo(M, N, C, R2=R2)
+    fb = rails.fabric(M, N, R2, S=S, Rs=0.5 * R2)
+    pol = torch.tensor([rails.FS_POLICIES[p] for p in POLS], dtype=torch.int32, device=DEV)
+    cct, lb, st = rails.flowsim(tp, fb, pol, torch.from_numpy(np.stack([msg] * len(POLS))).to(DEV))
+    cct = cct.cpu().numpy()
+    for i, p in enumerate(POLS):
+        o = oracle.flowsim(M, N, S, fb.R1, R2, fb.Rs, C, p, msg)
+        _close(cct[i], o["msg_cct"], f"{p} msg_cct (global link state)")
