@@ -217,7 +217,9 @@ int rails_eval_finalize(const rails_topo_t* topo, int32_t U, const int64_t* red_
  * all-reduce would) and finalizes -- one kernel, no NCCL call.
  *   buf[p]  rank p's exchange buffer as mapped in this process (own included),
  *           rails_peer_buffer_bytes() bytes, zero-filled before the first call;
- *   gen     call number: >= 1, equal on all ranks, +1 per call (flags compare to it).
+ *   gen     call number: >= 1, equal on all ranks, +1 per call (flags are waited on
+ *           as ">= gen"; partials are double-buffered by gen parity, so back-to-back
+ *           calls need no other synchronisation).
  * A rank that waits ~1 s for a peer sets RAILS_ECUDA-class error RAILS_ERANGE in the
  * device flag and finalizes what it has (rails_check reports it). */
 #define RAILS_PEER_MAX 8

@@ -418,14 +418,19 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* a) {
 
 __host__ __device__ static inline size_t al256e(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// [flags: U x world u32][slots: 2 (call parity) x world x U x rec int64]
 size_t peer_buffer_bytes(int U, int world, long long rsl) {
   const long long rec = rsl + RAILS_RED_MAX_LEN;
-  return al256e((size_t)U * world * 4) + (size_t)world * U * rec * 8;
+  return al256e((size_t)U * world * 4) + 2 * (size_t)world * U * rec * 8;
 }
 
 // One CTA per unit: push this rank's partials to every rank, release a flag per
 // (unit, rank), acquire every rank's flag, reduce the world's partials (in rank
-// order, so every rank computes identical sums) and finalize the unit.
+// order, so every rank computes identical sums) and finalize the unit.  Slots are
+// double-buffered by call parity and flags are waited on as ">= gen": a fast rank
+// may push call gen+1 (other half) and bump its flag while a slow rank is still
+// reading call gen, and it cannot get two calls ahead (call gen+1 waits for the
+// slow rank's gen+1 flag).
 __global__ void __launch_bounds__(256)
     k_finalize_peer(int M, int N, double R2, long long rsl, int U, int64_t* __restrict__ red_sum,
                     int64_t* __restrict__ red_max, PeerBufs pb, int rank, int world,
@@ -434,7 +439,8 @@ __global__ void __launch_bounds__(256)
   __shared__ long long stot[2];
   const long long u = blockIdx.x;
   const long long rec = rsl + RAILS_RED_MAX_LEN;
-  const size_t slots_off = al256e((size_t)U * world * 4);
+  const size_t slots_off = al256e((size_t)U * world * 4) +
+                           (size_t)(gen & 1u) * world * U * rec * 8;
   int64_t* rs = red_sum + u * rsl;
   int64_t* rmx = red_max + u * RAILS_RED_MAX_LEN;
   // 1. push (remote stores over NVLink for p != rank)
@@ -453,7 +459,7 @@ __global__ void __launch_bounds__(256)
   if (threadIdx.x < world) {
     const uint32_t* f = (const uint32_t*)pb.p[rank] + u * world + threadIdx.x;
     long long spins = 0;
-    while (ld_acquire_sys(f) != gen) {
+    while ((int)(ld_acquire_sys(f) - gen) < 0) {
       __nanosleep(64);
       if (++spins > (1LL << 24)) {
         flag_error(err, ERR_RANGE);

@@ -290,7 +290,7 @@ __device__ __forceinline__ uint32_t ld_acq_sys(const uint32_t* a) {
 }
 __device__ __forceinline__ bool wait_flag(const uint32_t* f, uint32_t gen, int* err) {
   long long spins = 0;
-  while (ld_acq_sys(f) != gen) {
+  while ((int)(ld_acq_sys(f) - gen) < 0) {  // monotonic call counters
     __nanosleep(64);
     if (++spins > (1LL << 24)) {
       flag_error(err, ERR_RANGE);

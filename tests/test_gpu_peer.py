@@ -72,6 +72,15 @@ def _worker_body(rank, world, port, cfg, q):
         for kk in ref.final:
             if not torch.equal(ref.final[kk], fused.final[kk]):
                 errors.append(f"it{it} {kk}")
+    # back-to-back calls with no host synchronisation (double-buffered partials,
+    # monotonic flags): still identical to the NCCL reference
+    for _ in range(20):
+        fused.step(msg, peer)
+    torch.cuda.synchronize()
+    rails.check()
+    for kk in ref.final:
+        if not torch.equal(ref.final[kk], fused.final[kk]):
+            errors.append(f"back-to-back {kk}")
     # the fused result against the oracle's evaluation of the whole unit
     for u in range(U):
         scheds = [oracle.schedule_node(msg_all[u, d], C) for d in range(M)]
