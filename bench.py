@@ -170,6 +170,27 @@ def oracle_sample(cfg_name: str, budget_s: float = 12.0, max_nodes: int = 16):
             "sample": sample, "seconds": round(t_used, 3)}
 
 
+def arm_config(args, P, nd=None):
+    """The workload description both arms print (weak scaling: U = P units, M/P
+    nodes of each per rank)."""
+    cfg = gen.CONFIGS[args.workload]
+    M, N = cfg["M"], cfg["N"]
+    U = P
+    nd = M // P if nd is None else nd
+    if cfg["kind"] == "routing":
+        return {"workload": "c3: Mixtral 8x7B EP routing shape, 64 nodes x 8 rails, "
+                "T=4096 tokens/GPU, top-2 of 8 experts, H=4096 bf16 rows (8 KiB), "
+                "32 KiB chunks" if args.workload == "c3" else args.workload,
+                "units": U, "nodes_per_rank": nd * U, "M": M, "N": N, "T": cfg["T"],
+                "k": cfg["k"], "row_bytes": cfg["H"] * 2, "chunk_bytes": cfg["C"],
+                "parallelism": f"nodes{P}", "a6": (args.reduce if P > 1 else "none"),
+                "l2": "inputs larger than L2: 16 GiB payload + 31.5 GiB rail buffers "
+                      "streamed per step per GPU"}
+    return {"workload": args.workload, "units": U, "nodes_per_rank": nd * U, "M": M, "N": N,
+            "chunk_bytes": cfg["C"], "parallelism": f"nodes{P}",
+            "a6": (args.reduce if P > 1 else "none")}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -187,7 +208,7 @@ def run_reference(args, rank, world):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000.0 * wall / max(1, args.steps), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-            "config": {"workload": args.workload}, "gpu_launches": 0,
+            "config": arm_config(args, max(1, world)), "gpu_launches": 0,
             "cpu_baseline": dict(info, value=v),
             "e2e": {"value": v, "unit": "nodes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(line)
@@ -357,14 +378,7 @@ def main():
         pack_gbs = float(t2.item()) / (float(pk_t.item()) / 1000.0) / 1e9
         per_gpu_pack = pack_bytes / (pack_avg_ms / 1000.0) / 1e9
         out["pack_gbs"] = pack_gbs
-        out["config"] = {"workload": "c3: Mixtral 8x7B EP routing shape, 64 nodes x 8 rails, "
-                         "T=4096 tokens/GPU, top-2 of 8 experts, H=4096 bf16 rows (8 KiB), "
-                         "32 KiB chunks" if args.workload == "c3" else args.workload,
-                         "units": U, "nodes_per_rank": nd * U, "M": M, "N": N, "T": T, "k": k,
-                         "row_bytes": RB, "chunk_bytes": C, "parallelism": f"nodes{P}",
-                         "a6": (args.reduce if P > 1 else "none"),
-                         "l2": "inputs larger than L2: 16 GiB payload + 31.5 GiB rail buffers "
-                               "streamed per step per GPU"}
+        out["config"] = arm_config(args, P, nd)
         traffic = None
         tp = os.path.join(ROOT, "profiles", "pack_traffic.json")
         if os.path.exists(tp):
@@ -379,9 +393,7 @@ def main():
                            "avg_launch_ms": pack_avg_ms,
                            "share_of_step": pack_avg_ms / (total_ms / args.steps)}
     else:
-        out["config"] = {"workload": args.workload, "units": U, "nodes_per_rank": nd * U,
-                         "M": M, "N": N, "chunk_bytes": C, "parallelism": f"nodes{P}",
-                         "a6": (args.reduce if P > 1 else "none")}
+        out["config"] = arm_config(args, P, nd)
     out["quality"] = quality
     out["clocks"] = clk.summary()
     out["gpu_launches"] = int(launches)
