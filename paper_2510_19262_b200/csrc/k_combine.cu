@@ -104,6 +104,15 @@ __global__ void __launch_bounds__(CP_THREADS)
     const int f = d0 + (int)(ul - u * nd);
     const long long b = (long long)f * N + m;
     if (r >= rows_in[u * G + b]) continue;
+    // the row's first window of payload loads is in flight while the message and
+    // chunk lookups (a binary search, then the schedule) run
+    const uint4* src = y + row * nvec;
+    uint4 v[VPL];
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      const int vi = i * 32 + lane;
+      if (vi < nvec) v[i] = ld_stream(src + vi);
+    }
     // message a: largest a with in_off[a] <= r (empty messages share offsets)
     const int64_t* io = in_off + (u * G + b) * G;
     long long lo = 0, hi = G - 1;
@@ -122,20 +131,30 @@ __global__ void __launch_bounds__(CP_THREADS)
     }
     const long long nfull = cd.div(B);
     const int64_t* rbase = rail_base + ul * N;
-    const uint4* src = y + row * nvec;
+    // C >= RB: the row lies in at most two chunks (bytes [0, b0) and [b0, RB))
+    const long long c0 = cd.div(p0);
+    const long long b0 = min((c0 + 1) * C - p0, RB);
+    const long long dst0 = msg_byte_addr(p0, mi, nfull, s, N, C, cd, rbase);
+    const long long dst1 = (C >= RB && b0 < RB)
+                               ? msg_byte_addr(p0 + b0, mi, nfull, s, N, C, cd, rbase)
+                               : 0;
     for (int w0 = 0; w0 < nvec; w0 += VPL * 32) {
-      uint4 v[VPL];
+      if (w0 > 0) {
 #pragma unroll
-      for (int i = 0; i < VPL; ++i) {
-        const int vi = w0 + i * 32 + lane;
-        if (vi < nvec) v[i] = ld_stream(src + vi);
+        for (int i = 0; i < VPL; ++i) {
+          const int vi = w0 + i * 32 + lane;
+          if (vi < nvec) v[i] = ld_stream(src + vi);
+        }
       }
 #pragma unroll
       for (int i = 0; i < VPL; ++i) {
         const int vi = w0 + i * 32 + lane;
         if (vi < nvec) {
-          const long long addr =
-              msg_byte_addr(p0 + ((long long)vi << 4), mi, nfull, s, N, C, cd, rbase);
+          const long long o = (long long)vi << 4;
+          long long addr;
+          if (o < b0) addr = dst0 < 0 ? -1 : dst0 + o;
+          else if (C >= RB) addr = dst1 < 0 ? -1 : dst1 + (o - b0);
+          else addr = msg_byte_addr(p0 + o, mi, nfull, s, N, C, cd, rbase);
           if (addr >= 0 && addr + 16 <= out_cap)
             st_stream((uint4*)(out + addr), v[i]);
           else
