@@ -455,3 +455,21 @@ def test_schedule_parity_alternate_chain_kernels(impl, monkeypatch):
         for u in range(U):
             for d in range(M):
                 compare_schedule(s, u, d, oracle.schedule_node(msg[u, d], C), f"impl{impl} u{u} d{d}")
+
+
+@pytest.mark.parametrize("impl", ["2", "3"])
+def test_pack_parity_alternate_impls(impl, monkeypatch):
+    # the TMA bulk-copy packs (RAILS_PACK_IMPL=2: per-row metadata; 3: metadata
+    # batched per 32 rows) stay selectable and byte-exact
+    monkeypatch.setenv("RAILS_PACK_IMPL", impl)
+    for (M, N, T, k, E, RB, C, U, d0, nd) in [(4, 4, 512, 2, 8, 1024, 4096, 1, 0, 4),
+                                               (5, 8, 128, 2, 8, 8192, 32768, 1, 0, 5)]:
+        topk_all, lut = routing_inputs(M, N, T, k, E, 7, 0, U)
+        topk = topk_all[:, d0:d0 + nd].contiguous()
+        x = torch.stack([gen.payload(M, N, T, RB, 3, u, d0, nd) for u in range(U)])
+        pipe = RoutingPipeline(M, N, T, k, RB, C, U, d0, nd, lut.numel(), DEV)
+        pipe.step(topk.to(DEV), lut.to(DEV), x.to(DEV))
+        torch.cuda.synchronize()
+        for u in range(U):
+            for dl in range(nd):
+                _oracle_pack_check(pipe, topk, lut, x, u, dl)
