@@ -175,7 +175,7 @@ def arm_config(args, P, nd=None):
     nodes of each per rank)."""
     cfg = gen.CONFIGS[args.workload]
     M, N = cfg["M"], cfg["N"]
-    U = P
+    U = P * (cfg.get("U", 1) if cfg["kind"] == "matrix" else 1)
     nd = M // P if nd is None else nd
     if cfg["kind"] == "routing":
         return {"workload": "c3: Mixtral 8x7B EP routing shape, 64 nodes x 8 rails, "
@@ -252,7 +252,9 @@ def main():
     d0 = rank * nd
     if args.nd is not None:
         nd = min(nd, args.nd)
-    U = P  # weak scaling: per GPU, M/P nodes of each of P units = M node schedules
+    # weak scaling: per GPU, M/P nodes of each of P units = M node schedules; byte-
+    # matrix configs batch their iterations (C2: 1000) as units of one step
+    U = P * (cfg.get("U", 1) if cfg["kind"] == "matrix" else 1)
     seed = gen.config_seed(int(args.workload[1]))
     C = cfg["C"]
 
