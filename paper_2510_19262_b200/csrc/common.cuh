@@ -229,7 +229,7 @@ cudaError_t launch_unpack_combine(const LaunchCtx&, int U, int nd, int d0, int M
 
 size_t flowsim_workspace_bytes(const rails_topo_t& tp, const rails_fabric_t& fb, int n_sim,
                                long long capF, long long capS);
-size_t flowsim_smem_bytes(const rails_topo_t& tp, const rails_fabric_t& fb);
+size_t flowsim_smem_bytes(const rails_topo_t& tp, const rails_fabric_t& fb, long long capS);
 cudaError_t launch_flowsim_plan(const LaunchCtx&, const rails_topo_t& tp,
                                 const rails_fabric_t& fb, int n_sim, const int32_t* policy,
                                 const int64_t* msg, int64_t* totals);

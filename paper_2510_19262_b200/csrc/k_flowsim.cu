@@ -138,7 +138,8 @@ static FsLayout fs_layout(long long Q, int L, long long capF, long long capS) {
       (size_t)(L + 1) * 4, (size_t)capS * 16, (size_t)capF * 8, (size_t)capF * 8,
       (size_t)capF * 8, (size_t)capF, (size_t)capS * 8, (size_t)capS * 4, (size_t)capS,
       (size_t)capS * 4, (size_t)Q * 8, (size_t)Q * 8, (size_t)Q * 4, (size_t)Q * 4, 64, (size_t)Q * 8, (size_t)capS, (size_t)capS,
-      (size_t)capF * 4, (size_t)capF * 4, (size_t)capF * 4, (size_t)L * 40 + 64};
+      (size_t)capF * 4, (size_t)capF * 4, (size_t)capF * 4,
+      (size_t)L * 41 + 2 * (size_t)((capS + 31) / 32) * 4 + 64};
   FsLayout lo;
   size_t off = 0;
   const int n = (int)(sizeof(sz) / sizeof(sz[0]));
@@ -550,7 +551,10 @@ __global__ void __launch_bounds__(FS_THREADS)
   unsigned* dnew = wbase + t.L;                                      // [L]
   int* blist = (int*)(dnew + t.L);                                   // [L]
   int* bpre = blist + t.L;                                           // [L]
-  uint8_t* isb = (uint8_t*)(bpre + t.L);                             // [L] listed now
+  int* loffs = bpre + t.L;                                           // [L+1] link offsets
+  unsigned* actb = (unsigned*)(loffs + t.L + 1);                     // [capS/32] active bits
+  unsigned* frzb = actb + (capS + 31) / 32;                          // [capS/32] frozen bits
+  uint8_t* isb = (uint8_t*)(frzb + (capS + 31) / 32);                // [L] listed now
   __shared__ double dscr[32];
   __shared__ long long lscr[32];
   __shared__ long long lscan[33];
@@ -561,11 +565,14 @@ __global__ void __launch_bounds__(FS_THREADS)
   const int nflow = (int)w.foff[t.Q], nsub = (int)w.soff[t.Q];
   const double Sd = (double)t.S;
   unsigned long long* pair = w.pair;  // [M*M], global
+  const int nwords = (nsub + 31) / 32;
   for (int l = threadIdx.x; l < t.L; l += FS_THREADS) {
     wbase[l] = 0;
     dnew[l] = 0;
     lb[l] = 0.0;
   }
+  for (int l = threadIdx.x; l <= t.L; l += FS_THREADS) loffs[l] = w.loff[l];
+  for (int q = threadIdx.x; q < nwords; q += FS_THREADS) actb[q] = 0u;
   for (int i = threadIdx.x; i < nflow; i += FS_THREADS) {
     w.rem[i] = w.fbytes[i];
     w.done[i] = 0.0;
@@ -575,9 +582,8 @@ __global__ void __launch_bounds__(FS_THREADS)
   const bool plb = policy[sim] == RAILS_POL_PLB;
   const int ls0 = l_leaf_spine(t, 0, 0), ls1 = l_nic_down(t, 0, 0);  // spine layer
   for (int s = threadIdx.x; s < nsub; s += FS_THREADS) {
-    w.sact[s] = w.sinit[s];
-    w.fep[s] = -1;
     if (!w.sinit[s]) continue;
+    atomicOr(&actb[s >> 5], 1u << (s & 31));
     const int nl = w.snl[s];
     for (int a = 0; a < nl; ++a) atomicAdd(&wbase[w.slink[(long long)s * FS_MAXL + a]], w.swi[s]);
   }
@@ -596,6 +602,7 @@ __global__ void __launch_bounds__(FS_THREADS)
       wsum[l] = wbase[l];
       used[l] = 0.0;
     }
+    for (int q = threadIdx.x; q < nwords; q += FS_THREADS) frzb[q] = 0u;
     __syncthreads();
     double xu = 0.0;  // x*/S of the previous iteration, for its pending dnew
     for (int it = 0;; ++it) {
@@ -638,7 +645,7 @@ __global__ void __launch_bounds__(FS_THREADS)
       int ntot;
       if (nbl <= 32) {  // usual case: one warp scans the list lengths
         if (threadIdx.x < 32) {
-          const int len = threadIdx.x < nbl ? w.loff[blist[threadIdx.x] + 1] - w.loff[blist[threadIdx.x]] : 0;
+          const int len = threadIdx.x < nbl ? loffs[blist[threadIdx.x] + 1] - loffs[blist[threadIdx.x]] : 0;
           const int inc = warp_incl_scan(len);
           if (threadIdx.x < nbl) bpre[threadIdx.x] = inc - len;
           if (threadIdx.x == 31) lscan[32] = inc;
@@ -649,7 +656,7 @@ __global__ void __launch_bounds__(FS_THREADS)
         long long carry = 0;
         for (int b0 = 0; b0 < nbl; b0 += FS_THREADS) {
           const int b = b0 + threadIdx.x;
-          const long long len = b < nbl ? w.loff[blist[b] + 1] - w.loff[blist[b]] : 0;
+          const long long len = b < nbl ? loffs[blist[b] + 1] - loffs[blist[b]] : 0;
           long long tot;
           const long long ex = block_excl_scan(len, lscan, &tot);
           if (b < nbl) bpre[b] = (int)(carry + ex);
@@ -666,9 +673,10 @@ __global__ void __launch_bounds__(FS_THREADS)
           else hi_ = mid - 1;
         }
         const int l = blist[lo_];
-        const int s = w.lsub[w.loff[l] + (x - bpre[lo_])];
-        if (!w.sact[s] || w.fep[s] >= events) continue;
-        if (atomicMax(&w.fep[s], events) >= events) continue;  // claimed elsewhere
+        const int s = w.lsub[loffs[l] + (x - bpre[lo_])];
+        const unsigned bit = 1u << (s & 31);
+        if (!(actb[s >> 5] & bit) || (frzb[s >> 5] & bit)) continue;
+        if (atomicOr(&frzb[s >> 5], bit) & bit) continue;  // claimed by another link
         w.rate[s] = __dmul_rn(w.sw[s], xs);
         const int nl = w.snl[s];
         bool sp = false;
@@ -689,7 +697,7 @@ __global__ void __launch_bounds__(FS_THREADS)
       if (!w.fact[i]) continue;
       double r = 0.0;
       for (int s = w.fsub0[i]; s < w.fsub0[i + 1]; ++s)
-        if (w.sact[s]) r = __dadd_rn(r, w.rate[s]);
+        if (actb[s >> 5] & (1u << (s & 31))) r = __dadd_rn(r, w.rate[s]);
       w.frate[i] = r;
       dmin = fmin(dmin, __ddiv_rn(w.rem[i], r));
       const int q = w.fmsg[i];
@@ -718,8 +726,8 @@ __global__ void __launch_bounds__(FS_THREADS)
         w.fact[i] = 0;
         ++ndone;
         for (int s = w.fsub0[i]; s < w.fsub0[i + 1]; ++s) {
-          if (!w.sact[s]) continue;
-          w.sact[s] = 0;
+          if (!(actb[s >> 5] & (1u << (s & 31)))) continue;
+          atomicAnd(&actb[s >> 5], ~(1u << (s & 31)));
           const int nl = w.snl[s];
           for (int a = 0; a < nl; ++a)
             atomicSub(&wbase[w.slink[(long long)s * FS_MAXL + a]], (unsigned)w.swi[s]);
@@ -735,8 +743,8 @@ __global__ void __launch_bounds__(FS_THREADS)
           w.flast[i] = events;
           const int nxt = w.fsub0[i] + j;
           if (nxt != cur) {
-            w.sact[cur] = 0;
-            w.sact[nxt] = 1;
+            atomicAnd(&actb[cur >> 5], ~(1u << (cur & 31)));
+            atomicOr(&actb[nxt >> 5], 1u << (nxt & 31));
             w.fcur[i] = nxt;
             for (int a = 0; a < w.snl[cur]; ++a)
               atomicSub(&wbase[w.slink[(long long)cur * FS_MAXL + a]], (unsigned)w.swi[cur]);
@@ -866,9 +874,10 @@ size_t flowsim_workspace_bytes(const rails_topo_t& tp, const rails_fabric_t& fb,
   return 256 + lo.stride * (size_t)n_sim + al256(sched) + sarr;
 }
 
-size_t flowsim_smem_bytes(const rails_topo_t& tp, const rails_fabric_t& fb) {
+size_t flowsim_smem_bytes(const rails_topo_t& tp, const rails_fabric_t& fb, long long capS) {
   const FsTopo t = fs_topo(tp, fb);
-  return (size_t)t.L * (8 + 8 + 4 + 4 + 4 + 4 + 4 + 1) + 16;
+  const size_t bits = 2 * (size_t)((capS + 31) / 32) * 4;
+  return (size_t)t.L * (8 + 8 + 4 + 4 + 4 + 4 + 4 + 4 + 1) + 4 + bits + 16;
 }
 
 cudaError_t launch_flowsim_plan(const LaunchCtx& c, const rails_topo_t& tp,
@@ -926,7 +935,7 @@ cudaError_t launch_flowsim(const LaunchCtx& c, const rails_topo_t& tp, const rai
   int nbits = 1;
   while ((1LL << nbits) <= t.L) ++nbits;
   k_fs_csr<<<n_sim, 512, 0, c.stream>>>(t, sims, o, lay.stride, nbits, capF, capS);
-  const size_t ssm = flowsim_smem_bytes(tp, fb);
+  const size_t ssm = flowsim_smem_bytes(tp, fb, capS);
   const char* gv = getenv("RAILS_FS_GLOBAL");
   if (ssm > 200 * 1024 || (gv && gv[0] == '1')) {
     k_fs_sim<true><<<n_sim, FS_THREADS, 0, c.stream>>>(t, policy, sims, o, lay.stride, capF,
