@@ -238,10 +238,9 @@ static cudaError_t launch_om(const LaunchCtx& c, int U, int nd, int d0, int M, i
   RAILS_OWN_CASE(2)
   RAILS_OWN_CASE(4)
   RAILS_OWN_CASE(8)
-  RAILS_OWN_CASE(16)
-  RAILS_OWN_CASE(24)
 #undef RAILS_OWN_CASE
-  return launch_ov<32, MULTI>(c, U, nd, d0, M, N, g0, ng, T, k, C, cshift, x, topk, lut, n_inst,
+  // rows over 8 KiB in 8 KiB windows, as k_pack (more resident warps)
+  return launch_ov<16, MULTI>(c, U, nd, d0, M, N, g0, ng, T, k, C, cshift, x, topk, lut, n_inst,
                               rank, msg, RB, s, rail_base, rp);
 }
 
