@@ -219,27 +219,53 @@ __global__ void __launch_bounds__(EV2_THREADS)
     const int tm = N * ft * N;
     __syncthreads();
     if (threadIdx.x < 64) sCol[threadIdx.x] = 0;
-    // stage 1: per-message fields, t -> (g, fl, m) with h contiguous for fixed g
-    for (int t = threadIdx.x; t < tm; t += EV2_THREADS) {
-      const int g = t / (ft * N);
-      const int rest = t - g * (ft * N);
+    // stage 1: per-message fields, t = g * (ft*N) + rest with h = f0*N + rest; a
+    // thread takes one `rest` for every g, all N loads in flight before any use
+    // (small tiles: threads beyond the tile's width split the g range)
+    const int tn = ft * N;
+    const int gsp = tn >= EV2_THREADS ? 1 : EV2_THREADS / tn;
+    for (int r0 = 0; r0 < tn; r0 += EV2_THREADS) {
+      const int rest = r0 + (gsp > 1 ? threadIdx.x % tn : threadIdx.x);
+      const int gq = gsp > 1 ? threadIdx.x / tn : 0;
+      if (rest >= tn || gq >= gsp) continue;
       const long long h = (long long)f0 * N + rest;
-      const long long idx = (long long)g * G + h;
-      long long B = mg[idx];
-      uint32_t rem = 0;
-      int rr = -1, e = -1;
-      if (B > 0 && (int)(h / N) != d) {
-        const long long nf = cd.div(B);
-        rem = (uint32_t)(B - nf * C);
-        if (rem) rr = rrp[idx];
-        e = ecmp_rail(seed, (long long)d * N + g, h, N);
-      } else {
-        B = 0;
+      constexpr int GB = NT ? (NT < 4 ? NT : 4) : 1;  // loads in flight per batch
+      for (int g0 = gq; g0 < N; g0 += GB * gsp) {
+        long long Bv[GB];
+        int8_t Rv[GB];
+#pragma unroll
+        for (int q = 0; q < GB; ++q) {
+          const int g = g0 + q * gsp;
+          Bv[q] = 0;
+          Rv[q] = -1;
+          if (g < N) {
+            const long long idx = (long long)g * G + h;
+            Bv[q] = mg[idx];
+            Rv[q] = rrp[idx];
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < GB; ++q) {
+          const int g = g0 + q * gsp;
+          if (g >= N) break;
+          const int t = g * tn + rest;
+          long long B = Bv[q];
+          uint32_t rem = 0;
+          int rr = -1, e = -1;
+          if (B > 0 && (int)(h / N) != d) {
+            const long long nf = cd.div(B);
+            rem = (uint32_t)(B - nf * C);
+            if (rem) rr = Rv[q];
+            e = ecmp_rail(seed, (long long)d * N + g, h, N);
+          } else {
+            B = 0;
+          }
+          sB[t] = B;
+          sRem[t] = rem;
+          sRr[t] = (int8_t)rr;
+          sE[t] = (int8_t)e;
+        }
       }
-      sB[t] = B;
-      sRem[t] = rem;
-      sRr[t] = (int8_t)rr;
-      sE[t] = (int8_t)e;
     }
     // block boundaries: full index at message (g, (f0+fl)*N), fl = 0..ft
     for (int t = threadIdx.x; t < N * (ft + 1); t += EV2_THREADS) {
