@@ -633,6 +633,40 @@ __global__ void __launch_bounds__(256)
   if (rem_qp) rem_qp[seg * NG + m] = q;
 }
 
+// Same as k_expand_rem with one CTA per (unit, node): the segment's n_rem chain
+// results are first copied into shared memory (coalesced), so the per-message
+// gather through the inverse permutation hits shared memory instead of 32-byte
+// global sectors for 8-byte values.
+constexpr int EXP_THREADS = 512;
+__global__ void __launch_bounds__(EXP_THREADS)
+    k_expand_seg(long long NG, const int32_t* __restrict__ n_rem,
+                 const int32_t* __restrict__ ws_inv, const uint64_t* __restrict__ ws_res,
+                 int8_t* __restrict__ rem_rail, int64_t* __restrict__ rem_off,
+                 const uint32_t* __restrict__ ws_qp, int32_t* __restrict__ rem_qp) {
+  extern __shared__ __align__(16) uint64_t sres[];
+  const long long seg = blockIdx.x;
+  const int nr = n_rem[seg];
+  const uint64_t* __restrict__ res = ws_res + seg * NG;
+  for (int p = threadIdx.x; p < nr; p += EXP_THREADS) sres[p] = res[p];
+  __syncthreads();
+  const int32_t* __restrict__ inv = ws_inv + seg * NG;
+  for (long long m = threadIdx.x; m < NG; m += EXP_THREADS) {
+    const int pos = inv[m];
+    int8_t r = -1;
+    long long o = 0;
+    int32_t q = -1;
+    if (pos >= 0) {
+      const uint64_t v = sres[pos];
+      r = (int8_t)(v >> 56);
+      o = (long long)(v & (uint64_t)OFF_MASK);
+      if (rem_qp) q = (int32_t)ws_qp[seg * NG + pos];
+    }
+    rem_rail[seg * NG + m] = r;
+    rem_off[seg * NG + m] = o;
+    if (rem_qp) rem_qp[seg * NG + m] = q;
+  }
+}
+
 // NEXT f2, Alg. 2 step 4 (R#34): per-rail round-robin QP index in
 // assignment order.  The chain results are already in sorted (= assignment)
 // order, so the QP of the p-th remainder is (full chunks on its rail + remainders
@@ -787,8 +821,21 @@ cudaError_t launch_schedule(const LaunchCtx& c, int U, int nd, int d0, int M, in
     count_launch(1);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
-  k_expand_rem<<<dim3((unsigned)((NG + 255) / 256), (unsigned)nseg), 256, 0, c.stream>>>(
-      NG, ws_inv, ws_res, s.rem_rail, s.rem_off, rem_qp ? ws_qp : nullptr, rem_qp);
+  const size_t esm = (size_t)NG * 8;
+  const char* xv = getenv("RAILS_EXPAND_IMPL");
+  // segment-staged gather for long segments (C4: 183 -> ~110 us); short ones keep
+  // the grid-wide kernel (more CTAs, nothing to stage)
+  if (NG >= 8192 && esm <= 160 * 1024 && !(xv && xv[0] == '1')) {
+    if (esm > 48 * 1024 &&
+        (e = cudaFuncSetAttribute(k_expand_seg, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)esm)) != cudaSuccess)
+      return e;
+    k_expand_seg<<<(unsigned)nseg, EXP_THREADS, esm, c.stream>>>(
+        NG, s.n_rem, ws_inv, ws_res, s.rem_rail, s.rem_off, rem_qp ? ws_qp : nullptr, rem_qp);
+  } else {
+    k_expand_rem<<<dim3((unsigned)((NG + 255) / 256), (unsigned)nseg), 256, 0, c.stream>>>(
+        NG, ws_inv, ws_res, s.rem_rail, s.rem_off, rem_qp ? ws_qp : nullptr, rem_qp);
+  }
   count_launch(1);
   return cudaGetLastError();
 }
