@@ -1,0 +1,101 @@
+"""Randomised parity sweep (-m gpu): seeded random topologies, chunk sizes, traffic
+shapes and shards through schedule + eval (byte matrices) and histogram + schedule
++ pack (routing), each compared with the oracle -- bit-exact integers, floats within
+1e-6.  Complements the hand-picked cases of test_gpu_parity.py with shapes nobody
+chose (odd N, non-power-of-two C, ragged shards, equal-size runs, empty nodes)."""
+import numpy as np
+import pytest
+import torch
+
+import gen
+import oracle
+from helpers import compare_schedule, oracle_eval_from_scheds, rel_err, routing_inputs
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2510_19262_b200 import rails
+    from paper_2510_19262_b200.pipeline import MatrixPipeline, RoutingPipeline
+
+DEV = "cuda:0"
+
+
+@pytest.fixture(autouse=True)
+def _need_cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    yield
+    rails.check()
+
+
+def _matrix(rng, U, M, N):
+    G = M * N
+    kind = rng.integers(0, 4)
+    if kind == 0:    # random sizes
+        msg = rng.integers(1, int(rng.choice([50, 5000, 3_000_000])), size=(U, M, N, G))
+    elif kind == 1:  # row multiples: long runs of equal remainders
+        msg = rng.integers(0, 30, size=(U, M, N, G)) * int(rng.choice([48, 4096, 12288]))
+    elif kind == 2:  # one size for everything
+        msg = np.full((U, M, N, G), int(rng.integers(1, 100000)))
+    else:            # sparse rows, some nodes silent
+        msg = rng.integers(1, 1_000_000, size=(U, M, N, G)) * (rng.random((U, M, N, G)) < 0.1)
+        msg[:, rng.integers(0, M)] = 0
+    msg = msg * (rng.random((U, M, N, G)) < rng.uniform(0.3, 1.0))
+    for d in range(M):
+        msg[:, d, :, d * N:(d + 1) * N] = 0
+    return msg.astype(np.int64)
+
+
+@pytest.mark.parametrize("seed", range(32))
+def test_fuzz_schedule_eval(seed):
+    rng = np.random.default_rng(1000 + seed)
+    M = int(rng.integers(2, 13))
+    N = int(rng.choice([1, 2, 3, 4, 5, 7, 8, 16]))
+    C = int(rng.choice([1, 16, 100, 1000, 4096, 65536, 1 << 20, 12345]))
+    U = int(rng.integers(1, 4))
+    msg = _matrix(rng, U, M, N)
+    d0 = int(rng.integers(0, M))
+    nd = int(rng.integers(1, M - d0 + 1))
+    tp, sh = rails.topo(M, N, C), rails.shard(U, d0, nd)
+    s = rails.lpt_schedule(tp, sh, torch.from_numpy(msg[:, d0:d0 + nd].copy()).to(DEV))
+    scheds = {}
+    for u in range(U):
+        for dl in range(nd):
+            o = oracle.schedule_node(msg[u, d0 + dl], C)
+            scheds[(u, dl)] = o
+            compare_schedule(s, u, dl, o, f"seed{seed} u{u} d{d0 + dl}")
+    # eval of whole units (all nodes) against the oracle
+    pipe = MatrixPipeline(M, N, C, U, 0, M, DEV)
+    pipe.step(torch.from_numpy(msg).to(DEV))
+    for u in range(U):
+        ev = oracle_eval_from_scheds(M, N, msg[u], [oracle.schedule_node(msg[u, d], C)
+                                                     for d in range(M)])
+        assert int(pipe.final["maxload"][u]) == ev["maxload"]
+        assert int(pipe.final["total"][u]) == ev["total"]
+        for k in ("T", "T_star", "busbw", "T_e", "busbw_e"):
+            assert rel_err(float(pipe.final[k][u]), ev[k]) <= 1e-6, (seed, k)
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_fuzz_routing_pack(seed):
+    from test_gpu_parity import _oracle_pack_check
+    rng = np.random.default_rng(2000 + seed)
+    M = int(rng.integers(2, 7))
+    N = int(rng.choice([1, 2, 3, 4, 8]))
+    E = int(rng.integers(max(2, N), 3 * N + 3))
+    k = int(rng.integers(1, min(E, 4) + 1))
+    T = int(rng.integers(1, 300))
+    RB = 16 * int(rng.integers(1, 300))
+    C = 16 * int(rng.integers(1, 2000))
+    U = int(rng.integers(1, 3))
+    topk_all, lut = routing_inputs(M, N, T, k, E, 50 + seed, 0, U)
+    d0 = int(rng.integers(0, M))
+    nd = int(rng.integers(1, M - d0 + 1))
+    topk = topk_all[:, d0:d0 + nd].contiguous()
+    x = torch.stack([gen.payload(M, N, T, RB, 9, u, d0, nd) for u in range(U)])
+    pipe = RoutingPipeline(M, N, T, k, RB, C, U, d0, nd, lut.numel(), DEV)
+    pipe.step(topk.to(DEV), lut.to(DEV), x.to(DEV))
+    torch.cuda.synchronize()
+    for u in range(U):
+        for dl in range(nd):
+            _oracle_pack_check(pipe, topk, lut, x, u, dl)
