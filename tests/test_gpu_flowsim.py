@@ -144,3 +144,25 @@ def test_flowsim_global_link_state_path(monkeypatch):
     for i, p in enumerate(POLS):
         o = oracle.flowsim(M, N, S, fb.R1, R2, fb.Rs, C, p, msg)
         _close(cct[i], o["msg_cct"], f"{p} msg_cct (global link state)")
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_flowsim_fuzz(seed):
+    # random fabrics (spines, oversubscription), chunk sizes and traffic; every
+    # policy in one batch against the oracle
+    rng = np.random.default_rng(3000 + seed)
+    M = int(rng.integers(2, 6))
+    N = int(rng.choice([1, 2, 3, 4]))
+    S = int(rng.integers(1, 5))
+    C = int(rng.choice([4096, 65536, 300000, 1 << 20]))
+    rs = float(rng.choice([0.25, 0.5, 1.0, 4.0]))
+    msg = _rand(rng, M, N, int(rng.choice([20000, 2_000_000])), p=float(rng.uniform(0.2, 1.0)))
+    tp = rails.topo(M, N, C, R2=R2)
+    fb = rails.fabric(M, N, R2, S=S, Rs=rs * R2)
+    pol = torch.tensor([rails.FS_POLICIES[p] for p in POLS], dtype=torch.int32, device=DEV)
+    cct, lb, st = rails.flowsim(tp, fb, pol, torch.from_numpy(np.stack([msg] * len(POLS))).to(DEV))
+    cct, st = cct.cpu().numpy(), st.cpu().numpy()
+    for i, p in enumerate(POLS):
+        o = oracle.flowsim(M, N, S, fb.R1, R2, fb.Rs, C, p, msg)
+        _close(cct[i], o["msg_cct"], f"seed{seed} {p} msg_cct")
+        _close(st[i, 0], o["T"], f"seed{seed} {p} T")
