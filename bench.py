@@ -298,10 +298,17 @@ def main():
 
     peer = None
     if dist is not None and args.reduce == "peer":
-        # a6 + finalize in one kernel over NVLink peer memory
+        # a6 + finalize in one kernel over NVLink peer memory;
+        # GPUs without peer access keep the NCCL all-reduce (noted in config.a6)
         from paper_2510_19262_b200.dist import PeerFinalize
         peer = PeerFinalize(pipe.tp, U, dev)
-        reduce = peer  # noqa: F811 -- the pipelines call reduce.finalize
+        if peer.ok():
+            reduce = peer  # noqa: F811 -- the pipelines call reduce.finalize
+        else:
+            print(f"peer a6 unavailable ({peer.error}); using NCCL", file=sys.stderr)
+            peer.close()
+            peer = None
+            args.reduce = "nccl"
 
     def evpair():
         return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

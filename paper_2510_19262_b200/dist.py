@@ -64,20 +64,31 @@ class PeerFinalize:
         torch.cuda.synchronize(device)
         objs = [None] * self.world
         dist.all_gather_object(objs, (handle, torch.device(device).index), group=group)
-        for _, di in objs:
-            if di != torch.device(device).index:
-                rails.enable_peer_access(di)
         self.opened = []
         self.bufs = []
-        for q, (h, _) in enumerate(objs):
-            if q == self.rank:
-                self.bufs.append(self.own_ptr)
-            else:
-                ptr = rails.ipc_open(h)
-                self.opened.append(ptr)
-                self.bufs.append(ptr)
+        self.error = None
+        try:  # every rank reaches the barrier below even if its mapping fails
+            for _, di in objs:
+                if di != torch.device(device).index:
+                    rails.enable_peer_access(di)
+            for q, (h, _) in enumerate(objs):
+                if q == self.rank:
+                    self.bufs.append(self.own_ptr)
+                else:
+                    ptr = rails.ipc_open(h)
+                    self.opened.append(ptr)
+                    self.bufs.append(ptr)
+        except Exception as exc:  # noqa: BLE001 -- surfaced through .ok()
+            self.error = str(exc)
         self.gen = 0
         dist.barrier(group=group)
+
+    def ok(self) -> bool:
+        """True on every rank iff every rank mapped every peer (collective)."""
+        import torch
+        f = torch.tensor([0.0 if self.error else 1.0], device=torch.cuda.current_device())
+        self.dist.all_reduce(f, op=self.dist.ReduceOp.MIN, group=self.group)
+        return f.item() == 1.0
 
     def finalize(self, red_sum, red_max, out, stream=None):
         from . import rails
