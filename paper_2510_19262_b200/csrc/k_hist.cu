@@ -133,7 +133,24 @@ __global__ void __launch_bounds__(W * 32)
 // bytes are written once at the end.
 constexpr int HW_WARPS = 4;
 
-template <int UNR, bool RANK>
+__device__ __forceinline__ void cp_async16(void* dst_smem, const void* src, int src_bytes) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst_smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src),
+               "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// ASYNC: the routing ids stream through a per-warp double buffer in shared memory
+// filled by cp.async two batches ahead (no registers held for the prefetch, more
+// bytes in flight per SM); needs T*k % 4 == 0 for 16-byte copies.
+template <int UNR, bool RANK, bool ASYNC = false>
 __global__ void __launch_bounds__(HW_WARPS * 32)
     k_hist_w1(const int32_t* __restrict__ topk, const int32_t* __restrict__ lut, int n_inst,
               int M, int N, int ngs, int d0, int nd, int T, int k, long long RB,
@@ -157,17 +174,49 @@ __global__ void __launch_bounds__(HW_WARPS * 32)
   __syncwarp();
   // routing ids of the next batch are loaded while this batch is ranked (software
   // pipelining: the HBM latency of the stream overlaps the shared-memory work)
-  int nx[UNR];
+  int nx[ASYNC ? 1 : UNR];
+  int32_t* stage = nullptr;
+  const int32_t* __restrict__ seg_src = topk + sg * (long long)ne;
+  auto issue = [&](int b, int buf) {  // batch starting at id b into stage[buf]
 #pragma unroll
-  for (int j = 0; j < UNR; ++j) nx[j] = (j * 32 + lane < ne) ? __ldg(src + j * 32) : -1;
-  for (int base = 0; base < ne; base += 32 * UNR) {
+    for (int q = 0; q < UNR / 4; ++q) {
+      const int i0 = b + (lane + 32 * q) * 4;
+      if (i0 < ne) {
+        const int nbytes = (ne - i0 >= 4 ? 4 : ne - i0) * 4;
+        cp_async16(stage + buf * (UNR * 32) + (lane + 32 * q) * 4, seg_src + i0, nbytes);
+      }
+    }
+    cp_async_commit();
+  };
+  if constexpr (ASYNC) {
+    stage = (int32_t*)(sw1 + (((size_t)HW_WARPS * (G + 1) + 3) & ~(size_t)3)) +
+            (size_t)wid * 2 * UNR * 32;
+    issue(0, 0);
+    issue(32 * UNR, 1);
+  } else {
+#pragma unroll
+    for (int j = 0; j < UNR; ++j) nx[j] = (j * 32 + lane < ne) ? __ldg(src + j * 32) : -1;
+  }
+  int bi = 0;
+  for (int base = 0; base < ne; base += 32 * UNR, ++bi) {
     int hv[UNR];
-#pragma unroll
-    for (int j = 0; j < UNR; ++j) hv[j] = nx[j];
     const int nb = base + 32 * UNR;
+    if constexpr (ASYNC) {
+      cp_async_wait<1>();  // this batch has landed (the next may still be in flight)
+      __syncwarp();
 #pragma unroll
-    for (int j = 0; j < UNR; ++j)
-      nx[j] = (nb + j * 32 + lane < ne) ? __ldg(src + nb + j * 32) : -1;
+      for (int j = 0; j < UNR; ++j)
+        hv[j] = (base + j * 32 + lane < ne) ? stage[(bi & 1) * (UNR * 32) + j * 32 + lane] : -1;
+      __syncwarp();
+      if (nb + 32 * UNR < ne) issue(nb + 32 * UNR, bi & 1);
+      else cp_async_commit();  // empty group keeps the wait count aligned
+    } else {
+#pragma unroll
+      for (int j = 0; j < UNR; ++j) hv[j] = nx[j];
+#pragma unroll
+      for (int j = 0; j < UNR; ++j)
+        nx[j] = (nb + j * 32 + lane < ne) ? __ldg(src + nb + j * 32) : -1;
+    }
 #pragma unroll
     for (int j = 0; j < UNR; ++j)  // all LUT lookups of the batch in flight together
       hv[j] = ((unsigned)hv[j] < (unsigned)n_inst) ? __ldg(lut + hv[j]) : -1;
@@ -260,14 +309,24 @@ cudaError_t launch_histogram(const LaunchCtx& c, int U, int nd, int d0, int M, i
   const bool many = grid >= (long long)c.num_sms * 16;
   if (!(hv && (hv[0] == '1' || hv[0] == '2')) && G <= 12288 && ne <= 65535 &&
       (many || (hv && hv[0] == '3'))) {
-    const size_t smem = (size_t)HW_WARPS * (G + 1) * 4;
+    size_t smem = (size_t)HW_WARPS * (G + 1) * 4;
     // 16 groups of 32 routing ids per batch (measured best on C4: 8 -> 16 took the
-    // batch from 0.610 to 0.573 ms); RAILS_HIST_UNR=8|32 overrides
+    // batch from 0.610 to 0.573 ms); RAILS_HIST_UNR=8|32 overrides.
+    // RAILS_HIST_ASYNC=1: ids through cp.async shared-memory stages (needs T*k % 4
+    // == 0) -- measured slower (0.637 ms: 32 KiB per CTA costs occupancy), kept as
+    // an alternative.
     const char* uv = getenv("RAILS_HIST_UNR");
     const int unr = uv ? atoi(uv) : 16;
+    const char* av = getenv("RAILS_HIST_ASYNC");
+    const bool async_ok = ne % 4 == 0 && av && av[0] == '1';
     auto kern = unr == 32 ? (rank ? k_hist_w1<32, true> : k_hist_w1<32, false>)
               : unr == 8  ? (rank ? k_hist_w1<8, true> : k_hist_w1<8, false>)
                           : (rank ? k_hist_w1<16, true> : k_hist_w1<16, false>);
+    if (async_ok) {
+      kern = rank ? k_hist_w1<16, true, true> : k_hist_w1<16, false, true>;
+      smem = (((size_t)HW_WARPS * (G + 1) + 3) & ~(size_t)3) * 4 +
+             (size_t)HW_WARPS * 2 * 16 * 32 * 4;
+    }
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -473,3 +473,18 @@ def test_pack_parity_alternate_impls(impl, monkeypatch):
         for u in range(U):
             for dl in range(nd):
                 _oracle_pack_check(pipe, topk, lut, x, u, dl)
+
+
+def test_histogram_parity_async_stage(monkeypatch):
+    # the cp.async-staged histogram variant (RAILS_HIST_ASYNC=1) stays exact
+    monkeypatch.setenv("RAILS_HIST_ASYNC", "1")
+    monkeypatch.setenv("RAILS_HIST_IMPL", "3")  # warp-per-segment kernel at any size
+    M, N, T, k, E, U = 300, 8, 64, 2, 8, 1   # G = 2400
+    topk_all, lut = routing_inputs(M, N, T, k, E, 11, 0, U)
+    topk = topk_all[:, 0:2].contiguous()
+    tp, sh = rails.topo(M, N, 65536), rails.shard(U, 0, 2)
+    counts, msg, rank = rails.histogram(tp, sh, topk.to(DEV), lut.to(DEV), 8192)
+    for dl in range(2):
+        c, m, r = oracle.histogram_node(M, N, dl, T, k, topk[0, dl].numpy(), lut.numpy(), 8192)
+        assert np.array_equal(counts[0, dl].cpu().numpy(), c)
+        assert np.array_equal(rank[0, dl].cpu().numpy(), r)
