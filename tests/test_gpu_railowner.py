@@ -91,6 +91,7 @@ def _worker_body(rank, world, port, cfg, q):
     dict(M=4, N=4, T=300, k=2, E=8, RB=1024, C=4096, U=2, d=1),   # 2-piece path
     dict(M=3, N=4, T=128, k=2, E=6, RB=2048, C=1024, U=1, d=2),   # C < RB multi-piece
     dict(M=4, N=4, T=300, k=2, E=8, RB=1024, C=4096, U=2, d=1, ex="nccl"),  # NCCL exchange
+    dict(M=3, N=4, T=100, k=2, E=8, RB=12288, C=32768, U=1, d=0),  # 12 KiB rows: windows
 ])
 def test_railowner_pack_matches_oracle(cfg):
     ngpu = torch.cuda.device_count() if torch.cuda.is_available() else 0
