@@ -5,9 +5,11 @@ Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline``
 CUDA path (``paper_2510_19262_b200``) and never imports it.
 
 The arithmetic lives in ``oracle.c`` (plain C, one function per paper step, each
-citing the PAPER.md passage it follows); this module only marshals numpy arrays
-through ctypes and strings the per-node steps together in the paper's order
-(Alg. 2).  ``brute.py`` holds the exhaustive optimum for tiny inputs.
+citing the PAPER.md passage it follows) and ``flowsim.c`` (the NEXT f4 fluid
+simulator: plain progressive filling and an event loop, R#35-R#39); this module only
+marshals numpy arrays through ctypes and strings the per-node steps together in the
+paper's order (Alg. 2).  ``brute.py`` holds the exhaustive optimum for
+tiny inputs.
 """
 from __future__ import annotations
 
