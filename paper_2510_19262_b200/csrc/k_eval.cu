@@ -7,11 +7,14 @@
 // rails fb mod N, fb+1 mod N, ... (q = n div N, r = n mod N), and its remainder on
 // rem_rail.  So eval is O(messages * N), never O(chunks).
 //
-// k_eval_node: one CTA per (unit, node); warp w handles destination nodes f = w,
-// w+W, ...; lane j accumulates R_d[f][j] (bytes of node d into NIC (f,j)) over the
-// N*N messages into f, which 32 lanes load cooperatively and broadcast by shuffle.
-// Then R[f][j] += R_d[f][j] (int64 atomics: order-independent, hence
-// deterministic), S[d][j] = sum_f R_d[f][j], colsum[f] += sum_j R_d[f][j].  The ECMP
+// k_eval_node2 (default): one CTA per (unit, node), destination nodes in tiles of
+// 256/N; stage 1 stages each message's bytes, remainder, remainder rail and ECMP
+// rail in shared memory (loads batched per thread), stage 2 runs one thread per
+// (f, j) over the tile's N*N messages into f and adds the full chunks by the
+// closed form above.  Then R[f][j] += R_d[f][j] (int64 atomics: order-independent,
+// hence deterministic), S[d][j] = sum_f R_d[f][j] (register partials per rail),
+// colsum[f] += sum_j R_d[f][j].  (k_eval_node, the first version, is kept behind
+// RAILS_EVAL_IMPL=1.)  The ECMP
 // baseline (R#13-R#14) hashes each whole message onto one rail.
 // MSE (Eq. 6; Alg. 2 step 6; R#11) is the exact integer
 // sum_j (N*S_j - sum S)^2 over N^3, converted once (R#25).

@@ -11,10 +11,11 @@
 // B200 design: one CTA per simulation, so a batch of (unit, policy) simulations
 // fills the SMs; every step of a simulation -- flow construction, MinRTT route
 // choice, the link->subflow index, the whole event loop and the CCT statistics --
-// runs on the device with no host round trip.  Per-link sums run one warp per link
-// over a link-sorted subflow list (CSR) with a fixed shuffle tree, so a run is
-// deterministic.  Floating point: IEEE binary64, no FMA contraction on the paths
-// that feed discrete decisions (__dmul_rn / __dadd_rn / __dsub_rn / __ddiv_rn).
+// runs on the device with no host round trip.  The event loop keeps link state in
+// shared memory and updates it incrementally with integer weight sums and
+// claim-based freezing (bitmaps), so a run is deterministic.  Floating point: IEEE
+// binary64, no FMA contraction on the paths that feed discrete decisions
+// (__dmul_rn / __dadd_rn / __dsub_rn / __ddiv_rn).
 #include <cfloat>
 #include <climits>
 #include <cstdlib>

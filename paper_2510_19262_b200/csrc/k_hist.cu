@@ -5,7 +5,12 @@
 // GPU h; msg_bytes = counts * RB for remote h (R#2); row_rank = position of (t,s)
 // among the earlier slots of GPU g with the same h (R#18), which the pack needs.
 //
-// Design (B200): one CTA per (unit, node, source GPU).  The T*k routing entries are
+// Batched default (>= 16 segments per SM): k_hist_w1, one warp per (unit, node,
+// source GPU) with one packed (count | tag) shared word per bin -- ties inside a
+// 32-entry group resolved by a tag write / read-back and a loser-ballot loop, 16
+// groups of ids per batch with the next batch's loads in flight.  Few segments
+// (C3: 512): k_hist_rank below, W warps per segment.
+// k_hist_rank: one CTA per (unit, node, source GPU).  The T*k routing entries are
 // split into W contiguous warp segments.  Pass 1: each warp counts its segment
 // into its private shared-memory sub-histogram (shared atomics that only ever
 // collide within the warp; counts are order-free).  Scan: per bin, an exclusive prefix across warps

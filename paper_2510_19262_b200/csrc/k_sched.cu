@@ -14,11 +14,16 @@
 //    over the segment are skipped).  Stability keeps (g,h) order among equal sizes,
 //    which is exactly the tie-break R#4.  One CTA per (unit, node); the segment
 //    lives in shared memory when it fits (generic pointers, global otherwise).
-// a4: one warp per (unit, node) runs the serial argmin chain over the
-//    sorted remainders.  Lane j holds rail j's load relative to a running base
-//    (the current minimum); with rel <= C < 2^26 the 32-bit key (rel << 5) | j
-//    makes argmin-with-lowest-index-tie a single redux.sync.min.u32.  Offsets are
-//    base + rel of the chosen rail before the add (R#19).
+// a4: one warp per (unit, node) runs the serial chain over the sorted
+//    remainders.  Default (N in {2,4,8,16}, C < 2^23): k_lpt_wstage -- every lane
+//    holds the N rail keys (rel << 5) | rail sorted in registers (argmin = K[0],
+//    lowest rail on ties), runs of equal sizes are dealt by the exact cyclic
+//    closed form with all 32 lanes writing, and the sorted size list is staged
+//    through shared memory one batch ahead.  Otherwise k_lpt_chain: lane j holds
+//    rail j's load relative to a running base and argmin-with-lowest-index-tie is
+//    one redux.sync.min.u32 on (rel << 5) | j.  Offsets are base + rel of the
+//    chosen rail before the add (R#19).  Results are written in sorted order and
+//    expanded to per-message rem_rail / rem_off through the inverse permutation.
 #include <climits>
 #include <cstdlib>
 
