@@ -87,18 +87,23 @@ __global__ void __launch_bounds__(THREADS)
     for (int j = 0; j < IPT; ++j) B[j] = m0 + j < NG ? mg[m0 + j] : 0;
     long long snf = 0;
     int srem = 0;
+    long long nfv[IPT];
+    // destination GPU h = m mod G of the first item, then stepped (one division
+    // per thread and tile instead of one per message)
+    int h = (int)((unsigned long long)m0 % (unsigned long long)G);
+    const int lo = d * N, hi = d * N + N;  // the source node's own GPUs (R#2)
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
-      const long long m = m0 + j;
       // negative bytes, or bytes to a GPU of the source node (R#2), are invalid
-      if (B[j] < 0 || (B[j] != 0 && (int)((unsigned)m % (unsigned)G) / N == d)) {
+      if (B[j] < 0 || (B[j] != 0 && h >= lo && h < hi)) {
         flag_error(err, ERR_RANGE);
         B[j] = 0;
       }
-      const long long nf = cd.div(B[j]);
-      if (nf >= (1LL << 40)) flag_error(err, ERR_OVERFLOW);
-      snf += nf;
-      srem += (B[j] - nf * C) > 0;
+      if (++h >= G) h -= G;
+      nfv[j] = cd.div(B[j]);
+      if (nfv[j] >= (1LL << 40)) flag_error(err, ERR_OVERFLOW);
+      snf += nfv[j];
+      srem += (B[j] - nfv[j] * C) > 0;
     }
     long long tot;
     const long long ex = block_excl_scan((snf << 16) | srem, scan_scratch, &tot);
@@ -108,7 +113,7 @@ __global__ void __launch_bounds__(THREADS)
     for (int j = 0; j < IPT; ++j) {
       const long long m = m0 + j;
       if (m >= NG) break;
-      const long long nf = cd.div(B[j]);
+      const long long nf = nfv[j];
       const long long rem = B[j] - nf * C;
       full_base[seg * NG + m] = fb;
       fb += nf;
