@@ -174,6 +174,15 @@ __device__ __forceinline__ void divmod_n(long long a, int N, long long& q, int& 
   }
 }
 
+// 64-bit accumulation as two 32-bit shared atomics (the carry out of the low half
+// goes to the high half); exact and order-independent.
+__device__ __forceinline__ void add64_split(unsigned* lo, unsigned* hi, unsigned long long v) {
+  const unsigned l = (unsigned)v, h = (unsigned)(v >> 32);
+  const unsigned old = atomicAdd(lo, l);
+  const unsigned carry = (old + l < old) ? 1u : 0u;
+  if (h + carry) atomicAdd(hi, h + carry);
+}
+
 template <int NT>  // NT = N when it is a power of two <= 32 (divisions by shifts), else 0
 __global__ void __launch_bounds__(EV2_THREADS)
     k_eval_node2(int M, int N_rt, int nd, int d0, long long C, int cshift, uint64_t seed, int FT,
@@ -200,15 +209,13 @@ __global__ void __launch_bounds__(EV2_THREADS)
   unsigned long long* col = Re + M * (long long)N;
   unsigned long long* tot = col + M;
 
-  const int TM = N * FT * N;          // messages per tile
-  long long* sB = (long long*)ev_smem;                 // [TM]
-  uint32_t* sRem = (uint32_t*)(sB + TM);               // [TM]
-  int8_t* sRr = (int8_t*)(sRem + TM);                  // [TM]
-  int8_t* sE = sRr + TM;                               // [TM]
-  // (offsets from ev_smem, not integer casts, so the compiler keeps shared loads)
-  long long* sQ = (long long*)(ev_smem + ((size_t)TM * 14 + 15) / 16 * 16);  // [N][FT+1]
+  long long* sQ = (long long*)ev_smem;                 // [N][FT+1]
   int* sR = (int*)(sQ + N * (FT + 1));                 // [N][FT+1]
   __shared__ unsigned long long sCol[64];
+  // per (fl, j) of the tile: remainder bytes into NIC (f, j) and ECMP bytes, as
+  // 64-bit sums split into 32-bit halves (32-bit shared atomics are native)
+  __shared__ unsigned aRlo[EV2_THREADS], aRhi[EV2_THREADS], aElo[EV2_THREADS],
+      aEhi[EV2_THREADS];
 
   if (threadIdx.x < 32) {
     sS[threadIdx.x] = 0;
@@ -219,9 +226,10 @@ __global__ void __launch_bounds__(EV2_THREADS)
   __shared__ unsigned long long sAcc[2][EV2_THREADS];
   for (int f0 = 0; f0 < M; f0 += FT) {
     const int ft = min(FT, M - f0);
-    const int tm = N * ft * N;
     __syncthreads();
     if (threadIdx.x < 64) sCol[threadIdx.x] = 0;
+    aRlo[threadIdx.x] = aRhi[threadIdx.x] = aElo[threadIdx.x] = aEhi[threadIdx.x] = 0u;
+    __syncthreads();
     // stage 1: per-message fields, t = g * (ft*N) + rest with h = f0*N + rest; a
     // thread takes one `rest` for every g, all N loads in flight before any use
     // (small tiles: threads beyond the tile's width split the g range)
@@ -251,22 +259,16 @@ __global__ void __launch_bounds__(EV2_THREADS)
         for (int q = 0; q < GB; ++q) {
           const int g = g0 + q * gsp;
           if (g >= N) break;
-          const int t = g * tn + rest;
-          long long B = Bv[q];
-          uint32_t rem = 0;
-          int rr = -1, e = -1;
+          const long long B = Bv[q];
           if (B > 0 && (int)(h / N) != d) {
+            const int fb = (rest / N) * N;  // (fl, 0) of this message's destination
             const long long nf = cd.div(B);
-            rem = (uint32_t)(B - nf * C);
-            if (rem) rr = Rv[q];
-            e = ecmp_rail(seed, (long long)d * N + g, h, N);
-          } else {
-            B = 0;
+            const long long rem = B - nf * C;
+            if (rem && Rv[q] >= 0 && Rv[q] < N)
+              add64_split(&aRlo[fb + Rv[q]], &aRhi[fb + Rv[q]], (unsigned long long)rem);
+            const int e = ecmp_rail(seed, (long long)d * N + g, h, N);
+            add64_split(&aElo[fb + e], &aEhi[fb + e], (unsigned long long)B);
           }
-          sB[t] = B;
-          sRem[t] = rem;
-          sRr[t] = (int8_t)rr;
-          sE[t] = (int8_t)e;
         }
       }
     }
@@ -297,13 +299,9 @@ __global__ void __launch_bounds__(EV2_THREADS)
           const long long qa = sQ[g * (FT + 1) + fl], qb = sQ[g * (FT + 1) + fl + 1];
           const int ra = sR[g * (FT + 1) + fl], rb = sR[g * (FT + 1) + fl + 1];
           full += (qb - qa) + (j < rb ? 1 : 0) - (j < ra ? 1 : 0);
-          const int mb = g * (ft * N) + fl * N;
-          for (int m = 0; m < N; ++m) {
-            if (sRr[mb + m] == j) Rv += sRem[mb + m];
-            if (sE[mb + m] == j) Rev += sB[mb + m];
-          }
         }
-        Rv += full * C;
+        Rv = full * C + (long long)(((unsigned long long)aRhi[t] << 32) | aRlo[t]);
+        Rev = (long long)(((unsigned long long)aEhi[t] << 32) | aElo[t]);
       }
       if (Rv) atomicAdd(R + (long long)f * N + j, (unsigned long long)Rv);
       if (Rev) atomicAdd(Re + (long long)f * N + j, (unsigned long long)Rev);
@@ -587,8 +585,7 @@ cudaError_t launch_eval(const LaunchCtx& c, int U, int nd, int d0, int M, int N,
         e.nmse, e.red_sum, e.red_max, rsl);
   } else {
     const int FT = (EV2_THREADS / N) < 64 ? (EV2_THREADS / N) : 64;
-    const size_t tm = (size_t)N * FT * N;
-    const size_t smem = tm * (8 + 4 + 1 + 1) + 16 + (size_t)N * (FT + 1) * (8 + 4);
+    const size_t smem = 16 + (size_t)N * (FT + 1) * (8 + 4);
     void (*kern)(int, int, int, int, long long, int, uint64_t, int, const int64_t*,
                  const int64_t*, const int8_t*, const int64_t*, int64_t*, int64_t*, double*,
                  double*, int64_t*, int64_t*, long long) =
