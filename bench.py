@@ -52,6 +52,7 @@ def parse():
                     help="a6 at N > 1: fused finalize over NVLink peer memory, or NCCL")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-ring", action="store_true",
                     help="force the pinned-ring staging of the payload (testing)")
@@ -407,6 +408,22 @@ def main():
     out["clocks"] = clk.summary()
     out["gpu_launches"] = int(launches)
 
+    # ---- the same step replayed from a CUDA graph (N = 1: the a6 peer exchange's
+    # call counter lives on the host, so multi-rank steps are not captured)
+    if world == 1 and cfg["kind"] == "routing" and not args.no_graph:
+        from paper_2510_19262_b200.pipeline import GraphStep
+        g = GraphStep(lambda: pipe.step(topk, lut, x))
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(args.steps):
+            g()
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gms = g0.elapsed_time(g1) / args.steps
+        out["graph"] = {"value": nodes / (gms / 1000.0), "unit": "nodes/s", "ms_per_step": gms,
+                        "what": "the same step captured once into a CUDA graph and replayed"}
+        del g
     # ---- e2e: host buffers, H2D of the step's inputs + D2H of its results, timed
     if not args.no_e2e:
         out["e2e"] = e2e(args, cfg, pipe, rails, stream, dist, world, locals())

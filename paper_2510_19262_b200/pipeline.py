@@ -95,3 +95,31 @@ class MatrixPipeline:
             reduce(self.ev.red_sum, self.ev.red_max)
         rails.eval_finalize(self.tp, self.U, self.ev.red_sum, self.ev.red_max, out=self.final,
                             stream=stream)
+
+
+class GraphStep:
+    """A pipeline step captured once into a CUDA graph and replayed.
+
+    Every call the step makes is an asynchronous C-ABI launch on the capturing
+    stream with preallocated buffers (no host synchronisation, no allocation), so
+    `pipe.step(*args)` captures as is; replaying it re-runs the whole hot path with
+    one graph launch instead of ~8 host launches.  Inputs are read from the tensors
+    passed at capture time: refill them in place (tensor.copy_) between replays.
+    The a6 hook must be graph-safe (the peer-memory finalize is; an NCCL all-reduce
+    is capturable with NCCL's own graph support)."""
+
+    def __init__(self, step: Callable, *args, warmup: int = 2):
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(warmup):  # warm: lazy init (function attributes, modules)
+                step(*args)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            step(*args)
+        torch.cuda.synchronize()
+
+    def __call__(self):
+        self.graph.replay()

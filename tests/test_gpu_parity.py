@@ -488,3 +488,31 @@ def test_histogram_parity_async_stage(monkeypatch):
         c, m, r = oracle.histogram_node(M, N, dl, T, k, topk[0, dl].numpy(), lut.numpy(), 8192)
         assert np.array_equal(counts[0, dl].cpu().numpy(), c)
         assert np.array_equal(rank[0, dl].cpu().numpy(), r)
+
+
+def test_graph_replay_matches_eager():
+    # the whole routing step captured into a CUDA graph: replays give exactly the
+    # eager step's schedule, evaluation and packed bytes (also after new inputs)
+    from paper_2510_19262_b200.pipeline import GraphStep
+    M, N, T, k, E, RB, C, U = 4, 4, 512, 2, 8, 1024, 4096, 2
+    topk_all, lut = routing_inputs(M, N, T, k, E, 21, 0, U)
+    x = torch.stack([gen.payload(M, N, T, RB, 5, u, 0, M) for u in range(U)]).to(DEV)
+    topk = topk_all.to(DEV)
+    lut = lut.to(DEV)
+    eager = RoutingPipeline(M, N, T, k, RB, C, U, 0, M, lut.numel(), DEV)
+    graphed = RoutingPipeline(M, N, T, k, RB, C, U, 0, M, lut.numel(), DEV)
+    tk = topk.clone()
+    g = GraphStep(graphed.step, tk, lut, x)
+    for seed in (21, 22):
+        new, _ = routing_inputs(M, N, T, k, E, seed, 0, U)
+        tk.copy_(new.to(DEV))
+        eager.step(tk, lut, x)
+        graphed.out.zero_()
+        g()
+        torch.cuda.synchronize()
+        assert torch.equal(eager.sched.rem_off, graphed.sched.rem_off)
+        assert torch.equal(eager.sched.send_load, graphed.sched.send_load)
+        for kk in eager.final:
+            assert torch.equal(eager.final[kk], graphed.final[kk])
+        n = int(eager.total.item())
+        assert torch.equal(eager.out[:n], graphed.out[:n])
