@@ -15,10 +15,11 @@
 // into its private shared-memory sub-histogram (shared atomics that only ever
 // collide within the warp; counts are order-free).  Scan: per bin, an exclusive prefix across warps
 // turns the sub-histograms into the warp's starting rank; the column total is the
-// count.  Pass 2 re-walks the segment (L1/L2-resident) in 32-entry groups; a
-// ballot-per-bit multi-split (warp_match_bits) finds the lanes with the same
-// destination, and rank = warp base + running count + peers below in the group:
-// deterministic and identical to the sequential definition.  HBM traffic per CTA: read 4*T*k B of
+// count.  Pass 2 re-walks the segment (L1/L2-resident) in 32-entry groups; the
+// lanes with the same destination are found by the tag trick of k_hist_w1 (ranks
+// < 2^24; with 16 warps per segment: C3 36.9 -> 28.7 us) or a ballot-per-bit multi-split
+// (warp_match_nb, RAILS_HIST_MATCH=1), and rank = warp base + running count +
+// peers below in the group: deterministic and identical to the sequential definition.  HBM traffic per CTA: read 4*T*k B of
 // routing, write 4*T*k B of ranks + 12*G B of counts/bytes.
 #include <cstdlib>
 
@@ -44,34 +45,40 @@ __global__ void __launch_bounds__(W * 32)
   for (int i = threadIdx.x; i < W * G; i += W * 32) cnt[i] = 0;
   __syncthreads();
 
-  const long long seg = (((ne + W - 1) / W) + 31) & ~31LL;
-  const long long beg = (long long)wid * seg;
-  const long long end = min(ne, beg + seg);
+  // 32-bit indices inside the segment (T*k < 2^31: ranks are int32)
+  const int nei = (int)ne;
+  const int seg = (((nei + W - 1) / W) + 31) & ~31;
+  const int beg = wid * seg;
+  const int end = min(nei, beg + seg);
   int32_t* my = cnt + wid * G;
+  bool bad = false;
 
-  // ---- pass 1: per-warp sub-histogram
-  for (long long base = beg; base < end; base += 32 * UNR) {
-    int hv[UNR];
+  // ids of one batch -> destination GPUs (-1 = invalid or past the end); all
+  // loads of a batch, then all LUT lookups, are in flight together
+  auto fetch = [&](int base, int (&hv)[UNR]) {
 #pragma unroll
     for (int j = 0; j < UNR; ++j) {
-      long long e = base + j * 32 + lane;
+      const int e = base + j * 32 + lane;
       hv[j] = (e < end) ? __ldg(src + e) : -1;
     }
 #pragma unroll
     for (int j = 0; j < UNR; ++j) {
-      long long e = base + j * 32 + lane;
-      int h = -1;
-      if (e < end) {
-        int inst = hv[j];
-        if (inst >= 0 && inst < n_inst) {
-          h = __ldg(lut + inst);
-          if (h < 0 || h >= G) h = -1;
-        }
-        if (h < 0) flag_error(err, ERR_RANGE);
-      }
-      if (h >= 0) atomicAdd(&my[h], 1);  // private to this warp: order-free count
+      int h = ((unsigned)hv[j] < (unsigned)n_inst) ? __ldg(lut + hv[j]) : -1;
+      hv[j] = ((unsigned)h < (unsigned)G) ? h : -1;
+    }
+  };
+
+  // ---- pass 1: per-warp sub-histogram
+  for (int base = beg; base < end; base += 32 * UNR) {
+    int hv[UNR];
+    fetch(base, hv);
+#pragma unroll
+    for (int j = 0; j < UNR; ++j) {
+      bad |= hv[j] < 0 && base + j * 32 + lane < end;
+      if (hv[j] >= 0) atomicAdd(&my[hv[j]], 1);  // private to this warp: order-free count
     }
   }
+  if (bad) flag_error(err, ERR_RANGE);
   __syncthreads();
 
   // ---- scan across warps per bin; totals are the counts
@@ -91,31 +98,44 @@ __global__ void __launch_bounds__(W * 32)
 
   // ---- pass 2: stable ranks
   int32_t* __restrict__ dst = rank + cta * ne;
-  for (long long base = beg; base < end; base += 32 * UNR) {
+  const unsigned lt = lanemask_lt();
+  for (int base = beg; base < end; base += 32 * UNR) {
     int hv[UNR];
+    fetch(base, hv);
 #pragma unroll
     for (int j = 0; j < UNR; ++j) {
-      long long e = base + j * 32 + lane;
-      hv[j] = (e < end) ? __ldg(src + e) : -1;
-    }
-#pragma unroll
-    for (int j = 0; j < UNR; ++j) {
-      long long e = base + j * 32 + lane;
-      int h = -1;
-      if (e < end) {
-        int inst = hv[j];
-        if (inst >= 0 && inst < n_inst) {
-          h = __ldg(lut + inst);
-          if (h < 0 || h >= G) h = -1;
+      const int e = base + j * 32 + lane;
+      const int h = hv[j];
+      const bool valid = h >= 0;
+      if constexpr (HB == 0) {
+        // equal destinations by the tag trick of k_hist_w1 below (ranks < 2^24):
+        // tag byte write, one word read, a loop over the (rare) losers
+        if (valid) ((uint8_t*)(my + h))[3] = (uint8_t)lane;
+        __syncwarp();
+        const uint32_t word = valid ? (uint32_t)my[h] : 0u;
+        const int t = (int)(word >> 24);
+        const int c = (int)(word & 0xffffffu);
+        const bool loser = valid && t != lane;
+        unsigned peers = (1u << lane) | (loser ? (1u << t) : 0u);
+        unsigned lm = __ballot_sync(FULL, loser);
+        while (lm) {
+          const int b = __ffs(lm) - 1;
+          lm &= lm - 1;
+          if (__shfl_sync(FULL, h, b) == h) peers |= 1u << b;
         }
+        const unsigned below = peers & lt;
+        if (valid && below == 0) my[h] = (int32_t)((c + __popc(peers)) & 0xffffff);
+        __syncwarp();
+        if (e < end) dst[e] = valid ? c + __popc(below) : -1;
+      } else {
+        const unsigned peers = warp_match_nb<HB>((unsigned)h, valid);
+        int r = -1;
+        if (valid) r = my[h] + __popc(peers & lt);
+        __syncwarp();
+        if (valid && lane == __ffs(peers) - 1) my[h] += __popc(peers);
+        __syncwarp();
+        if (e < end) dst[e] = r;
       }
-      const unsigned peers = warp_match_nb<HB>((unsigned)h, h >= 0);
-      int r = -1;
-      if (h >= 0) r = my[h] + __popc(peers & lanemask_lt());
-      __syncwarp();
-      if (h >= 0 && lane == __ffs(peers) - 1) my[h] += __popc(peers);
-      __syncwarp();
-      if (e < end) dst[e] = r;
     }
   }
 }
@@ -287,15 +307,24 @@ static cudaError_t launch_w(const LaunchCtx& c, long long grid, int M, int N, in
                             long long RB, int32_t* counts, int64_t* msg, int32_t* rank) {
   int hb = 0;
   while ((1LL << hb) < (long long)M * N) ++hb;
+  // ranks below 2^24: the tag path (HB = 0) unless RAILS_HIST_MATCH=1 asks for the
+  // per-bit ballot match
+  const char* mv = getenv("RAILS_HIST_MATCH");
+  if ((long long)T * k < (1LL << 24) && !(mv && mv[0] == '1')) hb = 0;
   switch (hb) {
+#define RAILS_HB0                                                                          \
+  case 0:                                                                                   \
+    return launch_wh<W, 0>(c, grid, M, N, ngs, d0, nd, T, k, topk, lut, n_inst, RB, counts, msg, \
+                           rank);
 #define RAILS_HB(B)                                                                         \
   case B:                                                                                   \
     return launch_wh<W, B>(c, grid, M, N, ngs, d0, nd, T, k, topk, lut, n_inst, RB, counts, msg, \
                            rank);
-    RAILS_HB(1) RAILS_HB(2) RAILS_HB(3) RAILS_HB(4) RAILS_HB(5) RAILS_HB(6) RAILS_HB(7)
+    RAILS_HB0 RAILS_HB(1) RAILS_HB(2) RAILS_HB(3) RAILS_HB(4) RAILS_HB(5) RAILS_HB(6) RAILS_HB(7)
     RAILS_HB(8) RAILS_HB(9) RAILS_HB(10) RAILS_HB(11) RAILS_HB(12) RAILS_HB(13) RAILS_HB(14)
     RAILS_HB(15) RAILS_HB(16)
 #undef RAILS_HB
+#undef RAILS_HB0
     default:
       return cudaErrorInvalidValue;
   }
@@ -340,7 +369,17 @@ cudaError_t launch_histogram(const LaunchCtx& c, int U, int nd, int d0, int M, i
     count_launch(1);
     return cudaGetLastError();
   }
-  // Warps per CTA: as many private sub-histograms as fit in 64 KiB (>= 1).
+  // Warps per CTA: as many private sub-histograms as fit in 64 KiB (>= 1); 16 when
+  // the segments alone cannot fill the SMs' warp slots with 8 (RAILS_HIST_W=8|16|32
+  // overrides).
+  const char* wv = getenv("RAILS_HIST_W");
+  const int wo = wv ? atoi(wv) : 0;
+  if (wo == 32 && G * 32 * 4 <= 65536)
+    return launch_w<32>(c, grid, M, N, ngs, d0, nd, T, k, topk, lut, n_inst, row_bytes, counts,
+                        msg, rank);
+  if ((wo == 16 || (wo == 0 && grid * 16 <= (long long)c.num_sms * 64)) && G * 16 * 4 <= 65536)
+    return launch_w<16>(c, grid, M, N, ngs, d0, nd, T, k, topk, lut, n_inst, row_bytes, counts,
+                        msg, rank);
   if (G * 8 * 4 <= 65536)
     return launch_w<8>(c, grid, M, N, ngs, d0, nd, T, k, topk, lut, n_inst, row_bytes, counts, msg,
                        rank);

@@ -490,6 +490,30 @@ def test_histogram_parity_async_stage(monkeypatch):
         assert np.array_equal(rank[0, dl].cpu().numpy(), r)
 
 
+@pytest.mark.parametrize("match,w", [(None, None), ("0", "8"), ("0", "16"), ("0", "32"),
+                                     ("1", "16")])
+def test_histogram_parity_multiwarp_variants(match, w, monkeypatch):
+    # the multi-warp-per-segment kernel (C3's few segments): ranks by the tag path
+    # (default) or the per-bit ballot match (RAILS_HIST_MATCH=1), 8/16/32 warps
+    # per segment; G = 4 makes nearly every 32-id group collide, G = 512 almost never
+    monkeypatch.setenv("RAILS_HIST_IMPL", "1")
+    if match is not None:
+        monkeypatch.setenv("RAILS_HIST_MATCH", match)
+        monkeypatch.setenv("RAILS_HIST_W", w)
+    for (M, N, T, k, E) in [(2, 2, 1000, 2, 4), (64, 8, 777, 2, 8), (3, 4, 4096, 4, 8),
+                            (2, 4, 10000, 4, 8), (64, 8, 4096, 2, 8)]:
+        topk_all, lut = routing_inputs(M, N, T, k, E, 13, 0, 1)
+        nd = min(M, 2)
+        topk = topk_all[:, 0:nd].contiguous()
+        tp, sh = rails.topo(M, N, 65536), rails.shard(1, 0, nd)
+        counts, msg, rank = rails.histogram(tp, sh, topk.to(DEV), lut.to(DEV), 4096)
+        for dl in range(nd):
+            c, m, r = oracle.histogram_node(M, N, dl, T, k, topk[0, dl].numpy(), lut.numpy(), 4096)
+            assert np.array_equal(counts[0, dl].cpu().numpy(), c)
+            assert np.array_equal(msg[0, dl].cpu().numpy(), m)
+            assert np.array_equal(rank[0, dl].cpu().numpy(), r)
+
+
 def test_graph_replay_matches_eager():
     # the whole routing step captured into a CUDA graph: replays give exactly the
     # eager step's schedule, evaluation and packed bytes (also after new inputs)

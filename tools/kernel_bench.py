@@ -123,6 +123,23 @@ def bench_pack(res):
     torch.cuda.empty_cache()
 
 
+def bench_hist_c3(res):
+    """The C3 launch of a1 (64 nodes x 8 source GPUs = 512 segments of 8192 ids)."""
+    cfg = gen.CONFIGS["c3"]
+    M, N, T, k, E = cfg["M"], cfg["N"], cfg["T"], cfg["k"], cfg["E"]
+    topk = gen.routing(M, N, T, k, E, gen.config_seed(3), 0, device=DEV)[None].contiguous()
+    lut = gen.inst_lut(M, N, E).to(DEV)
+    tp, sh = rails.topo(M, N, cfg["C"]), rails.shard(1, 0, M)
+    G = M * N
+    out = (torch.empty((1, M, N, G), dtype=torch.int32, device=DEV),
+           torch.empty((1, M, N, G), dtype=torch.int64, device=DEV),
+           torch.empty((1, M, N, T, k), dtype=torch.int32, device=DEV))
+    t = timeit(lambda: rails.histogram(tp, sh, topk, lut, cfg["H"] * 2, out=out), iters=20)
+    algo = M * N * (T * k * 4 * 2 + G * 12)
+    gbs = algo / (t["median_ms"] / 1e3) / 1e9
+    res["hist_c3"] = dict(t, gbs=gbs, frac=gbs / PEAK, bytes=algo)
+
+
 def bench_hist_c4(res):
     cfg = gen.CONFIGS["c4"]
     M, N, T, k, E = cfg["M"], cfg["N"], cfg["T"], cfg["k"], cfg["E"]
@@ -201,6 +218,8 @@ def main():
         bench_bw(res)
     if "pack" in only:
         bench_pack(res)
+    if "hist3" in only:
+        bench_hist_c3(res)
     if "hist" in only:
         bench_hist_c4(res)
     if "c2" in only:
