@@ -1,6 +1,7 @@
 #!/usr/bin/env python
 """Per-step kernel shares from an ncu launch list (--metrics gpu__time_duration.sum
---csv).  Only this library's kernels (namespace rails::) are counted: the bench's
+--csv).  Only this library's kernels (namespace rails::, or k_* names when ncu ran
+with a -k filter) are counted: the bench's
 step consists of them alone (input generation and torch setup kernels in the same
 process run outside the timed region).  ncu times are cold-cache and serialised,
 so the SHARE of each kernel is what compares with bench.py's live measurement."""
@@ -17,9 +18,11 @@ def main(path, steps=None):
              "second": 1e6, "s": 1e6}
     agg = collections.defaultdict(list)
     for r in rows[1:]:
-        if "rails::" not in r[kn]:
-            continue
         name = r[kn].split("(")[0].replace("void ", "")
+        # with an ncu -k filter the names come without the rails:: namespace
+        if "rails::" not in name and not name.startswith("k_"):
+            continue
+        name = name if name.startswith("rails::") else "rails::" + name
         agg[name].append(float(r[mv].replace(",", "")) * scale.get(r[un], 1.0))
     tot = sum(sum(v) for v in agg.values())
     n = steps or max(len(v) for v in agg.values())
