@@ -93,6 +93,8 @@ def test_histogram_range_error_flagged():
     (6, 8, 1 << 24, 1, 0, 6, 0.8, 1 << 26, 1),       # 2^23 <= C < 2^26: warp relative-key chain
     (5, 16, 65536, 2, 0, 5, 0.6, 400000, 1),         # N = 16 register-network chain
     (40, 2, 8192, 30, 0, 40, 0.7, 100000, 1),        # N = 2, 1200 chains (thread chains)
+    (3, 32, 65536, 2, 0, 3, 0.7, 400000, 1),         # N = 32: the maximum (one rail per lane)
+    (4, 32, 4096, 1, 0, 4, 0.9, 40, 4096),           # N = 32, equal sizes (runs, ties)
 ])
 def test_schedule_parity(M, N, C, U, d0, nd, p, hi, mult):
     rng = np.random.default_rng(M * 1000 + N * 10 + U)
@@ -115,6 +117,7 @@ def test_schedule_parity(M, N, C, U, d0, nd, p, hi, mult):
     (64, 8, 1, 0, 4096, 0),          # RB = 0: size depends on the destination only,
     (64, 4, 1, 0, 65536, 3),         # so aligned groups of N equal sizes (C5-like)
     (64, 2, 1, 0, 1 << 20, 0),       # -> the warp-scan window path
+    (6, 32, 1, 8192, 32768, 2),      # N = 32 (the generic warp chain)
 ])
 def test_schedule_parity_equal_runs(M, N, U, RB, C, outliers):
     # routing-like traffic (row multiples) makes long runs of equal remainder sizes:
@@ -225,7 +228,7 @@ def _compare_eval(pipe, u, d0, nd, M, N, ev):
 
 
 @pytest.mark.parametrize("M,N,C,U", [(4, 4, 65536, 2), (7, 3, 1000, 1), (5, 8, 4096, 2),
-                                     (2, 1, 64, 1), (33, 8, 32768, 1)])
+                                     (2, 1, 64, 1), (33, 8, 32768, 1), (3, 32, 4096, 2)])
 def test_eval_parity(M, N, C, U):
     rng = np.random.default_rng(M + N + C)
     msg = random_msg(rng, U, M, N, p=0.5, hi=300000)
@@ -295,6 +298,7 @@ def _oracle_pack_check(pipe, topk, lut, x, u, dl, scheds_oracle=None):
     (2, 1, 100, 1, 3, 16, 16, 1, 0, 2),         # N = 1, smallest rows/chunks
     (5, 8, 128, 2, 8, 12288, 32768, 1, 0, 5),   # C4 row size (12 KiB) straddling 32 KiB
     (3, 2, 40, 2, 4, 20480, 8192, 1, 0, 3),     # rows > 16 KiB window, multi-piece
+    (2, 32, 64, 4, 32, 256, 1024, 1, 0, 2),     # N = 32 rails (maximum), G = 64
 ])
 def test_pack_parity(M, N, T, k, E, RB, C, U, d0, nd):
     topk_all, lut = routing_inputs(M, N, T, k, E, 7, 0, U)
