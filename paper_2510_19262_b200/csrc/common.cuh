@@ -1,6 +1,7 @@
 // common.cuh -- internal helpers of the B200 RailS kernels (sm_100a only).
 // Not part of the ABI; see include/rails.h.  No code here is shared with oracle/.
 #pragma once
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -239,4 +240,22 @@ cudaError_t launch_flowsim(const LaunchCtx&, const rails_topo_t& tp, const rails
                            double* stats);
 
 void count_launch(int n);
+
+// Grid of a row-streaming kernel (one warp per row inside a grid-stride loop):
+// about `rpw` rows per warp, the CTAs running in waves, instead of one persistent
+// wave of resident CTAs striding over every row.  On B200 the persistent grid held
+// the C3 pack at 90% of the copy peak, 8 rows per warp reach 99-100% (DESIGN.md
+// section 12); one row per warp pays a CTA launch per row.  `env` (e.g.
+// "RAILS_PACK_RPW") overrides rpw; 0 restores the persistent grid.
+inline long long wave_grid(int num_sms, int per_sm, long long need_ctas, const char* env,
+                           long long rpw = 8) {
+  if (const char* v = getenv(env)) rpw = atoll(v);
+  const long long resident = (long long)num_sms * (per_sm < 1 ? 1 : per_sm);
+  long long grid = rpw >= 1 ? (need_ctas + rpw - 1) / rpw : resident;
+  if (grid < resident) grid = resident;
+  if (grid > need_ctas) grid = need_ctas;
+  if (grid > 0x7fffffffLL) grid = 0x7fffffffLL;
+  return grid < 1 ? 1 : grid;
+}
+
 }  // namespace rails

@@ -211,10 +211,8 @@ static cudaError_t launch_ov(const LaunchCtx& c, int U, int nd, int d0, int M, i
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   const long long rows = (long long)U * nd * ng * T;
-  long long grid = (long long)c.num_sms * per_sm;
   const long long need = (rows + OWN_THREADS / 32 - 1) / (OWN_THREADS / 32);
-  if (grid > need) grid = need;
-  if (grid < 1) grid = 1;
+  const long long grid = wave_grid(c.num_sms, per_sm, need, "RAILS_OWNER_RPW");
   kern<<<(unsigned)grid, OWN_THREADS, 0, c.stream>>>(
       U, nd, d0, M, N, g0, ng, T, k, C, cshift, (const uint4*)x, topk, lut, n_inst, rank, msg,
       RB, s.full_base, s.rem_rail, s.rem_off, rail_base, rp, c.err);

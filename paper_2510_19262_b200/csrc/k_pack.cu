@@ -48,7 +48,7 @@ __device__ __forceinline__ long long chunk_addr(long long c, long long fb, long 
   return rr >= 0 ? rbase[rr] + ro : -(1LL << 62);
 }
 
-template <int VPL, bool MULTI, bool CS = false>
+template <int VPL, bool MULTI, int CS = 0>
 __global__ void __launch_bounds__(PACK_THREADS)
     k_pack(int U, int nd, int d0, int M, int N, int T, int k, long long C, int cshift,
            const uint4* __restrict__ x, const int32_t* __restrict__ topk,
@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(PACK_THREADS)
 #pragma unroll
     for (int i = 0; i < VPL; ++i) {
       const int vi = i * 32 + lane;
-      if (vi < nvec) v[i] = ld_stream(src + vi);
+      if (vi < nvec) v[i] = (CS & 2) ? __ldcs(src + vi) : ld_stream(src + vi);
     }
 
     // 2. slot metadata on lanes 0..k-1
@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(PACK_THREADS)
 #pragma unroll
         for (int i = 0; i < VPL; ++i) {
           const int vi = w0 + i * 32 + lane;
-          if (vi < nvec) v[i] = ld_stream(src + vi);
+          if (vi < nvec) v[i] = (CS & 2) ? __ldcs(src + vi) : ld_stream(src + vi);
         }
       }
       for (int s = 0; s < k; ++s) {
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(PACK_THREADS)
               const long long o = (long long)vi << 4;
               const long long a = (o < B0) ? D0 + o : D1 + (o - B0);
               if (a >= 0 && a + 16 <= out_cap) {
-                if (CS)
+                if (CS & 1)
                   st_cs((uint4*)(out + a), v[i]);
                 else
                   st_stream((uint4*)(out + a), v[i]);
@@ -181,16 +181,26 @@ static cudaError_t launch_v(const LaunchCtx& c, int U, int nd, int d0, int M, in
                             const int32_t* lut, int n_inst, const int32_t* rank,
                             const int64_t* msg, long long RB, const rails_sched_t& s,
                             const int64_t* rail_base, void* out, long long out_cap) {
+  // RAILS_PACK_ST: bit 0 = .cs (evict-first) stores, bit 1 = .cs payload loads
   const char* st = getenv("RAILS_PACK_ST");
-  auto kern = (st && st[0] == '1') ? k_pack<VPL, MULTI, true> : k_pack<VPL, MULTI, false>;
+  const int cs = st ? atoi(st) : 0;
+  auto kern = cs == 1 ? k_pack<VPL, MULTI, 1> : cs == 2 ? k_pack<VPL, MULTI, 2>
+            : cs == 3 ? k_pack<VPL, MULTI, 3> : k_pack<VPL, MULTI, 0>;
   int per_sm = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PACK_THREADS, 0);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   const long long rows = (long long)U * nd * N * T;
-  long long grid = (long long)c.num_sms * per_sm;
   const long long need = (rows + PACK_THREADS / 32 - 1) / (PACK_THREADS / 32);
-  if (grid > need) grid = need;
+  // waves of CTAs, ~8 rows per warp (wave_grid); RAILS_PACK_CTAS sets CTAs per SM
+  long long grid;
+  const char* pv = getenv("RAILS_PACK_CTAS");
+  if (pv && atoi(pv) >= 1) {
+    grid = (long long)c.num_sms * atoi(pv);
+    if (grid > need) grid = need;
+  } else {
+    grid = wave_grid(c.num_sms, per_sm, need, "RAILS_PACK_RPW");
+  }
   if (grid < 1) grid = 1;
   kern<<<(unsigned)grid, PACK_THREADS, 0, c.stream>>>(
       U, nd, d0, M, N, T, k, C, cshift, (const uint4*)x, topk, lut, n_inst, rank, msg, RB,
@@ -561,6 +571,10 @@ static cudaError_t launch_tma2(const LaunchCtx& c, int U, int nd, int d0, int M,
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
+  if (const char* pv = getenv("RAILS_PACK_CTAS")) {  // CTAs per SM (more than resident: waves)
+    const int v = atoi(pv);
+    if (v >= 1) per_sm = v;
+  }
   const long long rows = (long long)U * nd * N * T;
   long long grid = (long long)c.num_sms * per_sm;
   const long long need = (rows + W - 1) / W;
@@ -588,6 +602,10 @@ static cudaError_t launch_tma_sd(const LaunchCtx& c, int U, int nd, int d0, int 
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TMA_WARPS * 32, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
+  if (const char* pv = getenv("RAILS_PACK_CTAS")) {  // CTAs per SM (more than resident: waves)
+    const int v = atoi(pv);
+    if (v >= 1) per_sm = v;
+  }
   const long long rows = (long long)U * nd * N * T;
   long long grid = (long long)c.num_sms * per_sm;
   const long long need = (rows + TMA_WARPS - 1) / TMA_WARPS;

@@ -76,8 +76,14 @@ def bench_pack(res):
         os.environ.pop("RAILS_PACK_ST", None)
         os.environ.pop("RAILS_PACK_VPL", None)
         os.environ.pop("RAILS_PACK_TMA", None)
-        if impl == "1cs":
-            os.environ["RAILS_PACK_ST"] = "1"
+        os.environ.pop("RAILS_PACK_CTAS", None)
+        os.environ.pop("RAILS_PACK_RPW", None)
+        if impl.startswith("1r"):  # 1rN: N rows per warp
+            os.environ["RAILS_PACK_RPW"] = impl[2:]
+        if impl.startswith("1g"):  # 1gN: N CTAs per SM
+            os.environ["RAILS_PACK_CTAS"] = impl[2:]
+        if impl.startswith("1cs"):  # 1cs: .cs stores; 1cs2: .cs loads; 1cs3: both
+            os.environ["RAILS_PACK_ST"] = impl[3:] or "1"
         if impl.startswith("1v"):
             os.environ["RAILS_PACK_VPL"] = impl[2:]
         if impl.startswith("3s"):
