@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(W * 32)
       run += c;
     }
     counts[cta * G + h] = run;
-    msg[cta * G + h] = (h / N == d) ? 0LL : (long long)run * RB;
+    msg[cta * G + h] = ((unsigned)(h - d * N) < (unsigned)N) ? 0LL : (long long)run * RB;
   }
   if (rank == nullptr) return;
   __syncthreads();
@@ -262,6 +262,7 @@ __global__ void __launch_bounds__(HW_WARPS * 32)
       const int c = (int)(word & 0xffffffu);
       const bool loser = t != lane;
       // 3. peers: a loser knows the winner (its tag); every lane scans the losers
+      // (a 5-bit ballot match on the surviving tag instead measured slower)
       unsigned peers = (1u << lane) | (loser ? (1u << t) : 0u);
       unsigned lm = __ballot_sync(FULL, loser);
       while (lm) {
@@ -279,7 +280,7 @@ __global__ void __launch_bounds__(HW_WARPS * 32)
   for (int h = lane; h < G; h += 32) {
     const int c = (int)(bin[h] & 0xffffffu);
     counts[sg * G + h] = c;
-    msg[sg * G + h] = (h / N == d) ? 0LL : (long long)c * RB;
+    msg[sg * G + h] = ((unsigned)(h - d * N) < (unsigned)N) ? 0LL : (long long)c * RB;  // h / N == d
   }
 }
 
