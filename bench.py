@@ -399,6 +399,9 @@ def main():
         out["roofline"] = {"kernel": "k_pack", "bound": "hbm", "achieved": per_gpu_pack,
                            "peak": peak, "unit": "GB/s", "frac": per_gpu_pack / peak,
                            "peak_kind": peak_kind, "traffic": traffic,
+                           "peak_note": "peak = a 1:1 HBM copy; the pack moves 1 read : 2 "
+                                        "writes (writes stream faster), so frac can pass 1.0; "
+                                        "plain-kernel ceiling of this mix: tools/bw_mix.py",
                            "algorithmic_bytes_per_launch": pack_bytes,
                            "avg_launch_ms": pack_avg_ms,
                            "share_of_step": pack_avg_ms / (total_ms / args.steps)}
