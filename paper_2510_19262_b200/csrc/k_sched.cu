@@ -643,6 +643,54 @@ __global__ void __launch_bounds__(256)
   if (rem_qp) rem_qp[seg * NG + m] = q;
 }
 
+// k_expand_rem with 4 consecutive messages per thread (NG % 4 == 0, aligned
+// outputs): one 16-byte load of the inverse permutation, four gathers in flight,
+// 4-byte rail / 16-byte offset stores.  The one-per-thread kernel is latency-bound
+// (two dependent loads per thread: ncu long-scoreboard stalls); this keeps 4x the
+// loads in flight per warp.  Segments beyond gridDim.y are looped.
+__global__ void __launch_bounds__(256)
+    k_expand_rem4(long long NG, long long nseg, const int32_t* __restrict__ ws_inv,
+                  const uint64_t* __restrict__ ws_res, int8_t* __restrict__ rem_rail,
+                  int64_t* __restrict__ rem_off, const uint32_t* __restrict__ ws_qp,
+                  int32_t* __restrict__ rem_qp) {
+  const long long m = ((long long)blockIdx.x * 256 + threadIdx.x) * 4;
+  if (m >= NG) return;
+  for (long long seg = blockIdx.y; seg < nseg; seg += gridDim.y) {
+    const long long b = seg * NG;
+    const int4 pos = *(const int4*)(ws_inv + b + m);
+    const int p[4] = {pos.x, pos.y, pos.z, pos.w};
+    uint64_t v[4];
+    uint32_t qv[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = p[i] >= 0 ? ws_res[b + p[i]] : 0ull;
+    if (rem_qp) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) qv[i] = p[i] >= 0 ? ws_qp[b + p[i]] : 0u;
+    }
+    char4 r;
+    r.x = p[0] >= 0 ? (signed char)(v[0] >> 56) : (signed char)-1;
+    r.y = p[1] >= 0 ? (signed char)(v[1] >> 56) : (signed char)-1;
+    r.z = p[2] >= 0 ? (signed char)(v[2] >> 56) : (signed char)-1;
+    r.w = p[3] >= 0 ? (signed char)(v[3] >> 56) : (signed char)-1;
+    *(char4*)(rem_rail + b + m) = r;
+    longlong2 o0, o1;
+    o0.x = p[0] >= 0 ? (long long)(v[0] & (uint64_t)OFF_MASK) : 0;
+    o0.y = p[1] >= 0 ? (long long)(v[1] & (uint64_t)OFF_MASK) : 0;
+    o1.x = p[2] >= 0 ? (long long)(v[2] & (uint64_t)OFF_MASK) : 0;
+    o1.y = p[3] >= 0 ? (long long)(v[3] & (uint64_t)OFF_MASK) : 0;
+    *(longlong2*)(rem_off + b + m) = o0;
+    *(longlong2*)(rem_off + b + m + 2) = o1;
+    if (rem_qp) {
+      int4 q;
+      q.x = p[0] >= 0 ? (int32_t)qv[0] : -1;
+      q.y = p[1] >= 0 ? (int32_t)qv[1] : -1;
+      q.z = p[2] >= 0 ? (int32_t)qv[2] : -1;
+      q.w = p[3] >= 0 ? (int32_t)qv[3] : -1;
+      *(int4*)(rem_qp + b + m) = q;
+    }
+  }
+}
+
 // Same as k_expand_rem with one CTA per (unit, node): the segment's n_rem chain
 // results are first copied into shared memory (coalesced), so the per-message
 // gather through the inverse permutation hits shared memory instead of 32-byte
@@ -833,9 +881,20 @@ cudaError_t launch_schedule(const LaunchCtx& c, int U, int nd, int d0, int M, in
   }
   const size_t esm = (size_t)NG * 8;
   const char* xv = getenv("RAILS_EXPAND_IMPL");
-  // segment-staged gather for long segments (C4: 183 -> ~110 us); short ones keep
-  // the grid-wide kernel (more CTAs, nothing to stage)
-  if (NG >= 8192 && esm <= 160 * 1024 && !(xv && xv[0] == '1')) {
+  // Expand kernel: 4 messages per thread when the outputs are aligned (C2 chunk ->
+  // expand 94 -> ~60 us, C4 schedule 0.620 -> 0.605 ms against the staged kernel);
+  // else the segment-staged gather for long segments (C4: 183 -> ~110 us against
+  // one message per thread), else one message per thread.  RAILS_EXPAND_IMPL=1|2
+  // forces one per thread, 3 the staged kernel (where it fits).
+  const bool x1 = xv && (xv[0] == '1' || xv[0] == '2'), x3 = xv && xv[0] == '3';
+  const bool al4 = NG % 4 == 0 && ((uintptr_t)ws_inv & 15) == 0 &&
+                   ((uintptr_t)s.rem_rail & 3) == 0 && ((uintptr_t)s.rem_off & 15) == 0 &&
+                   ((uintptr_t)rem_qp & 15) == 0;
+  if (al4 && !x1 && !x3) {
+    const long long gy = nseg < 65535 ? nseg : 65535;
+    k_expand_rem4<<<dim3((unsigned)((NG / 4 + 255) / 256), (unsigned)gy), 256, 0, c.stream>>>(
+        NG, nseg, ws_inv, ws_res, s.rem_rail, s.rem_off, rem_qp ? ws_qp : nullptr, rem_qp);
+  } else if (esm <= 160 * 1024 && !x1 && (x3 || NG >= 8192)) {
     if (esm > 48 * 1024 &&
         (e = cudaFuncSetAttribute(k_expand_seg, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)esm)) != cudaSuccess)
@@ -843,6 +902,7 @@ cudaError_t launch_schedule(const LaunchCtx& c, int U, int nd, int d0, int M, in
     k_expand_seg<<<(unsigned)nseg, EXP_THREADS, esm, c.stream>>>(
         NG, s.n_rem, ws_inv, ws_res, s.rem_rail, s.rem_off, rem_qp ? ws_qp : nullptr, rem_qp);
   } else {
+    if (nseg > 65535) return cudaErrorInvalidConfiguration;
     k_expand_rem<<<dim3((unsigned)((NG + 255) / 256), (unsigned)nseg), 256, 0, c.stream>>>(
         NG, ws_inv, ws_res, s.rem_rail, s.rem_off, rem_qp ? ws_qp : nullptr, rem_qp);
   }

@@ -461,6 +461,22 @@ def test_schedule_parity_alternate_chain_kernels(impl, monkeypatch):
                 compare_schedule(s, u, d, oracle.schedule_node(msg[u, d], C), f"impl{impl} u{u} d{d}")
 
 
+@pytest.mark.parametrize("impl", ["1", "3"])
+def test_schedule_parity_alternate_expand(impl, monkeypatch):
+    # the expand of the chain results into rem_rail / rem_off (/ rem_qp): one
+    # message per thread (1) and the segment-staged gather (3) stay exact next to
+    # the default 4-messages-per-thread kernel
+    monkeypatch.setenv("RAILS_EXPAND_IMPL", impl)
+    rng = np.random.default_rng(78)
+    for (M, N, C, U) in [(16, 8, 1 << 20, 3), (5, 3, 1000, 2), (70, 8, 32768, 1)]:
+        msg = random_msg(rng, U, M, N, p=0.8, hi=3_000_000)
+        tp, sh = rails.topo(M, N, C), rails.shard(U, 0, M)
+        s = rails.lpt_schedule(tp, sh, torch.from_numpy(msg).to(DEV))
+        for u in range(U):
+            for d in range(M):
+                compare_schedule(s, u, d, oracle.schedule_node(msg[u, d], C), f"x{impl} u{u} d{d}")
+
+
 @pytest.mark.parametrize("impl", ["2", "3"])
 def test_pack_parity_alternate_impls(impl, monkeypatch):
     # the TMA bulk-copy packs (RAILS_PACK_IMPL=2: per-row metadata; 3: metadata
