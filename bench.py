@@ -127,48 +127,125 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- oracle (CPU) arm
-def oracle_sample(cfg_name: str, budget_s: float = 12.0, max_nodes: int = 16):
-    """Time the CPU oracle, as it stands, on a bounded sample of the same workload:
-    the full path (histogram, chunk, sort, LPT, eval, pack) for sampled nodes of unit 0."""
+def _oracle_inputs(cfg_name: str, i: int):
+    """Inputs of the i-th sampled node of unit 0 (generation is not timed)."""
+    cfg = gen.CONFIGS[cfg_name]
+    M, N = cfg["M"], cfg["N"]
+    seed = gen.config_seed(int(cfg_name[1]))
+    if cfg["kind"] == "routing":
+        T, k, E, RB = cfg["T"], cfg["k"], cfg["E"], cfg["H"] * 2
+        d = (i * 37) % M
+        return {"d": d, "lut": gen.inst_lut(M, N, E).numpy(),
+                "topk": gen.routing(M, N, T, k, E, seed, 0, d, 1)[0].numpy(),
+                "x": gen.payload(M, N, T, RB, seed, 0, d, 1)[0].numpy().view(np.uint8)}
+    return {"d": i % M, "msg": _d1_unit0(cfg_name)}
+
+
+_D1_CACHE = {}
+
+
+def _d1_unit0(cfg_name: str):
+    if cfg_name not in _D1_CACHE:
+        cfg = gen.CONFIGS[cfg_name]
+        _D1_CACHE[cfg_name] = gen.d1_units(cfg, gen.config_seed(int(cfg_name[1])), 0, 1)[0]
+    return _D1_CACHE[cfg_name]
+
+
+def _oracle_node(cfg_name: str, inp) -> None:
+    """One (unit, node) through the CPU oracle as it stands: routing configs run the
+    full path (histogram, chunk, sort, LPT, eval, pack), matrix configs schedule + eval."""
     import oracle
 
     cfg = gen.CONFIGS[cfg_name]
     M, N, C = cfg["M"], cfg["N"], cfg["C"]
-    seed = gen.config_seed(int(cfg_name[1]))
-    done, t_used = 0, 0.0
+    d = inp["d"]
     if cfg["kind"] == "routing":
-        T, k, E, RB = cfg["T"], cfg["k"], cfg["E"], cfg["H"] * 2
-        lut = gen.inst_lut(M, N, E).numpy()
-        while done < max_nodes and t_used < budget_s:
-            d = (done * 37) % M
-            topk = gen.routing(M, N, T, k, E, seed, 0, d, 1)[0].numpy()
-            x = gen.payload(M, N, T, RB, seed, 0, d, 1)[0].numpy().view(np.uint8)
-            t0 = time.perf_counter()
-            c, m, r = oracle.histogram_node(M, N, d, T, k, topk, lut, RB)
-            s = oracle.schedule_node(m, C)
-            ch = s["chunks"]
-            oracle.eval_unit(M, N, 5.0e10, gen.ECMP_SEED, np.pad(m[None], ((d, M - d - 1), (0, 0), (0, 0))),
-                             np.full(len(ch["size"]), d, np.int32), ch["h"], ch["size"], s["rail"])
-            L = s["send_load"]
-            base = np.concatenate([[0], np.cumsum(L)[:-1]]).astype(np.int64)
-            oracle.pack_node(M, N, d, T, k, RB, C, x, topk, lut, m, s, base, int(L.sum()))
-            t_used += time.perf_counter() - t0
-            done += 1
-        sample = f"{done} sampled nodes of unit 0 (full path incl. pack), single-threaded C oracle"
+        T, k, RB = cfg["T"], cfg["k"], cfg["H"] * 2
+        topk, lut = inp["topk"], inp["lut"]
+        c, m, r = oracle.histogram_node(M, N, d, T, k, topk, lut, RB)
+        s = oracle.schedule_node(m, C)
+        ch = s["chunks"]
+        oracle.eval_unit(M, N, 5.0e10, gen.ECMP_SEED, np.pad(m[None], ((d, M - d - 1), (0, 0), (0, 0))),
+                         np.full(len(ch["size"]), d, np.int32), ch["h"], ch["size"], s["rail"])
+        L = s["send_load"]
+        base = np.concatenate([[0], np.cumsum(L)[:-1]]).astype(np.int64)
+        oracle.pack_node(M, N, d, T, k, RB, C, inp["x"], topk, lut, m, s, base, int(L.sum()))
     else:
-        msg = gen.d1_units(cfg, seed, 0, 1)[0]
-        while done < max_nodes * 4 and t_used < budget_s:
-            d = done % M
-            t0 = time.perf_counter()
-            s = oracle.schedule_node(msg[d], C)
-            ch = s["chunks"]
-            oracle.eval_unit(M, N, 5.0e10, gen.ECMP_SEED, msg,
-                             np.full(len(ch["size"]), d, np.int32), ch["h"], ch["size"], s["rail"])
-            t_used += time.perf_counter() - t0
-            done += 1
-        sample = f"{done} sampled nodes of unit 0 (schedule + eval), single-threaded C oracle"
+        msg = inp["msg"]
+        s = oracle.schedule_node(msg[d], C)
+        ch = s["chunks"]
+        oracle.eval_unit(M, N, 5.0e10, gen.ECMP_SEED, msg,
+                         np.full(len(ch["size"]), d, np.int32), ch["h"], ch["size"], s["rail"])
+
+
+def oracle_sample(cfg_name: str, budget_s: float = 12.0, max_nodes: int = 40):
+    """Time the CPU oracle, as it stands, on a bounded sample of the same workload
+    (sampled nodes of unit 0), single-threaded: SURVEY 8(d) d.5 (i)."""
+    cfg = gen.CONFIGS[cfg_name]
+    routing = cfg["kind"] == "routing"
+    cap = max_nodes if routing else max_nodes * 1000
+    done, t_used = 0, 0.0
+    while done < cap and t_used < budget_s:
+        inp = _oracle_inputs(cfg_name, done)
+        t0 = time.perf_counter()
+        _oracle_node(cfg_name, inp)
+        t_used += time.perf_counter() - t0
+        done += 1
+    what = "full path incl. pack" if routing else "schedule + eval"
+    sample = f"{done} sampled nodes of unit 0 ({what}), single-threaded C oracle"
     return {"value": done / t_used, "unit": "nodes/s", "cores": 1, "kind": "oracle",
             "sample": sample, "seconds": round(t_used, 3)}
+
+
+def _oracle_worker(cfg_name, i, per, barrier, q):
+    try:
+        inps = [_oracle_inputs(cfg_name, i * per + j) for j in range(per)]
+        barrier.wait()
+        t0 = time.perf_counter()  # CLOCK_MONOTONIC: comparable across processes
+        for inp in inps:
+            _oracle_node(cfg_name, inp)
+        q.put((t0, time.perf_counter()))
+    except BaseException as e:  # noqa: BLE001 -- reported by the parent
+        try:
+            barrier.abort()
+        except Exception:
+            pass
+        q.put(repr(e))
+
+
+def oracle_sample_all_cores(cfg_name: str, max_procs: int = 16):
+    """the same single-threaded oracle on every host core at once
+    (one process per core, up to max_procs, each owning its own sampled nodes; the
+    oracle's comparator context is process-global, so processes, not threads).  Wall
+    time = first start to last end after a common barrier; input generation excluded."""
+    import multiprocessing as mp
+
+    cfg = gen.CONFIGS[cfg_name]
+    import psutil
+
+    routing = cfg["kind"] == "routing"
+    # a routing node holds ~0.8 GiB (payload + packed rail buffers) while it runs
+    fit = int(psutil.virtual_memory().available // (3 << 29)) if routing else max_procs
+    P = max(1, min(os.cpu_count() or 1, max_procs, fit))
+    per = 2 if routing else 2000
+    ctx = mp.get_context("fork")  # children run numpy + the C oracle only, never CUDA
+    barrier, q = ctx.Barrier(P), ctx.Queue()
+    ps = [ctx.Process(target=_oracle_worker, args=(cfg_name, i, per, barrier, q))
+          for i in range(P)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=600) for _ in ps]
+    for p in ps:
+        p.join()
+    bad = [r for r in res if not isinstance(r, tuple)]
+    if bad:
+        return {"error": bad[0]}
+    wall = max(r[1] for r in res) - min(r[0] for r in res)
+    what = "full path incl. pack" if cfg["kind"] == "routing" else "schedule + eval"
+    return {"value": P * per / wall, "unit": "nodes/s", "cores": P, "kind": "oracle",
+            "host_cpus": os.cpu_count(),
+            "sample": f"{P * per} sampled nodes of unit 0 ({what}), {per} per process, "
+                      f"{P} oracle processes in parallel", "seconds": round(wall, 3)}
 
 
 def arm_config(args, P, nd=None):
@@ -454,6 +531,7 @@ def main():
     # ---- cpu baseline (rank 0, N = 1 only)
     if world == 1 and not args.no_cpu:
         out["cpu_baseline"] = oracle_sample(args.workload)
+        out["cpu_baseline"]["all_cores"] = oracle_sample_all_cores(args.workload)
     if rank == 0:
         emit(out)
     if peer is not None:
