@@ -127,18 +127,29 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- oracle (CPU) arm
+_INPUT_CACHE = {}
+
+
 def _oracle_inputs(cfg_name: str, i: int):
-    """Inputs of the i-th sampled node of unit 0 (generation is not timed)."""
+    """Inputs of the i-th sampled node of unit 0 (generation is not timed; the first
+    16 are kept for the all-cores run, which must not generate after fork)."""
+    key = (cfg_name, i)
+    if key in _INPUT_CACHE:
+        return _INPUT_CACHE[key]
     cfg = gen.CONFIGS[cfg_name]
     M, N = cfg["M"], cfg["N"]
     seed = gen.config_seed(int(cfg_name[1]))
     if cfg["kind"] == "routing":
         T, k, E, RB = cfg["T"], cfg["k"], cfg["E"], cfg["H"] * 2
         d = (i * 37) % M
-        return {"d": d, "lut": gen.inst_lut(M, N, E).numpy(),
-                "topk": gen.routing(M, N, T, k, E, seed, 0, d, 1)[0].numpy(),
-                "x": gen.payload(M, N, T, RB, seed, 0, d, 1)[0].numpy().view(np.uint8)}
-    return {"d": i % M, "msg": _d1_unit0(cfg_name)}
+        inp = {"d": d, "lut": gen.inst_lut(M, N, E).numpy(),
+               "topk": gen.routing(M, N, T, k, E, seed, 0, d, 1)[0].numpy(),
+               "x": gen.payload(M, N, T, RB, seed, 0, d, 1)[0].numpy().view(np.uint8)}
+    else:
+        inp = {"d": i % M, "msg": _d1_unit0(cfg_name)}
+    if i < 16:
+        _INPUT_CACHE[key] = inp
+    return inp
 
 
 _D1_CACHE = {}
@@ -178,7 +189,7 @@ def _oracle_node(cfg_name: str, inp) -> None:
                          np.full(len(ch["size"]), d, np.int32), ch["h"], ch["size"], s["rail"])
 
 
-def oracle_sample(cfg_name: str, budget_s: float = 12.0, max_nodes: int = 40):
+def oracle_sample(cfg_name: str, budget_s: float = 12.0, max_nodes: int = 24):
     """Time the CPU oracle, as it stands, on a bounded sample of the same workload
     (sampled nodes of unit 0), single-threaded: SURVEY 8(d) d.5 (i)."""
     cfg = gen.CONFIGS[cfg_name]
@@ -197,10 +208,9 @@ def oracle_sample(cfg_name: str, budget_s: float = 12.0, max_nodes: int = 40):
             "sample": sample, "seconds": round(t_used, 3)}
 
 
-def _oracle_worker(cfg_name, i, per, barrier, q):
+def _oracle_worker(cfg_name, inps, barrier, q):
     try:
-        inps = [_oracle_inputs(cfg_name, i * per + j) for j in range(per)]
-        barrier.wait()
+        barrier.wait(timeout=300)
         t0 = time.perf_counter()  # CLOCK_MONOTONIC: comparable across processes
         for inp in inps:
             _oracle_node(cfg_name, inp)
@@ -227,16 +237,28 @@ def oracle_sample_all_cores(cfg_name: str, max_procs: int = 16):
     # a routing node holds ~0.8 GiB (payload + packed rail buffers) while it runs
     fit = int(psutil.virtual_memory().available // (3 << 29)) if routing else max_procs
     P = max(1, min(os.cpu_count() or 1, max_procs, fit))
-    per = 2 if routing else 2000
-    ctx = mp.get_context("fork")  # children run numpy + the C oracle only, never CUDA
+    per = 3 if routing else 2000
+    # every input is generated here, before the fork: the generator uses torch CPU ops,
+    # which deadlock in a forked child; the children run numpy + the C oracle only
+    inps = [[_oracle_inputs(cfg_name, (i * per + j) % 16) for j in range(per)] for i in range(P)]
+    ctx = mp.get_context("fork")
     barrier, q = ctx.Barrier(P), ctx.Queue()
-    ps = [ctx.Process(target=_oracle_worker, args=(cfg_name, i, per, barrier, q))
+    ps = [ctx.Process(target=_oracle_worker, args=(cfg_name, inps[i], barrier, q))
           for i in range(P)]
     for p in ps:
         p.start()
-    res = [q.get(timeout=600) for _ in ps]
+    import queue
+
+    res = []
+    try:
+        for _ in ps:
+            res.append(q.get(timeout=300))
+    except queue.Empty:
+        res.append("timeout: an oracle process did not report within 300 s")
     for p in ps:
-        p.join()
+        p.join(timeout=5)
+        if p.is_alive():
+            p.kill()
     bad = [r for r in res if not isinstance(r, tuple)]
     if bad:
         return {"error": bad[0]}
