@@ -175,8 +175,8 @@ __device__ __forceinline__ void cp_async_wait() {
 // ASYNC: the routing ids stream through a per-warp double buffer in shared memory
 // filled by cp.async two batches ahead (no registers held for the prefetch, more
 // bytes in flight per SM); needs T*k % 4 == 0 for 16-byte copies.
-template <int UNR, bool RANK, bool ASYNC = false, int MINB = 1>
-__global__ void __launch_bounds__(HW_WARPS * 32, MINB)
+template <int UNR, bool RANK, bool ASYNC = false>
+__global__ void __launch_bounds__(HW_WARPS * 32)
     k_hist_w1(const int32_t* __restrict__ topk, const int32_t* __restrict__ lut, int n_inst,
               int M, int N, int ngs, int d0, int nd, int T, int k, long long RB,
               long long nsegs, int32_t* __restrict__ counts, int64_t* __restrict__ msg,
@@ -354,13 +354,8 @@ cudaError_t launch_histogram(const LaunchCtx& c, int U, int nd, int d0, int M, i
     const int unr = uv ? atoi(uv) : 16;
     const char* av = getenv("RAILS_HIST_ASYNC");
     const bool async_ok = ne % 4 == 0 && av && av[0] == '1';
-    // RAILS_HIST_MINB=10: UNR 16 capped at 48 registers (40 warps per SM instead of 32)
-    const char* mbv = getenv("RAILS_HIST_MINB");
-    const bool capped = mbv && atoi(mbv) == 10;
     auto kern = unr == 32 ? (rank ? k_hist_w1<32, true> : k_hist_w1<32, false>)
               : unr == 8  ? (rank ? k_hist_w1<8, true> : k_hist_w1<8, false>)
-              : unr == 12 ? (rank ? k_hist_w1<12, true> : k_hist_w1<12, false>)
-              : capped    ? (rank ? k_hist_w1<16, true, false, 10> : k_hist_w1<16, false, false, 10>)
                           : (rank ? k_hist_w1<16, true> : k_hist_w1<16, false>);
     if (async_ok) {
       kern = rank ? k_hist_w1<16, true, true> : k_hist_w1<16, false, true>;
