@@ -5,10 +5,12 @@
 // GPU h; msg_bytes = counts * RB for remote h (R#2); row_rank = position of (t,s)
 // among the earlier slots of GPU g with the same h (R#18), which the pack needs.
 //
-// Batched default (>= 16 segments per SM): k_hist_w1, one warp per (unit, node,
-// source GPU) with one packed (count | tag) shared word per bin -- ties inside a
-// 32-entry group resolved by a tag write / read-back and a loser-ballot loop, 16
-// groups of ids per batch with the next batch's loads in flight.  Few segments
+// Batched default (>= 16 segments per SM): k_hist_w1a, one warp per (unit, node,
+// source GPU), one shared count per bin, atomicAdd + read-back ranking (below);
+// k_hist_w1 (RAILS_HIST_ATOM=0) packs (count | tag) per bin and resolves ties inside a
+// 32-entry group by a tag write / read-back and a loser-ballot loop.  Both: 16
+// groups of ids per batch with the next batch's loads in flight, the instance -> GPU
+// table in shared memory when it fits 16 KiB.  Few segments
 // (C3: 512): k_hist_rank below, W warps per segment.
 // k_hist_rank: one CTA per (unit, node, source GPU).  The T*k routing entries are
 // split into W contiguous warp segments.  Pass 1: each warp counts its segment
@@ -175,8 +177,11 @@ __device__ __forceinline__ void cp_async_wait() {
 // ASYNC: the routing ids stream through a per-warp double buffer in shared memory
 // filled by cp.async two batches ahead (no registers held for the prefetch, more
 // bytes in flight per SM); needs T*k % 4 == 0 for 16-byte copies.
-template <int UNR, bool RANK, bool ASYNC = false>
-__global__ void __launch_bounds__(HW_WARPS * 32)
+// SLUT: the instance -> GPU table is staged in shared memory once per CTA; its random
+// lookups then cost ~3.5 shared wavefronts per 32 ids instead of an L1 gather (ncu:
+// the L1 data pipe, shared + global wavefronts, is the kernel's saturated unit)
+template <int UNR, bool RANK, bool ASYNC = false, bool SLUT = false>
+__global__ void __launch_bounds__(HW_WARPS * 32, SLUT ? 8 : 1)
     k_hist_w1(const int32_t* __restrict__ topk, const int32_t* __restrict__ lut, int n_inst,
               int M, int N, int ngs, int d0, int nd, int T, int k, long long RB,
               long long nsegs, int32_t* __restrict__ counts, int64_t* __restrict__ msg,
@@ -187,6 +192,11 @@ __global__ void __launch_bounds__(HW_WARPS * 32)
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long sg = (long long)blockIdx.x * HW_WARPS + wid;  // ((u*nd)+dl)*ngs + gl
   uint32_t* const bin = sw1 + wid * (G + 1);  // bin G: sink for invalid ids
+  int32_t* const ls = (int32_t*)(sw1 + (size_t)HW_WARPS * (G + 1));  // SLUT only
+  if constexpr (SLUT) {
+    for (int i = threadIdx.x; i < n_inst; i += HW_WARPS * 32) ls[i] = __ldg(lut + i);
+    __syncthreads();
+  }
   if (sg >= nsegs) return;
   const long long ul = sg / ngs;
   const int d = d0 + (int)(ul % nd);
@@ -244,7 +254,8 @@ __global__ void __launch_bounds__(HW_WARPS * 32)
     }
 #pragma unroll
     for (int j = 0; j < UNR; ++j)  // all LUT lookups of the batch in flight together
-      hv[j] = ((unsigned)hv[j] < (unsigned)n_inst) ? __ldg(lut + hv[j]) : -1;
+      hv[j] = ((unsigned)hv[j] < (unsigned)n_inst) ? (SLUT ? ls[hv[j]] : __ldg(lut + hv[j]))
+                                                    : -1;
 #pragma unroll
     for (int j = 0; j < UNR; ++j) {
       const bool in = base + j * 32 + lane < ne;
@@ -281,6 +292,95 @@ __global__ void __launch_bounds__(HW_WARPS * 32)
     const int c = (int)(bin[h] & 0xffffffu);
     counts[sg * G + h] = c;
     msg[sg * G + h] = ((unsigned)(h - d * N) < (unsigned)N) ? 0LL : (long long)c * RB;  // h / N == d
+  }
+}
+
+// Atomic ranking (default; RAILS_HIST_ATOM=0 selects k_hist_w1 above): two shared
+// accesses per 32 ids instead of three -- ncu shows the L1 data pipe (shared + global
+// wavefronts) as the saturated unit of k_hist_w1 (93.6%).
+// Every lane does old = atomicAdd(&bin[h], 1) and then reads now = bin[h]; d = now - old
+// is 1 for a lane with no equal key in the group, and among p lanes with the same key
+// (hardware order) the d values are 1..p, so exactly one has d = 1.  Lanes with no
+// collision take rank = old.  Otherwise: loop over the d >= 2 lanes (shfl of their keys)
+// gives each member its d >= 2 peers (p - 1 of them), a second loop over the colliding
+// d = 1 lanes adds the last one; c = now - p and the stable rank is c + #peers below.
+// The count in shared memory is already c + p: no count store.
+template <int UNR, bool RANK, bool SLUT>
+__global__ void __launch_bounds__(HW_WARPS * 32, 8)
+    k_hist_w1a(const int32_t* __restrict__ topk, const int32_t* __restrict__ lut, int n_inst,
+               int M, int N, int ngs, int d0, int nd, int T, int k, long long RB,
+               long long nsegs, int32_t* __restrict__ counts, int64_t* __restrict__ msg,
+               int32_t* __restrict__ rank, int* err) {
+  extern __shared__ __align__(16) uint32_t sw1[];
+  const int G = M * N;
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long sg = (long long)blockIdx.x * HW_WARPS + wid;
+  uint32_t* const bin = sw1 + wid * (G + 1);  // bin G: sink for invalid ids
+  int32_t* const ls = (int32_t*)(sw1 + (size_t)HW_WARPS * (G + 1));  // SLUT only
+  if constexpr (SLUT) {
+    for (int i = threadIdx.x; i < n_inst; i += HW_WARPS * 32) ls[i] = __ldg(lut + i);
+    __syncthreads();
+  }
+  if (sg >= nsegs) return;
+  const long long ul = sg / ngs;
+  const int d = d0 + (int)(ul % nd);
+  const int ne = T * k;
+  const int32_t* __restrict__ src = topk + sg * (long long)ne + lane;
+  int32_t* __restrict__ dst = RANK ? rank + sg * (long long)ne + lane : nullptr;
+  for (int i = lane; i <= G; i += 32) bin[i] = 0;
+  const unsigned lt = lanemask_lt();
+  bool bad = false;
+  __syncwarp();
+  int nx[UNR];
+#pragma unroll
+  for (int j = 0; j < UNR; ++j) nx[j] = (j * 32 + lane < ne) ? __ldg(src + j * 32) : -1;
+  for (int base = 0; base < ne; base += 32 * UNR) {
+    int hv[UNR];
+    const int nb = base + 32 * UNR;
+#pragma unroll
+    for (int j = 0; j < UNR; ++j) hv[j] = nx[j];
+#pragma unroll
+    for (int j = 0; j < UNR; ++j) nx[j] = (nb + j * 32 + lane < ne) ? __ldg(src + nb + j * 32) : -1;
+#pragma unroll
+    for (int j = 0; j < UNR; ++j)
+      hv[j] = ((unsigned)hv[j] < (unsigned)n_inst) ? (SLUT ? ls[hv[j]] : __ldg(lut + hv[j]))
+                                                    : -1;
+#pragma unroll
+    for (int j = 0; j < UNR; ++j) {
+      const bool in = base + j * 32 + lane < ne;
+      const bool valid = (unsigned)hv[j] < (unsigned)G;
+      const int h = valid ? hv[j] : G;
+      bad |= in && !valid;
+      const uint32_t old = atomicAdd(&bin[h], 1u);
+      __syncwarp();
+      const uint32_t now = bin[h];
+      __syncwarp();  // the next group's atomics come after every lane's read
+      const uint32_t dd = now - old;
+      uint32_t r = old;
+      unsigned lm = __ballot_sync(FULL, dd >= 2);
+      if (lm) {
+        unsigned mine = 0;  // my key's d >= 2 members
+        for (unsigned m = lm; m; m &= m - 1) {
+          const int b = __ffs(m) - 1;
+          if (__shfl_sync(FULL, h, b) == h) mine |= 1u << b;
+        }
+        // colliding d = 1 lanes: one per colliding key
+        unsigned l1 = __ballot_sync(FULL, dd == 1 && mine != 0);
+        unsigned peers = mine;
+        for (; l1; l1 &= l1 - 1) {
+          const int b = __ffs(l1) - 1;
+          if (__shfl_sync(FULL, h, b) == h) peers |= 1u << b;
+        }
+        if (mine) r = now - (uint32_t)(__popc(mine) + 1) + (uint32_t)__popc(peers & lt);
+      }
+      if (RANK && in) dst[base + j * 32] = valid ? (int32_t)r : -1;
+    }
+  }
+  if (__any_sync(FULL, bad) && lane == 0) flag_error(err, ERR_RANGE);
+  for (int h = lane; h < G; h += 32) {
+    const int c = (int)bin[h];
+    counts[sg * G + h] = c;
+    msg[sg * G + h] = ((unsigned)(h - d * N) < (unsigned)N) ? 0LL : (long long)c * RB;
   }
 }
 
@@ -354,9 +454,20 @@ cudaError_t launch_histogram(const LaunchCtx& c, int U, int nd, int d0, int M, i
     const int unr = uv ? atoi(uv) : 16;
     const char* av = getenv("RAILS_HIST_ASYNC");
     const bool async_ok = ne % 4 == 0 && av && av[0] == '1';
+    // LUT in shared memory when it is small (RAILS_HIST_SLUT=0 keeps the L1 gather)
+    const char* slv = getenv("RAILS_HIST_SLUT");
+    const bool slut = (size_t)n_inst * 4 <= 16384 && !(slv && slv[0] == '0');
     auto kern = unr == 32 ? (rank ? k_hist_w1<32, true> : k_hist_w1<32, false>)
               : unr == 8  ? (rank ? k_hist_w1<8, true> : k_hist_w1<8, false>)
+              : slut      ? (rank ? k_hist_w1<16, true, false, true> : k_hist_w1<16, false, false, true>)
                           : (rank ? k_hist_w1<16, true> : k_hist_w1<16, false>);
+    if (slut && !async_ok && unr == 16) smem += (size_t)n_inst * 4;
+    // atomic-add ranking by default (C4 0.545 -> 0.481 ms); RAILS_HIST_ATOM=0 keeps the
+    // tag-trick kernel
+    const char* atv = getenv("RAILS_HIST_ATOM");
+    if (!(atv && atv[0] == '0') && unr == 16 && !async_ok)
+      kern = slut ? (rank ? k_hist_w1a<16, true, true> : k_hist_w1a<16, false, true>)
+                  : (rank ? k_hist_w1a<16, true, false> : k_hist_w1a<16, false, false>);
     if (async_ok) {
       kern = rank ? k_hist_w1<16, true, true> : k_hist_w1<16, false, true>;
       smem = (((size_t)HW_WARPS * (G + 1) + 3) & ~(size_t)3) * 4 +

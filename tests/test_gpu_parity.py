@@ -510,6 +510,28 @@ def test_histogram_parity_async_stage(monkeypatch):
         assert np.array_equal(rank[0, dl].cpu().numpy(), r)
 
 
+@pytest.mark.parametrize("atom,slut", [("0", "1"), ("0", "0"), ("1", "1"), ("1", "0")])
+def test_histogram_parity_w1_variants(atom, slut, monkeypatch):
+    # the warp-per-segment kernel with the LUT in shared memory or read through L1, and
+    # its atomic-add ranking variant (RAILS_HIST_ATOM=1); G = 4 makes nearly every
+    # 32-id group collide, G = 512 rarely; T*k values leave a ragged last batch
+    monkeypatch.setenv("RAILS_HIST_IMPL", "3")
+    monkeypatch.setenv("RAILS_HIST_ATOM", atom)
+    monkeypatch.setenv("RAILS_HIST_SLUT", slut)
+    for (M, N, T, k, E) in [(2, 2, 1000, 2, 4), (64, 8, 777, 2, 8), (3, 4, 4096, 4, 8),
+                            (128, 8, 4096, 2, 8), (2, 1, 33, 1, 2)]:
+        topk_all, lut = routing_inputs(M, N, T, k, E, 17, 0, 1)
+        nd = min(M, 3)
+        topk = topk_all[:, 0:nd].contiguous()
+        tp, sh = rails.topo(M, N, 65536), rails.shard(1, 0, nd)
+        counts, msg, rank = rails.histogram(tp, sh, topk.to(DEV), lut.to(DEV), 4096)
+        for dl in range(nd):
+            c, m, r = oracle.histogram_node(M, N, dl, T, k, topk[0, dl].numpy(), lut.numpy(), 4096)
+            assert np.array_equal(counts[0, dl].cpu().numpy(), c), (atom, slut, M, N, T)
+            assert np.array_equal(msg[0, dl].cpu().numpy(), m), (atom, slut, M, N, T)
+            assert np.array_equal(rank[0, dl].cpu().numpy(), r), (atom, slut, M, N, T)
+
+
 @pytest.mark.parametrize("match,w", [(None, None), ("0", "8"), ("0", "16"), ("0", "32"),
                                      ("1", "16")])
 def test_histogram_parity_multiwarp_variants(match, w, monkeypatch):
