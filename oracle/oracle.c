@@ -33,8 +33,9 @@
  *   orc_qp_map          NEXT f2: Alg. 2 step 4 round-robin QP index
  *                       per rail in assignment order (R#34).
  *
- * Parity pins live in tests/test_oracle_pins.py (worked examples from the paper /
- * SPEC, closed forms, invariants and brute force).  The ECMP hash is this build's
+ * Parity pins live in tests/test_oracle_pins.py and tests/test_oracle_pins_combine.py
+ * (worked examples from the paper / SPEC and hand-worked ones, closed forms,
+ * invariants, round trips and brute force).  The ECMP hash is this build's
  * choice (R#14): "parity unpinned" beyond the splitmix64 textbook value and the
  * hand-computed pins listed in DESIGN.md.
  *
