@@ -611,6 +611,11 @@ def e2e(args, cfg, pipe, rails, stream, dist, world, env):
                 h_res[kk].copy_(vv, non_blocking=True)
         h2d = h_msg.numel() * 8
     d2h = sum(v.numel() * v.element_size() for v in pipe.final.values())
+    # ranks may be seconds apart after pinning multi-GiB host buffers; the first call
+    # ends in the peer-memory a6, whose waits must not time out
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
     one()
     torch.cuda.synchronize()
     if dist is not None:
@@ -622,6 +627,7 @@ def e2e(args, cfg, pipe, rails, stream, dist, world, env):
         one()
     e1.record(stream)
     e1.synchronize()
+    rails.check()  # device-side errors (range, capacity, peer timeout) of the e2e steps
     ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     if dist is not None:
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)

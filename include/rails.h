@@ -50,7 +50,8 @@ enum {
     RAILS_ERANGE = -2,    /* routing id / LUT value / negative byte count out of range */
     RAILS_ENOSPC = -3,    /* workspace or output buffer too small, or size limit hit */
     RAILS_EOVERFLOW = -4, /* a load would overflow int64 */
-    RAILS_ECUDA = -5      /* CUDA launch or runtime failure (see rails_last_error) */
+    RAILS_ECUDA = -5,     /* CUDA launch or runtime failure (see rails_last_error) */
+    RAILS_ETIMEDOUT = -6  /* a peer rank of a peer-memory exchange never arrived */
 };
 
 /* Topology and method parameters -- the paper's problem statement (section 4.1). */
@@ -220,8 +221,12 @@ int rails_eval_finalize(const rails_topo_t* topo, int32_t U, const int64_t* red_
  *   gen     call number: >= 1, equal on all ranks, +1 per call (flags are waited on
  *           as ">= gen"; partials are double-buffered by gen parity, so back-to-back
  *           calls need no other synchronisation).
- * A rank that waits ~1 s for a peer sets RAILS_ECUDA-class error RAILS_ERANGE in the
- * device flag and finalizes what it has (rails_check reports it). */
+ * A rank that waits 30 s for a peer's flag gives up: it records RAILS_ETIMEDOUT in the
+ * device flag (rails_check reports it) and finalizes what it has, which is then
+ * undefined.  The exchange is out of step after a timeout (the call counters of the
+ * ranks disagree): free and rebuild the exchange buffers on every rank before the
+ * next call.  The call counter lives on the host, so a call captured into a CUDA
+ * graph would replay a stale gen: never capture these calls. */
 #define RAILS_PEER_MAX 8
 typedef struct {
     int32_t rank;
@@ -350,7 +355,8 @@ int rails_pack_owner(const rails_topo_t* topo, const rails_shard_t* shard, int32
  *     returns when all ranks' rows are in this rank's table (the schedule input);
  *   rails_peer_barrier: after rails_pack_owner, every rank's packed pieces are in
  *     their owners' buffers when the barrier kernel of every rank has completed.
- * A peer missing for ~1 s sets RAILS_ERANGE in the device flag. */
+ * A peer missing for 30 s sets RAILS_ETIMEDOUT in the device flag; the exchange must
+ * then be rebuilt (as for rails_eval_finalize_peer).  Not graph-capturable (gen). */
 int rails_owner_exchange_layout(const rails_topo_t* topo, int32_t U, int32_t world,
                                 size_t* bytes, size_t* msg_offset);
 int rails_gather_rows_peer(const rails_topo_t* topo, int32_t U, int32_t g0, int32_t ng,
@@ -435,8 +441,9 @@ int rails_flowsim(const rails_topo_t* topo, const rails_fabric_t* fabric, int32_
 
 /* ------------------------------------------------------------------ misc */
 /* Synchronise `stream`, then return (and clear) the first device-side error
- * recorded since the last check: RAILS_OK, RAILS_ERANGE, RAILS_ENOSPC or
- * RAILS_EOVERFLOW; RAILS_ECUDA if the stream reports a CUDA error. */
+ * recorded since the last check: RAILS_OK, RAILS_ERANGE, RAILS_ENOSPC,
+ * RAILS_EOVERFLOW or RAILS_ETIMEDOUT; RAILS_ECUDA if the stream reports a CUDA
+ * error. */
 int rails_check(void* stream);
 
 /* Thread-local description of the last failed call ("" if none). */

@@ -122,6 +122,11 @@ int rails_check(void* stream) {
     int zero = 0;
     cudaMemcpy(c.err, &zero, sizeof(int), cudaMemcpyHostToDevice);
   }
+  if (flag & ERR_TIMEOUT)
+    return fail(RAILS_ETIMEDOUT,
+                "device: a peer rank's flag did not arrive within %llu s; the peer exchange is "
+                "out of step -- rebuild it (PeerFinalize / RailOwnerNode) before the next call",
+                (unsigned long long)(PEER_TIMEOUT_NS / 1000000000ull));
   if (flag & ERR_RANGE) return fail(RAILS_ERANGE, "device: value out of range (routing id, LUT, rank or byte count)");
   if (flag & ERR_NOSPC) return fail(RAILS_ENOSPC, "device: output buffer too small");
   if (flag & ERR_OVERFLOW) return fail(RAILS_EOVERFLOW, "device: load overflow");

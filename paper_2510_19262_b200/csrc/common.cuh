@@ -16,7 +16,7 @@ namespace rails {
 constexpr unsigned FULL = 0xffffffffu;
 
 // Device error bits, OR-ed into the flag word passed to every kernel.
-enum : int { ERR_RANGE = 1, ERR_NOSPC = 2, ERR_OVERFLOW = 4 };
+enum : int { ERR_RANGE = 1, ERR_NOSPC = 2, ERR_OVERFLOW = 4, ERR_TIMEOUT = 8 };
 
 __device__ __forceinline__ void flag_error(int* err, int bit) {
   if ((*(volatile int*)err & bit) == 0) atomicOr(err, bit);
@@ -106,6 +106,41 @@ __device__ __forceinline__ long long block_excl_scan(long long v, long long* scr
   *total = scratch[32];
   __syncthreads();
   return r;
+}
+
+// ---- system-scope flags of the peer-memory exchanges (k_eval.cu, k_owner.cu)
+__device__ __forceinline__ void st_release_sys(uint32_t* a, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* a) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// A rank waits at most this long for a peer's flag.  Generous on purpose: ranks
+// sharing one GPU (the single-GPU multi-rank tests) only progress when the GPU's
+// time slicing runs their context.
+constexpr unsigned long long PEER_TIMEOUT_NS = 30ull * 1000000000ull;
+
+// Wait until the monotonic call counter at f reaches gen (wrap-safe compare).  On
+// timeout: ERR_TIMEOUT in the device flag and false; the exchange is then out of
+// step and must be rebuilt (include/rails.h, rails_eval_finalize_peer).
+__device__ __forceinline__ bool wait_flag_ge(const uint32_t* f, uint32_t gen, int* err) {
+  if ((int)(ld_acquire_sys(f) - gen) >= 0) return true;
+  const unsigned long long t0 = globaltimer_ns();
+  while ((int)(ld_acquire_sys(f) - gen) < 0) {
+    __nanosleep(128);
+    if (globaltimer_ns() - t0 > PEER_TIMEOUT_NS) {
+      flag_error(err, ERR_TIMEOUT);
+      return false;
+    }
+  }
+  return true;
 }
 
 // ECMP rail (R#14): splitmix64 output step, this library's own copy.

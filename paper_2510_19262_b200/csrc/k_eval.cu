@@ -434,15 +434,6 @@ struct PeerBufs {
   uint8_t* p[RAILS_PEER_MAX];
 };
 
-__device__ __forceinline__ void st_release_sys(uint32_t* a, uint32_t v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* a) {
-  uint32_t v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
-  return v;
-}
-
 __host__ __device__ static inline size_t al256e(size_t x) { return (x + 255) & ~(size_t)255; }
 
 // [flags: U x world u32][slots: 2 (call parity) x world x U x rec int64]
@@ -483,17 +474,8 @@ __global__ void __launch_bounds__(256)
       st_release_sys((uint32_t*)pb.p[p] + u * world + rank, gen);
   }
   // 2. wait for every rank's partials of this unit
-  if (threadIdx.x < world) {
-    const uint32_t* f = (const uint32_t*)pb.p[rank] + u * world + threadIdx.x;
-    long long spins = 0;
-    while ((int)(ld_acquire_sys(f) - gen) < 0) {
-      __nanosleep(64);
-      if (++spins > (1LL << 24)) {
-        flag_error(err, ERR_RANGE);
-        break;
-      }
-    }
-  }
+  if (threadIdx.x < world)
+    wait_flag_ge((const uint32_t*)pb.p[rank] + u * world + threadIdx.x, gen, err);
   __syncthreads();
   // 3. reduce in rank order (volatile loads: the data came from other GPUs)
   const volatile int64_t* slots = (const volatile int64_t*)(pb.p[rank] + slots_off);

@@ -277,26 +277,6 @@ cudaError_t launch_rail_offsets_owner(const LaunchCtx& c, long long ublk, int N,
 // Exchange buffer of a rail-owner rank (rails_owner_exchange_layout):
 //   [barrier flags: RAILS_PEER_MAX x u32, 256 B][gather flags: U x world x u32,
 //    256-aligned][msg_node: int64 [U][1][N][G]]
-__device__ __forceinline__ void st_rel_sys(uint32_t* a, uint32_t v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t ld_acq_sys(const uint32_t* a) {
-  uint32_t v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
-  return v;
-}
-__device__ __forceinline__ bool wait_flag(const uint32_t* f, uint32_t gen, int* err) {
-  long long spins = 0;
-  while ((int)(ld_acq_sys(f) - gen) < 0) {  // monotonic call counters
-    __nanosleep(64);
-    if (++spins > (1LL << 24)) {
-      flag_error(err, ERR_RANGE);
-      return false;
-    }
-  }
-  return true;
-}
-
 struct PeerBase {
   uint8_t* p[RAILS_PEER_MAX];
 };
@@ -334,10 +314,10 @@ __global__ void __launch_bounds__(256)
   if (threadIdx.x == 0) {
     __threadfence_system();
     for (int p = 0; p < world; ++p)
-      st_rel_sys((uint32_t*)(pb.p[p] + gflag_off) + u * world + rank, gen);
+      st_release_sys((uint32_t*)(pb.p[p] + gflag_off) + u * world + rank, gen);
   }
   if (threadIdx.x < world)
-    wait_flag((const uint32_t*)(pb.p[rank] + gflag_off) + u * world + threadIdx.x, gen, err);
+    wait_flag_ge((const uint32_t*)(pb.p[rank] + gflag_off) + u * world + threadIdx.x, gen, err);
   __syncthreads();
 }
 
@@ -346,10 +326,10 @@ __global__ void __launch_bounds__(256)
 __global__ void k_peer_barrier(PeerBase pb, int rank, int world, uint32_t gen, int* err) {
   if (threadIdx.x == 0) {
     __threadfence_system();
-    for (int p = 0; p < world; ++p) st_rel_sys((uint32_t*)pb.p[p] + rank, gen);
+    for (int p = 0; p < world; ++p) st_release_sys((uint32_t*)pb.p[p] + rank, gen);
   }
   __syncwarp();
-  if (threadIdx.x < world) wait_flag((const uint32_t*)pb.p[rank] + threadIdx.x, gen, err);
+  if (threadIdx.x < world) wait_flag_ge((const uint32_t*)pb.p[rank] + threadIdx.x, gen, err);
   __syncwarp();
 }
 

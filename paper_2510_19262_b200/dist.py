@@ -30,14 +30,37 @@ def weak_units(world: int, units_per_gpu_factor: int = 1) -> int:
 
 
 def make_reduce(group=None) -> Callable:
-    """a6 hook for pipeline.*.step: SUM the partial sums, MAX the partial maxima."""
+    """a6 hook for pipeline.*.step: SUM the partial sums, MAX the partial maxima.
+
+    NCCL reduces the device tensors in place.  Under gloo (the CPU tests, and several
+    ranks sharing one GPU, where NCCL refuses duplicate devices) device tensors are
+    staged through host copies."""
     import torch.distributed as dist
 
+    staged = dist.get_backend(group) == "gloo"
+
     def reduce(red_sum, red_max):
+        if staged and red_sum.is_cuda:
+            s, m = red_sum.cpu(), red_max.cpu()
+            dist.all_reduce(s, op=dist.ReduceOp.SUM, group=group)
+            dist.all_reduce(m, op=dist.ReduceOp.MAX, group=group)
+            red_sum.copy_(s)
+            red_max.copy_(m)
+            return
         dist.all_reduce(red_sum, op=dist.ReduceOp.SUM, group=group)
         dist.all_reduce(red_max, op=dist.ReduceOp.MAX, group=group)
 
     return reduce
+
+
+def check_not_capturing(what: str):
+    """The peer-memory exchanges count calls on the host (gen, passed by value to the
+    kernel): a CUDA-graph replay would reuse the captured gen and parity, so the flag
+    waits would pass at once and read stale or half-written partials.  Refuse."""
+    import torch
+    if torch.cuda.is_available() and torch.cuda.is_current_stream_capturing():
+        raise RuntimeError(f"{what} cannot be captured into a CUDA graph: its call counter "
+                           "lives on the host (include/rails.h)")
 
 
 class PeerFinalize:
@@ -84,14 +107,15 @@ class PeerFinalize:
         dist.barrier(group=group)
 
     def ok(self) -> bool:
-        """True on every rank iff every rank mapped every peer (collective)."""
-        import torch
-        f = torch.tensor([0.0 if self.error else 1.0], device=torch.cuda.current_device())
-        self.dist.all_reduce(f, op=self.dist.ReduceOp.MIN, group=self.group)
-        return f.item() == 1.0
+        """True on every rank iff every rank mapped every peer (collective; an object
+        collective, so it works under NCCL and gloo alike)."""
+        flags = [None] * self.world
+        self.dist.all_gather_object(flags, self.error is None, group=self.group)
+        return all(flags)
 
     def finalize(self, red_sum, red_max, out, stream=None):
         from . import rails
+        check_not_capturing("PeerFinalize.finalize")
         self.gen += 1
         rails.eval_finalize_peer(self.tp, self.U, red_sum, red_max, self.rank, self.world,
                                  self.gen, self.bufs, out=out, stream=stream)

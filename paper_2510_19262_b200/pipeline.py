@@ -105,8 +105,10 @@ class GraphStep:
     `pipe.step(*args)` captures as is; replaying it re-runs the whole hot path with
     one graph launch instead of ~8 host launches.  Inputs are read from the tensors
     passed at capture time: refill them in place (tensor.copy_) between replays.
-    The a6 hook must be graph-safe (the peer-memory finalize is; an NCCL all-reduce
-    is capturable with NCCL's own graph support)."""
+    The a6 hook must be graph-safe: an NCCL all-reduce is (NCCL's own graph
+    support); the peer-memory finalize is NOT -- its call counter lives on the host,
+    so a replay would reuse the captured counter and read stale partials -- and it
+    raises if called during capture (dist.check_not_capturing)."""
 
     def __init__(self, step: Callable, *args, warmup: int = 2):
         s = torch.cuda.Stream()

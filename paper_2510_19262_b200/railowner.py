@@ -11,7 +11,8 @@ rail j's send buffer lives in GPU j's HBM.  One step:
   4. rails_rail_offsets_owner + rails_pack_owner: each chunk piece is stored
      straight into the owner's buffer through a peer-mapped pointer   (kernel)
   5. rails_peer_barrier orders every rank's pack before any consumer (kernel).
-exchange="nccl" keeps the NCCL all-gather / all-reduce for steps 2 and 5.
+exchange="nccl" keeps the collective all-gather / all-reduce for steps 2 and 5 (NCCL;
+host-staged under gloo, when several ranks share one GPU).
 Peer mapping: CUDA IPC handles exported/imported by librails (rails_ipc_*), each
 rank mapping the peers' buffers under its own device.
 """
@@ -20,6 +21,7 @@ from __future__ import annotations
 import torch
 
 from . import rails
+from .dist import check_not_capturing
 
 
 def _enable_peer_access(dev: int, peers):
@@ -53,6 +55,9 @@ class RailOwnerNode:
         self.msg_loc = torch.empty((U, 1, self.ng, G), dtype=torch.int64, device=dev)
         self.rank_loc = torch.empty((U, 1, self.ng, T, k), dtype=torch.int32, device=dev)
         self.exchange = exchange
+        # the collective exchange stages through host memory under gloo (several
+        # ranks on one GPU: NCCL refuses duplicate devices)
+        self.staged = dist.get_backend(group) == "gloo"
         if exchange not in ("peer", "nccl"):
             raise ValueError("exchange must be 'peer' or 'nccl'")
         self.msg_node = torch.empty((U, 1, N, G), dtype=torch.int64, device=dev)
@@ -120,10 +125,17 @@ class RailOwnerNode:
     def schedule_part(self, topk: torch.Tensor, lut: torch.Tensor):
         rails.histogram_gpus(self.tp, self.sh, self.g0, topk, lut, self.RB,
                              out=(self.counts, self.msg_loc, self.rank_loc))
+        if self.exchange == "peer":
+            check_not_capturing("RailOwnerNode (peer exchange)")
         self.gen += 1
         if self.exchange == "peer":
             rails.gather_rows_peer(self.tp, self.U, self.g0, self.ng, self.msg_loc, self.p,
                                    self.P, self.gen, self.xbufs)
+        elif self.staged:  # gloo (ranks sharing one GPU): host-staged all-gather
+            for u in range(self.U):
+                parts = [torch.empty_like(self.msg_loc[u, 0], device="cpu") for _ in range(self.P)]
+                self.dist.all_gather(parts, self.msg_loc[u, 0].cpu(), group=self.group)
+                self.msg_node[u, 0].copy_(torch.cat(parts))
         else:
             for u in range(self.U):
                 self.dist.all_gather_into_tensor(self.msg_node[u, 0], self.msg_loc[u, 0],
@@ -142,6 +154,9 @@ class RailOwnerNode:
         # anywhere orders all peer writes before later consumers
         if self.exchange == "peer":
             rails.peer_barrier(self.p, self.P, self.gen, self.xbufs)
+        elif self.staged:
+            f = self.flag.cpu()
+            self.dist.all_reduce(f, group=self.group)
         else:
             self.dist.all_reduce(self.flag, group=self.group)
 

@@ -18,7 +18,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "librails.so")
 
 RAILS_OK, RAILS_EINVAL, RAILS_ERANGE, RAILS_ENOSPC, RAILS_EOVERFLOW, RAILS_ECUDA = 0, -1, -2, -3, -4, -5
-_NAMES = {-1: "EINVAL", -2: "ERANGE", -3: "ENOSPC", -4: "EOVERFLOW", -5: "ECUDA"}
+RAILS_ETIMEDOUT = -6
+_NAMES = {-1: "EINVAL", -2: "ERANGE", -3: "ENOSPC", -4: "EOVERFLOW", -5: "ECUDA", -6: "ETIMEDOUT"}
 RED_MAX_LEN = 4
 
 

@@ -1,53 +1,31 @@
-"""NEXT f2 -- rail-owner pack fused with the intra-node NVLink hop (-m gpu, >= 2 GPUs).
+"""NEXT f2 -- rail-owner pack fused with the intra-node hop (-m gpu, multi-rank).
 
-P processes (one per GPU, NCCL) form one RailS node: each packs its own source GPUs'
-rows into the rail buffers owned by the other GPUs through peer pointers.  Every
-owned rail buffer must equal, byte for byte, the oracle's rail buffer of the node
-(oracle.pack_node on all N source GPUs, by definition).  Skipped on 1-GPU boxes.
+P processes form one RailS node (NIC j hangs off GPU j; the intra-domain hop
+P:303): each packs its own source GPUs' rows into the rail buffers owned
+by the other ranks through CUDA-IPC peer pointers.  Every owned rail buffer must
+equal, byte for byte, the oracle's rail buffer of the node (oracle.pack_node on all
+N source GPUs, by definition), after two steps (flags reused: gen 2).
+
+Runs on any box: all ranks on cuda:0 (gloo) always, one rank per GPU (NCCL, NVLink
+stores) when the box has enough GPUs (tests/mp_ranks.py).
 """
-import os
-import socket
-
 import numpy as np
 import pytest
 import torch
-import torch.multiprocessing as mp
 
 import gen
+from mp_ranks import placements, run_ranks
 
 pytestmark = pytest.mark.gpu
 
 
-def _port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    p = s.getsockname()[1]
-    s.close()
-    return p
-
-
-def _worker(rank, world, port, cfg, q):
-    import traceback
-    try:
-        _worker_body(rank, world, port, cfg, q)
-    except BaseException:
-        q.put((rank, ["EXC " + traceback.format_exc()]))
-        raise
-
-
-def _worker_body(rank, world, port, cfg, q):
+def _body(rank, world, dev, cfg):
     import torch.distributed as dist
 
     import oracle
     from paper_2510_19262_b200 import rails
     from paper_2510_19262_b200.railowner import RailOwnerNode
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    torch.cuda.set_device(rank)
-    dist.init_process_group("nccl", rank=rank, world_size=world,
-                            device_id=torch.device("cuda", rank))
     M, N, T, k, E, RB, C, U, d = (cfg[x] for x in "M N T k E RB C U d".split())
-    dev = torch.device("cuda", rank)
     seed = 31
     topk_all = torch.stack([gen.routing(M, N, T, k, E, seed, u, d, 1) for u in range(U)])
     x_all = torch.stack([gen.payload(M, N, T, RB, seed, u, d, 1) for u in range(U)])
@@ -56,14 +34,17 @@ def _worker_body(rank, world, port, cfg, q):
     g0, ng = node.g0, node.ng
     topk = topk_all[:, :, g0:g0 + ng].contiguous().to(dev)
     x = x_all[:, :, g0:g0 + ng].contiguous().to(dev)
+    lut_d = lut.to(dev)
     node.buf.zero_()
     torch.cuda.synchronize()
     dist.barrier()
-    node.step(topk, lut.to(dev), x)
+    node.step(topk, lut_d, x)
+    torch.cuda.synchronize()
+    dist.barrier()
     node.buf.zero_()  # a second step re-gathers and re-packs (flags reused, gen 2)
     torch.cuda.synchronize()
     dist.barrier()
-    node.step(topk, lut.to(dev), x)
+    node.step(topk, lut_d, x)
     torch.cuda.synchronize()
     rails.check()
     errors = []
@@ -81,46 +62,20 @@ def _worker_body(rank, world, port, cfg, q):
             got = node.own_rail(j)[int(rb[j]):int(rb[j]) + int(L[j])].cpu().numpy()
             if not np.array_equal(got, want[base[j]:base[j] + L[j]]):
                 errors.append(f"u{u} rail{j}")
-    q.put((rank, errors))
-    node.close()
     dist.barrier()
-    dist.destroy_process_group()
+    node.close()
+    return errors
 
 
 @pytest.mark.parametrize("cfg", [
-    dict(M=4, N=4, T=300, k=2, E=8, RB=1024, C=4096, U=2, d=1),   # 2-piece path
-    dict(M=3, N=4, T=128, k=2, E=6, RB=2048, C=1024, U=1, d=2),   # C < RB multi-piece
-    dict(M=4, N=4, T=300, k=2, E=8, RB=1024, C=4096, U=2, d=1, ex="nccl"),  # NCCL exchange
-    dict(M=3, N=4, T=100, k=2, E=8, RB=12288, C=32768, U=1, d=0),  # 12 KiB rows: windows
+    dict(M=4, N=4, T=300, k=2, E=8, RB=1024, C=4096, U=2, d=1, P=2),   # 2-piece path
+    dict(M=4, N=4, T=300, k=2, E=8, RB=1024, C=4096, U=2, d=1, P=4),   # one rail per rank
+    dict(M=3, N=4, T=128, k=2, E=6, RB=2048, C=1024, U=1, d=2, P=2),   # C < RB multi-piece
+    dict(M=4, N=4, T=300, k=2, E=8, RB=1024, C=4096, U=2, d=1, P=2, ex="nccl"),  # collective
+    dict(M=3, N=4, T=100, k=2, E=8, RB=12288, C=32768, U=1, d=0, P=2),  # 12 KiB rows: windows
 ])
 def test_railowner_pack_matches_oracle(cfg):
-    ngpu = torch.cuda.device_count() if torch.cuda.is_available() else 0
-    if ngpu < 2:
-        pytest.skip("needs >= 2 GPUs")
-    world = 4 if ngpu >= 4 and cfg["N"] % 4 == 0 else 2
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    import queue
-    import time
-    res = {}
-    t_end = time.time() + 600
-    while len(res) < world and time.time() < t_end:
-        try:
-            r, errs = q.get(timeout=5)
-            res[r] = errs
-            if any(e.startswith("EXC") for e in errs):
-                break
-        except queue.Empty:
-            if any(p.exitcode not in (None, 0) for p in procs):
-                break
-    for p in procs:
-        p.join(timeout=30)
-        if p.is_alive():
-            p.kill()
-    for r, errs in res.items():
-        assert not errs, (r, errs)
-    assert len(res) == world, f"workers: exit codes {[p.exitcode for p in procs]}"
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    for placement in placements(cfg["P"]):
+        run_ranks(_body, cfg["P"], placement, cfg)
