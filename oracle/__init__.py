@@ -190,6 +190,21 @@ def eval_unit(M, N, R2, ecmp_seed, msg_unit, ch_d, ch_h, ch_size, ch_rail):
                 mse=ms, nmse=nms)
 
 
+def eval_uniform(M, N, R2, msg_unit):
+    """The uniform split P* = 1/N (Theorem 3, R#41) of one unit msg_unit [M][N][G]."""
+    L = lib()
+    P = ctypes.c_void_p
+    L.orc_eval_uniform.restype = None
+    L.orc_eval_uniform.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_double, P, P, P, P, P]
+    msg_unit = _c(msg_unit, np.int64)
+    S_u = np.zeros((M, N), np.int64)
+    R_u = np.zeros((M, N), np.int64)
+    mx = np.zeros(1, np.int64)
+    dbl = np.zeros(2, np.float64)
+    L.orc_eval_uniform(M, N, float(R2), _p(msg_unit), _p(S_u), _p(R_u), _p(mx), _p(dbl))
+    return dict(S_u=S_u, R_u=R_u, maxload_u=int(mx[0]), T_u=float(dbl[0]), busbw_u=float(dbl[1]))
+
+
 def pack_node(M, N, d, T, k, row_bytes, C, x_node, topk_node, lut, msg_node, sched,
               rail_base, out_cap):
     """a7 for one node by definition; returns the output byte buffer."""

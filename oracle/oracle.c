@@ -27,6 +27,8 @@
  *                       T* (Thm 2 + Thm 3); busbw (R#10);
  *                       MSE Eq. 6 / Alg. 2 step 6, nMSE (R#12);
  *                       ECMP whole-message hash baseline (R#13, R#14).
+ *   orc_eval_uniform    the uniform split P* = 1/N (Thm 3; R#41) on
+ *                       the same load model.
  *   orc_pack_node       rail buffers by definition (R#18-R#20): message byte
  *                       stream = concatenation of rows in (t,s) order, chunk c of
  *                       message (g,h) copied to rail[j] + offset.
@@ -316,6 +318,41 @@ void orc_eval(int32_t M, int32_t N, double R2, uint64_t ecmp_seed,
         mse[d] = orc_mse(N, S + (int64_t)d * N);
         nmse[d] = orc_nmse(N, S + (int64_t)d * N);
     }
+}
+
+/* Uniform policy (Theorem 3's continuous optimum P*_{k,f,n} = 1/N, P:452-455;
+ * reading R#41): every message of B bytes is split over all N rails, rail j taking
+ * floor(B/N) bytes plus one more when j < B mod N, on the same load model as the
+ * LPT and ECMP assignments (Eq. 4-5, R#7).  Outputs: S_u[M][N], R_u[M][N],
+ * *maxload_u, dbl[2] = T_u = maxload_u / R2, busbw_u = total / T_u (0 without
+ * traffic, R#40). */
+void orc_eval_uniform(int32_t M, int32_t N, double R2, const int64_t *msg, int64_t *S_u,
+                      int64_t *R_u, int64_t *maxload_u, double *dbl) {
+    int64_t G = (int64_t)M * N;
+    int64_t total = 0;
+    for (int64_t i = 0; i < (int64_t)M * N; i++) { S_u[i] = 0; R_u[i] = 0; }
+    for (int32_t d = 0; d < M; d++)
+        for (int32_t g = 0; g < N; g++)
+            for (int64_t h = 0; h < G; h++) {
+                int64_t B = msg[((int64_t)d * N + g) * G + h];
+                if (B <= 0) continue;
+                int64_t f = h / N;
+                for (int32_t j = 0; j < N; j++) {
+                    int64_t part = B / N + ((j < B % N) ? 1 : 0);
+                    S_u[(int64_t)d * N + j] += part;
+                    R_u[f * N + j] += part;
+                }
+                total += B;
+            }
+    int64_t mx = 0;
+    for (int64_t i = 0; i < (int64_t)M * N; i++) {
+        if (S_u[i] > mx) mx = S_u[i];
+        if (R_u[i] > mx) mx = R_u[i];
+    }
+    *maxload_u = mx;
+    double T_u = (double)mx / R2;
+    dbl[0] = T_u;
+    dbl[1] = (total > 0) ? (double)total / T_u : 0.0;
 }
 
 /* ---------------------------------------------------------------- pack */

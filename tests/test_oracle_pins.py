@@ -478,3 +478,38 @@ def test_qp_map_rejects_zero_qps():
     order, rail, off, load = oracle.lpt(np.array([3, 2], np.int64), 1)
     with pytest.raises(ValueError):
         oracle.qp_map(order, rail, 1, 0)
+
+
+# ------------------------------------------------------------------ uniform policy (f3)
+@pytest.mark.parametrize("ex", GOLD["uniform_hand"])
+def test_uniform_hand_examples(ex):
+    M, N = ex["M"], ex["N"]
+    msg = _msg_from_entries(M, N, ex["messages"])
+    u = oracle.eval_uniform(M, N, R2, msg)
+    assert u["S_u"].tolist() == ex["S_u"] and u["R_u"].tolist() == ex["R_u"]
+    assert u["maxload_u"] == ex["maxload_u"]
+    assert u["T_u"] * R2 == pytest.approx(ex["maxload_u"], rel=1e-15)
+
+
+def test_uniform_theorem3_and_bounds():
+    # Thm 3: with every message a multiple of N, N*S_u[k][n] = row sum k
+    # and N*R_u[f][n] = col sum f exactly, so T_u = T*; in general T_u >= T* (Thm 2),
+    # bytes are conserved and a rail differs from the mean by < one byte per message
+    rng = np.random.default_rng(16)
+    for trial in range(120):
+        M, N = int(rng.integers(2, 9)), int(rng.integers(1, 9))
+        div = trial % 2 == 0
+        msg = _random_msg(rng, M, N, p=0.4, hi=10000, mult=N if div else 1)
+        _, ev = oracle.run_unit_matrix(M, N, 4096, R2, SEED, msg)
+        u = oracle.eval_uniform(M, N, R2, msg)
+        D2 = msg.reshape(M, N, M, N).sum(axis=(1, 3))
+        rows, cols = D2.sum(axis=1), D2.sum(axis=0)
+        assert (u["S_u"].sum(axis=1) == rows).all() and (u["R_u"].sum(axis=1) == cols).all()
+        assert u["T_u"] >= ev["T_star"] * (1 - 1e-15)
+        nmsg = (msg > 0).reshape(M, -1).sum(axis=1)
+        assert (np.abs(N * u["S_u"] - rows[:, None]) <= N * nmsg[:, None]).all()
+        if div:
+            assert (u["S_u"] * N == rows[:, None]).all() and (u["R_u"] * N == cols[:, None]).all()
+            assert u["T_u"] == pytest.approx(ev["T_star"], rel=1e-15)
+        if ev["total"]:
+            assert u["busbw_u"] == pytest.approx(ev["total"] / u["T_u"], rel=1e-15)
