@@ -117,7 +117,8 @@ typedef struct {
     int32_t* n_rem;
 } rails_sched_t;
 
-/* Device workspace (bytes) rails_lpt_schedule needs for this topology/shard. */
+/* Device workspace (bytes) rails_lpt_schedule / rails_schedule_eval need for this
+ * topology/shard.  Zero-fill it once before its first use (rails_schedule_eval). */
 int rails_schedule_workspace(const rails_topo_t* topo, const rails_shard_t* shard,
                              size_t* workspace_bytes);
 
@@ -158,24 +159,29 @@ int rails_lpt_assign(int32_t N, int32_t n_seg, const int64_t* seg_off, int64_t F
 /* ------------------------------------------------------------------ a5 */
 /* Loads and balance of the shard's nodes plus reduction buffers for the global
  * quantities.  Load model (R#7): a chunk of node d on rail j bound for node
- * f = h/N adds to S[d][j] (Eq. 4) and R[f][j] (Eq. 5).  ECMP baseline (R#13,
- * R#14): each whole message (d,g,h) goes on rail ecmp(d*N+g, h).
- *   S, S_e    int64 [U][nd][N]   send loads (LPT, ECMP) of the shard's nodes;
+ * f = h/N adds to S[d][j] (Eq. 4) and R[f][j] (Eq. 5).  Two baselines on the same
+ * load model:
+ *   ECMP (R#13, R#14): each whole message (d,g,h) goes on rail ecmp(d*N+g, h);
+ *   uniform (Theorem 3's continuous optimum P* = 1/N; R#41): each
+ *     message of B bytes is split over all N rails, rail j taking floor(B/N) bytes
+ *     plus one more when j < B mod N.
+ *   S, S_e, S_u int64 [U][nd][N]  send loads (LPT, ECMP, uniform) of the shard's nodes;
  *   mse, nmse double [U][nd]     Eq. 6 of S[d][.] about its mean, exact
  *                                form sum_j (N*S_j - sum S)^2 / N^3 (R#11); nMSE =
  *                                mse / (sum S)^2, 0 if sum S = 0 (R#12);
  *   red_sum   int64 [U][RAILS_RED_SUM_LEN(M,N)]  PARTIAL sums over the shard's
- *             nodes, layout: R[M][N], R_e[M][N], colsum[M] (bytes into node f),
- *             total, total_e.  Overwritten (zeroed then accumulated) by the call.
- *   red_max   int64 [U][RAILS_RED_MAX_LEN]  PARTIAL maxima: max S, max S_e,
- *             max row sum (bytes out of one node), 0.
+ *             nodes, layout: R[M][N], R_e[M][N], R_u[M][N], colsum[M] (bytes into
+ *             node f), total, total_e.  Overwritten by the call.
+ *   red_max   int64 [U][RAILS_RED_MAX_LEN]  PARTIAL maxima: max S, max S_e, max row
+ *             sum (bytes out of one node), max S_u.
  * With the nodes of a unit split over ranks, all-reduce red_sum (SUM) and
  * red_max (MAX) across ranks before rails_eval_finalize (a6). */
-#define RAILS_RED_SUM_LEN(M, N) (2 * (int64_t)(M) * (int64_t)(N) + (int64_t)(M) + 2)
+#define RAILS_RED_SUM_LEN(M, N) (3 * (int64_t)(M) * (int64_t)(N) + (int64_t)(M) + 2)
 #define RAILS_RED_MAX_LEN 4
 typedef struct {
     int64_t* S;
     int64_t* S_e;
+    int64_t* S_u;
     double* mse;
     double* nmse;
     int64_t* red_sum;
@@ -189,26 +195,49 @@ int rails_eval(const rails_topo_t* topo, const rails_shard_t* shard,
 /* Per-unit results from fully reduced red_sum / red_max ([U][...] as above):
  *   maxload   = max(max S, max R)        (most loaded NIC, send or receive)
  *   T         = maxload / R2             (R#8)
- *   total     = inter-node bytes;  busbw = total / T, 0 if total = 0   (R#10)
+ *   total     = inter-node bytes;  busbw = total / T, 0 if total = 0   (R#10, R#40)
  *   rowmax, colmax = max row / column sum of D^(2) (Eq. 1);
  *   T_star    = max(rowmax, colmax) / (N * R2)   (Thm 2 + Thm 3)
- *   *_e       = the same for the ECMP-hash baseline.
- * All outputs are device arrays of length U (int64 or double). */
+ *   *_e       = the same for the ECMP-hash baseline;
+ *   *_u       = the same for the uniform split (R#41; T_u >= T_star, equal when
+ *               every message is a multiple of N bytes: Theorem 3).
+ * All outputs are device arrays of length U (int64 or double); any may be NULL. */
 typedef struct {
     int64_t* maxload;
     int64_t* maxload_e;
+    int64_t* maxload_u;
     int64_t* total;
     int64_t* rowmax;
     int64_t* colmax;
     double* T;
     double* T_e;
+    double* T_u;
     double* T_star;
     double* busbw;
     double* busbw_e;
+    double* busbw_u;
 } rails_final_t;
 
 int rails_eval_finalize(const rails_topo_t* topo, int32_t U, const int64_t* red_sum,
                         const int64_t* red_max, const rails_final_t* out, void* stream);
+
+/* a2-a5 fused (the hot path): ONE kernel computes the compact LPT schedule
+ * (exactly as rails_lpt_schedule), the evaluation of the shard's nodes (exactly as
+ * rails_eval: S, S_e, S_u, mse, nmse, partial red_sum / red_max) and, optionally,
+ * the per-unit finalize and the rail offsets:
+ *   final      NULL, or the rails_eval_finalize outputs -- only when the shard holds
+ *              every node of its units (d0 = 0, nd = M); with nodes split over ranks
+ *              pass NULL and finalize after the a6 exchange;
+ *   rail_base, rail_total  NULL, or the rails_rail_offsets outputs.
+ * workspace: rails_schedule_workspace() bytes, zero-filled before the FIRST call
+ * (the kernel keeps per-unit accumulators and arrival counters there and leaves them
+ * zeroed after every call).  Falls back to two launches (schedule, then eval) when
+ * N*M*N exceeds the fused kernel's shared-memory limit; the results are identical. */
+int rails_schedule_eval(const rails_topo_t* topo, const rails_shard_t* shard,
+                        const int64_t* msg_bytes, const rails_sched_t* sched,
+                        const rails_eval_t* eval, const rails_final_t* final,
+                        int64_t* rail_base, int64_t* rail_total, void* workspace,
+                        size_t workspace_bytes, void* stream);
 
 /* a6 fused with the finalize over NVLink peer memory (one process per GPU of a
  * box): every rank pushes its partial red_sum / red_max of each unit into every
@@ -238,6 +267,18 @@ int rails_peer_buffer_bytes(const rails_topo_t* topo, int32_t U, int32_t world, 
 int rails_eval_finalize_peer(const rails_topo_t* topo, int32_t U, int64_t* red_sum,
                              int64_t* red_max, const rails_peer_t* peer,
                              const rails_final_t* out, void* stream);
+
+/* The same exchange with EVERY rank driven by one process on one device (the
+ * single-GPU tests; one process serving several ranks).  Rank p's partials are
+ * red_sum[p] / red_max[p] and its outputs out[p] (host arrays of `world` entries);
+ * peer->buf[p] is rank p's exchange buffer (plain device memory, all in this
+ * process); peer->rank is ignored.  ONE cooperative launch plays every rank (CTA
+ * (u, p) is rank p), so the ranks' flag waits run co-resident: separate spinning
+ * launches or processes sharing one GPU are not guaranteed to run concurrently.
+ * RAILS_ECUDA if U * world CTAs cannot be co-resident. */
+int rails_eval_finalize_peer_local(const rails_topo_t* topo, int32_t U, int64_t* const* red_sum,
+                                   int64_t* const* red_max, const rails_peer_t* peer,
+                                   const rails_final_t* out, void* stream);
 
 /* ------------------------------------------------------------------ a7 */
 /* Rail buffer placement: rail_base int64 [U][nd][N] = exclusive prefix sum of
@@ -362,6 +403,13 @@ int rails_owner_exchange_layout(const rails_topo_t* topo, int32_t U, int32_t wor
 int rails_gather_rows_peer(const rails_topo_t* topo, int32_t U, int32_t g0, int32_t ng,
                            const int64_t* msg_loc, const rails_peer_t* peer, void* stream);
 int rails_peer_barrier(const rails_peer_t* peer, void* stream);
+/* Both for every rank driven by one process on one device (as
+ * rails_eval_finalize_peer_local): rank p holds source GPUs p*ng .. p*ng+ng-1
+ * (ng * world == N), msg_loc[p] is its [U][1][ng][G] rows; one cooperative launch. */
+int rails_gather_rows_peer_local(const rails_topo_t* topo, int32_t U, int32_t ng,
+                                 const int64_t* const* msg_loc, const rails_peer_t* peer,
+                                 void* stream);
+int rails_peer_barrier_local(const rails_peer_t* peer, void* stream);
 
 /* Inter-process rail buffers for rails_pack_owner (one process per GPU): the
  * owner allocates with rails_ipc_alloc (device memory of the current device, 256-B

@@ -237,6 +237,7 @@ def run_unit_matrix(M, N, C, R2, ecmp_seed, msg_unit):
         cs.append(s["chunks"]["size"]); cr.append(s["rail"])
     ev = eval_unit(M, N, R2, ecmp_seed, msg_unit, np.concatenate(cd), np.concatenate(chh),
                    np.concatenate(cs), np.concatenate(cr))
+    ev.update(eval_uniform(M, N, R2, msg_unit))  # the uniform P* = 1/N baseline (R#41)
     return scheds, ev
 
 

@@ -99,7 +99,7 @@ using namespace rails;
 
 extern "C" {
 
-int32_t rails_version(void) { return 100; }
+int32_t rails_version(void) { return 200; }
 
 const char* rails_last_error(void) { return t_err; }
 
@@ -159,7 +159,7 @@ int rails_schedule_workspace(const rails_topo_t* topo, const rails_shard_t* sh, 
   int rc = check_topo(topo);
   if (rc || (rc = check_shard(topo, sh))) return rc;
   if (!bytes) return fail(RAILS_EINVAL, "bytes is NULL");
-  *bytes = schedule_workspace_bytes(sh->U, sh->nd, (long long)topo->N * topo->M * topo->N);
+  *bytes = schedule_workspace_bytes(sh->U, sh->nd, topo->M, topo->N);
   return RAILS_OK;
 }
 
@@ -172,13 +172,13 @@ static int schedule_impl(const rails_topo_t* topo, const rails_shard_t* sh,
       !out->send_load || !out->n_full || !out->n_rem || !ws)
     return fail(RAILS_EINVAL, "NULL argument");
   if (!al(ws, 256)) return fail(RAILS_EINVAL, "workspace must be 256-byte aligned");
-  const size_t need =
-      schedule_workspace_bytes(sh->U, sh->nd, (long long)topo->N * topo->M * topo->N);
+  const size_t need = schedule_workspace_bytes(sh->U, sh->nd, topo->M, topo->N);
   if (ws_bytes < need) return fail(RAILS_ENOSPC, "workspace %zu < %zu bytes", ws_bytes, need);
   LaunchCtx c;
   if ((rc = ctx(stream, &c))) return rc;
-  return cuda_rc(launch_schedule(c, sh->U, sh->nd, sh->d0, topo->M, topo->N, topo->chunk_bytes,
-                                 msg_bytes, *out, ws, rem_qp, qps),
+  return cuda_rc(launch_node(c, sh->U, sh->nd, sh->d0, topo->M, topo->N, topo->chunk_bytes,
+                             topo->ecmp_seed, topo->R2, msg_bytes, *out, ws, rem_qp, qps, nullptr,
+                             nullptr, nullptr, nullptr, nullptr),
                  "rails_lpt_schedule launch");
 }
 
@@ -220,12 +220,16 @@ int rails_lpt_assign(int32_t N, int32_t n_seg, const int64_t* seg_off, int64_t F
                  "rails_lpt_assign launch");
 }
 
+static bool eval_ok(const rails_eval_t* e) {
+  return e && e->S && e->S_e && e->S_u && e->mse && e->nmse && e->red_sum && e->red_max;
+}
+
 int rails_eval(const rails_topo_t* topo, const rails_shard_t* sh, const int64_t* msg_bytes,
                const rails_sched_t* sched, const rails_eval_t* out, void* stream) {
   int rc = check_topo(topo);
   if (rc || (rc = check_shard(topo, sh))) return rc;
-  if (!msg_bytes || !sched || !sched->full_base || !sched->rem_rail || !out || !out->S ||
-      !out->S_e || !out->mse || !out->nmse || !out->red_sum || !out->red_max)
+  if (!msg_bytes || !sched || !sched->full_base || !sched->rem_rail || !sched->n_full ||
+      !eval_ok(out))
     return fail(RAILS_EINVAL, "NULL argument");
   LaunchCtx c;
   if ((rc = ctx(stream, &c))) return rc;
@@ -243,6 +247,41 @@ int rails_eval_finalize(const rails_topo_t* topo, int32_t U, const int64_t* red_
   if ((rc = ctx(stream, &c))) return rc;
   return cuda_rc(launch_finalize(c, U, topo->M, topo->N, topo->R2, red_sum, red_max, *out),
                  "rails_eval_finalize launch");
+}
+
+int rails_schedule_eval(const rails_topo_t* topo, const rails_shard_t* sh,
+                        const int64_t* msg_bytes, const rails_sched_t* sched,
+                        const rails_eval_t* ev, const rails_final_t* fin, int64_t* rail_base,
+                        int64_t* rail_total, void* ws, size_t ws_bytes, void* stream) {
+  int rc = check_topo(topo);
+  if (rc || (rc = check_shard(topo, sh))) return rc;
+  if (!msg_bytes || !sched || !sched->full_base || !sched->rem_rail || !sched->rem_off ||
+      !sched->send_load || !sched->n_full || !sched->n_rem || !ws || !eval_ok(ev))
+    return fail(RAILS_EINVAL, "NULL argument");
+  if (fin && (sh->d0 != 0 || sh->nd != topo->M))
+    return fail(RAILS_EINVAL, "final needs every node of the units (d0 = 0, nd = M); "
+                              "finalize after the a6 exchange instead");
+  if ((rail_base == nullptr) != (rail_total == nullptr))
+    return fail(RAILS_EINVAL, "rail_base and rail_total go together");
+  if (!al(ws, 256)) return fail(RAILS_EINVAL, "workspace must be 256-byte aligned");
+  const size_t need = schedule_workspace_bytes(sh->U, sh->nd, topo->M, topo->N);
+  if (ws_bytes < need) return fail(RAILS_ENOSPC, "workspace %zu < %zu bytes", ws_bytes, need);
+  LaunchCtx c;
+  if ((rc = ctx(stream, &c))) return rc;
+  bool fused = false;
+  cudaError_t e = launch_node(c, sh->U, sh->nd, sh->d0, topo->M, topo->N, topo->chunk_bytes,
+                              topo->ecmp_seed, topo->R2, msg_bytes, *sched, ws, nullptr, 0, ev,
+                              fin, rail_base, rail_total, &fused);
+  if (e == cudaSuccess && !fused) {  // node too large for the fused evaluation
+    e = launch_eval(c, sh->U, sh->nd, sh->d0, topo->M, topo->N, topo->chunk_bytes,
+                    topo->ecmp_seed, msg_bytes, *sched, *ev);
+    if (e == cudaSuccess && fin)
+      e = launch_finalize(c, sh->U, topo->M, topo->N, topo->R2, ev->red_sum, ev->red_max, *fin);
+    if (e == cudaSuccess && rail_base)
+      e = launch_rail_offsets(c, (long long)sh->U * sh->nd * topo->N, sched->send_load,
+                              rail_base, rail_total);
+  }
+  return cuda_rc(e, "rails_schedule_eval launch");
 }
 
 int rails_rail_offsets(const rails_topo_t* topo, const rails_shard_t* sh,
@@ -492,9 +531,25 @@ int rails_eval_finalize_peer(const rails_topo_t* topo, int32_t U, int64_t* red_s
   if ((rc = check_peer(peer))) return rc;
   LaunchCtx c;
   if ((rc = ctx(stream, &c))) return rc;
-  return cuda_rc(launch_finalize_peer(c, U, topo->M, topo->N, topo->R2, red_sum, red_max, *peer,
-                                      *out),
+  return cuda_rc(launch_finalize_peer(c, U, topo->M, topo->N, topo->R2, &red_sum, &red_max, *peer,
+                                      out, 1),
                  "rails_eval_finalize_peer launch");
+}
+
+int rails_eval_finalize_peer_local(const rails_topo_t* topo, int32_t U, int64_t* const* red_sum,
+                                   int64_t* const* red_max, const rails_peer_t* peer,
+                                   const rails_final_t* out, void* stream) {
+  int rc = check_topo(topo);
+  if (rc) return rc;
+  if ((rc = check_peer(peer))) return rc;
+  if (U < 1 || !red_sum || !red_max || !out) return fail(RAILS_EINVAL, "NULL argument");
+  for (int p = 0; p < peer->world; ++p)
+    if (!red_sum[p] || !red_max[p]) return fail(RAILS_EINVAL, "rank %d: NULL red_sum/red_max", p);
+  LaunchCtx c;
+  if ((rc = ctx(stream, &c))) return rc;
+  return cuda_rc(launch_finalize_peer(c, U, topo->M, topo->N, topo->R2, red_sum, red_max, *peer,
+                                      out, peer->world),
+                 "rails_eval_finalize_peer_local launch");
 }
 
 int rails_owner_exchange_layout(const rails_topo_t* topo, int32_t U, int32_t world,
@@ -516,9 +571,28 @@ int rails_gather_rows_peer(const rails_topo_t* topo, int32_t U, int32_t g0, int3
     return fail(RAILS_EINVAL, "bad arguments");
   LaunchCtx c;
   if ((rc = ctx(stream, &c))) return rc;
-  return cuda_rc(launch_gather_rows_peer(c, U, topo->N, (long long)topo->M * topo->N, g0, ng,
-                                         msg_loc, *peer),
+  return cuda_rc(launch_gather_rows_peer(c, U, topo->N, (long long)topo->M * topo->N, ng,
+                                         &msg_loc, &g0, *peer, 1),
                  "rails_gather_rows_peer launch");
+}
+
+int rails_gather_rows_peer_local(const rails_topo_t* topo, int32_t U, int32_t ng,
+                                 const int64_t* const* msg_loc, const rails_peer_t* peer,
+                                 void* stream) {
+  int rc = check_topo(topo);
+  if (rc || (rc = check_peer(peer))) return rc;
+  if (U < 1 || !msg_loc || ng < 1 || (long long)ng * peer->world != topo->N)
+    return fail(RAILS_EINVAL, "need ng * world == N");
+  int g0[RAILS_PEER_MAX];
+  for (int p = 0; p < peer->world; ++p) {
+    if (!msg_loc[p]) return fail(RAILS_EINVAL, "rank %d: NULL msg_loc", p);
+    g0[p] = p * ng;
+  }
+  LaunchCtx c;
+  if ((rc = ctx(stream, &c))) return rc;
+  return cuda_rc(launch_gather_rows_peer(c, U, topo->N, (long long)topo->M * topo->N, ng, msg_loc,
+                                         g0, *peer, peer->world),
+                 "rails_gather_rows_peer_local launch");
 }
 
 int rails_peer_barrier(const rails_peer_t* peer, void* stream) {
@@ -526,7 +600,15 @@ int rails_peer_barrier(const rails_peer_t* peer, void* stream) {
   if (rc) return rc;
   LaunchCtx c;
   if ((rc = ctx(stream, &c))) return rc;
-  return cuda_rc(launch_peer_barrier(c, *peer), "rails_peer_barrier launch");
+  return cuda_rc(launch_peer_barrier(c, *peer, 1), "rails_peer_barrier launch");
+}
+
+int rails_peer_barrier_local(const rails_peer_t* peer, void* stream) {
+  int rc = check_peer(peer);
+  if (rc) return rc;
+  LaunchCtx c;
+  if ((rc = ctx(stream, &c))) return rc;
+  return cuda_rc(launch_peer_barrier(c, *peer, peer->world), "rails_peer_barrier_local launch");
 }
 
 static int check_fabric(const rails_topo_t* topo, const rails_fabric_t* fb) {

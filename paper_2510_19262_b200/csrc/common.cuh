@@ -201,10 +201,12 @@ cudaError_t launch_histogram(const LaunchCtx&, int U, int nd, int d0, int M, int
                              long long row_bytes, int32_t* counts, int64_t* msg,
                              int32_t* rank);
 
-size_t schedule_workspace_bytes(int U, int nd, long long NG);
-cudaError_t launch_schedule(const LaunchCtx&, int U, int nd, int d0, int M, int N, long long C,
-                            const int64_t* msg, const rails_sched_t& s, void* ws,
-                            int32_t* rem_qp, int qps_per_rail);
+size_t schedule_workspace_bytes(int U, int nd, int M, int N);
+cudaError_t launch_node(const LaunchCtx&, int U, int nd, int d0, int M, int N, long long C,
+                        uint64_t seed, double R2, const int64_t* msg, const rails_sched_t& s,
+                        void* ws, int32_t* rem_qp, int qps_per_rail, const rails_eval_t* ev,
+                        const rails_final_t* fin, int64_t* rail_base, int64_t* rail_total,
+                        bool* fused);
 
 size_t assign_workspace_bytes(int n_seg, long long F);
 cudaError_t launch_assign(const LaunchCtx&, int N, int n_seg, const int64_t* seg_off,
@@ -221,12 +223,13 @@ cudaError_t launch_finalize(const LaunchCtx&, int U, int M, int N, double R2,
 size_t peer_buffer_bytes(int U, int world, long long rsl);
 void owner_exchange_layout(int U, int world, long long N, long long G, size_t* bytes,
                            size_t* gflag_off, size_t* msg_off);
-cudaError_t launch_gather_rows_peer(const LaunchCtx&, int U, int N, long long G, int g0, int ng,
-                                    const int64_t* msg_loc, const rails_peer_t& peer);
-cudaError_t launch_peer_barrier(const LaunchCtx&, const rails_peer_t& peer);
+cudaError_t launch_gather_rows_peer(const LaunchCtx&, int U, int N, long long G, int ng,
+                                    const int64_t* const* msg_loc, const int* g0,
+                                    const rails_peer_t& peer, int nplay);
+cudaError_t launch_peer_barrier(const LaunchCtx&, const rails_peer_t& peer, int nplay);
 cudaError_t launch_finalize_peer(const LaunchCtx&, int U, int M, int N, double R2,
-                                 int64_t* red_sum, int64_t* red_max, const rails_peer_t& peer,
-                                 const rails_final_t& f);
+                                 int64_t* const* red_sum, int64_t* const* red_max,
+                                 const rails_peer_t& peer, const rails_final_t* f, int nplay);
 
 cudaError_t launch_rail_offsets(const LaunchCtx&, long long n, const int64_t* send_load,
                                 int64_t* rail_base, int64_t* total);

@@ -868,7 +868,7 @@ size_t flowsim_workspace_bytes(const rails_topo_t& tp, const rails_fabric_t& fb,
                                long long capF, long long capS) {
   const FsTopo t = fs_topo(tp, fb);
   const FsLayout lo = fs_layout(t.Q, t.L, capF, capS);
-  const size_t sched = schedule_workspace_bytes(n_sim, tp.M, (long long)tp.N * t.G);
+  const size_t sched = schedule_workspace_bytes(n_sim, tp.M, tp.M, tp.N);
   const size_t sarr = al256((size_t)n_sim * t.Q * 8) + al256((size_t)n_sim * t.Q) +
                       al256((size_t)n_sim * t.Q * 8) + al256((size_t)n_sim * tp.M * tp.N * 8) +
                       al256((size_t)n_sim * tp.M * 8) + al256((size_t)n_sim * tp.M * 4);
@@ -903,7 +903,7 @@ cudaError_t launch_flowsim(const LaunchCtx& c, const rails_topo_t& tp, const rai
   uint8_t* base = (uint8_t*)ws_ + 256;
   uint8_t* sims = base;
   uint8_t* schw = sims + lay.stride * (size_t)n_sim;
-  const size_t schb = al256(schedule_workspace_bytes(n_sim, tp.M, (long long)tp.N * t.G));
+  const size_t schb = al256(schedule_workspace_bytes(n_sim, tp.M, tp.M, tp.N));
   uint8_t* sa = schw + schb;
   rails_sched_t s;
   s.full_base = (int64_t*)sa;
@@ -919,8 +919,9 @@ cudaError_t launch_flowsim(const LaunchCtx& c, const rails_topo_t& tp, const rai
   s.n_rem = (int32_t*)sa;
   cudaError_t e;
   // the LPT schedule of every (simulation, node); only LPT simulations use it
-  if ((e = launch_schedule(c, n_sim, tp.M, 0, tp.M, tp.N, tp.chunk_bytes, msg, s, schw,
-                           nullptr, 0)) != cudaSuccess)
+  if ((e = launch_node(c, n_sim, tp.M, 0, tp.M, tp.N, tp.chunk_bytes, tp.ecmp_seed, tp.R2, msg,
+                       s, schw, nullptr, 0, nullptr, nullptr, nullptr, nullptr, nullptr)) !=
+      cudaSuccess)
     return e;
   k_fs_count<<<n_sim, FS_THREADS, 0, c.stream>>>(t, policy, msg, sims, o, lay.stride, nullptr, 0,
                                                  c.err);

@@ -1,0 +1,585 @@
+// k_node.cu -- a2-a5 fused: one CTA per (unit, node) computes the node's compact
+// LPT schedule and its evaluation in ONE kernel (sm_100a).
+//
+// a2 (R#3): message B of (g,h) -> floor(B/C) full chunks + one remainder of
+//    B mod C bytes.  Full chunks are never materialised: every full chunk (size C)
+//    is larger than every remainder (< C) and full chunks are emitted in (g,h,c)
+//    order, so under Alg. 2's sort (size desc, ties by GPU index, R#4) they form
+//    the prefix of the sorted list in emission order, and LPT from all-zero loads
+//     deals them round-robin: full chunk i -> rail i mod N at offset
+//    floor(i/N)*C (lowest-index argmin, R#5).  Phase A writes full_base = exclusive
+//    prefix of floor(B/C) in (g,h) order (one block scan per tile of messages) and
+//    compacts the remainders (at most one per message) in (g,h) order.
+// a3: phase B sorts the remainders by size descending with a stable
+//    LSD radix sort on key = C-1-size (constant digits skipped); stability keeps
+//    (g,h) order among equal sizes = the tie-break R#4.  In shared memory when the
+//    node fits (N*G <= 16384), else in a global scratch.
+// a4: phase C, warp 0 runs the serial chain (lpt.cuh) over the sorted
+//    list; results land in sorted order (shared memory when they fit).  Phase D
+//    expands them to per-message rem_rail / rem_off through the sort's inverse
+//    permutation (and the QP map of Alg. 2 step 4, R#34, when asked).
+// a5 (EVAL): while warp 0 runs the chain, the other warps add the full chunks into
+//    R_d[f][j] by the closed form (message block (g, f*N..f*N+N-1) holds the
+//    node-global full chunks [P_gf, P_g,f+1); rail j receives cnt_j(b) - cnt_j(a),
+//    cnt_j(x) = floor(x/N) + (j < x mod N)); phase A already added the ECMP bytes
+//    (R#13-R#14) and the uniform split (R#41) per destination node; phase D adds
+//    the remainders.  S[d] is the chain's LoadState (Eq. 4); R_d is added into a
+//    per-unit accumulator (int64 atomics: exact, order-free); MSE/nMSE as Eq. 6.
+//    The last CTA of a unit to arrive (arrival counter) moves the accumulator into
+//    red_sum / red_max, re-zeroes it, and -- when the call holds every node of the
+//    unit -- finalizes T, T*, busbw (Thm 2 + 3); the last CTA of the
+//    grid computes the rail offsets.  So a whole single-rank schedule + evaluation
+//    is one launch, and the workspace is left zeroed for the next call.
+#include "common.cuh"
+#include "eval.cuh"
+#include "lpt.cuh"
+#include "radix.cuh"
+
+namespace rails {
+
+constexpr int NODE_MAX_THREADS = 512;
+constexpr long long NODE_SMEM_ITEMS = 16384;  // N*G kept in shared memory
+
+struct NodeArgs {
+  const int64_t* msg;
+  long long NG;
+  int M, N, d0, nd, U;
+  long long C;
+  int cshift, nbits;
+  uint64_t seed;
+  double R2;
+  rails_sched_t s;
+  int32_t* rem_qp;
+  int Q;
+  uint64_t* res_g;     // [nseg][NG] chain results when not in shared memory
+  uint32_t* qp_g;      // [nseg][NG] QP of each sorted remainder (QP map only)
+  uint8_t* scratch;    // sort buffers when !SMEM
+  rails_eval_t e;
+  int64_t* acc;        // [U][rsl + RAILS_RED_MAX_LEN], zero between calls
+  unsigned* cnt;       // [U + 1] arrival counters, zero between calls
+  rails_final_t fin;
+  int do_final;
+  int64_t* rail_base;
+  int64_t* rail_total;
+  size_t res_off;      // byte offset of the shared result buffer (res_smem)
+  size_t ev_off;       // byte offset of the eval arrays in shared memory
+  int res_smem;        // chain results in shared memory, else res_g
+  int* err;
+};
+
+// Alg. 2 step 4 (R#34): per-rail round-robin QP index in assignment
+// order.  The chain results are in sorted (= assignment) order, so the QP of the
+// p-th remainder is (full chunks on its rail + remainders on its rail before p) mod
+// Q, full chunks being assigned first (i mod N).  Warp w owns a contiguous slice:
+// pass 1 counts the slice's items per rail; the per-warp starting counters are an
+// exclusive scan over warps (plus rail j's full chunks); pass 2 ranks each 32-item
+// batch by rail with a ballot multi-split and advances the counters.
+__device__ void qp_rank_block(int N, int Q, long long nf, int nr, const uint64_t* res,
+                              uint32_t* out) {
+  __shared__ unsigned cnt[NODE_MAX_THREADS / 32][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, W = blockDim.x >> 5;
+  const int per = (((nr + W - 1) / W) + 31) & ~31;
+  const int beg = wid * per, end = min(nr, beg + per);
+  const unsigned lt = lanemask_lt();
+  cnt[wid][lane] = 0;
+  __syncwarp();
+  for (int p0 = beg; p0 < end; p0 += 32) {
+    const int p = p0 + lane;
+    const unsigned r = p < end ? (unsigned)(res[p] >> 56) : 0u;
+    const unsigned peers = warp_match_nb<5>(r, p < end);
+    if (p < end && (peers & lt) == 0) cnt[wid][r] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  const unsigned q = (unsigned)Q;
+  if (threadIdx.x < 32) {  // counters are kept modulo Q from here on (32-bit math)
+    const int j = threadIdx.x;
+    unsigned run = (unsigned)((nf / N + ((long long)j < nf % N ? 1 : 0)) % Q);
+    for (int w = 0; w < W; ++w) {
+      const unsigned c = cnt[w][j] % q;
+      cnt[w][j] = run;
+      run = (run + c) % q;
+    }
+  }
+  __syncthreads();
+  for (int p0 = beg; p0 < end; p0 += 32) {
+    const int p = p0 + lane;
+    const unsigned r = p < end ? (unsigned)(res[p] >> 56) : 0u;
+    const unsigned peers = warp_match_nb<5>(r, p < end);
+    if (p < end) out[p] = (cnt[wid][r] + __popc(peers & lt)) % q;
+    __syncwarp();
+    if (p < end && (peers & lt) == 0) cnt[wid][r] = (cnt[wid][r] + __popc(peers)) % q;
+    __syncwarp();
+  }
+  __syncthreads();
+}
+
+// number of the node-global full chunks 0..x-1 that land on rail j (i mod N == j)
+__device__ __forceinline__ long long full_on_rail(long long x, int N, int j) {
+  long long q;
+  int r;
+  divmod_n(x, N, q, r);
+  return q + (j < r ? 1 : 0);
+}
+
+template <typename KeyT, int NT, bool SMEM, bool EVAL>
+__global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
+  using IdxT = typename std::conditional<SMEM, uint16_t, uint32_t>::type;
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ long long scan_scratch[33];
+  __shared__ int hist[(NODE_MAX_THREADS / 32) * 256];
+  __shared__ int sc[256];
+  __shared__ uint32_t red32[32];
+  __shared__ long long sL[32], sSe[32], sSu[32];
+  __shared__ int s_last;
+
+  const long long seg = blockIdx.x;
+  const long long NG = a.NG;
+  const int N = NT ? NT : a.N;
+  const int M = a.M;
+  const long long C = a.C;
+  const ChunkDiv cd{C, a.cshift};
+  const int64_t* __restrict__ mg = a.msg + seg * NG;
+  const long long G = NG / N;
+  const long long u = seg / a.nd;
+  const int d = a.d0 + (int)(seg % a.nd);
+  const long long MN = (long long)M * N;
+
+  KeyT *kA, *kB;
+  IdxT *iA, *iB;
+  {
+    uint8_t* base;
+    if constexpr (SMEM) base = smem;
+    else base = a.scratch + seg * (NG * (2 * sizeof(KeyT) + 2 * sizeof(IdxT)) + 64);
+    kA = (KeyT*)base;
+    kB = kA + NG;
+    iA = (IdxT*)(kB + NG);
+    iB = iA + NG;
+  }
+  // eval arrays (EVAL): block starts P[G+1] (int64), then u32 arrays of MN:
+  // R lo/hi (full chunks + remainders), ECMP lo/hi, uniform remainder histogram
+  // cU[f][r]; then uniform quotient sums lo/hi per destination node [M]
+  long long* sP = nullptr;
+  unsigned *aRlo = nullptr, *aRhi = nullptr, *aElo = nullptr, *aEhi = nullptr, *cU = nullptr,
+           *aQlo = nullptr, *aQhi = nullptr;
+  if constexpr (EVAL) {
+    sP = (long long*)(smem + a.ev_off);
+    aRlo = (unsigned*)(sP + G + 1);
+    aRhi = aRlo + MN;
+    aElo = aRhi + MN;
+    aEhi = aElo + MN;
+    cU = aEhi + MN;
+    aQlo = cU + MN;
+    aQhi = aQlo + M;
+    for (long long i = threadIdx.x; i < MN; i += blockDim.x) aElo[i] = aEhi[i] = cU[i] = 0u;
+    for (int i = threadIdx.x; i < M; i += blockDim.x) aQlo[i] = aQhi[i] = 0u;
+    __syncthreads();
+  }
+
+  // ---- phase A: full_base scan + remainder compaction (+ ECMP and uniform sums)
+  // Tiles of blockDim * IPT messages, each thread owning IPT consecutive messages:
+  // its loads are all in flight at once, one block scan per tile.
+  constexpr int IPT = 8;
+  long long carry_full = 0;
+  int carry_rem = 0;
+  KeyT kor = 0, kand = (KeyT)~(KeyT)0;
+  const int lo = d * N, hi = d * N + N;  // the source node's own GPUs (R#2)
+  for (long long t0 = 0; t0 < NG; t0 += (long long)blockDim.x * IPT) {
+    const long long m0 = t0 + (long long)threadIdx.x * IPT;
+    long long B[IPT];
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) B[j] = m0 + j < NG ? mg[m0 + j] : 0;
+    long long snf = 0;
+    int srem = 0;
+    long long nfv[IPT];
+    // destination GPU h = m mod G and source GPU g = m div G of the first item, then
+    // stepped (one division per thread and tile instead of one per message)
+    const int h0 = (int)((unsigned long long)m0 % (unsigned long long)G);
+    const int g0 = (int)((unsigned long long)m0 / (unsigned long long)G);
+    int h = h0;
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+      // negative bytes, or bytes to a GPU of the source node (R#2), are invalid
+      if (B[j] < 0 || (B[j] != 0 && h >= lo && h < hi)) {
+        flag_error(a.err, ERR_RANGE);
+        B[j] = 0;
+      }
+      if (++h >= G) h -= (int)G;
+      nfv[j] = cd.div(B[j]);
+      if (nfv[j] >= (1LL << 40)) flag_error(a.err, ERR_OVERFLOW);
+      snf += nfv[j];
+      srem += (B[j] - nfv[j] * C) > 0;
+    }
+    long long tot;
+    const long long ex = block_excl_scan((snf << 16) | srem, scan_scratch, &tot);
+    long long fb = carry_full + (ex >> 16);
+    int pos = carry_rem + (int)(ex & 0xffff);
+    h = h0;
+    int g = g0;
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+      const long long m = m0 + j;
+      if (m >= NG) break;
+      const long long nf = nfv[j];
+      const long long rem = B[j] - nf * C;
+      a.s.full_base[seg * NG + m] = fb;
+      if constexpr (EVAL) {
+        if (h % N == 0) sP[m / N] = fb;  // block (g, f = h/N) starts here
+        if (B[j] > 0) {
+          const int f = h / N;
+          const int e = ecmp_rail(a.seed, (long long)d * N + g, h, N);
+          add64_split(&aElo[f * N + e], &aEhi[f * N + e], (unsigned long long)B[j]);
+          long long qb;
+          int rb;
+          divmod_n(B[j], N, qb, rb);
+          if (qb) add64_split(&aQlo[f], &aQhi[f], (unsigned long long)qb);
+          if (rb) atomicAdd(&cU[f * N + rb], 1u);
+        }
+      }
+      fb += nf;
+      if (rem > 0) {
+        const KeyT key = (KeyT)(C - 1 - rem);
+        kA[pos] = key;
+        iA[pos] = (IdxT)m;
+        kor |= key;
+        kand &= key;
+        ++pos;
+      }
+      if (++h >= G) {
+        h -= (int)G;
+        ++g;
+      }
+    }
+    carry_full += tot >> 16;
+    carry_rem += (int)(tot & 0xffff);
+  }
+  kor = (KeyT)block_reduce_or((uint32_t)kor, red32);
+  kand = (KeyT)block_reduce_and((uint32_t)kand, red32);
+  const long long nf_node = carry_full;
+  const int n = carry_rem;
+  if (threadIdx.x == 0) {
+    a.s.n_full[seg] = nf_node;
+    a.s.n_rem[seg] = n;
+    if constexpr (EVAL) sP[G] = nf_node;
+  }
+  __syncthreads();
+
+  // ---- phase B: stable radix sort of the remainder keys
+  const int which = radix_sort<KeyT, IdxT>(kA, iA, kB, iB, n, kor, kand, a.nbits, hist, sc);
+  const KeyT* ks = which ? kB : kA;
+  const IdxT* is = which ? iB : iA;
+  IdxT* inv = which ? iA : iB;  // inverse permutation: message -> sorted position
+  constexpr IdxT NONE = (IdxT)~(IdxT)0;
+  for (long long m = threadIdx.x; m < NG; m += blockDim.x) inv[m] = NONE;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) inv[is[i]] = (IdxT)i;
+
+  // ---- phase C: warp 0 runs the LPT chain; the other warps add the full chunks
+  uint64_t* res = a.res_smem ? (uint64_t*)(smem + a.res_off) : a.res_g + seg * NG;
+  if (threadIdx.x < 32) {
+    if constexpr (NT != 0) {
+      lpt_chain_net<NT, KeyT>(ks, n, C, nf_node, res, sL);
+    } else {
+      const long long L = lpt_chain_generic<KeyT>(ks, n, N, C, nf_node, res, a.err);
+      if (threadIdx.x < N) sL[threadIdx.x] = L;
+    }
+    __syncwarp();
+    if (threadIdx.x < N) a.s.send_load[seg * N + threadIdx.x] = sL[threadIdx.x];
+  } else if constexpr (EVAL) {
+    for (long long t = threadIdx.x - 32; t < MN; t += blockDim.x - 32) {
+      const int f = (int)(t / N), j = (int)(t - (long long)f * N);
+      long long full = 0;
+      if (f != d) {
+        for (int g = 0; g < N; ++g) {
+          const long long pa = sP[(long long)g * M + f], pb = sP[(long long)g * M + f + 1];
+          full += full_on_rail(pb, N, j) - full_on_rail(pa, N, j);
+        }
+      }
+      const unsigned long long v = (unsigned long long)(full * C);
+      aRlo[t] = (unsigned)v;
+      aRhi[t] = (unsigned)(v >> 32);
+    }
+  }
+  __syncthreads();
+
+  // ---- phase D: QP map (optional), expand, remainders into R_d
+  if (a.rem_qp) qp_rank_block(N, a.Q, nf_node, n, res, a.qp_g + seg * NG);
+  for (long long m = threadIdx.x; m < NG; m += blockDim.x) {
+    const IdxT p = inv[m];
+    int8_t r = -1;
+    long long o = 0;
+    int32_t q = -1;
+    if (p != NONE) {
+      const uint64_t v = res[p];
+      r = (int8_t)(v >> 56);
+      o = (long long)(v & (uint64_t)OFF_MASK);
+      if (a.rem_qp) q = (int32_t)a.qp_g[seg * NG + p];
+      if constexpr (EVAL) {
+        const int f = (int)((m % G) / N);
+        add64_split(&aRlo[f * N + r], &aRhi[f * N + r],
+                    (unsigned long long)(C - 1 - (long long)ks[p]));
+      }
+    }
+    a.s.rem_rail[seg * NG + m] = r;
+    a.s.rem_off[seg * NG + m] = o;
+    if (a.rem_qp) a.rem_qp[seg * NG + m] = q;
+  }
+  if constexpr (!EVAL) return;
+
+  // ---- phase E: this node's receive contributions into the unit's accumulator
+  __syncthreads();
+  const long long rsl = RAILS_RED_SUM_LEN(M, N);
+  const long long rec = rsl + RAILS_RED_MAX_LEN;
+  const RedLayout RL{MN, M};
+  unsigned long long* acc = (unsigned long long*)(a.acc + u * rec);
+  for (long long t = threadIdx.x; t < MN; t += blockDim.x) {
+    const int f = (int)(t / N), j = (int)(t - (long long)f * N);
+    const unsigned long long R = ((unsigned long long)aRhi[t] << 32) | aRlo[t];
+    const unsigned long long Re = ((unsigned long long)aEhi[t] << 32) | aElo[t];
+    unsigned long long Ru = ((unsigned long long)aQhi[f] << 32) | aQlo[f];
+    for (int r = j + 1; r < N; ++r) Ru += cU[(long long)f * N + r];
+    if (R) atomicAdd(acc + RL.R() + t, R);
+    if (Re) atomicAdd(acc + RL.Re() + t, Re);
+    if (Ru) atomicAdd(acc + RL.Ru() + t, Ru);
+  }
+  for (int f = threadIdx.x; f < M; f += blockDim.x) {
+    unsigned long long cf = 0;
+    for (int j = 0; j < N; ++j)
+      cf += ((unsigned long long)aRhi[(long long)f * N + j] << 32) | aRlo[(long long)f * N + j];
+    if (cf) atomicAdd(acc + RL.col() + f, cf);
+  }
+  if (threadIdx.x < N) {  // S_e, S_u of this node per rail j
+    const int j = threadIdx.x;
+    unsigned long long se = 0, su = 0;
+    for (int f = 0; f < M; ++f) {
+      se += ((unsigned long long)aEhi[(long long)f * N + j] << 32) | aElo[(long long)f * N + j];
+      su += ((unsigned long long)aQhi[f] << 32) | aQlo[f];
+      for (int r = j + 1; r < N; ++r) su += cU[(long long)f * N + r];
+    }
+    sSe[j] = (long long)se;
+    sSu[j] = (long long)su;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    const long long s = lane < N ? sL[lane] : 0, se = lane < N ? sSe[lane] : 0,
+                    su = lane < N ? sSu[lane] : 0;
+    if (lane < N) {
+      a.e.S[seg * N + lane] = s;
+      a.e.S_e[seg * N + lane] = se;
+      a.e.S_u[seg * N + lane] = su;
+    }
+    const long long total = warp_sum(s), total_e = warp_sum(se);
+    const long long mx = warp_max(s), mxe = warp_max(se), mxu = warp_max(su);
+    double mse, nmse;
+    warp_mse(s, N, total, &mse, &nmse);
+    if (lane == 0) {
+      a.e.mse[seg] = mse;
+      a.e.nmse[seg] = nmse;
+      if (total) atomicAdd(acc + RL.tot(), (unsigned long long)total);
+      if (total_e) atomicAdd(acc + RL.tot() + 1, (unsigned long long)total_e);
+      long long* am = (long long*)acc + rsl;
+      atomicMax(am + RMAX_S, mx);
+      atomicMax(am + RMAX_SE, mxe);
+      atomicMax(am + RMAX_ROW, total);  // row sum of node d = its inter-node bytes
+      atomicMax(am + RMAX_SU, mxu);
+    }
+  }
+
+  // ---- phase F: the unit's last CTA publishes (and finalizes); the grid's last
+  // CTA computes the rail offsets
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&a.cnt[u], 1u) == (unsigned)(a.nd - 1);
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    int64_t* rs = a.e.red_sum + u * rsl;
+    int64_t* rm = a.e.red_max + u * RAILS_RED_MAX_LEN;
+    for (long long i = threadIdx.x; i < rec; i += blockDim.x) {
+      const long long v = (long long)__ldcg((const long long*)acc + i);
+      if (i < rsl) rs[i] = v;
+      else rm[i - rsl] = v;
+      acc[i] = 0;
+    }
+    if (threadIdx.x == 0) a.cnt[u] = 0;
+    __syncthreads();
+    if (a.do_final) block_finalize_unit<false>(u, M, N, a.R2, rs, rm, a.fin);
+  }
+  if (a.rail_base) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      s_last = atomicAdd(&a.cnt[a.U], 1u) == (unsigned)(gridDim.x - 1);
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      block_rail_offsets<true>((long long)gridDim.x * N, a.s.send_load, a.rail_base,
+                               a.rail_total);
+      if (threadIdx.x == 0) a.cnt[a.U] = 0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- host side
+static int ceil_log2(long long x) {  // bits needed for values 0..x-1
+  int b = 0;
+  while ((1LL << b) < x) ++b;
+  return b;
+}
+
+struct NodePlan {
+  bool smem_sort, k16, res_smem, eval_fused;
+  int threads;
+  size_t sort_bytes, res_off, ev_off, smem;
+};
+
+// Shared-memory plan of the fused kernel for N*G messages per node.
+static NodePlan node_plan(int M, int N, long long C, bool eval) {
+  const long long G = (long long)M * N, NG = (long long)N * G;
+  NodePlan p{};
+  constexpr size_t DYN_LIMIT = 200 * 1024;  // + ~20 KiB static stays under 227 KiB
+  const size_t ev_bytes = (size_t)(G + 1) * 8 + (size_t)G * 4 * 5 + (size_t)M * 8;
+  p.eval_fused = eval && ev_bytes <= 96 * 1024;
+  const bool k16 = C <= 65536;
+  const size_t sort_smem = (size_t)NG * 2 * ((k16 ? 2 : 4) + 2);
+  p.smem_sort = NG <= NODE_SMEM_ITEMS &&
+                sort_smem + (p.eval_fused ? ev_bytes + 32 : 0) <= DYN_LIMIT;
+  p.k16 = p.smem_sort && k16;
+  p.threads = NG <= 1024 ? 128 : (NG <= 8192 ? 256 : NODE_MAX_THREADS);
+  p.sort_bytes = p.smem_sort ? sort_smem : 0;
+  size_t off = (p.sort_bytes + 15) & ~(size_t)15;
+  if (p.eval_fused) {
+    p.ev_off = off;
+    off = (off + ev_bytes + 15) & ~(size_t)15;
+  }
+  // chain results in shared memory when the CTA still fits twice per SM
+  const size_t res_bytes = (size_t)NG * 8;
+  p.res_smem = off + res_bytes <= 110 * 1024;
+  if (p.res_smem) {
+    p.res_off = off;
+    off += res_bytes;
+  }
+  p.smem = off;
+  if (p.smem < 16) p.smem = 16;
+  return p;
+}
+
+// workspace: [256 B header][acc: U x rec int64][counters: U + 1 u32, 256-aligned]
+//            [res_g u64: nseg x NG][qp_g u32: nseg x NG][sort spill when N*G > 16384]
+static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct NodeWs {
+  int64_t* acc;
+  unsigned* cnt;
+  uint64_t* res_g;
+  uint32_t* qp_g;
+  uint8_t* scratch;
+  size_t bytes;
+};
+
+static NodeWs node_ws(void* ws, int U, int nd, int M, int N) {
+  const long long NG = (long long)N * M * N, nseg = (long long)U * nd;
+  const long long rec = RAILS_RED_SUM_LEN(M, N) + RAILS_RED_MAX_LEN;
+  uint8_t* b = (uint8_t*)ws;
+  NodeWs w{};
+  size_t o = 256;
+  w.acc = (int64_t*)(b + o);
+  o = al256(o + (size_t)U * rec * 8);
+  w.cnt = (unsigned*)(b + o);
+  o = al256(o + (size_t)(U + 1) * 4);
+  w.res_g = (uint64_t*)(b + o);
+  o = al256(o + (size_t)nseg * NG * 8);
+  w.qp_g = (uint32_t*)(b + o);
+  o = al256(o + (size_t)nseg * NG * 4);
+  w.scratch = b + o;
+  if (NG > NODE_SMEM_ITEMS / 4) o += (size_t)nseg * (NG * (2 * 4 + 2 * 4) + 64);
+  w.bytes = o;
+  return w;
+}
+
+size_t schedule_workspace_bytes(int U, int nd, int M, int N) {
+  return node_ws(nullptr, U, nd, M, N).bytes;
+}
+
+template <typename KeyT, int NT, bool SMEM, bool EVAL>
+static cudaError_t launch_k(const LaunchCtx& c, const NodePlan& p, unsigned grid,
+                            const NodeArgs& a) {
+  auto kern = k_node<KeyT, NT, SMEM, EVAL>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)p.smem);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, p.threads, p.smem, c.stream>>>(a);
+  count_launch(1);
+  return cudaGetLastError();
+}
+
+template <bool EVAL>
+static cudaError_t launch_eval_t(const LaunchCtx& c, const NodePlan& p, unsigned grid,
+                                 const NodeArgs& a, int N) {
+  const bool net = N == 8 && a.C < (1LL << 23);
+  if (p.smem_sort) {
+    if (p.k16)
+      return net ? launch_k<uint16_t, 8, true, EVAL>(c, p, grid, a)
+                 : launch_k<uint16_t, 0, true, EVAL>(c, p, grid, a);
+    return net ? launch_k<uint32_t, 8, true, EVAL>(c, p, grid, a)
+               : launch_k<uint32_t, 0, true, EVAL>(c, p, grid, a);
+  }
+  return net ? launch_k<uint32_t, 8, false, EVAL>(c, p, grid, a)
+             : launch_k<uint32_t, 0, false, EVAL>(c, p, grid, a);
+}
+
+// rails_lpt_schedule[_qp] (ev == nullptr) and rails_schedule_eval.  Returns
+// *fused = false when the evaluation could not be fused (the caller then runs
+// rails_eval's kernel).
+cudaError_t launch_node(const LaunchCtx& c, int U, int nd, int d0, int M, int N, long long C,
+                        uint64_t seed, double R2, const int64_t* msg, const rails_sched_t& s,
+                        void* ws, int32_t* rem_qp, int qps_per_rail, const rails_eval_t* ev,
+                        const rails_final_t* fin, int64_t* rail_base, int64_t* rail_total,
+                        bool* fused) {
+  const long long NG = (long long)N * M * N, nseg = (long long)U * nd;
+  NodePlan p = node_plan(M, N, C, ev != nullptr);
+  if (fused) *fused = p.eval_fused;
+  const NodeWs w = node_ws(ws, U, nd, M, N);
+  NodeArgs a{};
+  a.msg = msg;
+  a.NG = NG;
+  a.M = M;
+  a.N = N;
+  a.d0 = d0;
+  a.nd = nd;
+  a.U = U;
+  a.C = C;
+  a.cshift = (C & (C - 1)) == 0 ? ceil_log2(C) : -1;
+  a.nbits = ceil_log2(C > 1 ? C - 1 : 1) + 1;
+  a.seed = seed;
+  a.R2 = R2;
+  a.s = s;
+  a.rem_qp = rem_qp;
+  a.Q = qps_per_rail;
+  a.res_g = w.res_g;
+  a.qp_g = w.qp_g;
+  a.scratch = w.scratch;
+  a.acc = w.acc;
+  a.cnt = w.cnt;
+  a.res_off = p.res_off;
+  a.res_smem = p.res_smem ? 1 : 0;
+  a.ev_off = p.ev_off;
+  a.err = c.err;
+  if (p.eval_fused) {
+    a.e = *ev;
+    if (fin) {
+      a.fin = *fin;
+      a.do_final = 1;
+    }
+    a.rail_base = rail_base;
+    a.rail_total = rail_total;
+    return launch_eval_t<true>(c, p, (unsigned)nseg, a, N);
+  }
+  return launch_eval_t<false>(c, p, (unsigned)nseg, a, N);
+}
+
+}  // namespace rails

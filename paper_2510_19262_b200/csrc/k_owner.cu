@@ -290,16 +290,24 @@ void owner_exchange_layout(int U, int world, long long N, long long G, size_t* b
   *bytes = *msg_off + (size_t)U * N * G * 8;
 }
 
-// One CTA per unit: this rank's message rows (source GPUs g0..g0+ng-1) go into
-// every rank's msg_node (NVLink stores), then a per-(unit, rank) flag; the CTA
-// returns when every rank's rows of the unit have arrived here.
+// One CTA per (unit, played rank p): rank p's message rows (source GPUs g0[p] ..
+// g0[p]+ng-1) go into every rank's msg_node (NVLink stores), then a per-(unit,
+// rank) flag; the CTA returns when every rank's rows of the unit have arrived at
+// rank p.  One played rank in the one-process-per-rank launch; every rank in the
+// cooperative single-process launch (rails_gather_rows_peer_local).
+struct RowSrc {
+  const int64_t* msg_loc[RAILS_PEER_MAX];
+  int g0[RAILS_PEER_MAX];
+};
+
 __global__ void __launch_bounds__(256)
-    k_gather_rows_peer(int U, int N, long long G, int g0, int ng,
-                       const int64_t* __restrict__ msg_loc, PeerBase pb, int rank, int world,
-                       uint32_t gen, size_t gflag_off, size_t msg_off, int* err) {
+    k_gather_rows_peer(int U, int N, long long G, int ng, RowSrc rsrc, PeerBase pb, int rank0,
+                       int world, uint32_t gen, size_t gflag_off, size_t msg_off, int* err) {
   const long long u = blockIdx.x;
+  const int rank = rank0 + (int)blockIdx.y;
+  const int g0 = rsrc.g0[blockIdx.y];
   const long long n = (long long)ng * G;  // int64 per unit and rank
-  const int64_t* src = msg_loc + u * n;
+  const int64_t* src = rsrc.msg_loc[blockIdx.y] + u * n;
   for (int p = 0; p < world; ++p) {
     int64_t* dst = (int64_t*)(pb.p[p] + msg_off) + (u * N + g0) * G;
     if (((uintptr_t)dst & 15) == 0 && ((uintptr_t)src & 15) == 0) {
@@ -322,8 +330,9 @@ __global__ void __launch_bounds__(256)
 }
 
 // Every rank's earlier stream work (its stores included) precedes every rank's
-// later work: flag all ranks, wait for all ranks' flags.
-__global__ void k_peer_barrier(PeerBase pb, int rank, int world, uint32_t gen, int* err) {
+// later work: flag all ranks, wait for all ranks' flags (one warp per played rank).
+__global__ void k_peer_barrier(PeerBase pb, int rank0, int world, uint32_t gen, int* err) {
+  const int rank = rank0 + (int)blockIdx.y;
   if (threadIdx.x == 0) {
     __threadfence_system();
     for (int p = 0; p < world; ++p) st_release_sys((uint32_t*)pb.p[p] + rank, gen);
@@ -340,22 +349,45 @@ static PeerBase peer_base(const rails_peer_t& peer) {
   return pb;
 }
 
-cudaError_t launch_gather_rows_peer(const LaunchCtx& c, int U, int N, long long G, int g0,
-                                    int ng, const int64_t* msg_loc, const rails_peer_t& peer) {
+cudaError_t launch_gather_rows_peer(const LaunchCtx& c, int U, int N, long long G, int ng,
+                                    const int64_t* const* msg_loc, const int* g0,
+                                    const rails_peer_t& peer, int nplay) {
   size_t bytes, gf, mo;
   owner_exchange_layout(U, peer.world, N, G, &bytes, &gf, &mo);
-  k_gather_rows_peer<<<(unsigned)U, 256, 0, c.stream>>>(U, N, G, g0, ng, msg_loc,
-                                                        peer_base(peer), peer.rank, peer.world,
-                                                        peer.gen, gf, mo, c.err);
+  RowSrc rs{};
+  for (int i = 0; i < nplay; ++i) {
+    rs.msg_loc[i] = msg_loc[i];
+    rs.g0[i] = g0[i];
+  }
+  PeerBase pb = peer_base(peer);
+  int U_ = U, N_ = N, ng_ = ng, world = peer.world, rank0 = nplay == 1 ? peer.rank : 0;
+  long long G_ = G;
+  uint32_t gen = peer.gen;
+  int* err = c.err;
   count_launch(1);
-  return cudaGetLastError();
+  if (nplay == 1) {
+    k_gather_rows_peer<<<dim3((unsigned)U, 1), 256, 0, c.stream>>>(U, N, G, ng, rs, pb, rank0,
+                                                                   world, gen, gf, mo, err);
+    return cudaGetLastError();
+  }
+  void* args[] = {&U_, &N_, &G_, &ng_, &rs, &pb, &rank0, &world, &gen, &gf, &mo, &err};
+  return cudaLaunchCooperativeKernel((const void*)k_gather_rows_peer, dim3((unsigned)U, nplay),
+                                     dim3(256), args, 0, c.stream);
 }
 
-cudaError_t launch_peer_barrier(const LaunchCtx& c, const rails_peer_t& peer) {
-  k_peer_barrier<<<1, 32, 0, c.stream>>>(peer_base(peer), peer.rank, peer.world, peer.gen,
-                                         c.err);
+cudaError_t launch_peer_barrier(const LaunchCtx& c, const rails_peer_t& peer, int nplay) {
+  PeerBase pb = peer_base(peer);
+  int rank0 = nplay == 1 ? peer.rank : 0, world = peer.world;
+  uint32_t gen = peer.gen;
+  int* err = c.err;
   count_launch(1);
-  return cudaGetLastError();
+  if (nplay == 1) {
+    k_peer_barrier<<<dim3(1, 1), 32, 0, c.stream>>>(pb, rank0, world, gen, err);
+    return cudaGetLastError();
+  }
+  void* args[] = {&pb, &rank0, &world, &gen, &err};
+  return cudaLaunchCooperativeKernel((const void*)k_peer_barrier, dim3(1, nplay), dim3(32), args,
+                                     0, c.stream);
 }
 
 }  // namespace rails

@@ -32,9 +32,9 @@ def weak_units(world: int, units_per_gpu_factor: int = 1) -> int:
 def make_reduce(group=None) -> Callable:
     """a6 hook for pipeline.*.step: SUM the partial sums, MAX the partial maxima.
 
-    NCCL reduces the device tensors in place.  Under gloo (the CPU tests, and several
-    ranks sharing one GPU, where NCCL refuses duplicate devices) device tensors are
-    staged through host copies."""
+    NCCL reduces the device tensors in place.  Under gloo (the CPU tests; test
+    processes sharing one GPU, where NCCL refuses duplicate devices -- fine here, no
+    kernel waits on another rank) device tensors are staged through host copies."""
     import torch.distributed as dist
 
     staged = dist.get_backend(group) == "gloo"

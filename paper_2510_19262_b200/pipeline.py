@@ -1,8 +1,9 @@
 """One pass of the whole hot path (all SURVEY section 8(a) rows) over preallocated buffers.
 
-Routing configs (C1, C3, C4):  a1 histogram -> a2-a4 LPT schedule -> a5 eval ->
-[a6 cross-rank reduction] -> finalize -> a7 rail offsets + pack.
-Matrix configs (C2, C5):       a2-a4 -> a5 -> [a6] -> finalize.
+Routing configs (C1, C3, C4):  a1 histogram -> a2-a5 fused (LPT schedule + eval +
+rail offsets, + finalize when this call holds every node) -> [a6 cross-rank
+reduction + finalize] -> a7 pack.
+Matrix configs (C2, C5):       a2-a5 fused -> [a6 + finalize].
 
 Only buffer management and call sequencing live here; every step is a C-ABI call
 into librails.so (``rails.py``).  ``reduce`` is the a6 hook: a callable taking
@@ -32,35 +33,41 @@ class RoutingPipeline:
         self.msg = torch.empty((U, nd, N, G), dtype=torch.int64, device=dev)
         self.rank = torch.empty((U, nd, N, T, k), dtype=torch.int32, device=dev)
         self.sched = rails.Schedule.empty(self.tp, self.sh, dev)
-        self.ws = torch.empty(rails.schedule_workspace(self.tp, self.sh), dtype=torch.uint8,
-                              device=dev)
+        self.ws = rails.new_workspace(self.tp, self.sh, dev)
         self.ev = rails.EvalOut.empty(self.tp, self.sh, dev)
         self.final = rails.empty_final(U, dev)
         self.rail_base = torch.empty((U, nd, N), dtype=torch.int64, device=dev)
         self.total = torch.empty(1, dtype=torch.int64, device=dev)
+        self.holds_all = d0 == 0 and nd == M  # the fused kernel can finalize the units
         # every remote (t,s) copy is at most one row: a tight upper bound needing no sync
         cap = out_cap if out_cap is not None else U * nd * N * T * k * row_bytes
         self.out = torch.empty(cap, dtype=torch.uint8, device=dev)
 
     def schedule_part(self, topk: torch.Tensor, lut: torch.Tensor, stream=None):
+        """a1 + the fused a2-a5 kernel (schedule, eval, rail offsets; the finalize too
+        when this pipeline holds every node of its units)."""
         rails.histogram(self.tp, self.sh, topk, lut, self.RB,
                         out=(self.counts, self.msg, self.rank), stream=stream)
-        rails.lpt_schedule(self.tp, self.sh, self.msg, out=self.sched, workspace=self.ws,
-                           stream=stream)
-        rails.eval(self.tp, self.sh, self.msg, self.sched, out=self.ev, stream=stream)
+        rails.schedule_eval(self.tp, self.sh, self.msg, self.sched, self.ev, self.ws,
+                            final=self.final if self.holds_all else None,
+                            rail_base=self.rail_base, rail_total=self.total, stream=stream)
 
     def finalize_part(self, reduce: Callable | None = None, stream=None):
-        if reduce is not None and hasattr(reduce, "finalize"):  # fused a6 + finalize
+        """a6 + finalize for pipelines holding a subset of the nodes (no-op otherwise:
+        the fused kernel already finalized)."""
+        if reduce is None:
+            if not self.holds_all:
+                rails.eval_finalize(self.tp, self.U, self.ev.red_sum, self.ev.red_max,
+                                    out=self.final, stream=stream)
+            return
+        if hasattr(reduce, "finalize"):  # fused a6 + finalize over peer memory
             reduce.finalize(self.ev.red_sum, self.ev.red_max, self.final, stream=stream)
             return
-        if reduce is not None:
-            reduce(self.ev.red_sum, self.ev.red_max)
+        reduce(self.ev.red_sum, self.ev.red_max)
         rails.eval_finalize(self.tp, self.U, self.ev.red_sum, self.ev.red_max, out=self.final,
                             stream=stream)
 
     def pack_part(self, topk, lut, x, stream=None):
-        rails.rail_offsets(self.tp, self.sh, self.sched.send_load, self.rail_base, self.total,
-                           stream=stream)
         rails.pack(self.tp, self.sh, self.T, self.k, x, topk, lut, self.rank, self.msg, self.RB,
                    self.sched, self.rail_base, self.out, stream=stream)
 
@@ -80,14 +87,17 @@ class MatrixPipeline:
         self.U = U
         dev = torch.device(device)
         self.sched = rails.Schedule.empty(self.tp, self.sh, dev)
-        self.ws = torch.empty(rails.schedule_workspace(self.tp, self.sh), dtype=torch.uint8,
-                              device=dev)
+        self.ws = rails.new_workspace(self.tp, self.sh, dev)
         self.ev = rails.EvalOut.empty(self.tp, self.sh, dev)
         self.final = rails.empty_final(U, dev)
+        self.holds_all = d0 == 0 and nd == M
 
     def step(self, msg: torch.Tensor, reduce: Callable | None = None, stream=None):
-        rails.lpt_schedule(self.tp, self.sh, msg, out=self.sched, workspace=self.ws, stream=stream)
-        rails.eval(self.tp, self.sh, msg, self.sched, out=self.ev, stream=stream)
+        fin = self.final if (self.holds_all and reduce is None) else None
+        rails.schedule_eval(self.tp, self.sh, msg, self.sched, self.ev, self.ws, final=fin,
+                            stream=stream)
+        if fin is not None:
+            return
         if reduce is not None and hasattr(reduce, "finalize"):  # fused a6 + finalize
             reduce.finalize(self.ev.red_sum, self.ev.red_max, self.final, stream=stream)
             return

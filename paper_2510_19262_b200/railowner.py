@@ -11,8 +11,7 @@ rail j's send buffer lives in GPU j's HBM.  One step:
   4. rails_rail_offsets_owner + rails_pack_owner: each chunk piece is stored
      straight into the owner's buffer through a peer-mapped pointer   (kernel)
   5. rails_peer_barrier orders every rank's pack before any consumer (kernel).
-exchange="nccl" keeps the collective all-gather / all-reduce for steps 2 and 5 (NCCL;
-host-staged under gloo, when several ranks share one GPU).
+exchange="nccl" keeps the NCCL all-gather / all-reduce for steps 2 and 5.
 Peer mapping: CUDA IPC handles exported/imported by librails (rails_ipc_*), each
 rank mapping the peers' buffers under its own device.
 """
@@ -55,15 +54,11 @@ class RailOwnerNode:
         self.msg_loc = torch.empty((U, 1, self.ng, G), dtype=torch.int64, device=dev)
         self.rank_loc = torch.empty((U, 1, self.ng, T, k), dtype=torch.int32, device=dev)
         self.exchange = exchange
-        # the collective exchange stages through host memory under gloo (several
-        # ranks on one GPU: NCCL refuses duplicate devices)
-        self.staged = dist.get_backend(group) == "gloo"
         if exchange not in ("peer", "nccl"):
             raise ValueError("exchange must be 'peer' or 'nccl'")
         self.msg_node = torch.empty((U, 1, N, G), dtype=torch.int64, device=dev)
         self.sched = rails.Schedule.empty(self.tp, self.sh, dev)
-        self.ws = torch.empty(rails.schedule_workspace(self.tp, self.sh), dtype=torch.uint8,
-                              device=dev)
+        self.ws = rails.new_workspace(self.tp, self.sh, dev)
         self.rail_base = torch.empty((U, 1, N), dtype=torch.int64, device=dev)
         self.rail_total = torch.empty(N, dtype=torch.int64, device=dev)
         self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -131,11 +126,6 @@ class RailOwnerNode:
         if self.exchange == "peer":
             rails.gather_rows_peer(self.tp, self.U, self.g0, self.ng, self.msg_loc, self.p,
                                    self.P, self.gen, self.xbufs)
-        elif self.staged:  # gloo (ranks sharing one GPU): host-staged all-gather
-            for u in range(self.U):
-                parts = [torch.empty_like(self.msg_loc[u, 0], device="cpu") for _ in range(self.P)]
-                self.dist.all_gather(parts, self.msg_loc[u, 0].cpu(), group=self.group)
-                self.msg_node[u, 0].copy_(torch.cat(parts))
         else:
             for u in range(self.U):
                 self.dist.all_gather_into_tensor(self.msg_node[u, 0], self.msg_loc[u, 0],
@@ -154,9 +144,6 @@ class RailOwnerNode:
         # anywhere orders all peer writes before later consumers
         if self.exchange == "peer":
             rails.peer_barrier(self.p, self.P, self.gen, self.xbufs)
-        elif self.staged:
-            f = self.flag.cpu()
-            self.dist.all_reduce(f, group=self.group)
         else:
             self.dist.all_reduce(self.flag, group=self.group)
 

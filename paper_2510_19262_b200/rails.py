@@ -24,7 +24,7 @@ RED_MAX_LEN = 4
 
 
 def red_sum_len(M: int, N: int) -> int:
-    return 2 * M * N + M + 2
+    return 3 * M * N + M + 2
 
 
 class RailsError(RuntimeError):
@@ -52,11 +52,13 @@ class _Sched(ctypes.Structure):
 
 
 class _Eval(ctypes.Structure):
-    _fields_ = [(n, ctypes.c_void_p) for n in ("S", "S_e", "mse", "nmse", "red_sum", "red_max")]
+    _fields_ = [(n, ctypes.c_void_p) for n in
+                ("S", "S_e", "S_u", "mse", "nmse", "red_sum", "red_max")]
 
 
-_FINAL_FIELDS = ("maxload", "maxload_e", "total", "rowmax", "colmax", "T", "T_e", "T_star",
-                 "busbw", "busbw_e")
+_FINAL_FIELDS = ("maxload", "maxload_e", "maxload_u", "total", "rowmax", "colmax", "T", "T_e",
+                 "T_u", "T_star", "busbw", "busbw_e", "busbw_u")
+_FINAL_FLOAT = ("T", "T_e", "T_u", "T_star", "busbw", "busbw_e", "busbw_u")
 
 
 class _Final(ctypes.Structure):
@@ -99,6 +101,10 @@ def lib():
         L.rails_lpt_assign.argtypes = [i32, i32, P, i64, P, P, P, P, P, sz, P]
         L.rails_eval.argtypes = [PT, PS, P, ctypes.POINTER(_Sched), ctypes.POINTER(_Eval), P]
         L.rails_eval_finalize.argtypes = [PT, i32, P, P, ctypes.POINTER(_Final), P]
+        L.rails_schedule_eval.argtypes = [PT, PS, P, ctypes.POINTER(_Sched),
+                                          ctypes.POINTER(_Eval), ctypes.POINTER(_Final), P, P, P,
+                                          sz, P]
+        L.rails_schedule_eval.restype = ctypes.c_int
         L.rails_peer_buffer_bytes.argtypes = [PT, i32, i32, ctypes.POINTER(sz)]
         L.rails_peer_buffer_bytes.restype = ctypes.c_int
         L.rails_eval_finalize_peer.argtypes = [PT, i32, P, P, ctypes.POINTER(Peer),
@@ -111,6 +117,13 @@ def lib():
         L.rails_gather_rows_peer.restype = ctypes.c_int
         L.rails_peer_barrier.argtypes = [ctypes.POINTER(Peer), P]
         L.rails_peer_barrier.restype = ctypes.c_int
+        L.rails_eval_finalize_peer_local.argtypes = [PT, i32, P, P, ctypes.POINTER(Peer),
+                                                     P, P]
+        L.rails_gather_rows_peer_local.argtypes = [PT, i32, i32, P, ctypes.POINTER(Peer), P]
+        L.rails_peer_barrier_local.argtypes = [ctypes.POINTER(Peer), P]
+        for n in ("rails_eval_finalize_peer_local", "rails_gather_rows_peer_local",
+                  "rails_peer_barrier_local"):
+            getattr(L, n).restype = ctypes.c_int
         L.rails_rail_offsets.argtypes = [PT, PS, P, P, P, P]
         L.rails_pack.argtypes = [PT, PS, i32, i32, P, P, P, i32, P, P, i64,
                                  ctypes.POINTER(_Sched), P, P, i64, P]
@@ -239,13 +252,18 @@ def schedule_workspace(tp: Topo, sh: Shard) -> int:
     return int(n.value)
 
 
+def new_workspace(tp: Topo, sh: Shard, device) -> torch.Tensor:
+    """Schedule workspace, zero-filled once as rails_schedule_eval requires (the
+    kernels leave it zeroed)."""
+    return torch.zeros(schedule_workspace(tp, sh), dtype=torch.uint8, device=device)
+
+
 def lpt_schedule(tp: Topo, sh: Shard, msg: torch.Tensor, out: Schedule | None = None,
                  workspace: torch.Tensor | None = None, stream=None) -> Schedule:
     if out is None:
         out = Schedule.empty(tp, sh, msg.device)
-    need = schedule_workspace(tp, sh)
     if workspace is None:
-        workspace = torch.empty(need, dtype=torch.uint8, device=msg.device)
+        workspace = new_workspace(tp, sh, msg.device)
     cs = out.c()
     _ok(lib().rails_lpt_schedule(ctypes.byref(tp), ctypes.byref(sh), _ptr(msg, torch.int64, "msg"),
                                  ctypes.byref(cs), _ptr(workspace, torch.uint8, "workspace"),
@@ -262,7 +280,7 @@ def lpt_schedule_qp(tp: Topo, sh: Shard, msg: torch.Tensor, qps_per_rail: int,
     if rem_qp is None:
         rem_qp = torch.empty(out.rem_rail.shape, dtype=torch.int32, device=msg.device)
     if workspace is None:
-        workspace = torch.empty(schedule_workspace(tp, sh), dtype=torch.uint8, device=msg.device)
+        workspace = new_workspace(tp, sh, msg.device)
     cs = out.c()
     _ok(lib().rails_lpt_schedule_qp(ctypes.byref(tp), ctypes.byref(sh),
                                     _ptr(msg, torch.int64, "msg"), ctypes.byref(cs),
@@ -294,9 +312,10 @@ def lpt_assign(N: int, seg_off: torch.Tensor, w: torch.Tensor, stream=None):
 class EvalOut:
     S: torch.Tensor        # int64 [U][nd][N]
     S_e: torch.Tensor      # int64 [U][nd][N]
+    S_u: torch.Tensor      # int64 [U][nd][N]
     mse: torch.Tensor      # float64 [U][nd]
     nmse: torch.Tensor     # float64 [U][nd]
-    red_sum: torch.Tensor  # int64 [U][2MN+M+2]
+    red_sum: torch.Tensor  # int64 [U][3MN+M+2]
     red_max: torch.Tensor  # int64 [U][4]
 
     @staticmethod
@@ -305,6 +324,7 @@ class EvalOut:
         z = dict(device=device)
         return EvalOut(torch.empty((U, nd, N), dtype=torch.int64, **z),
                        torch.empty((U, nd, N), dtype=torch.int64, **z),
+                       torch.empty((U, nd, N), dtype=torch.int64, **z),
                        torch.empty((U, nd), dtype=torch.float64, **z),
                        torch.empty((U, nd), dtype=torch.float64, **z),
                        torch.empty((U, red_sum_len(tp.M, N)), dtype=torch.int64, **z),
@@ -312,8 +332,9 @@ class EvalOut:
 
     def c(self) -> _Eval:
         return _Eval(_ptr(self.S, torch.int64), _ptr(self.S_e, torch.int64),
-                     _ptr(self.mse, torch.float64), _ptr(self.nmse, torch.float64),
-                     _ptr(self.red_sum, torch.int64), _ptr(self.red_max, torch.int64))
+                     _ptr(self.S_u, torch.int64), _ptr(self.mse, torch.float64),
+                     _ptr(self.nmse, torch.float64), _ptr(self.red_sum, torch.int64),
+                     _ptr(self.red_max, torch.int64))
 
     def R(self, M: int, N: int) -> torch.Tensor:
         return self.red_sum[:, :M * N].view(-1, M, N)
@@ -321,8 +342,11 @@ class EvalOut:
     def R_e(self, M: int, N: int) -> torch.Tensor:
         return self.red_sum[:, M * N:2 * M * N].view(-1, M, N)
 
+    def R_u(self, M: int, N: int) -> torch.Tensor:
+        return self.red_sum[:, 2 * M * N:3 * M * N].view(-1, M, N)
+
     def colsum(self, M: int, N: int) -> torch.Tensor:
-        return self.red_sum[:, 2 * M * N:2 * M * N + M]
+        return self.red_sum[:, 3 * M * N:3 * M * N + M]
 
 
 def eval(tp: Topo, sh: Shard, msg: torch.Tensor, sched: Schedule, out: EvalOut | None = None,
@@ -338,7 +362,7 @@ def eval(tp: Topo, sh: Shard, msg: torch.Tensor, sched: Schedule, out: EvalOut |
 def empty_final(U: int, device) -> dict:
     f = {}
     for n in _FINAL_FIELDS:
-        dt = torch.float64 if n in ("T", "T_e", "T_star", "busbw", "busbw_e") else torch.int64
+        dt = torch.float64 if n in _FINAL_FLOAT else torch.int64
         f[n] = torch.empty(U, dtype=dt, device=device)
     return f
 
@@ -352,6 +376,25 @@ def eval_finalize(tp: Topo, U: int, red_sum: torch.Tensor, red_max: torch.Tensor
                                   _ptr(red_max, torch.int64, "red_max"), ctypes.byref(cf),
                                   _stream(stream)))
     return out
+
+
+def schedule_eval(tp: Topo, sh: Shard, msg: torch.Tensor, sched: Schedule, ev: EvalOut,
+                  workspace: torch.Tensor, final: dict | None = None,
+                  rail_base: torch.Tensor | None = None, rail_total: torch.Tensor | None = None,
+                  stream=None):
+    """a2-a5 fused (rails_schedule_eval): schedule + evaluation of the shard's nodes in
+    one kernel, plus the per-unit finalize when the shard holds every node (`final`)
+    and the rail offsets (`rail_base`, `rail_total`).  `workspace` must come from
+    new_workspace()."""
+    cs, ce = sched.c(), ev.c()
+    cf = _Final(*[_ptr(final[n]) for n in _FINAL_FIELDS]) if final is not None else None
+    _ok(lib().rails_schedule_eval(ctypes.byref(tp), ctypes.byref(sh),
+                                  _ptr(msg, torch.int64, "msg"), ctypes.byref(cs),
+                                  ctypes.byref(ce), ctypes.byref(cf) if cf is not None else None,
+                                  _ptr(rail_base, torch.int64, "rail_base"),
+                                  _ptr(rail_total, torch.int64, "rail_total"),
+                                  _ptr(workspace, torch.uint8, "workspace"), workspace.numel(),
+                                  _stream(stream)))
 
 
 def peer_buffer_bytes(tp: Topo, U: int, world: int) -> int:
@@ -400,6 +443,36 @@ def gather_rows_peer(tp: Topo, U: int, g0: int, ng: int, msg_loc: torch.Tensor, 
 
 def peer_barrier(rank: int, world: int, gen: int, bufs, stream=None):
     _ok(lib().rails_peer_barrier(ctypes.byref(_peer(rank, world, gen, bufs)), _stream(stream)))
+
+
+# -- every rank driven by this process on one device (one cooperative launch each)
+def _ptr_array(ts, dtype, what):
+    return (ctypes.c_void_p * len(ts))(*[_ptr(t, dtype, what).value for t in ts])
+
+
+def eval_finalize_peer_local(tp: Topo, U: int, red_sums: list, red_maxs: list, gen: int,
+                             bufs: list, outs: list, stream=None):
+    """rails_eval_finalize_peer_local: rank p = (red_sums[p], red_maxs[p], outs[p])."""
+    world = len(red_sums)
+    finals = (_Final * world)(*[_Final(*[_ptr(o[n]) for n in _FINAL_FIELDS]) for o in outs])
+    _ok(lib().rails_eval_finalize_peer_local(
+        ctypes.byref(tp), U, _ptr_array(red_sums, torch.int64, "red_sum"),
+        _ptr_array(red_maxs, torch.int64, "red_max"), ctypes.byref(_peer(0, world, gen, bufs)),
+        finals, _stream(stream)))
+
+
+def gather_rows_peer_local(tp: Topo, U: int, ng: int, msg_locs: list, gen: int, bufs,
+                           stream=None):
+    world = len(msg_locs)
+    _ok(lib().rails_gather_rows_peer_local(ctypes.byref(tp), U, ng,
+                                           _ptr_array(msg_locs, torch.int64, "msg_loc"),
+                                           ctypes.byref(_peer(0, world, gen, bufs)),
+                                           _stream(stream)))
+
+
+def peer_barrier_local(world: int, gen: int, bufs, stream=None):
+    _ok(lib().rails_peer_barrier_local(ctypes.byref(_peer(0, world, gen, bufs)),
+                                       _stream(stream)))
 
 
 # ---------------------------------------------------------------- a7

@@ -37,8 +37,10 @@ def oracle_eval_from_scheds(M, N, msg_unit, scheds, R2=R2, seed=SEED):
         F = len(s["chunks"]["size"])
         cd.append(np.full(F, d, np.int32)); chh.append(s["chunks"]["h"])
         cs.append(s["chunks"]["size"]); cr.append(s["rail"])
-    return oracle.eval_unit(M, N, R2, seed, msg_unit, np.concatenate(cd), np.concatenate(chh),
-                            np.concatenate(cs), np.concatenate(cr))
+    ev = oracle.eval_unit(M, N, R2, seed, msg_unit, np.concatenate(cd), np.concatenate(chh),
+                          np.concatenate(cs), np.concatenate(cr))
+    ev.update(oracle.eval_uniform(M, N, R2, msg_unit))  # S_u, R_u, maxload_u, T_u, busbw_u
+    return ev
 
 
 def rel_err(a: float, b: float) -> float:

@@ -1,13 +1,11 @@
-"""Run a multi-rank GPU test body as P spawned processes (one rank each).
+"""Run a multi-rank GPU test body as P spawned processes, one per GPU ("per_gpu":
+rank r on cuda:r, process group over NCCL; CUDA-IPC mappings and NVLink stores).
 
-Two placements, both real multi-process runs through the product's peer-memory
-code (CUDA-IPC mappings, system-scope flags, NVLink stores when ranks sit on
-different GPUs):
-  * "per_gpu": rank r on cuda:r, process group over NCCL -- needs P GPUs;
-  * "shared":  every rank on cuda:0, process group over gloo (NCCL refuses two
-    ranks on one device).  The IPC mappings then alias the same HBM and the GPU
-    time-slices the ranks' contexts, so every flag wait really crosses processes.
-A 1-GPU box runs the shared placement; larger boxes run both.
+Ranks whose kernels wait on each other's flags must never share one GPU as separate
+processes (nothing guarantees their kernels run concurrently; on this driver it has
+raised Xid 109): the single-GPU variants of the multi-rank tests play every rank in
+one process with the *_local cooperative launches instead.  `placement` "shared"
+(gloo, every rank on cuda:0) is only for bodies without cross-rank waits.
 """
 from __future__ import annotations
 
@@ -19,11 +17,6 @@ import traceback
 
 import torch
 import torch.multiprocessing as mp
-
-
-def placements(world: int) -> list[str]:
-    ngpu = torch.cuda.device_count() if torch.cuda.is_available() else 0
-    return ["shared"] + (["per_gpu"] if ngpu >= world else [])
 
 
 def _port() -> int:

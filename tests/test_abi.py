@@ -27,6 +27,7 @@ def declared_symbols():
 def test_header_declares_the_boundary():
     syms = declared_symbols()
     for s in ("rails_histogram", "rails_lpt_schedule", "rails_eval", "rails_pack",
+              "rails_schedule_eval",
               "rails_eval_finalize", "rails_lpt_assign", "rails_rail_offsets", "rails_check",
               "rails_last_error"):
         assert s in syms
@@ -46,7 +47,7 @@ def test_kernels_are_sm100a(L):
 
 
 def test_version_and_error_string(L):
-    assert L.version() == 100
+    assert L.version() == 200
     assert isinstance(L.lib().rails_last_error(), bytes)
 
 

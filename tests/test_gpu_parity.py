@@ -215,12 +215,15 @@ def _compare_eval(pipe, u, d0, nd, M, N, ev):
     assert np.array_equal(e.S_e[u].cpu().numpy(), ev["S_e"][d0:d0 + nd])
     assert np.array_equal(e.R(M, N)[u].cpu().numpy(), ev["R"])
     assert np.array_equal(e.R_e(M, N)[u].cpu().numpy(), ev["R_e"])
+    # uniform P* = 1/N split (Theorem 3, R#41)
+    assert np.array_equal(e.S_u[u].cpu().numpy(), ev["S_u"][d0:d0 + nd])
+    assert np.array_equal(e.R_u(M, N)[u].cpu().numpy(), ev["R_u"])
     # send_load from the LPT chain equals S recomputed from the schedule
     assert np.array_equal(pipe.sched.send_load[u].cpu().numpy(), S)
     f = {k: v[u].item() for k, v in pipe.final.items()}
-    for key in ("maxload", "maxload_e", "total", "rowmax", "colmax"):
+    for key in ("maxload", "maxload_e", "maxload_u", "total", "rowmax", "colmax"):
         assert f[key] == ev[key], key
-    for key in ("T", "T_e", "T_star", "busbw", "busbw_e"):
+    for key in ("T", "T_e", "T_u", "T_star", "busbw", "busbw_e", "busbw_u"):
         _cmp_float(f[key], ev[key], key)
     for dl in range(nd):
         _cmp_float(e.mse[u, dl].item(), ev["mse"][d0 + dl], "mse")

@@ -6,6 +6,7 @@
 #   bench[:ARGS]   python bench.py ARGS (default N=1)       -> gpurun_out/bench*.json
 #   ref            bench.py --impl reference                -> gpurun_out/bench_ref.json
 #   launches       ncu launch list of the default bench    -> gpurun_out/launches.csv
+#   py:SCRIPT ARGS python SCRIPT ARGS                       -> gpurun_out/<script>.json
 # Exit codes of every step go to gpurun_out/rc.txt.
 mkdir -p gpurun_out
 python -c "from paper_2510_19262_b200 import build as b; b.build()" > gpurun_out/build.log 2>&1
@@ -26,6 +27,10 @@ for step in "$@"; do
       timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
         --log-file gpurun_out/launches.csv python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu --no-graph $arg \
         > gpurun_out/launches.log 2>&1 ;;
+    py)
+      scr="${arg%% *}"; rest="${arg#* }"; [ "$rest" = "$arg" ] && rest=""
+      out=$(basename "$scr" .py)
+      timeout 1500 python $scr $rest > "gpurun_out/$out.json" 2> "gpurun_out/$out.err" ;;
     *) echo "unknown step $step" ;;
   esac
   echo "$step rc=$?" >> gpurun_out/rc.txt
