@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
   const IdxT* is = which ? iB : iA;
   IdxT* inv = which ? iA : iB;  // inverse permutation: message -> sorted position
   constexpr IdxT NONE = (IdxT)~(IdxT)0;
-  for (long long m = threadIdx.x; m < NG; m += blockDim.x) inv[m] = NONE;
+  for (int m = threadIdx.x; m < (int)NG; m += blockDim.x) inv[m] = NONE;
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += blockDim.x) inv[is[i]] = (IdxT)i;
 
@@ -304,7 +304,8 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
 
   // ---- phase D: QP map (optional), expand, remainders into R_d
   if (a.rem_qp) qp_rank_block(N, a.Q, nf_node, n, res, a.qp_g + seg * NG);
-  for (long long m = threadIdx.x; m < NG; m += blockDim.x) {
+  const unsigned NGu = (unsigned)NG, Gu = (unsigned)G;  // N*G < 2^26 (M*N <= 2^20, N <= 32)
+  for (unsigned m = threadIdx.x; m < NGu; m += blockDim.x) {
     const IdxT p = inv[m];
     int8_t r = -1;
     long long o = 0;
@@ -315,7 +316,7 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
       o = (long long)(v & (uint64_t)OFF_MASK);
       if (a.rem_qp) q = (int32_t)a.qp_g[seg * NG + p];
       if constexpr (EVAL) {
-        const int f = (int)((m % G) / N);
+        const int f = (int)((m % Gu) / (unsigned)N);
         add64_split(&aRlo[f * N + r], &aRhi[f * N + r],
                     (unsigned long long)(C - 1 - (long long)ks[p]));
       }
@@ -332,29 +333,69 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
   const long long rec = rsl + RAILS_RED_MAX_LEN;
   const RedLayout RL{MN, M};
   unsigned long long* acc = (unsigned long long*)(a.acc + u * rec);
-  for (long long t = threadIdx.x; t < MN; t += blockDim.x) {
-    const int f = (int)(t / N), j = (int)(t - (long long)f * N);
-    const unsigned long long R = ((unsigned long long)aRhi[t] << 32) | aRlo[t];
-    const unsigned long long Re = ((unsigned long long)aEhi[t] << 32) | aElo[t];
-    unsigned long long Ru = ((unsigned long long)aQhi[f] << 32) | aQlo[f];
-    for (int r = j + 1; r < N; ++r) Ru += cU[(long long)f * N + r];
-    if (R) atomicAdd(acc + RL.R() + t, R);
-    if (Re) atomicAdd(acc + RL.Re() + t, Re);
-    if (Ru) atomicAdd(acc + RL.Ru() + t, Ru);
+  // thread per (f, j): R, R_e, R_u into the unit's accumulator.  When N divides the
+  // block, every thread keeps one rail j (register partials of S_e, S_u, reduced
+  // below); when N divides 32, the N rails of one f sit in consecutive lanes and the
+  // column sum is a shuffle reduction.  Otherwise shared split atomics / a loop.
+  const bool jfix = (blockDim.x % N) == 0;
+  const bool wlanes = (32 % N) == 0;
+  __shared__ unsigned sEU[4][32];  // S_e lo/hi, S_u lo/hi when !jfix
+  if (threadIdx.x < 32) sEU[0][threadIdx.x] = sEU[1][threadIdx.x] = sEU[2][threadIdx.x] =
+      sEU[3][threadIdx.x] = 0u;
+  __syncthreads();
+  unsigned long long pe = 0, pu = 0;
+  for (int t0 = 0; t0 < (int)MN; t0 += blockDim.x) {
+    const int t = t0 + threadIdx.x;
+    const bool act = t < (int)MN;
+    const int f = act ? t / N : 0, j = act ? t - f * N : 0;
+    unsigned long long R = 0, Re = 0, Ru = 0;
+    if (act) {
+      R = ((unsigned long long)aRhi[t] << 32) | aRlo[t];
+      Re = ((unsigned long long)aEhi[t] << 32) | aElo[t];
+      Ru = ((unsigned long long)aQhi[f] << 32) | aQlo[f];
+      for (int r = j + 1; r < N; ++r) Ru += cU[f * N + r];
+      if (R) atomicAdd(acc + RL.R() + t, R);
+      if (Re) atomicAdd(acc + RL.Re() + t, Re);
+      if (Ru) atomicAdd(acc + RL.Ru() + t, Ru);
+    }
+    if (jfix) {
+      pe += Re;
+      pu += Ru;
+    } else if (act) {
+      if (Re) add64_split(&sEU[0][j], &sEU[1][j], Re);
+      if (Ru) add64_split(&sEU[2][j], &sEU[3][j], Ru);
+    }
+    if (wlanes) {
+      unsigned long long v = R;
+      for (int o = 1; o < N; o <<= 1) v += __shfl_xor_sync(FULL, v, o);
+      if (act && j == 0 && v) atomicAdd(acc + RL.col() + f, v);
+    }
   }
-  for (int f = threadIdx.x; f < M; f += blockDim.x) {
-    unsigned long long cf = 0;
-    for (int j = 0; j < N; ++j)
-      cf += ((unsigned long long)aRhi[(long long)f * N + j] << 32) | aRlo[(long long)f * N + j];
-    if (cf) atomicAdd(acc + RL.col() + f, cf);
+  if (!wlanes) {
+    for (int f = threadIdx.x; f < M; f += blockDim.x) {
+      unsigned long long cf = 0;
+      for (int j = 0; j < N; ++j)
+        cf += ((unsigned long long)aRhi[f * N + j] << 32) | aRlo[f * N + j];
+      if (cf) atomicAdd(acc + RL.col() + f, cf);
+    }
   }
+  unsigned long long* part = reinterpret_cast<unsigned long long*>(hist);  // free after the sort
+  if (jfix) {
+    part[threadIdx.x] = pe;
+    part[NODE_MAX_THREADS + threadIdx.x] = pu;
+  }
+  __syncthreads();
   if (threadIdx.x < N) {  // S_e, S_u of this node per rail j
     const int j = threadIdx.x;
     unsigned long long se = 0, su = 0;
-    for (int f = 0; f < M; ++f) {
-      se += ((unsigned long long)aEhi[(long long)f * N + j] << 32) | aElo[(long long)f * N + j];
-      su += ((unsigned long long)aQhi[f] << 32) | aQlo[f];
-      for (int r = j + 1; r < N; ++r) su += cU[(long long)f * N + r];
+    if (jfix) {
+      for (int t = j; t < (int)blockDim.x; t += N) {
+        se += part[t];
+        su += part[NODE_MAX_THREADS + t];
+      }
+    } else {
+      se = ((unsigned long long)sEU[1][j] << 32) | sEU[0][j];
+      su = ((unsigned long long)sEU[3][j] << 32) | sEU[2][j];
     }
     sSe[j] = (long long)se;
     sSu[j] = (long long)su;
@@ -438,7 +479,7 @@ struct NodePlan {
 };
 
 // Shared-memory plan of the fused kernel for N*G messages per node.
-static NodePlan node_plan(int M, int N, long long C, bool eval) {
+static NodePlan node_plan(int M, int N, long long C, bool eval, long long nseg, int num_sms) {
   const long long G = (long long)M * N, NG = (long long)N * G;
   NodePlan p{};
   constexpr size_t DYN_LIMIT = 200 * 1024;  // + ~20 KiB static stays under 227 KiB
@@ -449,7 +490,10 @@ static NodePlan node_plan(int M, int N, long long C, bool eval) {
   p.smem_sort = NG <= NODE_SMEM_ITEMS &&
                 sort_smem + (p.eval_fused ? ev_bytes + 32 : 0) <= DYN_LIMIT;
   p.k16 = p.smem_sort && k16;
+  // few segments (C3: 64 on 148 SMs): the node's latency is the step's, so give each
+  // CTA the most threads; many segments: 256 (128 registers each -> 2 CTAs per SM)
   p.threads = NG <= 1024 ? 128 : (NG <= 8192 ? 256 : NODE_MAX_THREADS);
+  if (nseg <= num_sms && NG >= 2048) p.threads = NODE_MAX_THREADS;
   p.sort_bytes = p.smem_sort ? sort_smem : 0;
   size_t off = (p.sort_bytes + 15) & ~(size_t)15;
   if (p.eval_fused) {
@@ -541,7 +585,7 @@ cudaError_t launch_node(const LaunchCtx& c, int U, int nd, int d0, int M, int N,
                         const rails_final_t* fin, int64_t* rail_base, int64_t* rail_total,
                         bool* fused) {
   const long long NG = (long long)N * M * N, nseg = (long long)U * nd;
-  NodePlan p = node_plan(M, N, C, ev != nullptr);
+  NodePlan p = node_plan(M, N, C, ev != nullptr, nseg, c.num_sms);
   if (fused) *fused = p.eval_fused;
   const NodeWs w = node_ws(ws, U, nd, M, N);
   NodeArgs a{};

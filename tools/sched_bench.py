@@ -75,12 +75,17 @@ def bench_routing(res, name, U):
                                         rail_total=pipe.total)
     th = timeit(hist)
     tf = timeit(fused)
+    split = lambda: (rails.lpt_schedule(pipe.tp, pipe.sh, pipe.msg, out=pipe.sched,  # noqa: E731
+                                        workspace=pipe.ws),
+                     rails.eval(pipe.tp, pipe.sh, pipe.msg, pipe.sched, out=pipe.ev))
+    tsp = timeit(split)
     tb = timeit(lambda: pipe.schedule_part(topk, lut))
     ne = topk.numel()
     G = pipe.M * pipe.N
     nseg = U * pipe.M * pipe.N
     hbytes = ne * 4 * 2 + nseg * G * (4 + 8)  # ids in, ranks out, counts + bytes out
     out = {"units": U, "nodes": U * pipe.M, "histogram": th, "fused_sched_eval": tf,
+           "schedule_then_eval": tsp,
            "schedule_part": tb, "hist_algorithmic_bytes": hbytes,
            "hist_gbs": round(hbytes / (th["median_us"] * 1e-6) / 1e9, 1),
            "nodes_per_s_schedule_part": round(U * pipe.M / (tb["median_us"] * 1e-6))}
@@ -96,8 +101,11 @@ def bench_matrix(res, name, C=None, U=None):
     msg = torch.from_numpy(gen.d1_units(cfg, gen.config_seed(int(name[1])), 0, U)).to(DEV)
     pipe = MatrixPipeline(M, N, cfg["C"], U, 0, M, DEV)
     t = timeit(lambda: pipe.step(msg))
+    tsp = timeit(lambda: (rails.lpt_schedule(pipe.tp, pipe.sh, msg, out=pipe.sched,
+                                             workspace=pipe.ws),
+                          rails.eval(pipe.tp, pipe.sh, msg, pipe.sched, out=pipe.ev)))
     key = name if C is None else f"{name}_C{C}"
-    res[key] = {"units": U, "nodes": U * M, "fused_sched_eval": t,
+    res[key] = {"units": U, "nodes": U * M, "fused_sched_eval": t, "schedule_then_eval": tsp,
                 "nodes_per_s": round(U * M / (t["median_us"] * 1e-6))}
 
 
