@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librails.so")
-SOURCES = ["abi.cu", "k_hist.cu", "k_node.cu", "k_sched.cu", "k_eval.cu", "k_pack.cu", "k_owner.cu",
+SOURCES = ["abi.cu", "k_hist.cu", "k_node.cu", "k_chains.cu", "k_sched.cu", "k_eval.cu", "k_pack.cu", "k_owner.cu",
            "k_combine.cu", "k_flowsim.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

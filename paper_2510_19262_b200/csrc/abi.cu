@@ -86,13 +86,6 @@ static int check_shard(const rails_topo_t* t, const rails_shard_t* s) {
 
 static bool al(const void* p, size_t a) { return ((uintptr_t)p % a) == 0; }
 
-// Pack implementation: RAILS_PACK_IMPL=1 (LDG/STG), 2 (TMA bulk), 3 (TMA bulk with
-// batched metadata); default below.
-static int pack_impl() {
-  const char* e = getenv("RAILS_PACK_IMPL");
-  if (e && e[0] >= '1' && e[0] <= '3') return e[0] - '0';
-  return 1;
-}
 }  // namespace rails
 
 using namespace rails;
@@ -320,7 +313,7 @@ int rails_pack(const rails_topo_t* topo, const rails_shard_t* sh, int32_t T, int
   if ((rc = ctx(stream, &c))) return rc;
   return cuda_rc(launch_pack(c, sh->U, sh->nd, sh->d0, topo->M, topo->N, T, k, topo->chunk_bytes,
                              x, topk_inst, inst_to_gpu, n_inst, row_rank, msg_bytes, row_bytes,
-                             *sched, rail_base, out, out_cap, pack_impl()),
+                             *sched, rail_base, out, out_cap),
                  "rails_pack launch");
 }
 

@@ -173,15 +173,14 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
                : "l"(p));
   return r;
 }
+__device__ __forceinline__ void st_cs(uint4* p, const uint4& v) {  // evict-first store
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
 __device__ __forceinline__ void st_stream(uint4* p, const uint4& v) {
   asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
                "r"(v.y), "r"(v.z), "r"(v.w)
-               : "memory");
-}
-
-__device__ __forceinline__ void st_cs(uint4* p, const uint4& v) {
-  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
-               "r"(v.z), "r"(v.w)
                : "memory");
 }
 
@@ -207,6 +206,11 @@ cudaError_t launch_node(const LaunchCtx&, int U, int nd, int d0, int M, int N, l
                         void* ws, int32_t* rem_qp, int qps_per_rail, const rails_eval_t* ev,
                         const rails_final_t* fin, int64_t* rail_base, int64_t* rail_total,
                         bool* fused);
+
+cudaError_t launch_chains(const LaunchCtx&, int U, int nd, int d0, int M, int N, long long C,
+                          const int64_t* msg, const rails_sched_t& s, uint64_t* ws_res,
+                          uint32_t* ws_qp, uint32_t* ws_w, int32_t* ws_inv, uint8_t* scratch,
+                          int32_t* rem_qp, int qps_per_rail, int cshift, int nbits);
 
 size_t assign_workspace_bytes(int n_seg, long long F);
 cudaError_t launch_assign(const LaunchCtx&, int N, int n_seg, const int64_t* seg_off,
@@ -237,7 +241,7 @@ cudaError_t launch_pack(const LaunchCtx&, int U, int nd, int d0, int M, int N, i
                         long long C, const void* x, const int32_t* topk, const int32_t* lut,
                         int n_inst, const int32_t* rank, const int64_t* msg,
                         long long row_bytes, const rails_sched_t& s, const int64_t* rail_base,
-                        void* out, long long out_cap, int impl);
+                        void* out, long long out_cap);
 
 cudaError_t launch_pack_owner(const LaunchCtx&, int U, int nd, int d0, int M, int N, int g0,
                               int ng, int T, int k, long long C, const void* x,
@@ -283,11 +287,9 @@ void count_launch(int n);
 // about `rpw` rows per warp, the CTAs running in waves, instead of one persistent
 // wave of resident CTAs striding over every row.  On B200 the persistent grid held
 // the C3 pack at 90% of the copy peak, 8 rows per warp reach 99-100% (DESIGN.md
-// section 12); one row per warp pays a CTA launch per row.  `env` (e.g.
-// "RAILS_PACK_RPW") overrides rpw; 0 restores the persistent grid.
-inline long long wave_grid(int num_sms, int per_sm, long long need_ctas, const char* env,
-                           long long rpw = 8) {
-  if (const char* v = getenv(env)) rpw = atoll(v);
+// section 12); one row per warp pays a CTA launch per row.  rpw = 0: the persistent
+// grid (one wave of resident CTAs).
+inline long long wave_grid(int num_sms, int per_sm, long long need_ctas, long long rpw) {
   const long long resident = (long long)num_sms * (per_sm < 1 ? 1 : per_sm);
   long long grid = rpw >= 1 ? (need_ctas + rpw - 1) / rpw : resident;
   if (grid < resident) grid = resident;

@@ -399,7 +399,7 @@ static cudaError_t launch_pc(const LaunchCtx& c, int U, int nd, int d0, int M, i
   const long long rows = (long long)U * nd * N * Rcap;
   const long long need = (rows + CP_THREADS / 32 - 1) / (CP_THREADS / 32);
   // persistent grid by default: waves of CTAs measured equal here (RAILS_COMBINE_RPW=8)
-  const long long grid = wave_grid(c.num_sms, per_sm, need, "RAILS_COMBINE_RPW", 0);
+  const long long grid = wave_grid(c.num_sms, per_sm, need, 0);
   CSched cs{s.full_base, s.rem_rail, s.rem_off};
   k_pack_combine<VPL><<<(unsigned)grid, CP_THREADS, 0, c.stream>>>(
       U, nd, d0, M, N, Rcap, C, cshift_of(C), (const uint4*)y, in_off, rows_in, msgc, cs,
@@ -440,7 +440,7 @@ cudaError_t launch_unpack_combine(const LaunchCtx& c, int U, int nd, int d0, int
   const long long toks = (long long)U * nd * N * T;
   const long long need = (toks + UP_THREADS / 32 - 1) / (UP_THREADS / 32);
   // persistent grid by default: waves of CTAs measured 2% slower here (RAILS_UNPACK_RPW=8)
-  const long long grid = wave_grid(c.num_sms, per_sm, need, "RAILS_UNPACK_RPW", 0);
+  const long long grid = wave_grid(c.num_sms, per_sm, need, 0);
   CSched cs{s.full_base, s.rem_rail, s.rem_off};
   kern<<<(unsigned)grid, UP_THREADS, 0, c.stream>>>(
       U, nd, d0, M, N, T, k, C, cshift_of(C), topk, lut, n_inst, rank, w, (const uint4*)y, Rcap,

@@ -60,6 +60,8 @@ __global__ void __launch_bounds__(EV2_THREADS)
   long long* sQ = (long long*)ev_smem;  // [N][FT+1]
   int* sR = (int*)(sQ + N * (FT + 1));  // [N][FT+1]
   if (threadIdx.x < 32) sS[threadIdx.x] = sSe[threadIdx.x] = sSu[threadIdx.x] = 0;
+  const bool jfix = (EV2_THREADS % N) == 0, wlanes = (32 % N) == 0;
+  unsigned long long ps = 0, pe = 0, pu = 0;
   for (int f0 = 0; f0 < M; f0 += FT) {
     const int ft = min(FT, M - f0);
     __syncthreads();
@@ -107,35 +109,72 @@ __global__ void __launch_bounds__(EV2_THREADS)
       sR[g * (FT + 1) + fl] = r;
     }
     __syncthreads();
-    // stage 2: thread per (fl, j)
-    for (int t = threadIdx.x; t < ft * N; t += EV2_THREADS) {
+    // stage 2: thread per (fl, j).  When N divides the block, j = t mod N is the
+    // same for a thread in every tile, so S / S_e / S_u accumulate in registers;
+    // when N divides 32 the column sum of fl is a shuffle reduction over its N
+    // consecutive lanes (64-bit shared atomics are CAS loops on this GPU); other N
+    // use shared atomics.
+    for (int t0 = 0; t0 < ft * N; t0 += EV2_THREADS) {
+      const int t = t0 + threadIdx.x;
       const int fl = t / N, j = t - (t / N) * N;
       const int f = f0 + fl;
-      if (f == d) continue;
-      long long full = 0;
-      for (int g = 0; g < N; ++g) {
-        const long long qa = sQ[g * (FT + 1) + fl], qb = sQ[g * (FT + 1) + fl + 1];
-        const int ra = sR[g * (FT + 1) + fl], rb = sR[g * (FT + 1) + fl + 1];
-        full += (qb - qa) + (j < rb ? 1 : 0) - (j < ra ? 1 : 0);
+      const bool act = t < ft * N && f != d;
+      unsigned long long Rv = 0, Rev = 0, Ruv = 0;
+      if (act) {
+        long long full = 0;
+        for (int g = 0; g < N; ++g) {
+          const long long qa = sQ[g * (FT + 1) + fl], qb = sQ[g * (FT + 1) + fl + 1];
+          const int ra = sR[g * (FT + 1) + fl], rb = sR[g * (FT + 1) + fl + 1];
+          full += (qb - qa) + (j < rb ? 1 : 0) - (j < ra ? 1 : 0);
+        }
+        Rv = (unsigned long long)(full * C) + (((unsigned long long)aRhi[t] << 32) | aRlo[t]);
+        Rev = ((unsigned long long)aEhi[t] << 32) | aElo[t];
+        Ruv = ((unsigned long long)aQhi[fl] << 32) | aQlo[fl];
+        for (int r = j + 1; r < N; ++r) Ruv += cU[fl * N + r];
+        if (Rv) atomicAdd(rs + RL.R() + (long long)f * N + j, Rv);
+        if (Rev) atomicAdd(rs + RL.Re() + (long long)f * N + j, Rev);
+        if (Ruv) atomicAdd(rs + RL.Ru() + (long long)f * N + j, Ruv);
       }
-      const unsigned long long Rv =
-          (unsigned long long)(full * C) + (((unsigned long long)aRhi[t] << 32) | aRlo[t]);
-      const unsigned long long Rev = ((unsigned long long)aEhi[t] << 32) | aElo[t];
-      unsigned long long Ruv = ((unsigned long long)aQhi[fl] << 32) | aQlo[fl];
-      for (int r = j + 1; r < N; ++r) Ruv += cU[fl * N + r];
-      if (Rv) atomicAdd(rs + RL.R() + (long long)f * N + j, Rv);
-      if (Rev) atomicAdd(rs + RL.Re() + (long long)f * N + j, Rev);
-      if (Ruv) atomicAdd(rs + RL.Ru() + (long long)f * N + j, Ruv);
-      if (Rv) {
-        atomicAdd(&sS[j], Rv);  // 64-bit shared atomics: few per (f, j), off the hot loop
+      if (jfix) {
+        ps += Rv;
+        pe += Rev;
+        pu += Ruv;
+      } else if (act) {
+        if (Rv) atomicAdd(&sS[j], Rv);
+        if (Rev) atomicAdd(&sSe[j], Rev);
+        if (Ruv) atomicAdd(&sSu[j], Ruv);
+      }
+      if (wlanes) {
+        unsigned long long v = Rv;
+        for (int o = 1; o < N; o <<= 1) v += __shfl_xor_sync(FULL, v, o);
+        if (act && j == 0 && v) atomicAdd(rs + RL.col() + f, v);
+      } else if (act && Rv) {
         atomicAdd(&sCol[fl], Rv);
       }
-      if (Rev) atomicAdd(&sSe[j], Rev);
-      if (Ruv) atomicAdd(&sSu[j], Ruv);
     }
     __syncthreads();
-    for (int fl = threadIdx.x; fl < ft; fl += EV2_THREADS)
-      if (sCol[fl]) atomicAdd(rs + RL.col() + f0 + fl, sCol[fl]);
+    if (!wlanes)
+      for (int fl = threadIdx.x; fl < ft; fl += EV2_THREADS)
+        if (sCol[fl]) atomicAdd(rs + RL.col() + f0 + fl, sCol[fl]);
+  }
+  if (jfix) {  // per-rail totals of the register partials (thread t holds rail t mod N)
+    __syncthreads();
+    __shared__ unsigned long long part[3][EV2_THREADS];
+    part[0][threadIdx.x] = ps;
+    part[1][threadIdx.x] = pe;
+    part[2][threadIdx.x] = pu;
+    __syncthreads();
+    if (threadIdx.x < N) {
+      unsigned long long a = 0, b = 0, c2 = 0;
+      for (int t = threadIdx.x; t < EV2_THREADS; t += N) {
+        a += part[0][t];
+        b += part[1][t];
+        c2 += part[2][t];
+      }
+      sS[threadIdx.x] = a;
+      sSe[threadIdx.x] = b;
+      sSu[threadIdx.x] = c2;
+    }
   }
   __syncthreads();
   if (threadIdx.x >= 32) return;

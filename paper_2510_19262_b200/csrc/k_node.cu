@@ -67,53 +67,6 @@ struct NodeArgs {
   int* err;
 };
 
-// Alg. 2 step 4 (R#34): per-rail round-robin QP index in assignment
-// order.  The chain results are in sorted (= assignment) order, so the QP of the
-// p-th remainder is (full chunks on its rail + remainders on its rail before p) mod
-// Q, full chunks being assigned first (i mod N).  Warp w owns a contiguous slice:
-// pass 1 counts the slice's items per rail; the per-warp starting counters are an
-// exclusive scan over warps (plus rail j's full chunks); pass 2 ranks each 32-item
-// batch by rail with a ballot multi-split and advances the counters.
-__device__ void qp_rank_block(int N, int Q, long long nf, int nr, const uint64_t* res,
-                              uint32_t* out) {
-  __shared__ unsigned cnt[NODE_MAX_THREADS / 32][32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, W = blockDim.x >> 5;
-  const int per = (((nr + W - 1) / W) + 31) & ~31;
-  const int beg = wid * per, end = min(nr, beg + per);
-  const unsigned lt = lanemask_lt();
-  cnt[wid][lane] = 0;
-  __syncwarp();
-  for (int p0 = beg; p0 < end; p0 += 32) {
-    const int p = p0 + lane;
-    const unsigned r = p < end ? (unsigned)(res[p] >> 56) : 0u;
-    const unsigned peers = warp_match_nb<5>(r, p < end);
-    if (p < end && (peers & lt) == 0) cnt[wid][r] += __popc(peers);
-    __syncwarp();
-  }
-  __syncthreads();
-  const unsigned q = (unsigned)Q;
-  if (threadIdx.x < 32) {  // counters are kept modulo Q from here on (32-bit math)
-    const int j = threadIdx.x;
-    unsigned run = (unsigned)((nf / N + ((long long)j < nf % N ? 1 : 0)) % Q);
-    for (int w = 0; w < W; ++w) {
-      const unsigned c = cnt[w][j] % q;
-      cnt[w][j] = run;
-      run = (run + c) % q;
-    }
-  }
-  __syncthreads();
-  for (int p0 = beg; p0 < end; p0 += 32) {
-    const int p = p0 + lane;
-    const unsigned r = p < end ? (unsigned)(res[p] >> 56) : 0u;
-    const unsigned peers = warp_match_nb<5>(r, p < end);
-    if (p < end) out[p] = (cnt[wid][r] + __popc(peers & lt)) % q;
-    __syncwarp();
-    if (p < end && (peers & lt) == 0) cnt[wid][r] = (cnt[wid][r] + __popc(peers)) % q;
-    __syncwarp();
-  }
-  __syncthreads();
-}
-
 // number of the node-global full chunks 0..x-1 that land on rail j (i mod N == j)
 __device__ __forceinline__ long long full_on_rail(long long x, int N, int j) {
   long long q;
@@ -513,7 +466,8 @@ static NodePlan node_plan(int M, int N, long long C, bool eval, long long nseg, 
 }
 
 // workspace: [256 B header][acc: U x rec int64][counters: U + 1 u32, 256-aligned]
-//            [res_g u64: nseg x NG][qp_g u32: nseg x NG][sort spill when N*G > 16384]
+//            [res_g u64: nseg x NG][qp_g u32][w_g u32][inv_g i32 (k_chains)]
+//            [sort spill when N*G > 4096]
 static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct NodeWs {
@@ -521,6 +475,8 @@ struct NodeWs {
   unsigned* cnt;
   uint64_t* res_g;
   uint32_t* qp_g;
+  uint32_t* w_g;    // k_chains: sorted sizes
+  int32_t* inv_g;   // k_chains: inverse permutation
   uint8_t* scratch;
   size_t bytes;
 };
@@ -538,6 +494,10 @@ static NodeWs node_ws(void* ws, int U, int nd, int M, int N) {
   w.res_g = (uint64_t*)(b + o);
   o = al256(o + (size_t)nseg * NG * 8);
   w.qp_g = (uint32_t*)(b + o);
+  o = al256(o + (size_t)nseg * NG * 4);
+  w.w_g = (uint32_t*)(b + o);
+  o = al256(o + (size_t)nseg * NG * 4);
+  w.inv_g = (int32_t*)(b + o);
   o = al256(o + (size_t)nseg * NG * 4);
   w.scratch = b + o;
   if (NG > NODE_SMEM_ITEMS / 4) o += (size_t)nseg * (NG * (2 * 4 + 2 * 4) + 64);
@@ -572,8 +532,12 @@ static cudaError_t launch_eval_t(const LaunchCtx& c, const NodePlan& p, unsigned
     return net ? launch_k<uint32_t, 8, true, EVAL>(c, p, grid, a)
                : launch_k<uint32_t, 0, true, EVAL>(c, p, grid, a);
   }
-  return net ? launch_k<uint32_t, 8, false, EVAL>(c, p, grid, a)
-             : launch_k<uint32_t, 0, false, EVAL>(c, p, grid, a);
+  if constexpr (EVAL) {
+    return cudaErrorInvalidConfiguration;  // the fused evaluation needs the sort in smem
+  } else {
+    return net ? launch_k<uint32_t, 8, false, false>(c, p, grid, a)
+               : launch_k<uint32_t, 0, false, false>(c, p, grid, a);
+  }
 }
 
 // rails_lpt_schedule[_qp] (ev == nullptr) and rails_schedule_eval.  Returns
@@ -585,9 +549,23 @@ cudaError_t launch_node(const LaunchCtx& c, int U, int nd, int d0, int M, int N,
                         const rails_final_t* fin, int64_t* rail_base, int64_t* rail_total,
                         bool* fused) {
   const long long NG = (long long)N * M * N, nseg = (long long)U * nd;
-  NodePlan p = node_plan(M, N, C, ev != nullptr, nseg, c.num_sms);
-  if (fused) *fused = p.eval_fused;
   const NodeWs w = node_ws(ws, U, nd, M, N);
+  const int cshift = (C & (C - 1)) == 0 ? ceil_log2(C) : -1;
+  const int nbits = ceil_log2(C > 1 ? C - 1 : 1) + 1;
+  if (fused) *fused = false;
+  if (nseg > 2LL * c.num_sms) {
+    // many segments (C2's 16 000, a C4 iteration's 4 096): per-phase kernels at their
+    // own occupancy measured faster than one CTA walking every phase (k_chains.cu)
+    return launch_chains(c, U, nd, d0, M, N, C, msg, s, w.res_g, w.qp_g, w.w_g, w.inv_g,
+                         w.scratch, rem_qp, qps_per_rail, cshift, nbits);
+  }
+  NodePlan p = node_plan(M, N, C, ev != nullptr, nseg, c.num_sms);
+  if (p.eval_fused && !p.smem_sort) {
+    // the sort would spill to global memory to make room for the evaluation: the
+    // schedule alone (sort in shared memory) plus rails_eval's kernel measured faster
+    p = node_plan(M, N, C, false, nseg, c.num_sms);
+  }
+  if (fused) *fused = p.eval_fused;
   NodeArgs a{};
   a.msg = msg;
   a.NG = NG;
@@ -597,8 +575,8 @@ cudaError_t launch_node(const LaunchCtx& c, int U, int nd, int d0, int M, int N,
   a.nd = nd;
   a.U = U;
   a.C = C;
-  a.cshift = (C & (C - 1)) == 0 ? ceil_log2(C) : -1;
-  a.nbits = ceil_log2(C > 1 ? C - 1 : 1) + 1;
+  a.cshift = cshift;
+  a.nbits = nbits;
   a.seed = seed;
   a.R2 = R2;
   a.s = s;

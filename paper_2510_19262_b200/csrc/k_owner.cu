@@ -212,7 +212,7 @@ static cudaError_t launch_ov(const LaunchCtx& c, int U, int nd, int d0, int M, i
   if (per_sm < 1) per_sm = 1;
   const long long rows = (long long)U * nd * ng * T;
   const long long need = (rows + OWN_THREADS / 32 - 1) / (OWN_THREADS / 32);
-  const long long grid = wave_grid(c.num_sms, per_sm, need, "RAILS_OWNER_RPW");
+  const long long grid = wave_grid(c.num_sms, per_sm, need, 8);
   kern<<<(unsigned)grid, OWN_THREADS, 0, c.stream>>>(
       U, nd, d0, M, N, g0, ng, T, k, C, cshift, (const uint4*)x, topk, lut, n_inst, rank, msg,
       RB, s.full_base, s.rem_rail, s.rem_off, rail_base, rp, c.err);
@@ -232,10 +232,7 @@ static cudaError_t launch_om(const LaunchCtx& c, int U, int nd, int d0, int M, i
   if (vpl <= V)                                                                            \
     return launch_ov<V, MULTI>(c, U, nd, d0, M, N, g0, ng, T, k, C, cshift, x, topk, lut,  \
                                n_inst, rank, msg, RB, s, rail_base, rp);
-  RAILS_OWN_CASE(1)
-  RAILS_OWN_CASE(2)
   RAILS_OWN_CASE(4)
-  RAILS_OWN_CASE(8)
 #undef RAILS_OWN_CASE
   // rows over 8 KiB in 8 KiB windows, as k_pack (more resident warps)
   return launch_ov<16, MULTI>(c, U, nd, d0, M, N, g0, ng, T, k, C, cshift, x, topk, lut, n_inst,

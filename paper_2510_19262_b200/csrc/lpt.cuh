@@ -1,6 +1,7 @@
 // lpt.cuh -- a4: the LPT assignment chain of one (unit, node) (Alg. 2 step 3,
 // P:634-640), run by one warp over the node's remainder chunks already sorted by
-// size descending (R#4).  Included by k_node.cu only.
+// size descending (R#4), and the QP map of Alg. 2 step 4 (qp_rank_block).  Included
+// by k_node.cu and k_chains.cu.
 //
 // Full chunks are never materialised (k_node.cu header): they form the prefix of
 // the LPT order and are dealt round-robin, so the chain starts from the closed-form
@@ -337,6 +338,55 @@ __device__ long long lpt_chain_generic(const KeyT* __restrict__ key, int nr, int
   }
   if (lane < N && L < 0) flag_error(err, ERR_OVERFLOW);
   return L;
+}
+
+constexpr int QP_MAX_WARPS = 16;
+
+// Alg. 2 step 4 (R#34): per-rail round-robin QP index in assignment
+// order.  The chain results are in sorted (= assignment) order, so the QP of the
+// p-th remainder is (full chunks on its rail + remainders on its rail before p) mod
+// Q, full chunks being assigned first (i mod N).  Warp w owns a contiguous slice:
+// pass 1 counts the slice's items per rail; the per-warp starting counters are an
+// exclusive scan over warps (plus rail j's full chunks); pass 2 ranks each 32-item
+// batch by rail with a ballot multi-split and advances the counters.
+__device__ inline void qp_rank_block(int N, int Q, long long nf, int nr, const uint64_t* res,
+                              uint32_t* out) {
+  __shared__ unsigned cnt[QP_MAX_WARPS][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, W = blockDim.x >> 5;
+  const int per = (((nr + W - 1) / W) + 31) & ~31;
+  const int beg = wid * per, end = min(nr, beg + per);
+  const unsigned lt = lanemask_lt();
+  cnt[wid][lane] = 0;
+  __syncwarp();
+  for (int p0 = beg; p0 < end; p0 += 32) {
+    const int p = p0 + lane;
+    const unsigned r = p < end ? (unsigned)(res[p] >> 56) : 0u;
+    const unsigned peers = warp_match_nb<5>(r, p < end);
+    if (p < end && (peers & lt) == 0) cnt[wid][r] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  const unsigned q = (unsigned)Q;
+  if (threadIdx.x < 32) {  // counters are kept modulo Q from here on (32-bit math)
+    const int j = threadIdx.x;
+    unsigned run = (unsigned)((nf / N + ((long long)j < nf % N ? 1 : 0)) % Q);
+    for (int w = 0; w < W; ++w) {
+      const unsigned c = cnt[w][j] % q;
+      cnt[w][j] = run;
+      run = (run + c) % q;
+    }
+  }
+  __syncthreads();
+  for (int p0 = beg; p0 < end; p0 += 32) {
+    const int p = p0 + lane;
+    const unsigned r = p < end ? (unsigned)(res[p] >> 56) : 0u;
+    const unsigned peers = warp_match_nb<5>(r, p < end);
+    if (p < end) out[p] = (cnt[wid][r] + __popc(peers & lt)) % q;
+    __syncwarp();
+    if (p < end && (peers & lt) == 0) cnt[wid][r] = (cnt[wid][r] + __popc(peers)) % q;
+    __syncwarp();
+  }
+  __syncthreads();
 }
 
 }  // namespace rails

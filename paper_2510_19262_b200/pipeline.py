@@ -12,6 +12,7 @@ that hold different source nodes of the same units (torch.distributed / NCCL).
 """
 from __future__ import annotations
 
+import contextlib
 from typing import Callable
 
 import torch
@@ -19,10 +20,16 @@ import torch
 from . import rails
 
 
+def _nvtx(on: bool, name: str):
+    """NVTX range around one phase (seen by nsys / ncu range filters) when enabled."""
+    return torch.cuda.nvtx.range(name) if on else contextlib.nullcontext()
+
+
 class RoutingPipeline:
     def __init__(self, M: int, N: int, T: int, k: int, row_bytes: int, chunk_bytes: int,
                  U: int, d0: int, nd: int, n_inst: int, device, R2: float = 5.0e10,
-                 ecmp_seed: int = 0x9E3779B97F4A7C15, out_cap: int | None = None):
+                 ecmp_seed: int = 0x9E3779B97F4A7C15, out_cap: int | None = None,
+                 nvtx: bool = False):
         self.tp = rails.topo(M, N, chunk_bytes, R2, 0.0, ecmp_seed)
         self.sh = rails.shard(U, d0, nd)
         self.M, self.N, self.T, self.k, self.RB, self.C = M, N, T, k, row_bytes, chunk_bytes
@@ -39,6 +46,7 @@ class RoutingPipeline:
         self.rail_base = torch.empty((U, nd, N), dtype=torch.int64, device=dev)
         self.total = torch.empty(1, dtype=torch.int64, device=dev)
         self.holds_all = d0 == 0 and nd == M  # the fused kernel can finalize the units
+        self.nvtx = nvtx
         # every remote (t,s) copy is at most one row: a tight upper bound needing no sync
         cap = out_cap if out_cap is not None else U * nd * N * T * k * row_bytes
         self.out = torch.empty(cap, dtype=torch.uint8, device=dev)
@@ -46,30 +54,34 @@ class RoutingPipeline:
     def schedule_part(self, topk: torch.Tensor, lut: torch.Tensor, stream=None):
         """a1 + the fused a2-a5 kernel (schedule, eval, rail offsets; the finalize too
         when this pipeline holds every node of its units)."""
-        rails.histogram(self.tp, self.sh, topk, lut, self.RB,
-                        out=(self.counts, self.msg, self.rank), stream=stream)
-        rails.schedule_eval(self.tp, self.sh, self.msg, self.sched, self.ev, self.ws,
-                            final=self.final if self.holds_all else None,
-                            rail_base=self.rail_base, rail_total=self.total, stream=stream)
+        with _nvtx(self.nvtx, "a1 histogram"):
+            rails.histogram(self.tp, self.sh, topk, lut, self.RB,
+                            out=(self.counts, self.msg, self.rank), stream=stream)
+        with _nvtx(self.nvtx, "a2-a5 schedule+eval"):
+            rails.schedule_eval(self.tp, self.sh, self.msg, self.sched, self.ev, self.ws,
+                                final=self.final if self.holds_all else None,
+                                rail_base=self.rail_base, rail_total=self.total, stream=stream)
 
     def finalize_part(self, reduce: Callable | None = None, stream=None):
         """a6 + finalize for pipelines holding a subset of the nodes (no-op otherwise:
         the fused kernel already finalized)."""
-        if reduce is None:
-            if not self.holds_all:
+        if reduce is None and self.holds_all:
+            return
+        with _nvtx(self.nvtx, "a6 exchange + finalize"):
+            if reduce is None:
                 rails.eval_finalize(self.tp, self.U, self.ev.red_sum, self.ev.red_max,
                                     out=self.final, stream=stream)
-            return
-        if hasattr(reduce, "finalize"):  # fused a6 + finalize over peer memory
-            reduce.finalize(self.ev.red_sum, self.ev.red_max, self.final, stream=stream)
-            return
-        reduce(self.ev.red_sum, self.ev.red_max)
-        rails.eval_finalize(self.tp, self.U, self.ev.red_sum, self.ev.red_max, out=self.final,
-                            stream=stream)
+            elif hasattr(reduce, "finalize"):  # fused a6 + finalize over peer memory
+                reduce.finalize(self.ev.red_sum, self.ev.red_max, self.final, stream=stream)
+            else:
+                reduce(self.ev.red_sum, self.ev.red_max)
+                rails.eval_finalize(self.tp, self.U, self.ev.red_sum, self.ev.red_max,
+                                    out=self.final, stream=stream)
 
     def pack_part(self, topk, lut, x, stream=None):
-        rails.pack(self.tp, self.sh, self.T, self.k, x, topk, lut, self.rank, self.msg, self.RB,
-                   self.sched, self.rail_base, self.out, stream=stream)
+        with _nvtx(self.nvtx, "a7 pack"):
+            rails.pack(self.tp, self.sh, self.T, self.k, x, topk, lut, self.rank, self.msg,
+                       self.RB, self.sched, self.rail_base, self.out, stream=stream)
 
     def step(self, topk, lut, x, reduce: Callable | None = None, stream=None):
         self.schedule_part(topk, lut, stream)

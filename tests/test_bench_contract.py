@@ -31,5 +31,22 @@ def test_reference_arm_line():
     assert d["cpu_baseline"]["cores"] >= 1 and d["cpu_baseline"]["sample"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     # the same workload description as the GPU arm (bench.arm_config)
-    assert d["config"]["workload"] == "c2" and d["config"]["units"] == 1000
+    assert d["config"]["workload"].startswith("c2") and d["config"]["units"] == 1000
     assert d["config"]["parallelism"] == "nodes1"
+    assert "l2" in d["config"]
+
+
+def test_arm_config_per_workload():
+    sys.path.insert(0, ROOT)
+    import bench
+
+    class A:
+        workload, scaling, reduce = "c3", "weak", "peer"
+    c = bench.arm_config(A, 1)
+    assert c["units"] == 1 and c["nodes_per_rank"] == 64 and "16.0 GiB payload" in c["l2"]
+    A.workload = "c4"
+    c = bench.arm_config(A, 8)
+    assert c["layers_per_rank"] == 4 and c["units"] == 32 and "routing ids" in c["l2"]
+    A.workload, A.scaling = "c3", "strong"
+    c = bench.arm_config(A, 4)
+    assert c["units"] == 1 and c["nodes_per_rank"] == 16 and "4.0 GiB payload" in c["l2"]

@@ -99,3 +99,30 @@ def test_fuzz_routing_pack(seed):
     for u in range(U):
         for dl in range(nd):
             _oracle_pack_check(pipe, topk, lut, x, u, dl)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_fuzz_many_segments(seed):
+    """More (unit, node) segments than 2 x the SM count: the per-phase kernels of
+    k_chains.cu schedule them and rails_eval's kernel evaluates them (the fused
+    per-node kernel covers the few-segment shapes above) -- same outputs."""
+    rng = np.random.default_rng(3000 + seed)
+    M = int(rng.integers(2, 6))
+    N = int(rng.choice([1, 3, 4, 8, 8, 8]))
+    C = int(rng.choice([7, 100, 4096, 32768, 1 << 20]))
+    U = int(rng.integers(320 // M + 1, 700 // M + 2))
+    msg = _matrix(rng, U, M, N)
+    pipe = MatrixPipeline(M, N, C, U, 0, M, DEV)
+    pipe.step(torch.from_numpy(msg).to(DEV))
+    torch.cuda.synchronize()
+    for u in rng.choice(U, size=6, replace=False):
+        scheds = [oracle.schedule_node(msg[u, d], C) for d in range(M)]
+        for d in range(M):
+            compare_schedule(pipe.sched, u, d, scheds[d], f"seed{seed} u{u} d{d}")
+        ev = oracle_eval_from_scheds(M, N, msg[u], scheds)
+        assert np.array_equal(pipe.ev.S[u].cpu().numpy(), ev["S"])
+        assert np.array_equal(pipe.ev.S_u[u].cpu().numpy(), ev["S_u"])
+        for k in ("maxload", "maxload_e", "maxload_u", "total"):
+            assert int(pipe.final[k][u]) == ev[k], (seed, k)
+        for k in ("T", "T_star", "busbw", "T_e", "busbw_e", "T_u", "busbw_u"):
+            assert rel_err(float(pipe.final[k][u]), ev[k]) <= 1e-6, (seed, k)

@@ -449,114 +449,90 @@ def test_report_max_float_error():
     print(f"max relative float error observed vs oracle: {MAX_ERR['v']:.3g}")
 
 
-@pytest.mark.parametrize("impl", ["1", "3"])
-def test_schedule_parity_alternate_chain_kernels(impl, monkeypatch):
-    # the generic warp chain (1) and the thread-per-chain kernel (3) stay
-    # selectable (RAILS_CHAIN_IMPL) and exact
-    monkeypatch.setenv("RAILS_CHAIN_IMPL", impl)
-    rng = np.random.default_rng(77)
-    for (M, N, C, U, mult) in [(40, 8, 32768, 4, 12288), (5, 4, 65536, 2, 1), (30, 2, 4096, 3, 100)]:
-        msg = random_msg(rng, U, M, N, p=0.8, hi=40, mult=mult) if mult > 1 else \
-            random_msg(rng, U, M, N, p=0.8, hi=400000)
-        s = rails.lpt_schedule(rails.topo(M, N, C), rails.shard(U, 0, M), torch.from_numpy(msg).to(DEV))
-        for u in range(U):
-            for d in range(M):
-                compare_schedule(s, u, d, oracle.schedule_node(msg[u, d], C), f"impl{impl} u{u} d{d}")
+@pytest.mark.parametrize("M,N,C,U,mult", [
+    (40, 8, 32768, 4, 12288),     # 160 segments: fused per-node kernel, N = 8 network
+    (40, 8, 32768, 12, 12288),    # 480 segments: k_chains (warp-staged chain)
+    (5, 4, 65536, 2, 1),          # N = 4: generic redux chain (fused kernel)
+    (5, 4, 65536, 80, 1),         # N = 4, 400 segments: generic chain of k_chains
+    (30, 2, 4096, 3, 100),
+    (6, 8, 1 << 24, 2, 1),        # C >= 2^23: generic chain on N = 8
+    (6, 8, 1 << 24, 60, 1),       # ... in k_chains
+    (3, 5, 1 << 27, 2, 1),        # C >= 2^26: 64-bit butterfly argmin
+])
+def test_schedule_parity_both_paths(M, N, C, U, mult):
+    """rails_lpt_schedule picks the fused per-node kernel for few segments and the
+    per-phase kernels (k_chains.cu) for more than 2 x the SM count; within each, the
+    N = 8 sorted-register network or the generic chain by N and C.  All exact."""
+    rng = np.random.default_rng(77 + U)
+    msg = random_msg(rng, U, M, N, p=0.8, hi=40, mult=mult) if mult > 1 else \
+        random_msg(rng, U, M, N, p=0.8, hi=min(4 * C, 1 << 40))
+    s = rails.lpt_schedule(rails.topo(M, N, C), rails.shard(U, 0, M), torch.from_numpy(msg).to(DEV))
+    for u in sorted(set([0, U - 1, U // 2])):
+        for d in range(M):
+            compare_schedule(s, u, d, oracle.schedule_node(msg[u, d], C), f"U{U} u{u} d{d}")
 
 
-@pytest.mark.parametrize("impl", ["1", "3"])
-def test_schedule_parity_alternate_expand(impl, monkeypatch):
-    # the expand of the chain results into rem_rail / rem_off (/ rem_qp): one
-    # message per thread (1) and the segment-staged gather (3) stay exact next to
-    # the default 4-messages-per-thread kernel
-    monkeypatch.setenv("RAILS_EXPAND_IMPL", impl)
-    rng = np.random.default_rng(78)
-    for (M, N, C, U) in [(16, 8, 1 << 20, 3), (5, 3, 1000, 2), (70, 8, 32768, 1)]:
-        msg = random_msg(rng, U, M, N, p=0.8, hi=3_000_000)
-        tp, sh = rails.topo(M, N, C), rails.shard(U, 0, M)
-        s = rails.lpt_schedule(tp, sh, torch.from_numpy(msg).to(DEV))
-        for u in range(U):
-            for d in range(M):
-                compare_schedule(s, u, d, oracle.schedule_node(msg[u, d], C), f"x{impl} u{u} d{d}")
-
-
-@pytest.mark.parametrize("impl", ["2", "3"])
-def test_pack_parity_alternate_impls(impl, monkeypatch):
-    # the TMA bulk-copy packs (RAILS_PACK_IMPL=2: per-row metadata; 3: metadata
-    # batched per 32 rows) stay selectable and byte-exact
-    monkeypatch.setenv("RAILS_PACK_IMPL", impl)
-    for (M, N, T, k, E, RB, C, U, d0, nd) in [(4, 4, 512, 2, 8, 1024, 4096, 1, 0, 4),
-                                               (5, 8, 128, 2, 8, 8192, 32768, 1, 0, 5)]:
-        topk_all, lut = routing_inputs(M, N, T, k, E, 7, 0, U)
-        topk = topk_all[:, d0:d0 + nd].contiguous()
-        x = torch.stack([gen.payload(M, N, T, RB, 3, u, d0, nd) for u in range(U)])
-        pipe = RoutingPipeline(M, N, T, k, RB, C, U, d0, nd, lut.numel(), DEV)
-        pipe.step(topk.to(DEV), lut.to(DEV), x.to(DEV))
-        torch.cuda.synchronize()
-        for u in range(U):
-            for dl in range(nd):
-                _oracle_pack_check(pipe, topk, lut, x, u, dl)
-
-
-def test_histogram_parity_async_stage(monkeypatch):
-    # the cp.async-staged histogram variant (RAILS_HIST_ASYNC=1) stays exact
-    monkeypatch.setenv("RAILS_HIST_ASYNC", "1")
-    monkeypatch.setenv("RAILS_HIST_IMPL", "3")  # warp-per-segment kernel at any size
-    M, N, T, k, E, U = 300, 8, 64, 2, 8, 1   # G = 2400
-    topk_all, lut = routing_inputs(M, N, T, k, E, 11, 0, U)
-    topk = topk_all[:, 0:2].contiguous()
-    tp, sh = rails.topo(M, N, 65536), rails.shard(U, 0, 2)
-    counts, msg, rank = rails.histogram(tp, sh, topk.to(DEV), lut.to(DEV), 8192)
-    for dl in range(2):
-        c, m, r = oracle.histogram_node(M, N, dl, T, k, topk[0, dl].numpy(), lut.numpy(), 8192)
-        assert np.array_equal(counts[0, dl].cpu().numpy(), c)
-        assert np.array_equal(rank[0, dl].cpu().numpy(), r)
-
-
-@pytest.mark.parametrize("atom,slut", [("0", "1"), ("0", "0"), ("1", "1"), ("1", "0")])
-def test_histogram_parity_w1_variants(atom, slut, monkeypatch):
-    # the warp-per-segment kernel with the LUT in shared memory or read through L1, and
-    # its atomic-add ranking variant (RAILS_HIST_ATOM=1); G = 4 makes nearly every
-    # 32-id group collide, G = 512 rarely; T*k values leave a ragged last batch
-    monkeypatch.setenv("RAILS_HIST_IMPL", "3")
-    monkeypatch.setenv("RAILS_HIST_ATOM", atom)
-    monkeypatch.setenv("RAILS_HIST_SLUT", slut)
-    for (M, N, T, k, E) in [(2, 2, 1000, 2, 4), (64, 8, 777, 2, 8), (3, 4, 4096, 4, 8),
-                            (128, 8, 4096, 2, 8), (2, 1, 33, 1, 2)]:
-        topk_all, lut = routing_inputs(M, N, T, k, E, 17, 0, 1)
-        nd = min(M, 3)
-        topk = topk_all[:, 0:nd].contiguous()
-        tp, sh = rails.topo(M, N, 65536), rails.shard(1, 0, nd)
-        counts, msg, rank = rails.histogram(tp, sh, topk.to(DEV), lut.to(DEV), 4096)
+@pytest.mark.parametrize("M,N,T,k,E,RB,C,U,d0,nd", [
+    (4, 4, 512, 2, 8, 1024, 4096, 1, 0, 4),     # rows <= 2 KiB: 4 vectors per lane
+    (5, 8, 128, 2, 8, 8192, 32768, 1, 0, 5),    # 8 KiB rows: 16 vectors per lane
+    (3, 4, 100, 2, 8, 4096, 1024, 2, 1, 2),     # C < RB: per-vector chunk lookup
+    (3, 2, 64, 3, 6, 20480, 4096, 1, 0, 3),     # 20 KiB rows in 8 KiB windows, C < RB
+])
+def test_pack_parity_row_shapes(M, N, T, k, E, RB, C, U, d0, nd):
+    topk_all, lut = routing_inputs(M, N, T, k, E, 7, 0, U)
+    topk = topk_all[:, d0:d0 + nd].contiguous()
+    x = torch.stack([gen.payload(M, N, T, RB, 3, u, d0, nd) for u in range(U)])
+    pipe = RoutingPipeline(M, N, T, k, RB, C, U, d0, nd, lut.numel(), DEV)
+    pipe.step(topk.to(DEV), lut.to(DEV), x.to(DEV))
+    torch.cuda.synchronize()
+    for u in range(U):
         for dl in range(nd):
-            c, m, r = oracle.histogram_node(M, N, dl, T, k, topk[0, dl].numpy(), lut.numpy(), 4096)
-            assert np.array_equal(counts[0, dl].cpu().numpy(), c), (atom, slut, M, N, T)
-            assert np.array_equal(msg[0, dl].cpu().numpy(), m), (atom, slut, M, N, T)
-            assert np.array_equal(rank[0, dl].cpu().numpy(), r), (atom, slut, M, N, T)
+            _oracle_pack_check(pipe, topk, lut, x, u, dl)
 
 
-@pytest.mark.parametrize("match,w", [(None, None), ("0", "8"), ("0", "16"), ("0", "32"),
-                                     ("1", "16")])
-def test_histogram_parity_multiwarp_variants(match, w, monkeypatch):
-    # the multi-warp-per-segment kernel (C3's few segments): ranks by the tag path
-    # (default) or the per-bit ballot match (RAILS_HIST_MATCH=1), 8/16/32 warps
-    # per segment; G = 4 makes nearly every 32-id group collide, G = 512 almost never
-    monkeypatch.setenv("RAILS_HIST_IMPL", "1")
-    if match is not None:
-        monkeypatch.setenv("RAILS_HIST_MATCH", match)
-        monkeypatch.setenv("RAILS_HIST_W", w)
-    for (M, N, T, k, E) in [(2, 2, 1000, 2, 4), (64, 8, 777, 2, 8), (3, 4, 4096, 4, 8),
-                            (2, 4, 10000, 4, 8), (64, 8, 4096, 2, 8)]:
-        topk_all, lut = routing_inputs(M, N, T, k, E, 13, 0, 1)
-        nd = min(M, 2)
-        topk = topk_all[:, 0:nd].contiguous()
-        tp, sh = rails.topo(M, N, 65536), rails.shard(1, 0, nd)
-        counts, msg, rank = rails.histogram(tp, sh, topk.to(DEV), lut.to(DEV), 4096)
-        for dl in range(nd):
-            c, m, r = oracle.histogram_node(M, N, dl, T, k, topk[0, dl].numpy(), lut.numpy(), 4096)
-            assert np.array_equal(counts[0, dl].cpu().numpy(), c)
-            assert np.array_equal(msg[0, dl].cpu().numpy(), m)
-            assert np.array_equal(rank[0, dl].cpu().numpy(), r)
+def _hist_check(M, N, T, k, E, U, nd, RB=4096, with_rank=True, seed=17, nodes=None):
+    topk_all, lut = routing_inputs(M, N, T, k, E, seed, 0, U)
+    topk = topk_all[:, 0:nd].contiguous()
+    tp, sh = rails.topo(M, N, 65536), rails.shard(U, 0, nd)
+    counts, msg, rank = rails.histogram(tp, sh, topk.to(DEV), lut.to(DEV), RB, with_rank=with_rank)
+    for u in range(U):
+        for dl in (range(nd) if nodes is None else nodes):
+            c, m, r = oracle.histogram_node(M, N, dl, T, k, topk[u, dl].numpy(), lut.numpy(), RB)
+            assert np.array_equal(counts[u, dl].cpu().numpy(), c), (M, N, T, u, dl)
+            assert np.array_equal(msg[u, dl].cpu().numpy(), m), (M, N, T, u, dl)
+            if with_rank:
+                assert np.array_equal(rank[u, dl].cpu().numpy(), r), (M, N, T, u, dl)
+
+
+@pytest.mark.parametrize("M,N,T,k,E,U,nd,with_rank", [
+    (2, 2, 1000, 2, 4, 600, 2, True),       # G = 4: nearly every 32-id group collides
+    (64, 8, 777, 2, 8, 5, 64, True),        # ragged last batch, shared LUT
+    (128, 8, 300, 2, 8, 3, 128, False),     # no ranks
+    (600, 8, 64, 2, 8, 1, 300, True),       # n_inst = 4800: LUT read through L1
+])
+def test_histogram_parity_batched(M, N, T, k, E, U, nd, with_rank):
+    """>= 16 segments per SM: the warp-per-segment atomic-ranking kernel."""
+    _hist_check(M, N, T, k, E, U, nd, with_rank=with_rank, nodes=[0, nd - 1])
+
+
+@pytest.mark.parametrize("M,N,T,k,E,nd", [
+    (2, 2, 1000, 2, 4, 2),        # G = 4: 16 warps per segment, collisions everywhere
+    (64, 8, 777, 2, 8, 2),        # G = 512, 16 warps
+    (3, 4, 4096, 4, 8, 2),
+    (2, 4, 10000, 4, 8, 2),
+    (300, 8, 500, 2, 8, 2),       # G = 2400: 4 warps (sub-histograms in 64 KiB)
+    (1500, 8, 200, 2, 8, 1),      # G = 12000: 2 warps
+    (5000, 4, 64, 2, 4, 1),       # G = 20000: 1 warp
+])
+def test_histogram_parity_few_segments(M, N, T, k, E, nd):
+    """Few segments: W warps per segment (by G), two passes, tag-trick ranks."""
+    _hist_check(M, N, T, k, E, 1, nd)
+
+
+def test_histogram_parity_huge_segment():
+    """T*k >= 2^24: ranks past the tag trick's 24 bits use the per-bit ballot match."""
+    _hist_check(2, 1, (1 << 23) + 77, 2, 2, 1, 1, RB=16)
+
 
 
 def test_graph_replay_matches_eager():

@@ -79,13 +79,15 @@ def bench_routing(res, name, U):
                                         workspace=pipe.ws),
                      rails.eval(pipe.tp, pipe.sh, pipe.msg, pipe.sched, out=pipe.ev))
     tsp = timeit(split)
+    tsch = timeit(lambda: rails.lpt_schedule(pipe.tp, pipe.sh, pipe.msg, out=pipe.sched,
+                                             workspace=pipe.ws))
     tb = timeit(lambda: pipe.schedule_part(topk, lut))
     ne = topk.numel()
     G = pipe.M * pipe.N
     nseg = U * pipe.M * pipe.N
     hbytes = ne * 4 * 2 + nseg * G * (4 + 8)  # ids in, ranks out, counts + bytes out
     out = {"units": U, "nodes": U * pipe.M, "histogram": th, "fused_sched_eval": tf,
-           "schedule_then_eval": tsp,
+           "schedule_then_eval": tsp, "schedule_only_kernel": tsch,
            "schedule_part": tb, "hist_algorithmic_bytes": hbytes,
            "hist_gbs": round(hbytes / (th["median_us"] * 1e-6) / 1e9, 1),
            "nodes_per_s_schedule_part": round(U * pipe.M / (tb["median_us"] * 1e-6))}
