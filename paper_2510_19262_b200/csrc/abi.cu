@@ -94,6 +94,8 @@ extern "C" {
 
 int32_t rails_version(void) { return 200; }
 
+
+
 const char* rails_last_error(void) { return t_err; }
 
 int64_t rails_launch_count(int32_t reset) {

@@ -143,6 +143,17 @@ __device__ __forceinline__ bool wait_flag_ge(const uint32_t* f, uint32_t gen, in
   return true;
 }
 
+// Programmatic dependent launch (PDL): a kernel launched with programmatic stream
+// serialization may start while the previous kernel of its stream runs; pdl_wait()
+// blocks until that kernel has completed and its memory is visible.  The previous
+// kernel's pdl_trigger() lets the dependent grid be scheduled early (its CTAs then
+// sit in pdl_wait() on SMs the previous grid leaves free).  Both are no-ops for
+// ordinary launches.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ECMP rail (R#14): splitmix64 output step, this library's own copy.
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z += 0x9E3779B97F4A7C15ull;

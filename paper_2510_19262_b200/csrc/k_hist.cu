@@ -30,22 +30,27 @@ namespace rails {
 constexpr int HR_MAX_WARPS = 16;
 
 template <int UNR, bool TAG>
-__global__ void __launch_bounds__(HR_MAX_WARPS * 32)
+__global__ void __launch_bounds__(HR_MAX_WARPS * 32, 4)  // 4 x 16 warps per SM: one wave for C3
     k_hist_rank(const int32_t* __restrict__ topk, const int32_t* __restrict__ lut, int n_inst,
                 int M, int N, int ngs, int d0, int nd, int T, int k, long long RB, int hbits,
                 int32_t* __restrict__ counts, int64_t* __restrict__ msg,
                 int32_t* __restrict__ rank, int* err) {
-  extern __shared__ int32_t cnt[];  // [W][G]
+  extern __shared__ __align__(16) int32_t cnt[];  // [W][G]
+  pdl_trigger();  // the schedule kernel may be scheduled on the SMs this grid leaves free
   const int W = blockDim.x >> 5;
   const int G = M * N;
-  const long long cta = blockIdx.x;  // ((u*nd) + dl)*ngs + gl
-  const long long ul = cta / ngs;
-  const int d = d0 + (int)(ul % nd);
+  const unsigned cta = blockIdx.x;  // ((u*nd) + dl)*ngs + gl  (32-bit index math)
+  const unsigned ul = cta / (unsigned)ngs;
+  const int d = d0 + (int)(ul % (unsigned)nd);
   const long long ne = (long long)T * k;
-  const int32_t* __restrict__ src = topk + cta * ne;
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  for (int i = threadIdx.x; i < W * G; i += W * 32) cnt[i] = 0;
+  {  // zero the sub-histograms, 16 bytes per store
+    int4* c4 = reinterpret_cast<int4*>(cnt);
+    const int n4 = (W * G) >> 2;
+    for (int i = threadIdx.x; i < n4; i += blockDim.x) c4[i] = make_int4(0, 0, 0, 0);
+    for (int i = (n4 << 2) + threadIdx.x; i < W * G; i += blockDim.x) cnt[i] = 0;
+  }
   __syncthreads();
 
   // 32-bit indices inside the segment (T*k < 2^31: ranks are int32)
@@ -55,14 +60,20 @@ __global__ void __launch_bounds__(HR_MAX_WARPS * 32)
   const int end = min(nei, beg + seg);
   int32_t* my = cnt + wid * G;
   bool bad = false;
+  // this lane's id stream: one 64-bit base per warp segment, 32-bit offsets after it
+  const int32_t* __restrict__ src = topk + (size_t)cta * (size_t)ne + beg + lane;
 
   // ids of one batch -> destination GPUs (-1 = invalid or past the end); all
-  // loads of a batch, then all LUT lookups, are in flight together
-  auto fetch = [&](int base, int (&hv)[UNR]) {
+  // loads of a batch, then all LUT lookups, are in flight together.  Full batches
+  // need no bounds test (immediate offsets off one address).
+  auto fetch = [&](int off, int (&hv)[UNR]) {
+    if (beg + off + 32 * UNR <= end) {
 #pragma unroll
-    for (int j = 0; j < UNR; ++j) {
-      const int e = base + j * 32 + lane;
-      hv[j] = (e < end) ? __ldg(src + e) : -1;
+      for (int j = 0; j < UNR; ++j) hv[j] = __ldg(src + off + j * 32);
+    } else {
+#pragma unroll
+      for (int j = 0; j < UNR; ++j)
+        hv[j] = (beg + off + j * 32 + lane < end) ? __ldg(src + off + j * 32) : -1;
     }
 #pragma unroll
     for (int j = 0; j < UNR; ++j) {
@@ -72,12 +83,12 @@ __global__ void __launch_bounds__(HR_MAX_WARPS * 32)
   };
 
   // ---- pass 1: per-warp sub-histogram
-  for (int base = beg; base < end; base += 32 * UNR) {
+  for (int off = 0; beg + off < end; off += 32 * UNR) {
     int hv[UNR];
-    fetch(base, hv);
+    fetch(off, hv);
 #pragma unroll
     for (int j = 0; j < UNR; ++j) {
-      bad |= hv[j] < 0 && base + j * 32 + lane < end;
+      bad |= hv[j] < 0 && beg + off + j * 32 + lane < end;
       if (hv[j] >= 0) atomicAdd(&my[hv[j]], 1);  // private to this warp: order-free count
     }
   }
@@ -93,21 +104,21 @@ __global__ void __launch_bounds__(HR_MAX_WARPS * 32)
       cnt[w * G + h] = run;
       run += c;
     }
-    counts[cta * G + h] = run;
-    msg[cta * G + h] = ((unsigned)(h - d * N) < (unsigned)N) ? 0LL : (long long)run * RB;
+    counts[(size_t)cta * G + h] = run;
+    msg[(size_t)cta * G + h] = ((unsigned)(h - d * N) < (unsigned)N) ? 0LL : (long long)run * RB;
   }
   if (rank == nullptr) return;
   __syncthreads();
 
   // ---- pass 2: stable ranks
-  int32_t* __restrict__ dst = rank + cta * ne;
+  int32_t* __restrict__ dst = rank + (size_t)cta * (size_t)ne + beg + lane;
   const unsigned lt = lanemask_lt();
-  for (int base = beg; base < end; base += 32 * UNR) {
+  for (int off = 0; beg + off < end; off += 32 * UNR) {
     int hv[UNR];
-    fetch(base, hv);
+    fetch(off, hv);
 #pragma unroll
     for (int j = 0; j < UNR; ++j) {
-      const int e = base + j * 32 + lane;
+      const bool in = beg + off + j * 32 + lane < end;
       const int h = hv[j];
       const bool valid = h >= 0;
       if constexpr (TAG) {
@@ -129,7 +140,7 @@ __global__ void __launch_bounds__(HR_MAX_WARPS * 32)
         const unsigned below = peers & lt;
         if (valid && below == 0) my[h] = (int32_t)((c + __popc(peers)) & 0xffffff);
         __syncwarp();
-        if (e < end) dst[e] = valid ? c + __popc(below) : -1;
+        if (in) dst[off + j * 32] = valid ? c + __popc(below) : -1;
       } else {
         const unsigned peers = warp_match_bits((unsigned)h, hbits, valid);
         int r = -1;
@@ -137,7 +148,7 @@ __global__ void __launch_bounds__(HR_MAX_WARPS * 32)
         __syncwarp();
         if (valid && lane == __ffs(peers) - 1) my[h] += __popc(peers);
         __syncwarp();
-        if (e < end) dst[e] = r;
+        if (in) dst[off + j * 32] = r;
       }
     }
   }
@@ -174,6 +185,7 @@ __global__ void __launch_bounds__(HW_WARPS * 32, 8)
                long long nsegs, int32_t* __restrict__ counts, int64_t* __restrict__ msg,
                int32_t* __restrict__ rank, int* err) {
   extern __shared__ __align__(16) uint32_t sw1[];
+  pdl_trigger();
   const int G = M * N;
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long sg = (long long)blockIdx.x * HW_WARPS + wid;

@@ -31,9 +31,45 @@
 //    grid computes the rail offsets.  So a whole single-rank schedule + evaluation
 //    is one launch, and the workspace is left zeroed for the next call.
 #include "common.cuh"
+#ifdef RAILS_NODE_TIMING
+__device__ unsigned long long g_node_t[16];
+// chain path counters of CTA 0 (slots 12..15): runs, single steps, windows, groups of 8
+#define LPT_COUNT(i)                                                   \
+  do {                                                                 \
+    if (blockIdx.x == 0 && threadIdx.x == 0) g_node_t[12 + (i)] += 1; \
+  } while (0)
+#endif
 #include "eval.cuh"
 #include "lpt.cuh"
 #include "radix.cuh"
+
+#ifdef RAILS_NODE_TIMING
+// phase timestamps of CTA 0 (globaltimer ns), debug builds only (tools/node_timing.py)
+#define NODE_T(i)                                                         \
+  do {                                                                    \
+    if (blockIdx.x == 0 && threadIdx.x == 0) g_node_t[i] = globaltimer_ns(); \
+  } while (0)
+#define NODE_TL(i)                              \
+  do {                                          \
+    if (threadIdx.x == 0) g_node_t[i] = globaltimer_ns(); \
+  } while (0)
+extern "C" int rails_debug_node_reset() {
+  unsigned long long z[16] = {0};
+  return cudaMemcpyToSymbol(g_node_t, z, sizeof(z)) == cudaSuccess ? 0 : -5;
+}
+extern "C" int rails_debug_node_times(unsigned long long* host16) {
+  return cudaMemcpyFromSymbol(host16, g_node_t, 16 * sizeof(unsigned long long)) == cudaSuccess
+             ? 0
+             : -5;
+}
+#else
+#define NODE_T(i) \
+  do {            \
+  } while (0)
+#define NODE_TL(i) \
+  do {             \
+  } while (0)
+#endif
 
 namespace rails {
 
@@ -128,7 +164,11 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
     for (int i = threadIdx.x; i < M; i += blockDim.x) aQlo[i] = aQhi[i] = 0u;
     __syncthreads();
   }
+  // launched with programmatic stream serialization: everything above overlapped the
+  // histogram kernel's tail; its outputs (msg) are read from here on
+  pdl_wait();
 
+  NODE_T(1);
   // ---- phase A: full_base scan + remainder compaction (+ ECMP and uniform sums)
   // Tiles of blockDim * IPT messages, each thread owning IPT consecutive messages:
   // its loads are all in flight at once, one block scan per tile.
@@ -178,16 +218,6 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
       a.s.full_base[seg * NG + m] = fb;
       if constexpr (EVAL) {
         if (h % N == 0) sP[m / N] = fb;  // block (g, f = h/N) starts here
-        if (B[j] > 0) {
-          const int f = h / N;
-          const int e = ecmp_rail(a.seed, (long long)d * N + g, h, N);
-          add64_split(&aElo[f * N + e], &aEhi[f * N + e], (unsigned long long)B[j]);
-          long long qb;
-          int rb;
-          divmod_n(B[j], N, qb, rb);
-          if (qb) add64_split(&aQlo[f], &aQhi[f], (unsigned long long)qb);
-          if (rb) atomicAdd(&cU[f * N + rb], 1u);
-        }
       }
       fb += nf;
       if (rem > 0) {
@@ -217,6 +247,7 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
   }
   __syncthreads();
 
+  NODE_T(2);
   // ---- phase B: stable radix sort of the remainder keys
   const int which = radix_sort<KeyT, IdxT>(kA, iA, kB, iB, n, kor, kand, a.nbits, hist, sc);
   const KeyT* ks = which ? kB : kA;
@@ -227,9 +258,11 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += blockDim.x) inv[is[i]] = (IdxT)i;
 
+  NODE_T(3);
   // ---- phase C: warp 0 runs the LPT chain; the other warps add the full chunks
   uint64_t* res = a.res_smem ? (uint64_t*)(smem + a.res_off) : a.res_g + seg * NG;
   if (threadIdx.x < 32) {
+    NODE_T(4);
     if constexpr (NT != 0) {
       lpt_chain_net<NT, KeyT>(ks, n, C, nf_node, res, sL);
     } else {
@@ -239,6 +272,21 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
     __syncwarp();
     if (threadIdx.x < N) a.s.send_load[seg * N + threadIdx.x] = sL[threadIdx.x];
   } else if constexpr (EVAL) {
+    // the ECMP rails (R#13-R#14) and the uniform split (R#41) of every message, off
+    // the critical path while warp 0 runs the chain (msg is L2-resident: phase A read it)
+    for (unsigned m = threadIdx.x - 32; m < (unsigned)NG; m += blockDim.x - 32) {
+      const long long B = mg[m];
+      const int h = (int)(m % (unsigned)G), g = (int)(m / (unsigned)G);
+      if (B <= 0 || (h >= lo && h < hi)) continue;  // invalid entries were flagged in A
+      const int f = h / N;
+      const int e = ecmp_rail(a.seed, (long long)d * N + g, h, N);
+      add64_split(&aElo[f * N + e], &aEhi[f * N + e], (unsigned long long)B);
+      long long qb;
+      int rb;
+      divmod_n(B, N, qb, rb);
+      if (qb) add64_split(&aQlo[f], &aQhi[f], (unsigned long long)qb);
+      if (rb) atomicAdd(&cU[f * N + rb], 1u);
+    }
     for (long long t = threadIdx.x - 32; t < MN; t += blockDim.x - 32) {
       const int f = (int)(t / N), j = (int)(t - (long long)f * N);
       long long full = 0;
@@ -255,6 +303,7 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
   }
   __syncthreads();
 
+  NODE_T(5);
   // ---- phase D: QP map (optional), expand, remainders into R_d
   if (a.rem_qp) qp_rank_block(N, a.Q, nf_node, n, res, a.qp_g + seg * NG);
   const unsigned NGu = (unsigned)NG, Gu = (unsigned)G;  // N*G < 2^26 (M*N <= 2^20, N <= 32)
@@ -280,6 +329,7 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
   }
   if constexpr (!EVAL) return;
 
+  NODE_T(6);
   // ---- phase E: this node's receive contributions into the unit's accumulator
   __syncthreads();
   const long long rsl = RAILS_RED_SUM_LEN(M, N);
@@ -380,6 +430,7 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
     }
   }
 
+  NODE_T(7);
   // ---- phase F: the unit's last CTA publishes (and finalizes); the grid's last
   // CTA computes the rail offsets
   __syncthreads();
@@ -390,19 +441,55 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
   __syncthreads();
   if (s_last) {
     __threadfence();
+    // publish the unit's record (red_sum / red_max), re-zero the accumulator, and
+    // take the maxima the finalize needs in the same pass
     int64_t* rs = a.e.red_sum + u * rsl;
     int64_t* rm = a.e.red_max + u * RAILS_RED_MAX_LEN;
-    for (long long i = threadIdx.x; i < rec; i += blockDim.x) {
-      const long long v = (long long)__ldcg((const long long*)acc + i);
-      if (i < rsl) rs[i] = v;
-      else rm[i - rsl] = v;
-      acc[i] = 0;
+    long long mx[4] = {0, 0, 0, 0};  // max R, R_e, R_u, colsum
+    for (long long i0 = threadIdx.x; i0 < rec; i0 += 4LL * blockDim.x) {
+      long long v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const long long i = i0 + (long long)q * blockDim.x;
+        v[q] = i < rec ? (long long)__ldcg((const long long*)acc + i) : 0;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const long long i = i0 + (long long)q * blockDim.x;
+        if (i >= rec) break;
+        if (i < rsl) rs[i] = v[q];
+        else rm[i - rsl] = v[q];
+        acc[i] = 0;
+        const int cls = i < MN ? 0 : i < 2 * MN ? 1 : i < 3 * MN ? 2 : i < 3 * MN + M ? 3 : 4;
+        if (cls < 4) mx[cls] = max(mx[cls], v[q]);
+      }
     }
     if (threadIdx.x == 0) a.cnt[u] = 0;
+    __shared__ long long s_mx[4][NODE_MAX_THREADS / 32];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const long long w = warp_max(mx[q]);
+      if ((threadIdx.x & 31) == 0) s_mx[q][threadIdx.x >> 5] = w;
+    }
     __syncthreads();
-    if (a.do_final) block_finalize_unit<false>(u, M, N, a.R2, rs, rm, a.fin);
+    if (threadIdx.x == 0 && a.do_final) {
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) s_mx[q][0] = max(s_mx[q][0], s_mx[q][w]);
+      long long rmv[RAILS_RED_MAX_LEN];
+#pragma unroll
+      for (int q = 0; q < RAILS_RED_MAX_LEN; ++q) rmv[q] = rm[q];
+      finalize_unit(u, N, a.R2, s_mx[0][0], s_mx[1][0], s_mx[2][0], s_mx[3][0], rmv,
+                    rs[RL.tot()], rs[RL.tot() + 1], a.fin);
+    }
+    NODE_TL(10);
+    if (a.rail_base && (int)gridDim.x == a.nd) {  // one unit: this CTA is also the grid's last
+      block_rail_offsets<true>((long long)gridDim.x * N, a.s.send_load, a.rail_base,
+                               a.rail_total);
+      NODE_TL(11);
+    }
   }
-  if (a.rail_base) {
+  if (a.rail_base && (int)gridDim.x != a.nd) {
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
@@ -414,8 +501,10 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
       block_rail_offsets<true>((long long)gridDim.x * N, a.s.send_load, a.rail_base,
                                a.rail_total);
       if (threadIdx.x == 0) a.cnt[a.U] = 0;
+      NODE_TL(11);
     }
   }
+  NODE_T(8);
 }
 
 // ---------------------------------------------------------------- host side
@@ -516,9 +605,21 @@ static cudaError_t launch_k(const LaunchCtx& c, const NodePlan& p, unsigned grid
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)p.smem);
   if (e != cudaSuccess) return e;
-  kern<<<grid, p.threads, p.smem, c.stream>>>(a);
+  // PDL: the CTAs may be scheduled while the previous kernel (the histogram) runs and
+  // wait for it in pdl_wait(), hiding this launch's latency
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(p.threads);
+  cfg.dynamicSmemBytes = p.smem;
+  cfg.stream = c.stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, a);
   count_launch(1);
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 template <bool EVAL>

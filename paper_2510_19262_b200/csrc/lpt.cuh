@@ -27,6 +27,12 @@
 
 #include "common.cuh"
 
+#ifndef LPT_COUNT
+#define LPT_COUNT(i) \
+  do {               \
+  } while (0)
+#endif
+
 namespace rails {
 
 constexpr long long OFF_MASK = (1LL << 56) - 1;
@@ -214,8 +220,10 @@ __device__ void lpt_chain_net(const KeyT* __restrict__ key, int nr, long long C,
     if (i + 32 <= nr && W(i + 31) == w) {
       // a run [i, e) of equal sizes: single steps until the cyclic condition holds,
       // then the closed form written by all lanes
+      LPT_COUNT(0);
       const int e = run_end(key, i, nr, lane);
       while (i < e && K[NT - 1] - K[0] >= (w << 5)) {
+        LPT_COUNT(1);
         const uint64_t rv = lpt_step_v<NT>(K, w, base);
         if (lane == 0) res[i] = rv;
         lpt_rebase<NT>(K, base);
@@ -229,6 +237,7 @@ __device__ void lpt_chain_net(const KeyT* __restrict__ key, int nr, long long C,
       // group is 8 equal sizes w_l with K[NT-1] - K[0] < w_l << 5, each is dealt
       // cyclically, K is unchanged and base grows by (8/NT)*w_l, so the groups'
       // bases are an exclusive scan of those increments
+      LPT_COUNT(2);
       const int at = i + 8 * lane;
       uint32_t a = 0, b = 0;
       if (at + 8 <= nr) {
@@ -259,6 +268,7 @@ __device__ void lpt_chain_net(const KeyT* __restrict__ key, int nr, long long C,
       base += (long long)tot;
       i += 8 * nok;
     } else if (i + 8 <= nr && (i & 7) == 0) {
+      LPT_COUNT(3);
       uint32_t g8[8];
       uint64_t rr[8];
 #pragma unroll
@@ -267,6 +277,7 @@ __device__ void lpt_chain_net(const KeyT* __restrict__ key, int nr, long long C,
       if (lane == 0) store8(res + i, rr);
       i += 8;
     } else {
+      LPT_COUNT(1);
       const uint64_t rv = lpt_step_v<NT>(K, w, base);
       if (lane == 0) res[i] = rv;
       lpt_rebase<NT>(K, base);

@@ -501,6 +501,57 @@ def pack(tp: Topo, sh: Shard, T: int, k: int, x: torch.Tensor, topk: torch.Tenso
                          out.numel() * out.element_size(), _stream(stream)))
 
 
+# ---------------------------------------------------------------- bound calls
+class Bound:
+    """One C entry point with its arguments marshalled ONCE (the pipelines call the
+    same buffers every step): calling it appends the current CUDA stream and checks
+    the return code.  Keeps the ctypes structs and tensors alive."""
+
+    def __init__(self, cfn, cargs, keep):
+        self.cfn, self.cargs, self.keep = cfn, tuple(cargs), keep
+
+    def __call__(self, stream=None):
+        rc = self.cfn(*self.cargs, _stream(stream))
+        if rc != RAILS_OK:
+            _ok(rc)
+
+
+def bind_histogram(tp: Topo, sh: Shard, topk, lut, row_bytes: int, out) -> Bound:
+    U, nd, N, T, k = topk.shape
+    counts, msg, rank = out
+    return Bound(lib().rails_histogram,
+                 [ctypes.byref(tp), ctypes.byref(sh), T, k, _ptr(topk, torch.int32, "topk"),
+                  _ptr(lut, torch.int32, "lut"), lut.numel(), row_bytes,
+                  _ptr(counts, torch.int32, "counts"), _ptr(msg, torch.int64, "msg"),
+                  _ptr(rank, torch.int32, "rank")], (tp, sh, topk, lut, out))
+
+
+def bind_schedule_eval(tp: Topo, sh: Shard, msg, sched: Schedule, ev: EvalOut, workspace,
+                       final: dict | None = None, rail_base=None, rail_total=None) -> Bound:
+    cs, ce = sched.c(), ev.c()
+    cf = _Final(*[_ptr(final[n]) for n in _FINAL_FIELDS]) if final is not None else None
+    return Bound(lib().rails_schedule_eval,
+                 [ctypes.byref(tp), ctypes.byref(sh), _ptr(msg, torch.int64, "msg"),
+                  ctypes.byref(cs), ctypes.byref(ce),
+                  ctypes.byref(cf) if cf is not None else None,
+                  _ptr(rail_base, torch.int64, "rail_base"),
+                  _ptr(rail_total, torch.int64, "rail_total"),
+                  _ptr(workspace, torch.uint8, "workspace"), workspace.numel()],
+                 (tp, sh, msg, sched, ev, workspace, final, rail_base, rail_total, cs, ce, cf))
+
+
+def bind_pack(tp: Topo, sh: Shard, T: int, k: int, x, topk, lut, rank, msg, row_bytes: int,
+              sched: Schedule, rail_base, out) -> Bound:
+    cs = sched.c()
+    return Bound(lib().rails_pack,
+                 [ctypes.byref(tp), ctypes.byref(sh), T, k, _ptr(x, None, "x"),
+                  _ptr(topk, torch.int32, "topk"), _ptr(lut, torch.int32, "lut"), lut.numel(),
+                  _ptr(rank, torch.int32, "rank"), _ptr(msg, torch.int64, "msg"), row_bytes,
+                  ctypes.byref(cs), _ptr(rail_base, torch.int64, "rail_base"),
+                  _ptr(out, None, "out"), out.numel() * out.element_size()],
+                 (tp, sh, x, topk, lut, rank, msg, sched, rail_base, out, cs))
+
+
 # ---------------------------------------------------------------- NEXT f1 (combine)
 def transpose_traffic(tp: Topo, msg: torch.Tensor, out=None, stream=None):
     """Dispatch traffic [U][M][N][G] -> combine traffic (same shape, transposed GPUs)."""

@@ -1,0 +1,68 @@
+#!/usr/bin/env python
+"""Phase timeline of the fused per-node kernel on C3 (debug build with
+-DRAILS_NODE_TIMING: globaltimer stamps of CTA 0 at each phase boundary, plus the
+unit's last CTA's finalize end and the grid's last CTA's rail-offset end).  Builds
+the debug library under gpurun_out/ and runs it; prints JSON.  Not part of the
+product (the product library has no timing code)."""
+import ctypes
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def build_debug(out_dir):
+    from paper_2510_19262_b200 import build as b
+    os.makedirs(out_dir, exist_ok=True)
+    objs = []
+    for src in b.SOURCES:
+        obj = os.path.join(out_dir, src.replace(".cu", ".o"))
+        subprocess.check_call([b.NVCC, *b.FLAGS, "-DRAILS_NODE_TIMING", "-c",
+                               os.path.join(b.CSRC, src), "-o", obj],
+                              stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        objs.append(obj)
+    lib = os.path.join(out_dir, "librails_timing.so")
+    subprocess.check_call([b.NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+                           "-o", lib, *objs])
+    return lib
+
+
+def main():
+    lib = build_debug(os.path.join(ROOT, "gpurun_out", "timing_build"))
+    from paper_2510_19262_b200 import rails
+    rails.LIB_PATH = lib
+    import torch
+    from tools.sched_bench import routing_pipe
+    L = rails.lib()
+    L.rails_debug_node_times.argtypes = [ctypes.c_void_p]
+    L.rails_debug_node_reset()
+    pipe, topk, lut = routing_pipe("c3", 1)
+    rails.histogram(pipe.tp, pipe.sh, topk, lut, pipe.RB, out=(pipe.counts, pipe.msg, pipe.rank))
+    runs = []
+    for it in range(6):
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record()
+        rails.schedule_eval(pipe.tp, pipe.sh, pipe.msg, pipe.sched, pipe.ev, pipe.ws,
+                            final=pipe.final, rail_base=pipe.rail_base, rail_total=pipe.total)
+        s1.record()
+        torch.cuda.synchronize()
+        t = (ctypes.c_ulonglong * 16)()
+        L.rails_debug_node_times(t)
+        t0 = t[1]
+        names = {1: "start A", 2: "B sort", 3: "C chain", 4: "chain start (warp 0)", 5: "D expand",
+                 6: "E eval", 7: "F publish", 8: "CTA0 end", 10: "unit-last finalize end",
+                 11: "grid-last rail offsets end"}
+        runs.append({"event_us": round(s0.elapsed_time(s1) * 1000, 2),
+                     **{names[i]: round((t[i] - t0) / 1000.0, 2) for i in names if t[i] >= t0},
+                     "chain_counts(runs,steps,windows,groups8)": [t[12], t[13], t[14], t[15]],
+                     "n_rem_node0": int(pipe.sched.n_rem[0, 0])})
+        L.rails_debug_node_reset()
+    print(json.dumps(runs[-3:], indent=1))
+
+
+if __name__ == "__main__":
+    main()
