@@ -7,6 +7,7 @@
 #   ref            bench.py --impl reference                -> gpurun_out/bench_ref.json
 #   launches       ncu launch list of the default bench    -> gpurun_out/launches.csv
 #   py:SCRIPT ARGS python SCRIPT ARGS                       -> gpurun_out/<script>.json
+#   dbench:N:ARGS  torchrun of bench.py on N GPUs           -> gpurun_out/dbench_N_*.json
 # Exit codes of every step go to gpurun_out/rc.txt.
 mkdir -p gpurun_out
 python -c "from paper_2510_19262_b200 import build as b; b.build()" > gpurun_out/build.log 2>&1
@@ -27,6 +28,12 @@ for step in "$@"; do
       timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
         --log-file gpurun_out/launches.csv python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu --no-graph $arg \
         > gpurun_out/launches.log 2>&1 ;;
+    dbench)
+      n="${arg%%:*}"; rest="${arg#*:}"; [ "$rest" = "$arg" ] && rest=""
+      tag=$(echo "$rest" | tr -c 'a-zA-Z0-9\n' '_')
+      timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node "$n" \
+        --master-addr 127.0.0.1 --master-port $((29500 + RANDOM % 1000)) bench.py --gpus "$n" $rest \
+        > "gpurun_out/dbench_${n}${tag:+_$tag}.json" 2> "gpurun_out/dbench_${n}${tag:+_$tag}.err" ;;
     py)
       scr="${arg%% *}"; rest="${arg#* }"; [ "$rest" = "$arg" ] && rest=""
       out=$(basename "$scr" .py)
