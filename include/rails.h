@@ -239,6 +239,21 @@ int rails_schedule_eval(const rails_topo_t* topo, const rails_shard_t* shard,
                         int64_t* rail_base, int64_t* rail_total, void* workspace,
                         size_t workspace_bytes, void* stream);
 
+/* a1-a5, the dispatch hot path in one call: rails_histogram followed by
+ * rails_schedule_eval on the same stream (the schedule kernel is launched with
+ * programmatic dependent launch, so it is scheduled while the histogram runs).
+ * Arguments and outputs are exactly those of the two calls (same workspace contract
+ * as rails_schedule_eval). */
+int rails_histogram_schedule_eval(const rails_topo_t* topo, const rails_shard_t* shard,
+                                  int32_t T, int32_t k, const int32_t* topk_inst,
+                                  const int32_t* inst_to_gpu, int32_t n_inst, int64_t row_bytes,
+                                  int32_t* counts, int64_t* msg_bytes, int32_t* row_rank,
+                                  const rails_sched_t* sched, const rails_eval_t* eval,
+                                  const rails_final_t* final, int64_t* rail_base,
+                                  int64_t* rail_total, void* workspace, size_t workspace_bytes,
+                                  void* stream);
+
+
 /* a6 fused with the finalize over NVLink peer memory (one process per GPU of a
  * box): every rank pushes its partial red_sum / red_max of each unit into every
  * rank's exchange buffer (remote stores through CUDA-IPC mappings), publishes a

@@ -279,6 +279,45 @@ int rails_schedule_eval(const rails_topo_t* topo, const rails_shard_t* sh,
   return cuda_rc(e, "rails_schedule_eval launch");
 }
 
+int rails_histogram_schedule_eval(const rails_topo_t* topo, const rails_shard_t* sh, int32_t T,
+                                  int32_t k, const int32_t* topk_inst, const int32_t* inst_to_gpu,
+                                  int32_t n_inst, int64_t row_bytes, int32_t* counts,
+                                  int64_t* msg_bytes, int32_t* row_rank,
+                                  const rails_sched_t* sched, const rails_eval_t* ev,
+                                  const rails_final_t* fin, int64_t* rail_base,
+                                  int64_t* rail_total, void* ws, size_t ws_bytes, void* stream) {
+  int rc = check_topo(topo);
+  if (rc || (rc = check_shard(topo, sh))) return rc;
+  if (T < 1 || k < 1 || k > 32) return fail(RAILS_EINVAL, "need T >= 1 and 1 <= k <= 32");
+  if ((long long)T * k > (1LL << 30)) return fail(RAILS_EINVAL, "T*k too large");
+  if (n_inst < 1 || row_bytes < 1) return fail(RAILS_EINVAL, "need n_inst >= 1, row_bytes >= 1");
+  if (!topk_inst || !inst_to_gpu || !counts || !msg_bytes)
+    return fail(RAILS_EINVAL, "NULL array argument");
+  if ((long long)topo->M * topo->N > 49152)
+    return fail(RAILS_ENOSPC, "G=%lld: histogram bins exceed shared memory",
+                (long long)topo->M * topo->N);
+  if (!sched || !sched->full_base || !sched->rem_rail || !sched->rem_off || !sched->send_load ||
+      !sched->n_full || !sched->n_rem || !ws || !eval_ok(ev))
+    return fail(RAILS_EINVAL, "NULL argument");
+  if (fin && (sh->d0 != 0 || sh->nd != topo->M))
+    return fail(RAILS_EINVAL, "final needs every node of the units (d0 = 0, nd = M); "
+                              "finalize after the a6 exchange instead");
+  if ((rail_base == nullptr) != (rail_total == nullptr))
+    return fail(RAILS_EINVAL, "rail_base and rail_total go together");
+  if (!al(ws, 256)) return fail(RAILS_EINVAL, "workspace must be 256-byte aligned");
+  const size_t need = schedule_workspace_bytes(sh->U, sh->nd, topo->M, topo->N);
+  if (ws_bytes < need) return fail(RAILS_ENOSPC, "workspace %zu < %zu bytes", ws_bytes, need);
+  LaunchCtx c;
+  if ((rc = ctx(stream, &c))) return rc;
+  // the histogram, then the fused schedule + eval kernel (launched with PDL behind it)
+  cudaError_t e = launch_histogram(c, sh->U, sh->nd, sh->d0, topo->M, topo->N, topo->N, T, k,
+                                   topk_inst, inst_to_gpu, n_inst, row_bytes, counts, msg_bytes,
+                                   row_rank);
+  if (e != cudaSuccess) return cuda_rc(e, "rails_histogram_schedule_eval launch");
+  return rails_schedule_eval(topo, sh, msg_bytes, sched, ev, fin, rail_base, rail_total, ws,
+                             ws_bytes, stream);
+}
+
 int rails_rail_offsets(const rails_topo_t* topo, const rails_shard_t* sh,
                        const int64_t* send_load, int64_t* rail_base, int64_t* total,
                        void* stream) {

@@ -223,6 +223,8 @@ cudaError_t launch_chains(const LaunchCtx&, int U, int nd, int d0, int M, int N,
                           uint32_t* ws_qp, uint32_t* ws_w, int32_t* ws_inv, uint8_t* scratch,
                           int32_t* rem_qp, int qps_per_rail, int cshift, int nbits);
 
+void schedule_workspace_ptrs(void* ws, int U, int nd, int M, int N, int64_t** acc,
+                             unsigned** cnt, uint64_t** res);
 size_t assign_workspace_bytes(int n_seg, long long F);
 cudaError_t launch_assign(const LaunchCtx&, int N, int n_seg, const int64_t* seg_off,
                           long long F, const int64_t* w, int32_t* rail, int64_t* off,

@@ -594,6 +594,14 @@ static NodeWs node_ws(void* ws, int U, int nd, int M, int N) {
   return w;
 }
 
+void schedule_workspace_ptrs(void* ws, int U, int nd, int M, int N, int64_t** acc,
+                             unsigned** cnt, uint64_t** res) {
+  const NodeWs w = node_ws(ws, U, nd, M, N);
+  *acc = w.acc;
+  *cnt = w.cnt;
+  *res = w.res_g;
+}
+
 size_t schedule_workspace_bytes(int U, int nd, int M, int N) {
   return node_ws(nullptr, U, nd, M, N).bytes;
 }

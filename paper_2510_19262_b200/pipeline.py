@@ -1,7 +1,7 @@
 """One pass of the whole hot path (all SURVEY section 8(a) rows) over preallocated buffers.
 
-Routing configs (C1, C3, C4):  a1 histogram -> a2-a5 fused (LPT schedule + eval +
-rail offsets, + finalize when this call holds every node) -> [a6 cross-rank
+Routing configs (C1, C3, C4):  a1-a5 (histogram, then the fused LPT schedule + eval
++ rail offsets, + finalize when this call holds every node) -> [a6 cross-rank
 reduction + finalize] -> a7 pack.
 Matrix configs (C2, C5):       a2-a5 fused -> [a6 + finalize].
 
@@ -61,19 +61,17 @@ class RoutingPipeline:
         return b
 
     def schedule_part(self, topk: torch.Tensor, lut: torch.Tensor, stream=None):
-        """a1 + the fused a2-a5 kernel (schedule, eval, rail offsets; the finalize too
-        when this pipeline holds every node of its units)."""
-        hist = self._bound(("hist", topk.data_ptr(), lut.data_ptr(), lut.numel()),
-                           lambda: rails.bind_histogram(self.tp, self.sh, topk, lut, self.RB,
-                                                        (self.counts, self.msg, self.rank)))
-        sched = self._bound(("sched",), lambda: rails.bind_schedule_eval(
-            self.tp, self.sh, self.msg, self.sched, self.ev, self.ws,
-            final=self.final if self.holds_all else None, rail_base=self.rail_base,
-            rail_total=self.total))
-        with _nvtx(self.nvtx, "a1 histogram"):
-            hist(stream)
-        with _nvtx(self.nvtx, "a2-a5 schedule+eval"):
-            sched(stream)
+        """a1-a5 (rails_histogram_schedule_eval): the histogram, then one kernel for
+        schedule, eval, rail offsets (and the finalize when this pipeline holds every
+        node of its units), launched with PDL behind the histogram."""
+        call = self._bound(("sched", topk.data_ptr(), lut.data_ptr(), lut.numel()),
+                           lambda: rails.bind_histogram_schedule_eval(
+                               self.tp, self.sh, topk, lut, self.RB,
+                               (self.counts, self.msg, self.rank), self.sched, self.ev, self.ws,
+                               final=self.final if self.holds_all else None,
+                               rail_base=self.rail_base, rail_total=self.total))
+        with _nvtx(self.nvtx, "a1-a5 histogram+schedule+eval"):
+            call(stream)
 
     def finalize_part(self, reduce: Callable | None = None, stream=None):
         """a6 + finalize for pipelines holding a subset of the nodes (no-op otherwise:

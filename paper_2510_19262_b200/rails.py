@@ -105,6 +105,11 @@ def lib():
                                           ctypes.POINTER(_Eval), ctypes.POINTER(_Final), P, P, P,
                                           sz, P]
         L.rails_schedule_eval.restype = ctypes.c_int
+        L.rails_histogram_schedule_eval.argtypes = [PT, PS, i32, i32, P, P, i32, i64, P, P, P,
+                                                    ctypes.POINTER(_Sched),
+                                                    ctypes.POINTER(_Eval),
+                                                    ctypes.POINTER(_Final), P, P, P, sz, P]
+        L.rails_histogram_schedule_eval.restype = ctypes.c_int
         L.rails_peer_buffer_bytes.argtypes = [PT, i32, i32, ctypes.POINTER(sz)]
         L.rails_peer_buffer_bytes.restype = ctypes.c_int
         L.rails_eval_finalize_peer.argtypes = [PT, i32, P, P, ctypes.POINTER(Peer),
@@ -538,6 +543,27 @@ def bind_schedule_eval(tp: Topo, sh: Shard, msg, sched: Schedule, ev: EvalOut, w
                   _ptr(rail_total, torch.int64, "rail_total"),
                   _ptr(workspace, torch.uint8, "workspace"), workspace.numel()],
                  (tp, sh, msg, sched, ev, workspace, final, rail_base, rail_total, cs, ce, cf))
+
+
+def bind_histogram_schedule_eval(tp: Topo, sh: Shard, topk, lut, row_bytes: int, hist_out,
+                                 sched: Schedule, ev: EvalOut, workspace, final: dict | None = None,
+                                 rail_base=None, rail_total=None) -> Bound:
+    """a1-a5 fused (rails_histogram_schedule_eval), marshalled once."""
+    U, nd, N, T, k = topk.shape
+    counts, msg, rank = hist_out
+    cs, ce = sched.c(), ev.c()
+    cf = _Final(*[_ptr(final[n]) for n in _FINAL_FIELDS]) if final is not None else None
+    return Bound(lib().rails_histogram_schedule_eval,
+                 [ctypes.byref(tp), ctypes.byref(sh), T, k, _ptr(topk, torch.int32, "topk"),
+                  _ptr(lut, torch.int32, "lut"), lut.numel(), row_bytes,
+                  _ptr(counts, torch.int32, "counts"), _ptr(msg, torch.int64, "msg"),
+                  _ptr(rank, torch.int32, "rank"), ctypes.byref(cs), ctypes.byref(ce),
+                  ctypes.byref(cf) if cf is not None else None,
+                  _ptr(rail_base, torch.int64, "rail_base"),
+                  _ptr(rail_total, torch.int64, "rail_total"),
+                  _ptr(workspace, torch.uint8, "workspace"), workspace.numel()],
+                 (tp, sh, topk, lut, hist_out, sched, ev, workspace, final, rail_base, rail_total,
+                  cs, ce, cf))
 
 
 def bind_pack(tp: Topo, sh: Shard, T: int, k: int, x, topk, lut, rank, msg, row_bytes: int,
