@@ -67,6 +67,18 @@ __device__ __forceinline__ void add64_split(unsigned* lo, unsigned* hi, unsigned
   if (h + carry) atomicAdd(hi, h + carry);
 }
 
+// 64-bit sums as two independent 32-bit shared reductions (no returned value, so the
+// adds are fire-and-forget): low 20 bits and the rest.  Exact while a bin receives at
+// most 4096 addends (low word < 2^32) and their sum stays below 2^52; the fused
+// kernel's bins get at most N^2 <= 1024 messages of < 2^40 bytes each.
+__device__ __forceinline__ void add_split20(unsigned* lo, unsigned* hi, unsigned long long v) {
+  atomicAdd(lo, (unsigned)(v & 0xFFFFFull));
+  if (v >> 20) atomicAdd(hi, (unsigned)(v >> 20));
+}
+__device__ __forceinline__ unsigned long long get_split20(unsigned lo, unsigned hi) {
+  return ((unsigned long long)hi << 20) + lo;
+}
+
 // T, T*, busbw of unit u from the reduced maxima and totals (R#8, R#10, Thm 2/3;
 // uniform policy R#41; busbw 0 without traffic, R#40).
 __device__ __forceinline__ void finalize_unit(long long u, int N, double R2, long long mR,

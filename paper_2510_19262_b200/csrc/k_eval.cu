@@ -32,16 +32,16 @@ namespace rails {
 constexpr int EV2_THREADS = 256;
 
 template <int NT>  // NT = 8 (divisions by shifts) or 0 (runtime N)
-__global__ void __launch_bounds__(EV2_THREADS)
+__global__ void __launch_bounds__(EV2_THREADS, 4)
     k_eval_node(int M, int N_rt, int nd, int d0, long long C, int cshift, uint64_t seed, int FT,
                 const int64_t* __restrict__ msg, const int64_t* __restrict__ full_base,
                 const int8_t* __restrict__ rem_rail, const int64_t* __restrict__ n_full,
                 rails_eval_t ev) {
   extern __shared__ __align__(16) uint8_t ev_smem[];
   __shared__ unsigned long long sS[32], sSe[32], sSu[32], sCol[EV2_THREADS];
-  // per (fl, j) of the tile: remainder bytes into NIC (f, j), ECMP bytes, 64-bit sums
-  // as 32-bit halves (32-bit shared atomics are native); uniform: remainder counts
-  // per (fl, B mod N) and quotient sums per fl
+  // per (fl, j) of the tile: remainder bytes into NIC (f, j), ECMP bytes; uniform:
+  // remainder counts per (fl, B mod N) and quotient sums per fl.  64-bit sums as two
+  // fire-and-forget 32-bit shared reductions (add_split20: a bin gets <= N^2 adds)
   __shared__ unsigned aRlo[EV2_THREADS], aRhi[EV2_THREADS], aElo[EV2_THREADS],
       aEhi[EV2_THREADS], cU[EV2_THREADS], aQlo[EV2_THREADS], aQhi[EV2_THREADS];
   const int N = NT ? NT : N_rt;
@@ -79,22 +79,36 @@ __global__ void __launch_bounds__(EV2_THREADS)
       if (rest >= tn || gq >= gsp) continue;
       const long long h = (long long)f0 * N + rest;
       const int fl = rest / N, fb = fl * N;  // (fl, 0) of this message's destination
-      for (int g = gq; g < N; g += gsp) {
-        const long long idx = (long long)g * G + h;
-        const long long B = mg[idx];
-        if (B <= 0 || (int)(h / N) == d) continue;
-        const int8_t rv = rrp[idx];
+      auto add_msg = [&](int g, long long B, int8_t rv) {
+        if (B <= 0 || (int)(h / N) == d) return;
         const long long nf = cd.div(B);
         const long long rem = B - nf * C;
         if (rem && rv >= 0 && rv < N)
-          add64_split(&aRlo[fb + rv], &aRhi[fb + rv], (unsigned long long)rem);
+          add_split20(&aRlo[fb + rv], &aRhi[fb + rv], (unsigned long long)rem);
         const int e = ecmp_rail(seed, (long long)d * N + g, h, N);
-        add64_split(&aElo[fb + e], &aEhi[fb + e], (unsigned long long)B);
+        add_split20(&aElo[fb + e], &aEhi[fb + e], (unsigned long long)B);
         long long qb;
         int rb;
         divmod_n(B, N, qb, rb);
-        if (qb) add64_split(&aQlo[fl], &aQhi[fl], (unsigned long long)qb);
+        if (qb) add_split20(&aQlo[fl], &aQhi[fl], (unsigned long long)qb);
         if (rb) atomicAdd(&cU[fb + rb], 1u);
+      };
+      if (NT != 0 && gsp == 1) {
+        // all N source GPUs' loads in flight at once (one DRAM latency per tile)
+        long long Bv[NT ? NT : 1];
+        int8_t rvv[NT ? NT : 1];
+#pragma unroll
+        for (int g = 0; g < NT; ++g) {
+          Bv[g] = mg[(long long)g * G + h];
+          rvv[g] = rrp[(long long)g * G + h];
+        }
+#pragma unroll
+        for (int g = 0; g < NT; ++g) add_msg(g, Bv[g], rvv[g]);
+      } else {
+        for (int g = gq; g < N; g += gsp) {
+          const long long idx = (long long)g * G + h;
+          add_msg(g, mg[idx], rrp[idx]);
+        }
       }
     }
     // block boundaries: full index at message (g, (f0+fl)*N), fl = 0..ft
@@ -127,9 +141,9 @@ __global__ void __launch_bounds__(EV2_THREADS)
           const int ra = sR[g * (FT + 1) + fl], rb = sR[g * (FT + 1) + fl + 1];
           full += (qb - qa) + (j < rb ? 1 : 0) - (j < ra ? 1 : 0);
         }
-        Rv = (unsigned long long)(full * C) + (((unsigned long long)aRhi[t] << 32) | aRlo[t]);
-        Rev = ((unsigned long long)aEhi[t] << 32) | aElo[t];
-        Ruv = ((unsigned long long)aQhi[fl] << 32) | aQlo[fl];
+        Rv = (unsigned long long)(full * C) + get_split20(aRlo[t], aRhi[t]);
+        Rev = get_split20(aElo[t], aEhi[t]);
+        Ruv = get_split20(aQlo[fl], aQhi[fl]);
         for (int r = j + 1; r < N; ++r) Ruv += cU[fl * N + r];
         if (Rv) atomicAdd(rs + RL.R() + (long long)f * N + j, Rv);
         if (Rev) atomicAdd(rs + RL.Re() + (long long)f * N + j, Rev);

@@ -36,7 +36,7 @@ __device__ unsigned long long g_node_t[16];
 // chain path counters of CTA 0 (slots 12..15): runs, single steps, windows, groups of 8
 #define LPT_COUNT(i)                                                   \
   do {                                                                 \
-    if (blockIdx.x == 0 && threadIdx.x == 0) g_node_t[12 + (i)] += 1; \
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (i) != 1) g_node_t[12 + (i)] += 1; \
   } while (0)
 #endif
 #include "eval.cuh"
@@ -52,6 +52,10 @@ __device__ unsigned long long g_node_t[16];
 #define NODE_TL(i)                              \
   do {                                          \
     if (threadIdx.x == 0) g_node_t[i] = globaltimer_ns(); \
+  } while (0)
+#define NODE_TW(i)                                                         \
+  do {                                                                     \
+    if (blockIdx.x == 0 && threadIdx.x == 32) g_node_t[i] = globaltimer_ns(); \
   } while (0)
 extern "C" int rails_debug_node_reset() {
   unsigned long long z[16] = {0};
@@ -69,11 +73,15 @@ extern "C" int rails_debug_node_times(unsigned long long* host16) {
 #define NODE_TL(i) \
   do {             \
   } while (0)
+#define NODE_TW(i) \
+  do {             \
+  } while (0)
 #endif
 
 namespace rails {
 
 constexpr int NODE_MAX_THREADS = 512;
+constexpr int NODE_MAX_RUNS = 32;  // deferred cyclic runs per chain (lpt.cuh RunList)
 constexpr long long NODE_SMEM_ITEMS = 16384;  // N*G kept in shared memory
 
 struct NodeArgs {
@@ -121,6 +129,8 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
   __shared__ uint32_t red32[32];
   __shared__ long long sL[32], sSe[32], sSu[32];
   __shared__ int s_last;
+  __shared__ RunDesc s_runs[NODE_MAX_RUNS];
+  __shared__ int s_nrun;
 
   const long long seg = blockIdx.x;
   const long long NG = a.NG;
@@ -151,6 +161,7 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
   long long* sP = nullptr;
   unsigned *aRlo = nullptr, *aRhi = nullptr, *aElo = nullptr, *aEhi = nullptr, *cU = nullptr,
            *aQlo = nullptr, *aQhi = nullptr;
+  uint8_t* sPr = nullptr;  // r of each block start (phase C)
   if constexpr (EVAL) {
     sP = (long long*)(smem + a.ev_off);
     aRlo = (unsigned*)(sP + G + 1);
@@ -160,6 +171,7 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
     cU = aEhi + MN;
     aQlo = cU + MN;
     aQhi = aQlo + M;
+    sPr = reinterpret_cast<uint8_t*>(aQhi + M);
     for (long long i = threadIdx.x; i < MN; i += blockDim.x) aElo[i] = aEhi[i] = cU[i] = 0u;
     for (int i = threadIdx.x; i < M; i += blockDim.x) aQlo[i] = aQhi[i] = 0u;
     __syncthreads();
@@ -264,47 +276,92 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
   if (threadIdx.x < 32) {
     NODE_T(4);
     if constexpr (NT != 0) {
-      lpt_chain_net<NT, KeyT>(ks, n, C, nf_node, res, sL);
+      lpt_chain_net<NT, KeyT>(ks, n, C, nf_node, res, sL,
+                              RunList{s_runs, NODE_MAX_RUNS, &s_nrun});
     } else {
       const long long L = lpt_chain_generic<KeyT>(ks, n, N, C, nf_node, res, a.err);
       if (threadIdx.x < N) sL[threadIdx.x] = L;
     }
     __syncwarp();
+    NODE_T(9);
     if (threadIdx.x < N) a.s.send_load[seg * N + threadIdx.x] = sL[threadIdx.x];
   } else if constexpr (EVAL) {
     // the ECMP rails (R#13-R#14) and the uniform split (R#41) of every message, off
-    // the critical path while warp 0 runs the chain (msg is L2-resident: phase A read it)
+    // the critical path while warp 0 runs the chain (msg is L2-resident: phase A read
+    // it); sums as fire-and-forget split reductions (add_split20)
     for (unsigned m = threadIdx.x - 32; m < (unsigned)NG; m += blockDim.x - 32) {
       const long long B = mg[m];
       const int h = (int)(m % (unsigned)G), g = (int)(m / (unsigned)G);
       if (B <= 0 || (h >= lo && h < hi)) continue;  // invalid entries were flagged in A
       const int f = h / N;
       const int e = ecmp_rail(a.seed, (long long)d * N + g, h, N);
-      add64_split(&aElo[f * N + e], &aEhi[f * N + e], (unsigned long long)B);
+      add_split20(&aElo[f * N + e], &aEhi[f * N + e], (unsigned long long)B);
       long long qb;
       int rb;
       divmod_n(B, N, qb, rb);
-      if (qb) add64_split(&aQlo[f], &aQhi[f], (unsigned long long)qb);
+      if (qb) add_split20(&aQlo[f], &aQhi[f], (unsigned long long)qb);
       if (rb) atomicAdd(&cU[f * N + rb], 1u);
     }
-    for (long long t = threadIdx.x - 32; t < MN; t += blockDim.x - 32) {
-      const int f = (int)(t / N), j = (int)(t - (long long)f * N);
-      long long full = 0;
-      if (f != d) {
-        for (int g = 0; g < N; ++g) {
-          const long long pa = sP[(long long)g * M + f], pb = sP[(long long)g * M + f + 1];
-          full += full_on_rail(pb, N, j) - full_on_rail(pa, N, j);
+    // full chunks: block boundary t (= g*M + f) starts at node-global full index
+    // sP[t] = q*N + r; rail j of block t receives (q_b - q_a) + [j < r_b] - [j < r_a]
+    for (int t = threadIdx.x - 32; t <= (int)G; t += blockDim.x - 32) {
+      long long q;
+      int r;
+      divmod_n(sP[t], N, q, r);
+      sP[t] = q;
+      sPr[t] = (uint8_t)r;
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"((int)blockDim.x - 32) : "memory");  // workers only
+    NODE_TW(13);  // workers' ECMP / uniform pass done
+    if constexpr (NT != 0) {
+      // thread per destination node f: the q difference is the same for every rail,
+      // the [j < r] terms for all NT rails in registers
+      for (int f = threadIdx.x - 32; f < M; f += blockDim.x - 32) {
+        long long qs = 0;
+        int cnt[NT];
+#pragma unroll
+        for (int j = 0; j < NT; ++j) cnt[j] = 0;
+        if (f != d) {
+          for (int g = 0; g < NT; ++g) {
+            const long long ia = (long long)g * M + f;
+            qs += sP[ia + 1] - sP[ia];
+            const int rb = sPr[ia + 1], ra = sPr[ia];
+#pragma unroll
+            for (int j = 0; j < NT; ++j) cnt[j] += (j < rb ? 1 : 0) - (j < ra ? 1 : 0);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          const unsigned long long v = f != d ? (unsigned long long)((qs + cnt[j]) * C) : 0ull;
+          aRlo[f * NT + j] = (unsigned)(v & 0xFFFFFull);
+          aRhi[f * NT + j] = (unsigned)(v >> 20);
         }
       }
-      const unsigned long long v = (unsigned long long)(full * C);
-      aRlo[t] = (unsigned)v;
-      aRhi[t] = (unsigned)(v >> 32);
+    } else {
+      for (long long t = threadIdx.x - 32; t < MN; t += blockDim.x - 32) {
+        const int f = (int)(t / N), j = (int)(t - (long long)f * N);
+        long long full = 0;
+        if (f != d) {
+          for (int g = 0; g < N; ++g) {
+            const long long ia = (long long)g * M + f;
+            full += (sP[ia + 1] - sP[ia]) + (j < sPr[ia + 1] ? 1 : 0) - (j < sPr[ia] ? 1 : 0);
+          }
+        }
+        const unsigned long long v = (unsigned long long)(full * C);
+        aRlo[t] = (unsigned)(v & 0xFFFFFull);
+        aRhi[t] = (unsigned)(v >> 20);
+      }
     }
   }
   __syncthreads();
 
   NODE_T(5);
-  // ---- phase D: QP map (optional), expand, remainders into R_d
+  // ---- phase D: the chain's deferred runs, QP map (optional), expand, remainders
+  // into R_d
+  if constexpr (NT != 0) {
+    lpt_runs_expand<NT>(s_runs, s_nrun, res);
+    __syncthreads();
+  }
   if (a.rem_qp) qp_rank_block(N, a.Q, nf_node, n, res, a.qp_g + seg * NG);
   const unsigned NGu = (unsigned)NG, Gu = (unsigned)G;  // N*G < 2^26 (M*N <= 2^20, N <= 32)
   for (unsigned m = threadIdx.x; m < NGu; m += blockDim.x) {
@@ -319,7 +376,7 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
       if (a.rem_qp) q = (int32_t)a.qp_g[seg * NG + p];
       if constexpr (EVAL) {
         const int f = (int)((m % Gu) / (unsigned)N);
-        add64_split(&aRlo[f * N + r], &aRhi[f * N + r],
+        add_split20(&aRlo[f * N + r], &aRhi[f * N + r],
                     (unsigned long long)(C - 1 - (long long)ks[p]));
       }
     }
@@ -353,9 +410,9 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
     const int f = act ? t / N : 0, j = act ? t - f * N : 0;
     unsigned long long R = 0, Re = 0, Ru = 0;
     if (act) {
-      R = ((unsigned long long)aRhi[t] << 32) | aRlo[t];
-      Re = ((unsigned long long)aEhi[t] << 32) | aElo[t];
-      Ru = ((unsigned long long)aQhi[f] << 32) | aQlo[f];
+      R = get_split20(aRlo[t], aRhi[t]);
+      Re = get_split20(aElo[t], aEhi[t]);
+      Ru = get_split20(aQlo[f], aQhi[f]);
       for (int r = j + 1; r < N; ++r) Ru += cU[f * N + r];
       if (R) atomicAdd(acc + RL.R() + t, R);
       if (Re) atomicAdd(acc + RL.Re() + t, Re);
@@ -378,7 +435,7 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
     for (int f = threadIdx.x; f < M; f += blockDim.x) {
       unsigned long long cf = 0;
       for (int j = 0; j < N; ++j)
-        cf += ((unsigned long long)aRhi[f * N + j] << 32) | aRlo[f * N + j];
+        cf += get_split20(aRlo[f * N + j], aRhi[f * N + j]);
       if (cf) atomicAdd(acc + RL.col() + f, cf);
     }
   }
@@ -525,7 +582,7 @@ static NodePlan node_plan(int M, int N, long long C, bool eval, long long nseg, 
   const long long G = (long long)M * N, NG = (long long)N * G;
   NodePlan p{};
   constexpr size_t DYN_LIMIT = 200 * 1024;  // + ~20 KiB static stays under 227 KiB
-  const size_t ev_bytes = (size_t)(G + 1) * 8 + (size_t)G * 4 * 5 + (size_t)M * 8;
+  const size_t ev_bytes = (size_t)(G + 1) * 8 + (size_t)G * 4 * 5 + (size_t)M * 8 + (size_t)G + 16;
   p.eval_fused = eval && ev_bytes <= 96 * 1024;
   const bool k16 = C <= 65536;
   const size_t sort_smem = (size_t)NG * 2 * ((k16 ? 2 : 4) + 2);

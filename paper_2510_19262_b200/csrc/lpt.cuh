@@ -153,6 +153,27 @@ __device__ __forceinline__ void lpt_group8_v(uint32_t (&K)[NT], const uint32_t (
 // more items, plus one for i < n mod NT: the sorted keys become K[rr..NT-1] + q*w,
 // K[0..rr-1] + (q+1)*w (still sorted, spread still < w).
 template <int NT>
+__device__ __forceinline__ void lpt_run_advance(uint32_t (&K)[NT], uint32_t w, int n,
+                                                long long& base) {
+  base += (long long)(n / NT) * w;
+  // rotate left by s = n mod NT, the wrapped keys + w: composed from rotations by
+  // 1, 2, 4, ... (each key wraps at most once since s < NT)
+  const uint32_t W = w << 5;
+  const int s = n % NT;
+#pragma unroll
+  for (int b = 1; b < NT; b <<= 1) {
+    if (s & b) {
+      uint32_t R[NT];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) R[j] = (j < NT - b) ? K[j + b] : K[j + b - NT] + W;
+#pragma unroll
+      for (int j = 0; j < NT; ++j) K[j] = R[j];
+    }
+  }
+  lpt_rebase<NT>(K, base);
+}
+
+template <int NT>
 __device__ __forceinline__ void lpt_run_cyclic(uint32_t (&K)[NT], uint32_t w, int n, int lane,
                                                uint64_t* __restrict__ out, long long& base) {
   uint32_t kl = K[0];
@@ -161,15 +182,37 @@ __device__ __forceinline__ void lpt_run_cyclic(uint32_t (&K)[NT], uint32_t w, in
     if ((lane % NT) == j) kl = K[j];
   const long long lb = base + (long long)(kl >> 5);
   for (int t = lane; t < n; t += 32) out[t] = pack_res(kl & 31u, lb + (long long)(t / NT) * w);
-  base += (long long)(n / NT) * w;
-  const uint32_t W = w << 5;
-  for (int s = n % NT; s > 0; --s) {
-    const uint32_t h = K[0] + W;
-#pragma unroll
-    for (int j = 0; j < NT - 1; ++j) K[j] = K[j + 1];
-    K[NT - 1] = h;
+  lpt_run_advance<NT>(K, w, n, base);
+}
+
+// A cyclic run whose writes are deferred: the chain records the run's start state
+// (K, base) and moves on; afterwards the whole CTA writes the run by the same closed
+// form (lpt_runs_expand), so the serial chain only pays for the runs' boundaries.
+struct RunDesc {
+  int start, n;
+  uint32_t w, pad;
+  long long base;
+  uint32_t K[8];
+};
+struct RunList {
+  RunDesc* d;  // shared memory, cap entries
+  int cap;
+  int* count;  // written by lane 0 when the chain ends
+};
+
+// Called by every thread of the block after the chain (and a barrier).
+template <int NT>
+__device__ __forceinline__ void lpt_runs_expand(const RunDesc* rl, int nrun,
+                                                uint64_t* __restrict__ out) {
+  for (int r = 0; r < nrun; ++r) {
+    const int start = rl[r].start, n = rl[r].n;
+    const uint32_t w = rl[r].w;
+    const long long base = rl[r].base;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+      const uint32_t kl = rl[r].K[t % NT];
+      out[start + t] = pack_res(kl & 31u, base + (long long)(kl >> 5) + (long long)(t / NT) * w);
+    }
   }
-  lpt_rebase<NT>(K, base);
 }
 
 // Sorted remainder sizes: w(i) = C - 1 - key[i] (keys ascending = sizes descending).
@@ -202,7 +245,10 @@ __device__ __forceinline__ int run_end(const KeyT* key, int i, int n, int lane) 
 // The sorted-register chain (one warp, every lane holds the same state).
 template <int NT, typename KeyT>
 __device__ void lpt_chain_net(const KeyT* __restrict__ key, int nr, long long C, long long nf,
-                              uint64_t* __restrict__ res, long long* __restrict__ load_out) {
+                              uint64_t* __restrict__ res, long long* __restrict__ load_out,
+                              RunList rl = RunList{nullptr, 0, nullptr}) {
+  static_assert(NT <= 8, "RunDesc holds at most 8 rail keys");
+  int nrun = 0;
   const int lane = threadIdx.x & 31;
   const SortedSizes<KeyT> W{key, (uint32_t)(C - 1)};
   const long long q = nf / NT;
@@ -229,7 +275,23 @@ __device__ void lpt_chain_net(const KeyT* __restrict__ key, int nr, long long C,
         lpt_rebase<NT>(K, base);
         ++i;
       }
-      if (i < e) lpt_run_cyclic<NT>(K, w, e - i, lane, res + i, base);
+      if (i < e) {
+        if (nrun < rl.cap) {
+          if (lane == 0) {
+            RunDesc& R = rl.d[nrun];
+            R.start = i;
+            R.n = e - i;
+            R.w = w;
+            R.base = base;
+#pragma unroll
+            for (int j = 0; j < NT; ++j) R.K[j] = K[j];
+          }
+          ++nrun;
+          lpt_run_advance<NT>(K, w, e - i, base);
+        } else {
+          lpt_run_cyclic<NT>(K, w, e - i, lane, res + i, base);
+        }
+      }
       i = e;
     } else if ((8 % NT) == 0 && (i & 7) == 0 && i + 8 <= nr && W(i + 7) == w &&
                K[NT - 1] - K[0] < (w << 5)) {
@@ -287,6 +349,7 @@ __device__ void lpt_chain_net(const KeyT* __restrict__ key, int nr, long long C,
   if (lane == 0) {  // final LoadState by rail (K holds every rail once)
 #pragma unroll
     for (int j = 0; j < NT; ++j) load_out[K[j] & 31u] = base + (long long)(K[j] >> 5);
+    if (rl.count) *rl.count = nrun;
   }
 }
 

@@ -1,6 +1,7 @@
 #!/usr/bin/env python
 """Per-CUDA-line warp-stall samples and executed instructions from an ncu report
-(`ncu -i REP --page source --csv --print-source cuda,sass`), top lines first."""
+(`ncu -i REP --page source --csv --print-source cuda,sass`), top lines first.
+Usage: ncu_lines.py REP [TOP] [KERNEL_REGEX]"""
 import csv
 import subprocess
 import sys
@@ -9,7 +10,8 @@ import sys
 def main():
     rep = sys.argv[1]
     top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source",
+    kfilt = ["-k", "regex:" + sys.argv[3]] if len(sys.argv) > 3 else []
+    out = subprocess.run(["ncu", "-i", rep, *kfilt, "--page", "source", "--csv", "--print-source",
                           "cuda,sass"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     fname, recs = "", []

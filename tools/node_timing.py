@@ -54,11 +54,12 @@ def main():
         L.rails_debug_node_times(t)
         t0 = t[1]
         names = {1: "start A", 2: "B sort", 3: "C chain", 4: "chain start (warp 0)", 5: "D expand",
-                 6: "E eval", 7: "F publish", 8: "CTA0 end", 10: "unit-last finalize end",
-                 11: "grid-last rail offsets end"}
+                 6: "E eval", 7: "F publish", 8: "CTA0 end", 9: "chain end (warp 0)",
+                 10: "unit-last finalize end", 11: "grid-last rail offsets end",
+                 13: "workers' message pass end"}
         runs.append({"event_us": round(s0.elapsed_time(s1) * 1000, 2),
                      **{names[i]: round((t[i] - t0) / 1000.0, 2) for i in names if t[i] >= t0},
-                     "chain_counts(runs,steps,windows,groups8)": [t[12], t[13], t[14], t[15]],
+                     "chain_counts(runs,steps,windows,groups8)": [t[12], 0, t[14], t[15]],
                      "n_rem_node0": int(pipe.sched.n_rem[0, 0])})
         L.rails_debug_node_reset()
     print(json.dumps(runs[-3:], indent=1))
