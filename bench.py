@@ -433,6 +433,14 @@ def timed(step, steps, stream, dist, local, flush=None):
     return total, launches, clk.summary()
 
 
+def sched_times(sev, kev, steps):
+    """Per-step schedule-part times (ms) between the step's first event and the pack's
+    start event.  Reported as the median: step 0 follows the synchronize that opens
+    the timed region, so its kernels wait on host launches (its time is in the list)."""
+    per = [sev[i].elapsed_time(kev[i][0]) for i in range(steps)]
+    return sorted(per)[len(per) // 2], per
+
+
 def quality_routing(pipe, C, N, dist, dev):
     """makespan/OPT and balance figures (report-side arithmetic on the kernels' outputs):
     T/T* for LPT, ECMP-hash (R#13), uniform (R#41) and the ecmp_nic reading (R#42);
@@ -611,7 +619,7 @@ def run_routing(args, cfg, rank, world, local, dev, dist):
     rails.check()
     total_ms = max_over_ranks(total_ms, dist, dev)
     pack_ms = sum(a.elapsed_time(b) for a, b in kev) / args.steps
-    sched_ms = sum(sev[i].elapsed_time(kev[i][0]) for i in range(args.steps)) / args.steps
+    sched_ms, sched_per = sched_times(sev, kev, args.steps)
     nodes = U * nd * P
     value = nodes * args.steps / (total_ms / 1000.0)
     peak, peak_kind = measured_peaks()
@@ -622,6 +630,8 @@ def run_routing(args, cfg, rank, world, local, dev, dist):
     sched_ms = max_over_ranks(sched_ms, dist, dev)
     out["schedule_only"] = {
         "value": nodes / (sched_ms / 1000.0), "unit": "nodes/s", "ms_per_step": sched_ms,
+        "stat": "median over the timed steps (max over ranks)",
+        "per_step_ms": [round(v, 5) for v in sched_per],
         "what": "a1 histogram + a2-a5 fused schedule/eval (+ rail offsets, + finalize at P = 1) "
                 "+ a6 exchange per step, pack excluded: SURVEY 8(d) d.1 'LPT-scheduled nodes/s', "
                 "eager launches"}
@@ -855,8 +865,8 @@ def run_c4(args, cfg, rank, world, local, dev, dist):
     rails.check()
     total_ms = max_over_ranks(total_ms, dist, dev)
     pack_ms = sum(a.elapsed_time(b) for a, b in kev) / args.steps
-    sched_ms = max_over_ranks(
-        sum(sev[i].elapsed_time(kev[i][0]) for i in range(args.steps)) / args.steps, dist, dev)
+    sched_ms, sched_per = sched_times(sev, kev, args.steps)
+    sched_ms = max_over_ranks(sched_ms, dist, dev)
     nodes = UT * M  # (node, layer) schedules of the whole iteration, all ranks together
     peak, peak_kind = measured_peaks()
     pack_bytes = SN * N * T * RB + int(stot.item())
@@ -868,6 +878,8 @@ def run_c4(args, cfg, rank, world, local, dev, dist):
            "config": arm_config(args, P),
            "schedule_only": {"value": nodes / (sched_ms / 1000.0), "unit": "nodes/s",
                              "ms_per_step": sched_ms,
+                             "stat": "median over the timed steps (max over ranks)",
+                             "per_step_ms": [round(v, 5) for v in sched_per],
                              "what": "histogram + schedule + eval + finalize of the rank's "
                                      "layers + the MAX exchange, sampled pack excluded"},
            "pack_gbs": max_over_ranks(pack_bytes, dist, dev, "sum") / (

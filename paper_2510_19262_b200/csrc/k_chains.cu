@@ -222,7 +222,7 @@ constexpr int WS_WARPS = 4;
 constexpr int WS_BATCH = 256;
 
 template <int NT>
-__global__ void __launch_bounds__(WS_WARPS * 32, 7)  // <= 72 registers: C4 (1024 CTAs) fits one wave
+__global__ void __launch_bounds__(WS_WARPS * 32)
     k_lpt_wstage(long long nseg, long long C, long long NG, const int64_t* __restrict__ n_full,
                  const int32_t* __restrict__ n_rem, const uint32_t* __restrict__ ws_w,
                  uint64_t* __restrict__ ws_res, int64_t* __restrict__ send_load) {
@@ -252,8 +252,12 @@ __global__ void __launch_bounds__(WS_WARPS * 32, 7)  // <= 72 registers: C4 (102
   }
   int cur = 0;
   for (int b0 = 0; b0 < nr; b0 += WS_BATCH) {
+    uint32_t cw[PL];
 #pragma unroll
-    for (int p = 0; p < PL; ++p) sW[wid][cur][p * 32 + lane] = pw[p];
+    for (int p = 0; p < PL; ++p) {
+      sW[wid][cur][p * 32 + lane] = pw[p];
+      cw[p] = pw[p];
+    }
     __syncwarp();
     const int nb = b0 + WS_BATCH;  // prefetch the next batch while this one is assigned
 #pragma unroll
@@ -283,7 +287,7 @@ __global__ void __launch_bounds__(WS_WARPS * 32, 7)  // <= 72 registers: C4 (102
 #pragma unroll
         for (int p = 0; p < PL; ++p) {
           const int j = p * 32 + lane;
-          e += __popc(__ballot_sync(0xffffffffu, j >= i && j < cnt && w_[j] == w));
+          e += __popc(__ballot_sync(0xffffffffu, j >= i && j < cnt && cw[p] == w));
         }
         while (i < e && K[NT - 1] - K[0] >= (w << 5)) {
           const uint64_t r = lpt_step_v<NT>(K, w, base);

@@ -242,6 +242,38 @@ def test_eval_parity(M, N, C, U):
         _compare_eval(pipe, u, 0, M, M, N, oracle_eval_from_scheds(M, N, msg[u], scheds))
 
 
+@pytest.mark.parametrize("nsizes,rep", [(20, 40), (45, 40), (60, 32)])
+def test_schedule_many_runs(nsizes, rep):
+    """Remainders in runs of >= 32 equal sizes (the chain's deferred cyclic runs,
+    lpt.cuh RunList): fewer and more runs than the fused kernel's run list holds
+    (32; the rest are written inline), with odd sizes and full chunks around them.
+    Schedule and eval both exact."""
+    M, N, C = 32, 8, 1 << 16
+    G = M * N
+    rng = np.random.default_rng(nsizes * 1000 + rep)
+    msg = np.zeros((1, M, N, G), np.int64)
+    for d in range(M):
+        sizes = rng.choice(np.arange(100, C - 1, 37), nsizes, replace=False)
+        vals = np.repeat(sizes, rep) + C * rng.integers(0, 3, nsizes * rep)
+        extra = rng.integers(1, 4 * C, 60)  # odd sizes between the runs
+        vals = np.concatenate([vals, extra])
+        slots = [(g, h) for g in range(N) for h in range(G) if h // N != d]
+        pick = rng.choice(len(slots), len(vals), replace=False)
+        for v, i in zip(vals, pick):
+            g, h = slots[i]
+            msg[0, d, g, h] = v
+    pipe = MatrixPipeline(M, N, C, 1, 0, M, DEV)
+    pipe.step(torch.from_numpy(msg).to(DEV))
+    torch.cuda.synchronize()
+    scheds = [oracle.schedule_node(msg[0, d], C) for d in range(M)]
+    for d in range(M):
+        compare_schedule(pipe.sched, 0, d, scheds[d], f"d{d}")
+    _compare_eval(pipe, 0, 0, M, M, N, oracle_eval_from_scheds(M, N, msg[0], scheds))
+    s = rails.lpt_schedule(rails.topo(M, N, C), rails.shard(1, 0, M), torch.from_numpy(msg).to(DEV))
+    for d in range(M):
+        compare_schedule(s, 0, d, scheds[d], f"schedule-only d{d}")
+
+
 def test_eval_no_traffic():
     M, N = 3, 2
     msg = np.zeros((1, M, N, M * N), np.int64)

@@ -114,9 +114,12 @@ def bench_matrix(res, name, C=None, U=None):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="c3,c2,c4,c5")
+    ap.add_argument("--lib", default=None, help="time another build (tools/ab_build.py)")
     args = ap.parse_args()
+    if args.lib:
+        rails.LIB_PATH = os.path.abspath(args.lib)
     want = args.only.split(",")
-    res = {"gpu": torch.cuda.get_device_name(0)}
+    res = {"gpu": torch.cuda.get_device_name(0), "lib": rails.LIB_PATH}
     jobs = []
     if "c3" in want:
         jobs.append(("c3", lambda: bench_routing(res, "c3", 1)))
