@@ -29,13 +29,13 @@ namespace rails {
 
 constexpr int HR_MAX_WARPS = 16;
 
-template <int UNR, bool TAG>
+template <int UNR, bool TAG, bool STASH>
 __global__ void __launch_bounds__(HR_MAX_WARPS * 32, 4)  // 4 x 16 warps per SM: one wave for C3
     k_hist_rank(const int32_t* __restrict__ topk, const int32_t* __restrict__ lut, int n_inst,
                 int M, int N, int ngs, int d0, int nd, int T, int k, long long RB, int hbits,
                 int32_t* __restrict__ counts, int64_t* __restrict__ msg,
                 int32_t* __restrict__ rank, int* err) {
-  extern __shared__ __align__(16) int32_t cnt[];  // [W][G]
+  extern __shared__ __align__(16) int32_t cnt[];  // [W][G], then (STASH) u16 h per entry
   pdl_trigger();  // the schedule kernel may be scheduled on the SMs this grid leaves free
   const int W = blockDim.x >> 5;
   const int G = M * N;
@@ -82,7 +82,9 @@ __global__ void __launch_bounds__(HR_MAX_WARPS * 32, 4)  // 4 x 16 warps per SM:
     }
   };
 
-  // ---- pass 1: per-warp sub-histogram
+  // ---- pass 1: per-warp sub-histogram (STASH: each entry's destination kept in
+  // shared memory as u16 for pass 2, instead of re-reading the id and the table)
+  uint16_t* stash = reinterpret_cast<uint16_t*>(cnt + W * G) + beg + lane;
   for (int off = 0; beg + off < end; off += 32 * UNR) {
     int hv[UNR];
     fetch(off, hv);
@@ -90,6 +92,7 @@ __global__ void __launch_bounds__(HR_MAX_WARPS * 32, 4)  // 4 x 16 warps per SM:
     for (int j = 0; j < UNR; ++j) {
       bad |= hv[j] < 0 && beg + off + j * 32 + lane < end;
       if (hv[j] >= 0) atomicAdd(&my[hv[j]], 1);  // private to this warp: order-free count
+      if (STASH && beg + off + j * 32 + lane < end) stash[off + j * 32] = (uint16_t)hv[j];
     }
   }
   if (bad) flag_error(err, ERR_RANGE);
@@ -115,7 +118,15 @@ __global__ void __launch_bounds__(HR_MAX_WARPS * 32, 4)  // 4 x 16 warps per SM:
   const unsigned lt = lanemask_lt();
   for (int off = 0; beg + off < end; off += 32 * UNR) {
     int hv[UNR];
-    fetch(off, hv);
+    if (STASH) {
+#pragma unroll
+      for (int j = 0; j < UNR; ++j) {
+        const int v = beg + off + j * 32 + lane < end ? stash[off + j * 32] : 0xffff;
+        hv[j] = v == 0xffff ? -1 : v;  // invalid entries were stashed as 0xffff
+      }
+    } else {
+      fetch(off, hv);
+    }
 #pragma unroll
     for (int j = 0; j < UNR; ++j) {
       const bool in = beg + off + j * 32 + lane < end;
@@ -258,13 +269,15 @@ __global__ void __launch_bounds__(HW_WARPS * 32, 8)
   }
 }
 
-template <bool TAG>
+template <bool TAG, bool STASH>
 static cudaError_t launch_rank(const LaunchCtx& c, long long grid, int W, int M, int N, int ngs,
                                int d0, int nd, int T, int k, const int32_t* topk,
                                const int32_t* lut, int n_inst, long long RB, int hbits,
                                int32_t* counts, int64_t* msg, int32_t* rank) {
-  const size_t smem = (size_t)W * M * N * sizeof(int32_t);
-  auto kern = k_hist_rank<8, TAG>;
+  const int seg = (int)(((T * k + W - 1) / W + 31) & ~31);  // entries per warp, padded
+  const size_t smem = (size_t)W * M * N * sizeof(int32_t) +
+                      (STASH ? (size_t)W * seg * sizeof(uint16_t) : 0);
+  auto kern = k_hist_rank<8, TAG, STASH>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
@@ -307,11 +320,19 @@ cudaError_t launch_histogram(const LaunchCtx& c, int U, int nd, int d0, int M, i
   // ranks below 2^24: the tag trick; else the per-bit ballot match on the bin index
   int hbits = 0;
   while ((1LL << hbits) < G) ++hbits;
+  // pass 2 reads the destinations pass 1 stashed (u16) when they fit next to the
+  // sub-histograms without costing the 4 CTAs per SM (C3: 32 + 16 KiB)
+  const long long stash_bytes = (long long)W * ((((ne + W - 1) / W) + 31) & ~31LL) * 2;
+  const bool stash = rank != nullptr && G < 65535 &&
+                     (long long)W * G * 4 + stash_bytes <= 56 * 1024;
+  if (ne < (1LL << 24) && stash)
+    return launch_rank<true, true>(c, grid, W, M, N, ngs, d0, nd, T, k, topk, lut, n_inst,
+                                   row_bytes, hbits, counts, msg, rank);
   if (ne < (1LL << 24))
-    return launch_rank<true>(c, grid, W, M, N, ngs, d0, nd, T, k, topk, lut, n_inst, row_bytes,
-                             hbits, counts, msg, rank);
-  return launch_rank<false>(c, grid, W, M, N, ngs, d0, nd, T, k, topk, lut, n_inst, row_bytes,
-                            hbits, counts, msg, rank);
+    return launch_rank<true, false>(c, grid, W, M, N, ngs, d0, nd, T, k, topk, lut, n_inst,
+                                    row_bytes, hbits, counts, msg, rank);
+  return launch_rank<false, false>(c, grid, W, M, N, ngs, d0, nd, T, k, topk, lut, n_inst,
+                                   row_bytes, hbits, counts, msg, rank);
 }
 
 }  // namespace rails

@@ -32,11 +32,11 @@
 //    is one launch, and the workspace is left zeroed for the next call.
 #include "common.cuh"
 #ifdef RAILS_NODE_TIMING
-__device__ unsigned long long g_node_t[16];
-// chain path counters of CTA 0 (slots 12..15): runs, single steps, windows, groups of 8
+__device__ unsigned long long g_node_t[24];
+// chain path counters of CTA 0 (slots 20..23): runs, single steps, windows, groups of 8
 #define LPT_COUNT(i)                                                   \
   do {                                                                 \
-    if (blockIdx.x == 0 && threadIdx.x == 0 && (i) != 1) g_node_t[12 + (i)] += 1; \
+    if (blockIdx.x == 0 && threadIdx.x == 0) g_node_t[20 + (i)] += 1; \
   } while (0)
 #endif
 #include "eval.cuh"
@@ -58,11 +58,11 @@ __device__ unsigned long long g_node_t[16];
     if (blockIdx.x == 0 && threadIdx.x == 32) g_node_t[i] = globaltimer_ns(); \
   } while (0)
 extern "C" int rails_debug_node_reset() {
-  unsigned long long z[16] = {0};
+  unsigned long long z[24] = {0};
   return cudaMemcpyToSymbol(g_node_t, z, sizeof(z)) == cudaSuccess ? 0 : -5;
 }
-extern "C" int rails_debug_node_times(unsigned long long* host16) {
-  return cudaMemcpyFromSymbol(host16, g_node_t, 16 * sizeof(unsigned long long)) == cudaSuccess
+extern "C" int rails_debug_node_times(unsigned long long* host24) {
+  return cudaMemcpyFromSymbol(host24, g_node_t, 24 * sizeof(unsigned long long)) == cudaSuccess
              ? 0
              : -5;
 }
@@ -178,6 +178,7 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
   }
   // launched with programmatic stream serialization: everything above overlapped the
   // histogram kernel's tail; its outputs (msg) are read from here on
+  NODE_T(0);
   pdl_wait();
 
   NODE_T(1);
@@ -215,8 +216,10 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
       snf += nfv[j];
       srem += (B[j] - nfv[j] * C) > 0;
     }
+    if (t0 == 0) NODE_T(14);
     long long tot;
     const long long ex = block_excl_scan((snf << 16) | srem, scan_scratch, &tot);
+    if (t0 == 0) NODE_T(15);
     long long fb = carry_full + (ex >> 16);
     int pos = carry_rem + (int)(ex & 0xffff);
     h = h0;
@@ -248,8 +251,10 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
     carry_full += tot >> 16;
     carry_rem += (int)(tot & 0xffff);
   }
+  NODE_T(16);
   kor = (KeyT)block_reduce_or((uint32_t)kor, red32);
   kand = (KeyT)block_reduce_and((uint32_t)kand, red32);
+  NODE_T(17);
   const long long nf_node = carry_full;
   const int n = carry_rem;
   if (threadIdx.x == 0) {

@@ -41,28 +41,37 @@ def main():
     L.rails_debug_node_reset()
     pipe, topk, lut = routing_pipe("c3", 1)
     rails.histogram(pipe.tp, pipe.sh, topk, lut, pipe.RB, out=(pipe.counts, pipe.msg, pipe.rank))
-    runs = []
-    for it in range(6):
-        s0 = torch.cuda.Event(enable_timing=True)
-        s1 = torch.cuda.Event(enable_timing=True)
-        s0.record()
-        rails.schedule_eval(pipe.tp, pipe.sh, pipe.msg, pipe.sched, pipe.ev, pipe.ws,
-                            final=pipe.final, rail_base=pipe.rail_base, rail_total=pipe.total)
-        s1.record()
-        torch.cuda.synchronize()
-        t = (ctypes.c_ulonglong * 16)()
-        L.rails_debug_node_times(t)
-        t0 = t[1]
-        names = {1: "start A", 2: "B sort", 3: "C chain", 4: "chain start (warp 0)", 5: "D expand",
-                 6: "E eval", 7: "F publish", 8: "CTA0 end", 9: "chain end (warp 0)",
-                 10: "unit-last finalize end", 11: "grid-last rail offsets end",
-                 13: "workers' message pass end"}
-        runs.append({"event_us": round(s0.elapsed_time(s1) * 1000, 2),
-                     **{names[i]: round((t[i] - t0) / 1000.0, 2) for i in names if t[i] >= t0},
-                     "chain_counts(runs,steps,windows,groups8)": [t[12], 0, t[14], t[15]],
-                     "n_rem_node0": int(pipe.sched.n_rem[0, 0])})
-        L.rails_debug_node_reset()
-    print(json.dumps(runs[-3:], indent=1))
+    names = {1: "start A", 2: "B sort", 3: "C chain", 4: "chain start (warp 0)", 5: "D expand",
+             6: "E eval", 7: "F publish", 8: "CTA0 end", 9: "chain end (warp 0)",
+             10: "unit-last finalize end", 11: "grid-last rail offsets end",
+             13: "workers' message pass end", 0: "kernel entry (before PDL wait)",
+             14: "A: first tile loads consumed", 15: "A: first tile scanned",
+             16: "A: tiles done", 17: "A: key or/and reduced"}
+    alone = lambda: rails.schedule_eval(  # noqa: E731
+        pipe.tp, pipe.sh, pipe.msg, pipe.sched, pipe.ev, pipe.ws, final=pipe.final,
+        rail_base=pipe.rail_base, rail_total=pipe.total)
+    part = lambda: pipe.schedule_part(topk, lut)  # noqa: E731 -- histogram + PDL launch
+    runs = {}
+    for mode, fn in (("schedule_eval alone", alone), ("schedule part (histogram, PDL)", part)):
+        out = []
+        for it in range(6):
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            s0.record()
+            fn()
+            s1.record()
+            torch.cuda.synchronize()
+            t = (ctypes.c_ulonglong * 24)()
+            L.rails_debug_node_times(t)
+            t0 = t[1]
+            out.append({"event_us": round(s0.elapsed_time(s1) * 1000, 2),
+                        **{names[i]: round((t[i] - t0) / 1000.0, 2) for i in sorted(names)
+                           if t[i] > 0},
+                        "chain_counts(runs,steps,windows,groups8)": [t[20], t[21], t[22], t[23]],
+                        "n_rem_node0": int(pipe.sched.n_rem[0, 0])})
+            L.rails_debug_node_reset()
+        runs[mode] = out[-2:]
+    print(json.dumps(runs, indent=1))
 
 
 if __name__ == "__main__":
