@@ -154,6 +154,25 @@ __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// Eight consecutive int64 per thread as two 256-bit accesses (sm_100 LDG/STG.256):
+// a warp's 2 KiB then moves in 64 whole sectors instead of 256 partial ones when
+// each thread owns 8 consecutive elements.  p must be 32-byte aligned.
+__device__ __forceinline__ void ld8_s64(const int64_t* p, long long (&v)[8]) {
+  asm volatile("ld.global.v4.s64 {%0,%1,%2,%3}, [%4];"
+               : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3]) : "l"(p));
+  asm volatile("ld.global.v4.s64 {%0,%1,%2,%3}, [%4];"
+               : "=l"(v[4]), "=l"(v[5]), "=l"(v[6]), "=l"(v[7]) : "l"(p + 4));
+}
+__device__ __forceinline__ void st8_s64(int64_t* p, const long long (&v)[8]) {
+  asm volatile("st.global.v4.s64 [%0], {%1,%2,%3,%4};" ::"l"(p), "l"(v[0]), "l"(v[1]),
+               "l"(v[2]), "l"(v[3]) : "memory");
+  asm volatile("st.global.v4.s64 [%0], {%1,%2,%3,%4};" ::"l"(p + 4), "l"(v[4]), "l"(v[5]),
+               "l"(v[6]), "l"(v[7]) : "memory");
+}
+__device__ __forceinline__ bool aligned32(const void* p) {
+  return (reinterpret_cast<uintptr_t>(p) & 31) == 0;
+}
+
 // ECMP rail (R#14): splitmix64 output step, this library's own copy.
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z += 0x9E3779B97F4A7C15ull;

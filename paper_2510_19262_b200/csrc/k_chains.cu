@@ -23,7 +23,7 @@ namespace rails {
 constexpr int SORT_THREADS = 256;
 
 template <typename KeyT, typename IdxT, bool SMEM>
-__global__ void __launch_bounds__(SORT_THREADS)
+__global__ void __launch_bounds__(SORT_THREADS, 3)
     k_chunk_sort(const int64_t* __restrict__ msg, long long NG, int N, int d0, int nd,
                  long long C, int cshift, int nbits, int64_t* __restrict__ full_base,
                  int32_t* __restrict__ ws_inv, int64_t* __restrict__ n_full_out,
@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(SORT_THREADS)
   __shared__ long long scan_scratch[33];
   __shared__ int hist[(SORT_THREADS / 32) * 256];
   __shared__ int sc[256];
-  __shared__ uint32_t red32[32];
+  __shared__ uint32_t red32[64];
 
   const long long seg = blockIdx.x;
   const ChunkDiv cd{C, cshift};
@@ -62,11 +62,18 @@ __global__ void __launch_bounds__(SORT_THREADS)
   long long carry_full = 0;
   int carry_rem = 0;
   KeyT kor = 0, kand = (KeyT)~(KeyT)0;
+  int64_t* __restrict__ fbg = full_base + seg * NG;
+  const bool vec = aligned32(mg) && aligned32(fbg);  // 256-bit accesses (ld8/st8_s64)
   for (long long t0 = 0; t0 < NG; t0 += (long long)blockDim.x * IPT) {
     const long long m0 = t0 + (long long)threadIdx.x * IPT;
+    const bool whole = vec && m0 + IPT <= NG;
     long long B[IPT];
+    if (whole) {
+      ld8_s64(mg + m0, B);
+    } else {
 #pragma unroll
-    for (int j = 0; j < IPT; ++j) B[j] = m0 + j < NG ? mg[m0 + j] : 0;
+      for (int j = 0; j < IPT; ++j) B[j] = m0 + j < NG ? mg[m0 + j] : 0;
+    }
     long long snf = 0;
     int srem = 0;
     long long nfv[IPT];
@@ -91,13 +98,15 @@ __global__ void __launch_bounds__(SORT_THREADS)
     const long long ex = block_excl_scan((snf << 16) | srem, scan_scratch, &tot);
     long long fb = carry_full + (ex >> 16);
     int pos = carry_rem + (int)(ex & 0xffff);
+    long long fbv[IPT];
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
       const long long m = m0 + j;
       if (m >= NG) break;
       const long long nf = nfv[j];
       const long long rem = B[j] - nf * C;
-      full_base[seg * NG + m] = fb;
+      fbv[j] = fb;
+      if (!whole) fbg[m] = fb;
       fb += nf;
       if (rem > 0) {
         const KeyT key = (KeyT)(C - 1 - rem);
@@ -108,11 +117,16 @@ __global__ void __launch_bounds__(SORT_THREADS)
         ++pos;
       }
     }
+    if (whole) st8_s64(fbg + m0, fbv);
     carry_full += tot >> 16;
     carry_rem += (int)(tot & 0xffff);
   }
-  kor = (KeyT)block_reduce_or((uint32_t)kor, red32);
-  kand = (KeyT)block_reduce_and((uint32_t)kand, red32);
+  {
+    uint32_t o = kor, an = kand;
+    block_reduce_or_and(o, an, red32);
+    kor = (KeyT)o;
+    kand = (KeyT)an;
+  }
   if (threadIdx.x == 0) {
     n_full_out[seg] = carry_full;
     n_rem_out[seg] = carry_rem;

@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
   __shared__ long long scan_scratch[33];
   __shared__ int hist[(NODE_MAX_THREADS / 32) * 256];
   __shared__ int sc[256];
-  __shared__ uint32_t red32[32];
+  __shared__ uint32_t red32[64];
   __shared__ long long sL[32], sSe[32], sSu[32];
   __shared__ int s_last;
   __shared__ RunDesc s_runs[NODE_MAX_RUNS];
@@ -190,11 +190,18 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
   int carry_rem = 0;
   KeyT kor = 0, kand = (KeyT)~(KeyT)0;
   const int lo = d * N, hi = d * N + N;  // the source node's own GPUs (R#2)
+  int64_t* __restrict__ fbg = a.s.full_base + seg * NG;
+  const bool vec = aligned32(mg) && aligned32(fbg);  // 256-bit accesses (ld8/st8_s64)
   for (long long t0 = 0; t0 < NG; t0 += (long long)blockDim.x * IPT) {
     const long long m0 = t0 + (long long)threadIdx.x * IPT;
+    const bool whole = vec && m0 + IPT <= NG;
     long long B[IPT];
+    if (whole) {
+      ld8_s64(mg + m0, B);
+    } else {
 #pragma unroll
-    for (int j = 0; j < IPT; ++j) B[j] = m0 + j < NG ? mg[m0 + j] : 0;
+      for (int j = 0; j < IPT; ++j) B[j] = m0 + j < NG ? mg[m0 + j] : 0;
+    }
     long long snf = 0;
     int srem = 0;
     long long nfv[IPT];
@@ -224,13 +231,15 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
     int pos = carry_rem + (int)(ex & 0xffff);
     h = h0;
     int g = g0;
+    long long fbv[IPT];
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
       const long long m = m0 + j;
       if (m >= NG) break;
       const long long nf = nfv[j];
       const long long rem = B[j] - nf * C;
-      a.s.full_base[seg * NG + m] = fb;
+      fbv[j] = fb;
+      if (!whole) fbg[m] = fb;
       if constexpr (EVAL) {
         if (h % N == 0) sP[m / N] = fb;  // block (g, f = h/N) starts here
       }
@@ -248,12 +257,17 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
         ++g;
       }
     }
+    if (whole) st8_s64(fbg + m0, fbv);
     carry_full += tot >> 16;
     carry_rem += (int)(tot & 0xffff);
   }
   NODE_T(16);
-  kor = (KeyT)block_reduce_or((uint32_t)kor, red32);
-  kand = (KeyT)block_reduce_and((uint32_t)kand, red32);
+  {
+    uint32_t o = kor, an = kand;
+    block_reduce_or_and(o, an, red32);
+    kor = (KeyT)o;
+    kand = (KeyT)an;
+  }
   NODE_T(17);
   const long long nf_node = carry_full;
   const int n = carry_rem;
