@@ -33,6 +33,7 @@
 #include "common.cuh"
 #ifdef RAILS_NODE_TIMING
 __device__ unsigned long long g_node_t[24];
+__device__ unsigned long long g_node_cta[4][512];  // per CTA: start A, C, D, F (first 512)
 // chain path counters of CTA 0 (slots 20..23): runs, single steps, windows, groups of 8
 #define LPT_COUNT(i)                                                   \
   do {                                                                 \
@@ -53,6 +54,10 @@ __device__ unsigned long long g_node_t[24];
   do {                                          \
     if (threadIdx.x == 0) g_node_t[i] = globaltimer_ns(); \
   } while (0)
+#define NODE_TC(k)                                                         \
+  do {                                                                     \
+    if (threadIdx.x == 0 && blockIdx.x < 512) g_node_cta[k][blockIdx.x] = globaltimer_ns(); \
+  } while (0)
 #define NODE_TW(i)                                                         \
   do {                                                                     \
     if (blockIdx.x == 0 && threadIdx.x == 32) g_node_t[i] = globaltimer_ns(); \
@@ -60,6 +65,12 @@ __device__ unsigned long long g_node_t[24];
 extern "C" int rails_debug_node_reset() {
   unsigned long long z[24] = {0};
   return cudaMemcpyToSymbol(g_node_t, z, sizeof(z)) == cudaSuccess ? 0 : -5;
+}
+extern "C" int rails_debug_node_cta(unsigned long long* host2048) {
+  return cudaMemcpyFromSymbol(host2048, g_node_cta, 2048 * sizeof(unsigned long long)) ==
+                 cudaSuccess
+             ? 0
+             : -5;
 }
 extern "C" int rails_debug_node_times(unsigned long long* host24) {
   return cudaMemcpyFromSymbol(host24, g_node_t, 24 * sizeof(unsigned long long)) == cudaSuccess
@@ -74,6 +85,9 @@ extern "C" int rails_debug_node_times(unsigned long long* host24) {
   do {             \
   } while (0)
 #define NODE_TW(i) \
+  do {             \
+  } while (0)
+#define NODE_TC(k) \
   do {             \
   } while (0)
 #endif
@@ -182,6 +196,7 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
   pdl_wait();
 
   NODE_T(1);
+  NODE_TC(0);
   // ---- phase A: full_base scan + remainder compaction (+ ECMP and uniform sums)
   // Tiles of blockDim * IPT messages, each thread owning IPT consecutive messages:
   // its loads are all in flight at once, one block scan per tile.
@@ -242,6 +257,18 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
       if (!whole) fbg[m] = fb;
       if constexpr (EVAL) {
         if (h % N == 0) sP[m / N] = fb;  // block (g, f = h/N) starts here
+        if (B[j] > 0) {  // own-node and invalid entries were zeroed above
+          // the ECMP rail (R#13-R#14) and the uniform split (R#41) of the message,
+          // as fire-and-forget split shared sums (add_split20)
+          const int f = h / N;
+          const int e = ecmp_rail(a.seed, (long long)d * N + g, h, N);
+          add_split20(&aElo[f * N + e], &aEhi[f * N + e], (unsigned long long)B[j]);
+          long long qb;
+          int rb;
+          divmod_n(B[j], N, qb, rb);
+          if (qb) add_split20(&aQlo[f], &aQhi[f], (unsigned long long)qb);
+          if (rb) atomicAdd(&cU[f * N + rb], 1u);
+        }
       }
       fb += nf;
       if (rem > 0) {
@@ -290,6 +317,7 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
   for (int i = threadIdx.x; i < n; i += blockDim.x) inv[is[i]] = (IdxT)i;
 
   NODE_T(3);
+  NODE_TC(1);
   // ---- phase C: warp 0 runs the LPT chain; the other warps add the full chunks
   uint64_t* res = a.res_smem ? (uint64_t*)(smem + a.res_off) : a.res_g + seg * NG;
   if (threadIdx.x < 32) {
@@ -305,22 +333,6 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
     NODE_T(9);
     if (threadIdx.x < N) a.s.send_load[seg * N + threadIdx.x] = sL[threadIdx.x];
   } else if constexpr (EVAL) {
-    // the ECMP rails (R#13-R#14) and the uniform split (R#41) of every message, off
-    // the critical path while warp 0 runs the chain (msg is L2-resident: phase A read
-    // it); sums as fire-and-forget split reductions (add_split20)
-    for (unsigned m = threadIdx.x - 32; m < (unsigned)NG; m += blockDim.x - 32) {
-      const long long B = mg[m];
-      const int h = (int)(m % (unsigned)G), g = (int)(m / (unsigned)G);
-      if (B <= 0 || (h >= lo && h < hi)) continue;  // invalid entries were flagged in A
-      const int f = h / N;
-      const int e = ecmp_rail(a.seed, (long long)d * N + g, h, N);
-      add_split20(&aElo[f * N + e], &aEhi[f * N + e], (unsigned long long)B);
-      long long qb;
-      int rb;
-      divmod_n(B, N, qb, rb);
-      if (qb) add_split20(&aQlo[f], &aQhi[f], (unsigned long long)qb);
-      if (rb) atomicAdd(&cU[f * N + rb], 1u);
-    }
     // full chunks: block boundary t (= g*M + f) starts at node-global full index
     // sP[t] = q*N + r; rail j of block t receives (q_b - q_a) + [j < r_b] - [j < r_a]
     for (int t = threadIdx.x - 32; t <= (int)G; t += blockDim.x - 32) {
@@ -331,7 +343,7 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
       sPr[t] = (uint8_t)r;
     }
     asm volatile("bar.sync 1, %0;" ::"r"((int)blockDim.x - 32) : "memory");  // workers only
-    NODE_TW(13);  // workers' ECMP / uniform pass done
+    NODE_TW(13);  // workers' block starts converted
     if constexpr (NT != 0) {
       // thread per destination node f: the q difference is the same for every rail,
       // the [j < r] terms for all NT rails in registers
@@ -375,6 +387,7 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
   __syncthreads();
 
   NODE_T(5);
+  NODE_TC(2);
   // ---- phase D: the chain's deferred runs, QP map (optional), expand, remainders
   // into R_d
   if constexpr (NT != 0) {
@@ -507,21 +520,26 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
   }
 
   NODE_T(7);
+  NODE_TC(3);
   // ---- phase F: the unit's last CTA publishes (and finalizes); the grid's last
   // CTA computes the rail offsets
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    s_last = atomicAdd(&a.cnt[u], 1u) == (unsigned)(a.nd - 1);
+    __threadfence();  // release: this CTA's accumulator adds (ordered by the barrier)
+    const bool last = atomicAdd(&a.cnt[u], 1u) == (unsigned)(a.nd - 1);
+    if (last) __threadfence();  // acquire: every CTA's adds, for the whole CTA (barrier)
+    s_last = last;
   }
   __syncthreads();
   if (s_last) {
-    __threadfence();
+    NODE_TL(12);
+    NODE_TL(18);
     // publish the unit's record (red_sum / red_max), re-zero the accumulator, and
     // take the maxima the finalize needs in the same pass
     int64_t* rs = a.e.red_sum + u * rsl;
     int64_t* rm = a.e.red_max + u * RAILS_RED_MAX_LEN;
     long long mx[4] = {0, 0, 0, 0};  // max R, R_e, R_u, colsum
+    __shared__ long long s_tail[2 + RAILS_RED_MAX_LEN];  // total, total_e, red_max
     for (long long i0 = threadIdx.x; i0 < rec; i0 += 4LL * blockDim.x) {
       long long v[4];
 #pragma unroll
@@ -535,12 +553,14 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
         if (i >= rec) break;
         if (i < rsl) rs[i] = v[q];
         else rm[i - rsl] = v[q];
+        if (i >= RL.tot()) s_tail[i - RL.tot()] = v[q];  // kept for the finalize below
         acc[i] = 0;
         const int cls = i < MN ? 0 : i < 2 * MN ? 1 : i < 3 * MN ? 2 : i < 3 * MN + M ? 3 : 4;
         if (cls < 4) mx[cls] = max(mx[cls], v[q]);
       }
     }
     if (threadIdx.x == 0) a.cnt[u] = 0;
+    NODE_TL(19);
     __shared__ long long s_mx[4][NODE_MAX_THREADS / 32];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -548,15 +568,18 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
       if ((threadIdx.x & 31) == 0) s_mx[q][threadIdx.x >> 5] = w;
     }
     __syncthreads();
-    if (threadIdx.x == 0 && a.do_final) {
-      for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+    if (threadIdx.x < 4 && a.do_final) {  // the four finalize parts on four lanes
+      long long m4[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) s_mx[q][0] = max(s_mx[q][0], s_mx[q][w]);
+      for (int q = 0; q < 4; ++q) {
+        m4[q] = s_mx[q][0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m4[q] = max(m4[q], s_mx[q][w]);
+      }
       long long rmv[RAILS_RED_MAX_LEN];
 #pragma unroll
-      for (int q = 0; q < RAILS_RED_MAX_LEN; ++q) rmv[q] = rm[q];
-      finalize_unit(u, N, a.R2, s_mx[0][0], s_mx[1][0], s_mx[2][0], s_mx[3][0], rmv,
-                    rs[RL.tot()], rs[RL.tot() + 1], a.fin);
+      for (int q = 0; q < RAILS_RED_MAX_LEN; ++q) rmv[q] = s_tail[2 + q];
+      finalize_unit_part((int)threadIdx.x, u, N, a.R2, m4[0], m4[1], m4[2], m4[3], rmv,
+                         s_tail[0], s_tail[1], a.fin);
     }
     NODE_TL(10);
     if (a.rail_base && (int)gridDim.x == a.nd) {  // one unit: this CTA is also the grid's last
@@ -569,11 +592,12 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
-      s_last = atomicAdd(&a.cnt[a.U], 1u) == (unsigned)(gridDim.x - 1);
+      const bool last = atomicAdd(&a.cnt[a.U], 1u) == (unsigned)(gridDim.x - 1);
+      if (last) __threadfence();
+      s_last = last;
     }
     __syncthreads();
     if (s_last) {
-      __threadfence();
       block_rail_offsets<true>((long long)gridDim.x * N, a.s.send_load, a.rail_base,
                                a.rail_total);
       if (threadIdx.x == 0) a.cnt[a.U] = 0;

@@ -121,4 +121,25 @@ __device__ __forceinline__ T block_reduce_and(T v, T* s) {
   return r;
 }
 
+// OR and AND of every thread's key bits in one pass (redux.sync per warp, one
+// barrier to combine; s holds 64 words).
+__device__ __forceinline__ void block_reduce_or_and(uint32_t& o, uint32_t& a, uint32_t* s) {
+  o = __reduce_or_sync(FULL, o);
+  a = __reduce_and_sync(FULL, a);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (lane == 0) {
+    s[wid] = o;
+    s[32 + wid] = a;
+  }
+  __syncthreads();
+  uint32_t ro = 0, ra = ~0u;
+  for (int w = 0; w < nw; ++w) {
+    ro |= s[w];
+    ra &= s[32 + w];
+  }
+  __syncthreads();
+  o = ro;
+  a = ra;
+}
+
 }  // namespace rails

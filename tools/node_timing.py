@@ -38,6 +38,7 @@ def main():
     from tools.sched_bench import routing_pipe
     L = rails.lib()
     L.rails_debug_node_times.argtypes = [ctypes.c_void_p]
+    L.rails_debug_node_cta.argtypes = [ctypes.c_void_p]
     L.rails_debug_node_reset()
     pipe, topk, lut = routing_pipe("c3", 1)
     rails.histogram(pipe.tp, pipe.sh, topk, lut, pipe.RB, out=(pipe.counts, pipe.msg, pipe.rank))
@@ -46,7 +47,9 @@ def main():
              10: "unit-last finalize end", 11: "grid-last rail offsets end",
              13: "workers' message pass end", 0: "kernel entry (before PDL wait)",
              14: "A: first tile loads consumed", 15: "A: first tile scanned",
-             16: "A: tiles done", 17: "A: key or/and reduced"}
+             16: "A: tiles done", 17: "A: key or/and reduced",
+             12: "F: unit-last CTA elected", 18: "F: its fence done",
+             19: "F: record copied (thread 0)"}
     alone = lambda: rails.schedule_eval(  # noqa: E731
         pipe.tp, pipe.sh, pipe.msg, pipe.sched, pipe.ev, pipe.ws, final=pipe.final,
         rail_base=pipe.rail_base, rail_total=pipe.total)
@@ -64,7 +67,24 @@ def main():
             t = (ctypes.c_ulonglong * 24)()
             L.rails_debug_node_times(t)
             t0 = t[1]
-            out.append({"event_us": round(s0.elapsed_time(s1) * 1000, 2),
+            ct = (ctypes.c_ulonglong * 2048)()
+            L.rails_debug_node_cta(ct)
+            nseg = pipe.sched.n_rem.numel()
+            cta = [[ct[k * 512 + b] for b in range(nseg)] for k in range(4)]
+            a0 = min(cta[0])
+            per = {"A start": [round((x - a0) / 1000.0, 2) for x in cta[0]],
+                   "A+B": [round((c - x) / 1000.0, 2) for x, c in zip(cta[0], cta[1])],
+                   "C": [round((c - x) / 1000.0, 2) for x, c in zip(cta[1], cta[2])],
+                   "D+E": [round((c - x) / 1000.0, 2) for x, c in zip(cta[2], cta[3])],
+                   "F arrival": [round((x - a0) / 1000.0, 2) for x in cta[3]]}
+            nrem = pipe.sched.n_rem.reshape(-1).tolist()
+            slow = sorted(range(nseg), key=lambda b: -per["F arrival"][b])[:4]
+            summ = {k: {"min": min(v), "median": sorted(v)[len(v) // 2], "max": max(v)}
+                    for k, v in per.items()}
+            summ["slowest CTAs"] = [{"cta": b, "n_rem": nrem[b], **{k: per[k][b] for k in per}}
+                                   for b in slow]
+            summ["fastest CTA"] = min(range(nseg), key=lambda b: per["F arrival"][b])
+            out.append({"per_cta": summ,"event_us": round(s0.elapsed_time(s1) * 1000, 2),
                         **{names[i]: round((t[i] - t0) / 1000.0, 2) for i in sorted(names)
                            if t[i] > 0},
                         "chain_counts(runs,steps,windows,groups8)": [t[20], t[21], t[22], t[23]],
