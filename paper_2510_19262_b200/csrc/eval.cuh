@@ -80,49 +80,34 @@ __device__ __forceinline__ unsigned long long get_split20(unsigned lo, unsigned 
 }
 
 // T, T*, busbw of unit u from the reduced maxima and totals (R#8, R#10, Thm 2/3;
-// uniform policy R#41; busbw 0 without traffic, R#40).  Four independent parts, so a
-// warp can compute them on four lanes: 0 = LPT (maxload, T, busbw), 1 = ECMP,
-// 2 = uniform, 3 = the lower bound T* and the row / column maxima and total.
-__device__ __forceinline__ void finalize_unit_part(int part, long long u, int N, double R2,
-                                                   long long mR, long long mRe, long long mRu,
-                                                   long long mc,
-                                                   const long long (&rm)[RAILS_RED_MAX_LEN],
-                                                   long long total, long long total_e,
-                                                   const rails_final_t& out) {
-  if (part == 0) {
-    const long long maxload = max(rm[RMAX_S], mR);
-    const double T = __ddiv_rn(__ll2double_rn(maxload), R2);
-    if (out.maxload) out.maxload[u] = maxload;
-    if (out.T) out.T[u] = T;
-    if (out.busbw) out.busbw[u] = total > 0 ? __ddiv_rn(__ll2double_rn(total), T) : 0.0;
-  } else if (part == 1) {
-    const long long maxload_e = max(rm[RMAX_SE], mRe);
-    const double T_e = __ddiv_rn(__ll2double_rn(maxload_e), R2);
-    if (out.maxload_e) out.maxload_e[u] = maxload_e;
-    if (out.T_e) out.T_e[u] = T_e;
-    if (out.busbw_e) out.busbw_e[u] = total_e > 0 ? __ddiv_rn(__ll2double_rn(total_e), T_e) : 0.0;
-  } else if (part == 2) {
-    const long long maxload_u = max(rm[RMAX_SU], mRu);
-    const double T_u = __ddiv_rn(__ll2double_rn(maxload_u), R2);
-    if (out.maxload_u) out.maxload_u[u] = maxload_u;
-    if (out.T_u) out.T_u[u] = T_u;
-    if (out.busbw_u) out.busbw_u[u] = total > 0 ? __ddiv_rn(__ll2double_rn(total), T_u) : 0.0;
-  } else if (part == 3) {
-    const long long rowmax = rm[RMAX_ROW];
-    const long long lb = max(rowmax, mc);
-    if (out.total) out.total[u] = total;
-    if (out.rowmax) out.rowmax[u] = rowmax;
-    if (out.colmax) out.colmax[u] = mc;
-    if (out.T_star) out.T_star[u] = __ddiv_rn(__ll2double_rn(lb), __dmul_rn((double)N, R2));
-  }
-}
+// uniform policy R#41; busbw 0 without traffic, R#40).
 __device__ __forceinline__ void finalize_unit(long long u, int N, double R2, long long mR,
                                               long long mRe, long long mRu, long long mc,
                                               const long long (&rm)[RAILS_RED_MAX_LEN],
                                               long long total, long long total_e,
                                               const rails_final_t& out) {
-  for (int p = 0; p < 4; ++p)
-    finalize_unit_part(p, u, N, R2, mR, mRe, mRu, mc, rm, total, total_e, out);
+  const long long maxload = max(rm[RMAX_S], mR);
+  const long long maxload_e = max(rm[RMAX_SE], mRe);
+  const long long maxload_u = max(rm[RMAX_SU], mRu);
+  const long long rowmax = rm[RMAX_ROW];
+  const double T = __ddiv_rn(__ll2double_rn(maxload), R2);
+  const double T_e = __ddiv_rn(__ll2double_rn(maxload_e), R2);
+  const double T_u = __ddiv_rn(__ll2double_rn(maxload_u), R2);
+  const long long lb = max(rowmax, mc);
+  const double T_star = __ddiv_rn(__ll2double_rn(lb), __dmul_rn((double)N, R2));
+  if (out.maxload) out.maxload[u] = maxload;
+  if (out.maxload_e) out.maxload_e[u] = maxload_e;
+  if (out.maxload_u) out.maxload_u[u] = maxload_u;
+  if (out.total) out.total[u] = total;
+  if (out.rowmax) out.rowmax[u] = rowmax;
+  if (out.colmax) out.colmax[u] = mc;
+  if (out.T) out.T[u] = T;
+  if (out.T_e) out.T_e[u] = T_e;
+  if (out.T_u) out.T_u[u] = T_u;
+  if (out.T_star) out.T_star[u] = T_star;
+  if (out.busbw) out.busbw[u] = total > 0 ? __ddiv_rn(__ll2double_rn(total), T) : 0.0;
+  if (out.busbw_e) out.busbw_e[u] = total_e > 0 ? __ddiv_rn(__ll2double_rn(total_e), T_e) : 0.0;
+  if (out.busbw_u) out.busbw_u[u] = total > 0 ? __ddiv_rn(__ll2double_rn(total), T_u) : 0.0;
 }
 
 // One CTA finalizes unit u from its fully reduced record (rs: red_sum of the unit,
@@ -155,18 +140,17 @@ __device__ void block_finalize_unit(long long u, int M, int N, double R2, const 
     s4[3][wid] = mc;
   }
   __syncthreads();
-  if (threadIdx.x < 4) {  // the four finalize parts on four lanes
-    long long m4[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      m4[q] = s4[q][0];
-      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m4[q] = max(m4[q], s4[q][w]);
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      mR = max(mR, s4[0][w]);
+      mRe = max(mRe, s4[1][w]);
+      mRu = max(mRu, s4[2][w]);
+      mc = max(mc, s4[3][w]);
     }
     long long rmv[RAILS_RED_MAX_LEN];
 #pragma unroll
     for (int i = 0; i < RAILS_RED_MAX_LEN; ++i) rmv[i] = ld(rm + i);
-    finalize_unit_part((int)threadIdx.x, u, N, R2, m4[0], m4[1], m4[2], m4[3], rmv,
-                       ld(rs + L.tot()), ld(rs + L.tot() + 1), out);
+    finalize_unit(u, N, R2, mR, mRe, mRu, mc, rmv, ld(rs + L.tot()), ld(rs + L.tot() + 1), out);
   }
   __syncthreads();
 }

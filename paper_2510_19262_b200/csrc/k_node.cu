@@ -539,7 +539,6 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
     int64_t* rs = a.e.red_sum + u * rsl;
     int64_t* rm = a.e.red_max + u * RAILS_RED_MAX_LEN;
     long long mx[4] = {0, 0, 0, 0};  // max R, R_e, R_u, colsum
-    __shared__ long long s_tail[2 + RAILS_RED_MAX_LEN];  // total, total_e, red_max
     for (long long i0 = threadIdx.x; i0 < rec; i0 += 4LL * blockDim.x) {
       long long v[4];
 #pragma unroll
@@ -553,7 +552,6 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
         if (i >= rec) break;
         if (i < rsl) rs[i] = v[q];
         else rm[i - rsl] = v[q];
-        if (i >= RL.tot()) s_tail[i - RL.tot()] = v[q];  // kept for the finalize below
         acc[i] = 0;
         const int cls = i < MN ? 0 : i < 2 * MN ? 1 : i < 3 * MN ? 2 : i < 3 * MN + M ? 3 : 4;
         if (cls < 4) mx[cls] = max(mx[cls], v[q]);
@@ -568,18 +566,17 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
       if ((threadIdx.x & 31) == 0) s_mx[q][threadIdx.x >> 5] = w;
     }
     __syncthreads();
-    if (threadIdx.x < 4 && a.do_final) {  // the four finalize parts on four lanes
-      long long m4[4];
+    if (threadIdx.x == 0 && a.do_final) {
+      // (the record's maxima and totals as this CTA just stored them; a four-warp
+      // finalize from a shared copy measured ~1 us slower)
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        m4[q] = s_mx[q][0];
-        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m4[q] = max(m4[q], s_mx[q][w]);
-      }
+        for (int q = 0; q < 4; ++q) s_mx[q][0] = max(s_mx[q][0], s_mx[q][w]);
       long long rmv[RAILS_RED_MAX_LEN];
 #pragma unroll
-      for (int q = 0; q < RAILS_RED_MAX_LEN; ++q) rmv[q] = s_tail[2 + q];
-      finalize_unit_part((int)threadIdx.x, u, N, a.R2, m4[0], m4[1], m4[2], m4[3], rmv,
-                         s_tail[0], s_tail[1], a.fin);
+      for (int q = 0; q < RAILS_RED_MAX_LEN; ++q) rmv[q] = rm[q];
+      finalize_unit(u, N, a.R2, s_mx[0][0], s_mx[1][0], s_mx[2][0], s_mx[3][0], rmv,
+                    rs[RL.tot()], rs[RL.tot() + 1], a.fin);
     }
     NODE_TL(10);
     if (a.rail_base && (int)gridDim.x == a.nd) {  // one unit: this CTA is also the grid's last

@@ -55,6 +55,22 @@ def timeit(fn, iters=20, warm=3):
     return {"median_us": round(ts[len(ts) // 2], 2), "best_us": round(ts[0], 2)}
 
 
+def loop_us(fn, iters=50, warm=5):
+    """Mean per call over `iters` back-to-back calls between one event pair (hot L2;
+    resolves differences far below the single-call event granularity)."""
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(iters):
+        fn()
+    b.record()
+    b.synchronize()
+    rails.check()
+    return round(a.elapsed_time(b) * 1000.0 / iters, 2)
+
+
 def routing_pipe(name, U=1):
     cfg = gen.CONFIGS[name]
     M, N, T, k, E, C = cfg["M"], cfg["N"], cfg["T"], cfg["k"], cfg["E"], cfg["C"]
@@ -82,6 +98,7 @@ def bench_routing(res, name, U):
     tsch = timeit(lambda: rails.lpt_schedule(pipe.tp, pipe.sh, pipe.msg, out=pipe.sched,
                                              workspace=pipe.ws))
     tb = timeit(lambda: pipe.schedule_part(topk, lut))
+    tb["loop_hot_us"] = loop_us(lambda: pipe.schedule_part(topk, lut))
     ne = topk.numel()
     G = pipe.M * pipe.N
     nseg = U * pipe.M * pipe.N
@@ -103,6 +120,7 @@ def bench_matrix(res, name, C=None, U=None):
     msg = torch.from_numpy(gen.d1_units(cfg, gen.config_seed(int(name[1])), 0, U)).to(DEV)
     pipe = MatrixPipeline(M, N, cfg["C"], U, 0, M, DEV)
     t = timeit(lambda: pipe.step(msg))
+    t["loop_hot_us"] = loop_us(lambda: pipe.step(msg), iters=10, warm=2)
     tsp = timeit(lambda: (rails.lpt_schedule(pipe.tp, pipe.sh, msg, out=pipe.sched,
                                              workspace=pipe.ws),
                           rails.eval(pipe.tp, pipe.sh, msg, pipe.sched, out=pipe.ev)))
