@@ -32,13 +32,26 @@
 //    is one launch, and the workspace is left zeroed for the next call.
 #include "common.cuh"
 #ifdef RAILS_NODE_TIMING
-__device__ unsigned long long g_node_t[24];
+__device__ unsigned long long g_node_t[32];
 __device__ unsigned long long g_node_cta[4][512];  // per CTA: start A, C, D, F (first 512)
-// chain path counters of CTA 0 (slots 20..23): runs, single steps, windows, groups of 8
+// chain instrumentation (off unless asked for: each adds work to the timed chain):
+// -DRAILS_LPT_CLK sums clock64 cycles of the chain's parts in registers (slots 25..28),
+// -DRAILS_LPT_COUNT counts its paths (slots 20..23: runs, single steps, windows, groups)
+#ifdef RAILS_LPT_CLK
+#define LPT_CLK() clock64()
+#define LPT_ACC_DECL long long lpt_acc_[4] = {0, 0, 0, 0};
+#define LPT_ACC(k, t0) lpt_acc_[k] += clock64() - (t0)
+#define LPT_ACC_FLUSH                                                \
+  if (blockIdx.x == 0 && threadIdx.x == 0) {                         \
+    for (int k_ = 0; k_ < 4; ++k_) g_node_t[25 + k_] = lpt_acc_[k_]; \
+  }
+#endif
+#ifdef RAILS_LPT_COUNT
 #define LPT_COUNT(i)                                                   \
   do {                                                                 \
     if (blockIdx.x == 0 && threadIdx.x == 0) g_node_t[20 + (i)] += 1; \
   } while (0)
+#endif
 #endif
 #include "eval.cuh"
 #include "lpt.cuh"
@@ -63,7 +76,7 @@ __device__ unsigned long long g_node_cta[4][512];  // per CTA: start A, C, D, F 
     if (blockIdx.x == 0 && threadIdx.x == 32) g_node_t[i] = globaltimer_ns(); \
   } while (0)
 extern "C" int rails_debug_node_reset() {
-  unsigned long long z[24] = {0};
+  unsigned long long z[32] = {0};
   return cudaMemcpyToSymbol(g_node_t, z, sizeof(z)) == cudaSuccess ? 0 : -5;
 }
 extern "C" int rails_debug_node_cta(unsigned long long* host2048) {
@@ -72,8 +85,8 @@ extern "C" int rails_debug_node_cta(unsigned long long* host2048) {
              ? 0
              : -5;
 }
-extern "C" int rails_debug_node_times(unsigned long long* host24) {
-  return cudaMemcpyFromSymbol(host24, g_node_t, 24 * sizeof(unsigned long long)) == cudaSuccess
+extern "C" int rails_debug_node_times(unsigned long long* host32) {
+  return cudaMemcpyFromSymbol(host32, g_node_t, 32 * sizeof(unsigned long long)) == cudaSuccess
              ? 0
              : -5;
 }
@@ -323,8 +336,18 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
   if (threadIdx.x < 32) {
     NODE_T(4);
     if constexpr (NT != 0) {
+#ifdef RAILS_CHAIN_TWICE  // debug: the same chain code twice (cold, then warm i-cache)
+#pragma unroll 1
+      for (int rep = 0; rep < 2; ++rep) {
+        if (rep == 1) NODE_T(24);
+        lpt_chain_net<NT, KeyT>(ks, n, C, nf_node, res, sL,
+                                RunList{s_runs, NODE_MAX_RUNS, &s_nrun});
+        __syncwarp();
+      }
+#else
       lpt_chain_net<NT, KeyT>(ks, n, C, nf_node, res, sL,
                               RunList{s_runs, NODE_MAX_RUNS, &s_nrun});
+#endif
     } else {
       const long long L = lpt_chain_generic<KeyT>(ks, n, N, C, nf_node, res, a.err);
       if (threadIdx.x < N) sL[threadIdx.x] = L;

@@ -27,6 +27,14 @@
 
 #include "common.cuh"
 
+#ifndef LPT_CLK
+#define LPT_CLK() 0LL  // debug builds: clock64(), sums in registers (k_node.cu)
+#define LPT_ACC(k, t0) \
+  do {                 \
+  } while (0)
+#define LPT_ACC_DECL
+#define LPT_ACC_FLUSH
+#endif
 #ifndef LPT_COUNT
 #define LPT_COUNT(i) \
   do {               \
@@ -248,6 +256,7 @@ __device__ void lpt_chain_net(const KeyT* __restrict__ key, int nr, long long C,
                               uint64_t* __restrict__ res, long long* __restrict__ load_out,
                               RunList rl = RunList{nullptr, 0, nullptr}) {
   static_assert(NT <= 8, "RunDesc holds at most 8 rail keys");
+  LPT_ACC_DECL
   int nrun = 0;
   const int lane = threadIdx.x & 31;
   const SortedSizes<KeyT> W{key, (uint32_t)(C - 1)};
@@ -261,13 +270,17 @@ __device__ void lpt_chain_net(const KeyT* __restrict__ key, int nr, long long C,
     K[i] = (((i < NT - r) ? 0u : (uint32_t)C) << 5) | (uint32_t)rail;
   }
   int i = 0;
+  const long long tchain = LPT_CLK();
   while (i < nr) {
     const uint32_t w = W(i);
     if (i + 32 <= nr && W(i + 31) == w) {
       // a run [i, e) of equal sizes: single steps until the cyclic condition holds,
       // then the closed form written by all lanes
       LPT_COUNT(0);
+      long long tc = LPT_CLK();
       const int e = run_end(key, i, nr, lane);
+      LPT_ACC(0, tc);
+      tc = LPT_CLK();
       while (i < e && K[NT - 1] - K[0] >= (w << 5)) {
         LPT_COUNT(1);
         const uint64_t rv = lpt_step_v<NT>(K, w, base);
@@ -275,6 +288,8 @@ __device__ void lpt_chain_net(const KeyT* __restrict__ key, int nr, long long C,
         lpt_rebase<NT>(K, base);
         ++i;
       }
+      LPT_ACC(1, tc);
+      tc = LPT_CLK();
       if (i < e) {
         if (nrun < rl.cap) {
           if (lane == 0) {
@@ -292,6 +307,7 @@ __device__ void lpt_chain_net(const KeyT* __restrict__ key, int nr, long long C,
           lpt_run_cyclic<NT>(K, w, e - i, lane, res + i, base);
         }
       }
+      LPT_ACC(2, tc);
       i = e;
     } else if ((8 % NT) == 0 && (i & 7) == 0 && i + 8 <= nr && W(i + 7) == w &&
                K[NT - 1] - K[0] < (w << 5)) {
@@ -346,6 +362,8 @@ __device__ void lpt_chain_net(const KeyT* __restrict__ key, int nr, long long C,
       ++i;
     }
   }
+  LPT_ACC(3, tchain);
+  LPT_ACC_FLUSH
   if (lane == 0) {  // final LoadState by rail (K holds every rail once)
 #pragma unroll
     for (int j = 0; j < NT; ++j) load_out[K[j] & 31u] = base + (long long)(K[j] >> 5);

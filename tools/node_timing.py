@@ -14,13 +14,13 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def build_debug(out_dir):
+def build_debug(out_dir, extra=()):
     from paper_2510_19262_b200 import build as b
     os.makedirs(out_dir, exist_ok=True)
     objs = []
     for src in b.SOURCES:
         obj = os.path.join(out_dir, src.replace(".cu", ".o"))
-        subprocess.check_call([b.NVCC, *b.FLAGS, "-DRAILS_NODE_TIMING", "-c",
+        subprocess.check_call([b.NVCC, *b.FLAGS, "-DRAILS_NODE_TIMING", *extra, "-c",
                                os.path.join(b.CSRC, src), "-o", obj],
                               stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
         objs.append(obj)
@@ -31,7 +31,8 @@ def build_debug(out_dir):
 
 
 def main():
-    lib = build_debug(os.path.join(ROOT, "gpurun_out", "timing_build"))
+    extra = [a for a in sys.argv[1:] if a.startswith("-D")]
+    lib = build_debug(os.path.join(ROOT, "gpurun_out", "timing_build"), extra)
     from paper_2510_19262_b200 import rails
     rails.LIB_PATH = lib
     import torch
@@ -49,7 +50,7 @@ def main():
              14: "A: first tile loads consumed", 15: "A: first tile scanned",
              16: "A: tiles done", 17: "A: key or/and reduced",
              12: "F: unit-last CTA elected", 18: "F: its fence done",
-             19: "F: record copied (thread 0)"}
+             19: "F: record copied (thread 0)", 24: "chain second pass start (CHAIN_TWICE)"}
     alone = lambda: rails.schedule_eval(  # noqa: E731
         pipe.tp, pipe.sh, pipe.msg, pipe.sched, pipe.ev, pipe.ws, final=pipe.final,
         rail_base=pipe.rail_base, rail_total=pipe.total)
@@ -64,7 +65,7 @@ def main():
             fn()
             s1.record()
             torch.cuda.synchronize()
-            t = (ctypes.c_ulonglong * 24)()
+            t = (ctypes.c_ulonglong * 32)()
             L.rails_debug_node_times(t)
             t0 = t[1]
             ct = (ctypes.c_ulonglong * 2048)()
@@ -88,6 +89,8 @@ def main():
                         **{names[i]: round((t[i] - t0) / 1000.0, 2) for i in sorted(names)
                            if t[i] > 0},
                         "chain_counts(runs,steps,windows,groups8)": [t[20], t[21], t[22], t[23]],
+                        "chain_cycles(run_end,lead,run_record,whole)": [t[25], t[26], t[27],
+                                                                        t[28]],
                         "n_rem_node0": int(pipe.sched.n_rem[0, 0])})
             L.rails_debug_node_reset()
         runs[mode] = out[-2:]
