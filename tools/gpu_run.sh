@@ -25,7 +25,7 @@ for step in "$@"; do
     ref)
       timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err ;;
     launches)
-      timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+      timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:^k_ -c 400 --csv \
         --log-file gpurun_out/launches.csv python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu --no-graph $arg \
         > gpurun_out/launches.log 2>&1 ;;
     dbench)

@@ -4,7 +4,7 @@
 mkdir -p gpurun_out
 B="python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu --no-graph --no-extra"
 $B > gpurun_out/plain_bench.json 2> gpurun_out/plain_bench.err && \
-  ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+  ncu --metrics gpu__time_duration.sum --clock-control none -k regex:^k_ -c 400 --csv \
       --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_launches.log 2>&1
 echo "launches rc=$?" >> gpurun_out/rc.txt
 python tools/sched_bench.py --only c3 > gpurun_out/sb3.json 2>&1 && \
