@@ -236,7 +236,7 @@ constexpr int WS_WARPS = 4;
 constexpr int WS_BATCH = 256;
 
 template <int NT>
-__global__ void __launch_bounds__(WS_WARPS * 32)
+__global__ void __launch_bounds__(WS_WARPS * 32, 7)  // <= 72 registers: C4 (1024 CTAs) fits one wave
     k_lpt_wstage(long long nseg, long long C, long long NG, const int64_t* __restrict__ n_full,
                  const int32_t* __restrict__ n_rem, const uint32_t* __restrict__ ws_w,
                  uint64_t* __restrict__ ws_res, int64_t* __restrict__ send_load) {
