@@ -240,7 +240,8 @@ cudaError_t launch_node(const LaunchCtx&, int U, int nd, int d0, int M, int N, l
 cudaError_t launch_chains(const LaunchCtx&, int U, int nd, int d0, int M, int N, long long C,
                           const int64_t* msg, const rails_sched_t& s, uint64_t* ws_res,
                           uint32_t* ws_qp, uint32_t* ws_w, int32_t* ws_inv, uint8_t* scratch,
-                          int32_t* rem_qp, int qps_per_rail, int cshift, int nbits);
+                          int32_t* rem_qp, int qps_per_rail, int cshift, int nbits,
+                          bool defer_expand = false);
 
 void schedule_workspace_ptrs(void* ws, int U, int nd, int M, int N, int64_t** acc,
                              unsigned** cnt, uint64_t** res);
@@ -249,9 +250,13 @@ cudaError_t launch_assign(const LaunchCtx&, int N, int n_seg, const int64_t* seg
                           long long F, const int64_t* w, int32_t* rail, int64_t* off,
                           int64_t* load, void* ws);
 
+// ex_inv / ex_res (optional): the chains' inverse permutation and sorted-order
+// results; the evaluation then also expands them into s.rem_rail / s.rem_off (the
+// k_expand pass fused into its message loop) instead of reading s.rem_rail.
 cudaError_t launch_eval(const LaunchCtx&, int U, int nd, int d0, int M, int N, long long C,
                         uint64_t seed, const int64_t* msg, const rails_sched_t& s,
-                        const rails_eval_t& e);
+                        const rails_eval_t& e, const int32_t* ex_inv = nullptr,
+                        const uint64_t* ex_res = nullptr);
 cudaError_t launch_finalize(const LaunchCtx&, int U, int M, int N, double R2,
                             const int64_t* red_sum, const int64_t* red_max,
                             const rails_final_t& f);

@@ -424,7 +424,8 @@ __global__ void __launch_bounds__(256)
 cudaError_t launch_chains(const LaunchCtx& c, int U, int nd, int d0, int M, int N, long long C,
                           const int64_t* msg, const rails_sched_t& s, uint64_t* ws_res,
                           uint32_t* ws_qp, uint32_t* ws_w, int32_t* ws_inv, uint8_t* scratch,
-                          int32_t* rem_qp, int qps_per_rail, int cshift, int nbits) {
+                          int32_t* rem_qp, int qps_per_rail, int cshift, int nbits,
+                          bool defer_expand) {
   const long long nseg = (long long)U * nd;
   const long long NG = (long long)N * M * N;
   cudaError_t e;
@@ -461,6 +462,7 @@ cudaError_t launch_chains(const LaunchCtx& c, int U, int nd, int d0, int M, int 
     count_launch(1);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
+  if (defer_expand && !rem_qp) return cudaSuccess;  // the evaluation expands (k_eval.cu)
   const long long gy = nseg < 65535 ? nseg : 65535;
   k_expand<<<dim3((unsigned)((NG / 4 + 256) / 256), (unsigned)gy), 256, 0, c.stream>>>(
       NG, nseg, ws_inv, ws_res, s.rem_rail, s.rem_off, rem_qp ? ws_qp : nullptr, rem_qp);

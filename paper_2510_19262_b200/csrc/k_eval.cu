@@ -36,7 +36,9 @@ __global__ void __launch_bounds__(EV2_THREADS, 4)
     k_eval_node(int M, int N_rt, int nd, int d0, long long C, int cshift, uint64_t seed, int FT,
                 const int64_t* __restrict__ msg, const int64_t* __restrict__ full_base,
                 const int8_t* __restrict__ rem_rail, const int64_t* __restrict__ n_full,
-                rails_eval_t ev) {
+                rails_eval_t ev, const int32_t* __restrict__ ex_inv,
+                const uint64_t* __restrict__ ex_res, int8_t* __restrict__ ex_rail,
+                int64_t* __restrict__ ex_off) {
   extern __shared__ __align__(16) uint8_t ev_smem[];
   __shared__ unsigned long long sS[32], sSe[32], sSu[32], sCol[EV2_THREADS];
   // per (fl, j) of the tile: remainder bytes into NIC (f, j), ECMP bytes; uniform:
@@ -53,6 +55,14 @@ __global__ void __launch_bounds__(EV2_THREADS, 4)
   const int64_t* __restrict__ mg = msg + seg * NG;
   const int64_t* __restrict__ fbp = full_base + seg * NG;
   const int8_t* __restrict__ rrp = rem_rail + seg * NG;
+  // expand mode (ex_inv != nullptr): rem_rail / rem_off of every message come from the
+  // chains' results through the inverse permutation and are written here
+  const bool ex = ex_inv != nullptr;
+  const int32_t* __restrict__ xinv = ex ? ex_inv + seg * NG : nullptr;
+  const uint64_t* __restrict__ xres = ex ? ex_res + seg * NG : nullptr;
+  int8_t* __restrict__ xrail = ex ? ex_rail + seg * NG : nullptr;
+  int64_t* __restrict__ xoff = ex ? ex_off + seg * NG : nullptr;
+  constexpr uint64_t XOFF_MASK = (1ull << 56) - 1;  // results: rail << 56 | offset
   const long long nfull_node = n_full[seg];
   const RedLayout RL{(long long)M * N, M};
   unsigned long long* rs = (unsigned long long*)(ev.red_sum + u * RL.len());
@@ -93,21 +103,49 @@ __global__ void __launch_bounds__(EV2_THREADS, 4)
         if (qb) add_split20(&aQlo[fl], &aQhi[fl], (unsigned long long)qb);
         if (rb) atomicAdd(&cU[fb + rb], 1u);
       };
+      // expand: message idx's remainder result (rail, offset), written out
+      auto expand = [&](long long idx, int p, uint64_t v) -> int8_t {
+        const int8_t r = p >= 0 ? (int8_t)(v >> 56) : (int8_t)-1;
+        xrail[idx] = r;
+        xoff[idx] = p >= 0 ? (long long)(v & XOFF_MASK) : 0;
+        return r;
+      };
       if (NT != 0 && gsp == 1) {
         // all N source GPUs' loads in flight at once (one DRAM latency per tile)
         long long Bv[NT ? NT : 1];
         int8_t rvv[NT ? NT : 1];
+        if (ex) {
+          int pv[NT ? NT : 1];
+          uint64_t vv[NT ? NT : 1];
 #pragma unroll
-        for (int g = 0; g < NT; ++g) {
-          Bv[g] = mg[(long long)g * G + h];
-          rvv[g] = rrp[(long long)g * G + h];
+          for (int g = 0; g < NT; ++g) {
+            Bv[g] = mg[(long long)g * G + h];
+            pv[g] = xinv[(long long)g * G + h];
+          }
+#pragma unroll
+          for (int g = 0; g < NT; ++g) vv[g] = pv[g] >= 0 ? xres[pv[g]] : 0ull;
+#pragma unroll
+          for (int g = 0; g < NT; ++g) rvv[g] = expand((long long)g * G + h, pv[g], vv[g]);
+        } else {
+#pragma unroll
+          for (int g = 0; g < NT; ++g) {
+            Bv[g] = mg[(long long)g * G + h];
+            rvv[g] = rrp[(long long)g * G + h];
+          }
         }
 #pragma unroll
         for (int g = 0; g < NT; ++g) add_msg(g, Bv[g], rvv[g]);
       } else {
         for (int g = gq; g < N; g += gsp) {
           const long long idx = (long long)g * G + h;
-          add_msg(g, mg[idx], rrp[idx]);
+          int8_t rv;
+          if (ex) {
+            const int p = xinv[idx];
+            rv = expand(idx, p, p >= 0 ? xres[p] : 0ull);
+          } else {
+            rv = rrp[idx];
+          }
+          add_msg(g, mg[idx], rv);
         }
       }
     }
@@ -344,7 +382,7 @@ __global__ void __launch_bounds__(1024)
 
 cudaError_t launch_eval(const LaunchCtx& c, int U, int nd, int d0, int M, int N, long long C,
                         uint64_t seed, const int64_t* msg, const rails_sched_t& s,
-                        const rails_eval_t& e) {
+                        const rails_eval_t& e, const int32_t* ex_inv, const uint64_t* ex_res) {
   const long long rsl = RAILS_RED_SUM_LEN(M, N);
   cudaError_t err =
       cudaMemsetAsync(e.red_sum, 0, (size_t)U * rsl * sizeof(int64_t), c.stream);
@@ -357,7 +395,8 @@ cudaError_t launch_eval(const LaunchCtx& c, int U, int nd, int d0, int M, int N,
   err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   kern<<<(unsigned)((long long)U * nd), EV2_THREADS, smem, c.stream>>>(
-      M, N, nd, d0, C, pow2_shift(C), seed, FT, msg, s.full_base, s.rem_rail, s.n_full, e);
+      M, N, nd, d0, C, pow2_shift(C), seed, FT, msg, s.full_base, s.rem_rail, s.n_full, e,
+      ex_inv, ex_res, ex_inv ? s.rem_rail : nullptr, ex_inv ? s.rem_off : nullptr);
   count_launch(1);
   return cudaGetLastError();
 }

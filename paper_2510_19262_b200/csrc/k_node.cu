@@ -785,8 +785,24 @@ cudaError_t launch_node(const LaunchCtx& c, int U, int nd, int d0, int M, int N,
   if (nseg > 2LL * c.num_sms) {
     // many segments (C2's 16 000, a C4 iteration's 4 096): per-phase kernels at their
     // own occupancy measured faster than one CTA walking every phase (k_chains.cu)
-    return launch_chains(c, U, nd, d0, M, N, C, msg, s, w.res_g, w.qp_g, w.w_g, w.inv_g,
-                         w.scratch, rem_qp, qps_per_rail, cshift, nbits);
+    // With an evaluation (and no QP map) the expand pass runs inside it: one pass over
+    // the messages instead of two.
+    const bool ex = ev != nullptr && rem_qp == nullptr;
+    cudaError_t e = launch_chains(c, U, nd, d0, M, N, C, msg, s, w.res_g, w.qp_g, w.w_g,
+                                  w.inv_g, w.scratch, rem_qp, qps_per_rail, cshift, nbits, ex);
+    if (e != cudaSuccess || !ex) return e;
+    if ((e = launch_eval(c, U, nd, d0, M, N, C, seed, msg, s, *ev, w.inv_g, w.res_g)) !=
+        cudaSuccess)
+      return e;
+    if (fin && (e = launch_finalize(c, U, M, N, R2, ev->red_sum, ev->red_max, *fin)) !=
+                   cudaSuccess)
+      return e;
+    if (rail_base &&
+        (e = launch_rail_offsets(c, (long long)U * nd * N, s.send_load, rail_base,
+                                 rail_total)) != cudaSuccess)
+      return e;
+    if (fused) *fused = true;  // evaluated (and finalized / offset) here
+    return cudaSuccess;
   }
   NodePlan p = node_plan(M, N, C, ev != nullptr, nseg, c.num_sms);
   if (p.eval_fused && !p.smem_sort) {
