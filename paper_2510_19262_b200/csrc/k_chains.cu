@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(SORT_THREADS, 3)
   KeyT kor = 0, kand = (KeyT)~(KeyT)0;
   int64_t* __restrict__ fbg = full_base + seg * NG;
   const bool vec = aligned32(mg) && aligned32(fbg);  // 256-bit accesses (ld8/st8_s64)
+  bool bad_range = false, bad_ovf = false;  // flagged once after the pass
   for (long long t0 = 0; t0 < NG; t0 += (long long)blockDim.x * IPT) {
     const long long m0 = t0 + (long long)threadIdx.x * IPT;
     const bool whole = vec && m0 + IPT <= NG;
@@ -84,13 +85,12 @@ __global__ void __launch_bounds__(SORT_THREADS, 3)
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
       // negative bytes, or bytes to a GPU of the source node (R#2), are invalid
-      if (B[j] < 0 || (B[j] != 0 && h >= lo && h < hi)) {
-        flag_error(err, ERR_RANGE);
-        B[j] = 0;
-      }
+      const bool inval = B[j] < 0 || (B[j] != 0 && h >= lo && h < hi);
+      bad_range |= inval;
+      if (inval) B[j] = 0;
       if (++h >= G) h -= G;
       nfv[j] = cd.div(B[j]);
-      if (nfv[j] >= (1LL << 40)) flag_error(err, ERR_OVERFLOW);
+      bad_ovf |= nfv[j] >= (1LL << 40);
       snf += nfv[j];
       srem += (B[j] - nfv[j] * C) > 0;
     }
@@ -121,6 +121,8 @@ __global__ void __launch_bounds__(SORT_THREADS, 3)
     carry_full += tot >> 16;
     carry_rem += (int)(tot & 0xffff);
   }
+  if (bad_range) flag_error(err, ERR_RANGE);
+  if (bad_ovf) flag_error(err, ERR_OVERFLOW);
   {
     uint32_t o = kor, an = kand;
     block_reduce_or_and(o, an, red32);
@@ -133,7 +135,8 @@ __global__ void __launch_bounds__(SORT_THREADS, 3)
   }
   __syncthreads();
   const int n = carry_rem;
-  const int which = radix_sort<KeyT, IdxT>(kA, iA, kB, iB, n, kor, kand, nbits, hist, sc);
+  const int which =
+      radix_sort_narrow<KeyT, IdxT>(kA, iA, kB, iB, n, kor, kand, nbits, hist, sc);
   const KeyT* ks = which ? kB : kA;
   const IdxT* is = which ? iB : iA;
   // inverse permutation in the free index buffer, then written out coalesced

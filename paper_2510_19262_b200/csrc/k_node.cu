@@ -220,6 +220,7 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
   const int lo = d * N, hi = d * N + N;  // the source node's own GPUs (R#2)
   int64_t* __restrict__ fbg = a.s.full_base + seg * NG;
   const bool vec = aligned32(mg) && aligned32(fbg);  // 256-bit accesses (ld8/st8_s64)
+  bool bad_range = false, bad_ovf = false;  // flagged once after the pass
   for (long long t0 = 0; t0 < NG; t0 += (long long)blockDim.x * IPT) {
     const long long m0 = t0 + (long long)threadIdx.x * IPT;
     const bool whole = vec && m0 + IPT <= NG;
@@ -241,13 +242,12 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
       // negative bytes, or bytes to a GPU of the source node (R#2), are invalid
-      if (B[j] < 0 || (B[j] != 0 && h >= lo && h < hi)) {
-        flag_error(a.err, ERR_RANGE);
-        B[j] = 0;
-      }
+      const bool inval = B[j] < 0 || (B[j] != 0 && h >= lo && h < hi);
+      bad_range |= inval;
+      if (inval) B[j] = 0;
       if (++h >= G) h -= (int)G;
       nfv[j] = cd.div(B[j]);
-      if (nfv[j] >= (1LL << 40)) flag_error(a.err, ERR_OVERFLOW);
+      bad_ovf |= nfv[j] >= (1LL << 40);
       snf += nfv[j];
       srem += (B[j] - nfv[j] * C) > 0;
     }
@@ -301,6 +301,8 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
     carry_full += tot >> 16;
     carry_rem += (int)(tot & 0xffff);
   }
+  if (bad_range) flag_error(a.err, ERR_RANGE);
+  if (bad_ovf) flag_error(a.err, ERR_OVERFLOW);
   NODE_T(16);
   {
     uint32_t o = kor, an = kand;

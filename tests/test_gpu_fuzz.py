@@ -9,7 +9,8 @@ import torch
 
 import gen
 import oracle
-from helpers import compare_schedule, oracle_eval_from_scheds, rel_err, routing_inputs
+from helpers import (compare_schedule, oracle_eval_from_scheds, random_msg, rel_err,
+                     routing_inputs)
 
 pytestmark = pytest.mark.gpu
 
@@ -99,6 +100,30 @@ def test_fuzz_routing_pack(seed):
     for u in range(U):
         for dl in range(nd):
             _oracle_pack_check(pipe, topk, lut, x, u, dl)
+
+
+@pytest.mark.parametrize("C,mult", [(65536, 4096), (65536, 12288), (32768, 8192),
+                                    (1 << 20, 3 << 14), (4096, 1), (65536, 1 << 15)])
+def test_many_segments_narrow_digits(C, mult):
+    """Message sizes on a granule (routing: multiples of the row size), so the
+    remainder keys vary in a few bits only and the many-segment sort runs 1-8-bit
+    digit passes over just those bits (radix.cuh radix_sort_narrow); with the
+    expand pass inside the evaluation.  Exact against the oracle on sampled units."""
+    rng = np.random.default_rng(C + mult)
+    M, N = 4, 8
+    U = 2 * 148 // M + 7  # > 2 x the SM count of segments: k_chains.cu
+    msg = random_msg(rng, U, M, N, p=0.7, hi=40, mult=mult)
+    pipe = MatrixPipeline(M, N, C, U, 0, M, DEV)
+    pipe.step(torch.from_numpy(msg).to(DEV))
+    torch.cuda.synchronize()
+    for u in rng.choice(U, size=4, replace=False):
+        scheds = [oracle.schedule_node(msg[u, d], C) for d in range(M)]
+        for d in range(M):
+            compare_schedule(pipe.sched, u, d, scheds[d], f"C{C} mult{mult} u{u} d{d}")
+        ev = oracle_eval_from_scheds(M, N, msg[u], scheds)
+        assert np.array_equal(pipe.ev.S[u].cpu().numpy(), ev["S"])
+        for k in ("maxload", "maxload_e", "maxload_u", "total"):
+            assert int(pipe.final[k][u]) == ev[k], (C, mult, k)
 
 
 @pytest.mark.parametrize("seed", range(8))
