@@ -322,7 +322,8 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
 
   NODE_T(2);
   // ---- phase B: stable radix sort of the remainder keys
-  const int which = radix_sort<KeyT, IdxT>(kA, iA, kB, iB, n, kor, kand, a.nbits, hist, sc);
+  const int which =
+      radix_sort_narrow<KeyT, IdxT>(kA, iA, kB, iB, n, kor, kand, a.nbits, hist, sc);
   const KeyT* ks = which ? kB : kA;
   const IdxT* is = which ? iB : iA;
   IdxT* inv = which ? iA : iB;  // inverse permutation: message -> sorted position

@@ -101,8 +101,9 @@ __device__ int radix_sort(KeyT* kA, IdxT* iA, KeyT* kB, IdxT* iB, int n, KeyT ko
 // NB ballots per 32 keys, 2^NB bins), and the sort that covers only the key bits that
 // vary (kor ^ kand) in windows of <= 8 bits ending on a varying bit.  Routing traffic
 // has few remainder sizes (multiples of the row size), so its keys vary in a few bits
-// (C4: 3) and one narrow pass replaces an 8-bit one.  Used by the many-segment sort
-// (k_chains.cu); the fused node kernel keeps the 8-bit passes (measured faster there).
+// (C4: 3, C3: 2) and one narrow pass replaces an 8-bit one.  Used by the schedule's
+// sorts (k_node.cu, k_chains.cu); radix_sort above keeps 8-bit passes (k_sched.cu's
+// 64-bit flow keys, the fluid simulator).
 template <typename KeyT, typename IdxT, int NB>
 __device__ void radix_pass_nb(const KeyT* kin, const IdxT* iin, KeyT* kout, IdxT* iout, int n,
                               int shift, int* hist, int* sc) {
