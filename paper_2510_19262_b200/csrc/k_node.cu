@@ -11,13 +11,17 @@
 //    prefix of floor(B/C) in (g,h) order (one block scan per tile of messages) and
 //    compacts the remainders (at most one per message) in (g,h) order.
 // a3: phase B sorts the remainders by size descending with a stable
-//    LSD radix sort on key = C-1-size (constant digits skipped); stability keeps
+//    LSD radix sort on key = C-1-size over only the key bits that vary (radix.cuh
+//    radix_sort_narrow: routing remainders are multiples of the row size, so C3's
+//    keys vary in 2 bits and one 2-bit pass sorts them); stability keeps
 //    (g,h) order among equal sizes = the tie-break R#4.  In shared memory when the
 //    node fits (N*G <= 16384), else in a global scratch.
 // a4: phase C, warp 0 runs the serial chain (lpt.cuh) over the sorted
-//    list; results land in sorted order (shared memory when they fit).  Phase D
-//    expands them to per-message rem_rail / rem_off through the sort's inverse
-//    permutation (and the QP map of Alg. 2 step 4, R#34, when asked).
+//    list; results land in sorted order (shared memory when they fit); runs of equal
+//    sizes are recorded as (start state, length) and written by the whole CTA at the
+//    start of phase D.  Phase D expands the results to per-message rem_rail /
+//    rem_off through the sort's inverse permutation (and the QP map of Alg. 2 step
+//    4, R#34, when asked).
 // a5 (EVAL): while warp 0 runs the chain, the other warps add the full chunks into
 //    R_d[f][j] by the closed form (message block (g, f*N..f*N+N-1) holds the
 //    node-global full chunks [P_gf, P_g,f+1); rail j receives cnt_j(b) - cnt_j(a),
