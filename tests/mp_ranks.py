@@ -50,7 +50,20 @@ def _entry(body, rank, world, port, placement, cfg, q):
 
 def run_ranks(body, world: int, placement: str, cfg: dict, timeout_s: float = 900.0):
     """Spawn `world` ranks running body(rank, world, device, cfg) -> list of error
-    strings; assert every rank reported and none reported an error."""
+    strings; assert every rank reported and none reported an error.  A rendezvous
+    port taken between picking it and binding it (EADDRINUSE) is retried on a new
+    port."""
+    for attempt in range(3):
+        res, procs = _spawn(body, world, placement, cfg, timeout_s)
+        taken = any("EADDRINUSE" in e for errs in res.values() for e in errs)
+        if not taken or attempt == 2:
+            break
+    for r, errs in res.items():
+        assert not errs, (placement, r, errs)
+    assert len(res) == world, f"{placement}: workers exit codes {[p.exitcode for p in procs]}"
+
+
+def _spawn(body, world, placement, cfg, timeout_s):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
@@ -73,6 +86,4 @@ def run_ranks(body, world: int, placement: str, cfg: dict, timeout_s: float = 90
         p.join(timeout=60)
         if p.is_alive():
             p.kill()
-    for r, errs in res.items():
-        assert not errs, (placement, r, errs)
-    assert len(res) == world, f"{placement}: workers exit codes {[p.exitcode for p in procs]}"
+    return res, procs
