@@ -90,6 +90,9 @@ def bench_routing(res, name, U):
                                         pipe.ws, final=pipe.final, rail_base=pipe.rail_base,
                                         rail_total=pipe.total)
     th = timeit(hist)
+    hb = rails.bind_histogram(pipe.tp, pipe.sh, topk, lut, pipe.RB,
+                              (pipe.counts, pipe.msg, pipe.rank))
+    th["loop_hot_us"] = loop_us(lambda: hb(None))
     tf = timeit(fused)
     split = lambda: (rails.lpt_schedule(pipe.tp, pipe.sh, pipe.msg, out=pipe.sched,  # noqa: E731
                                         workspace=pipe.ws),
