@@ -26,6 +26,8 @@ DEV = "cuda:0"
 
 
 def main():
+    if len(sys.argv) > 1:  # another build (tools/ab_build.py)
+        rails.LIB_PATH = os.path.abspath(sys.argv[1])
     cfg = gen.CONFIGS["c3"]
     M, N, T, k, E, C = cfg["M"], cfg["N"], cfg["T"], cfg["k"], cfg["E"], cfg["C"]
     RB = cfg["H"] * 2
@@ -72,7 +74,7 @@ def main():
                 pipe.schedule_part(topk, lut)
             torch.cuda.synchronize()
             one, hist, node = [], [], []
-            for _ in range(20):
+            for _ in range(40):
                 before(mode)
                 a, b = ev(), ev()
                 a.record()
