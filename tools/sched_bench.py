@@ -94,6 +94,10 @@ def bench_routing(res, name, U):
                               (pipe.counts, pipe.msg, pipe.rank))
     th["loop_hot_us"] = loop_us(lambda: hb(None))
     tf = timeit(fused)
+    fb = rails.bind_schedule_eval(pipe.tp, pipe.sh, pipe.msg, pipe.sched, pipe.ev, pipe.ws,
+                                  final=pipe.final, rail_base=pipe.rail_base,
+                                  rail_total=pipe.total)
+    tf["loop_hot_us"] = loop_us(lambda: fb(None))
     split = lambda: (rails.lpt_schedule(pipe.tp, pipe.sh, pipe.msg, out=pipe.sched,  # noqa: E731
                                         workspace=pipe.ws),
                      rails.eval(pipe.tp, pipe.sh, pipe.msg, pipe.sched, out=pipe.ev))
