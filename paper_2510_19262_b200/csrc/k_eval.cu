@@ -78,6 +78,19 @@ __global__ void __launch_bounds__(EV2_THREADS, 4)
     sCol[threadIdx.x] = 0;
     aRlo[threadIdx.x] = aRhi[threadIdx.x] = aElo[threadIdx.x] = aEhi[threadIdx.x] = 0u;
     cU[threadIdx.x] = aQlo[threadIdx.x] = aQhi[threadIdx.x] = 0u;
+    // block boundaries of this tile: full index at message (g, (f0+fl)*N), fl = 0..ft
+    // (N*(ft+1) <= 256 + N <= 2 per thread), loaded now so their latency overlaps
+    // stage 1; converted into sQ / sR after it
+    long long bnd[2] = {0, 0};
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int t = threadIdx.x + q * EV2_THREADS;
+      if (t < N * (ft + 1)) {
+        const int g = t / (ft + 1), fl = t - g * (ft + 1);
+        const long long p = (long long)g * G + (long long)(f0 + fl) * N;
+        bnd[q] = (p < NG) ? fbp[p] : nfull_node;
+      }
+    }
     __syncthreads();
     // stage 1: t = g * (ft*N) + rest with h = f0*N + rest; a thread takes one
     // `rest` for every g (small tiles: threads beyond the tile's width split g)
@@ -149,16 +162,17 @@ __global__ void __launch_bounds__(EV2_THREADS, 4)
         }
       }
     }
-    // block boundaries: full index at message (g, (f0+fl)*N), fl = 0..ft
-    for (int t = threadIdx.x; t < N * (ft + 1); t += EV2_THREADS) {
-      const int g = t / (ft + 1), fl = t - g * (ft + 1);
-      const long long p = (long long)g * G + (long long)(f0 + fl) * N;
-      const long long a = (p < NG) ? fbp[p] : nfull_node;
-      long long q;
-      int r;
-      divmod_n(a, N, q, r);
-      sQ[g * (FT + 1) + fl] = q;
-      sR[g * (FT + 1) + fl] = r;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int t = threadIdx.x + q * EV2_THREADS;
+      if (t < N * (ft + 1)) {
+        const int g = t / (ft + 1), fl = t - g * (ft + 1);
+        long long qq;
+        int r;
+        divmod_n(bnd[q], N, qq, r);
+        sQ[g * (FT + 1) + fl] = qq;
+        sR[g * (FT + 1) + fl] = r;
+      }
     }
     __syncthreads();
     // stage 2: thread per (fl, j).  When N divides the block, j = t mod N is the
