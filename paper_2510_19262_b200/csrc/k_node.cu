@@ -596,6 +596,7 @@ __global__ void __launch_bounds__(NODE_MAX_THREADS) k_node(NodeArgs a) {
       if ((threadIdx.x & 31) == 0) s_mx[q][threadIdx.x >> 5] = w;
     }
     __syncthreads();
+    NODE_TL(30);
     if (threadIdx.x == 0 && a.do_final) {
       // (the record's maxima and totals as this CTA just stored them; a four-warp
       // finalize from a shared copy measured ~1 us slower)

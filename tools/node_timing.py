@@ -50,7 +50,8 @@ def main():
              14: "A: first tile loads consumed", 15: "A: first tile scanned",
              16: "A: tiles done", 17: "A: key or/and reduced",
              12: "F: unit-last CTA elected", 18: "F: its fence done",
-             19: "F: record copied (thread 0)", 24: "chain second pass start (CHAIN_TWICE)"}
+             19: "F: record copied (thread 0)", 24: "chain second pass start (CHAIN_TWICE)",
+             30: "F: record copied (all threads)"}
     alone = lambda: rails.schedule_eval(  # noqa: E731
         pipe.tp, pipe.sh, pipe.msg, pipe.sched, pipe.ev, pipe.ws, final=pipe.final,
         rail_base=pipe.rail_base, rail_total=pipe.total)
