@@ -461,6 +461,25 @@ def test_config_c5_sweep_sampled(C):
         assert torch.equal(pipe.ev.S, pipe.sched.send_load)
 
 
+@pytest.mark.parametrize("C", [4 << 10, 64 << 10])
+def test_c5_family_small_chunks_full_eval(C):
+    """C5's receiver-skew Zipf family at the small chunk sizes where the full-size
+    sweep above only checks properties (the oracle materialises every chunk: 134 M at
+    4 KiB and 256 nodes): the same generator on 32 nodes x 8 rails, 16 MiB per source
+    GPU (32 K chunks per node at 4 KiB), schedule and evaluation exact for every node."""
+    cfg = dict(gen.CONFIGS["c5"])
+    cfg.update(M=32, V=16 << 20, C=C)
+    M, N = cfg["M"], cfg["N"]
+    msg = gen.d1_units(cfg, gen.config_seed(5), 0, 1)
+    pipe = MatrixPipeline(M, N, C, 1, 0, M, DEV)
+    pipe.step(torch.from_numpy(msg).to(DEV))
+    torch.cuda.synchronize()
+    scheds = [oracle.schedule_node(msg[0, d], C) for d in range(M)]
+    for d in range(M):
+        compare_schedule(pipe.sched, 0, d, scheds[d], f"C{C} d{d}")
+    _compare_eval(pipe, 0, 0, M, M, N, oracle_eval_from_scheds(M, N, msg[0], scheds))
+
+
 def test_determinism_repeat():
     M, N, T, k, E, RB, C = 6, 4, 700, 2, 8, 2048, 8192
     topk, lut = routing_inputs(M, N, T, k, E, 5, 0, 2)
