@@ -65,6 +65,12 @@ __global__ void __launch_bounds__(SORT_THREADS, 3)
   int64_t* __restrict__ fbg = full_base + seg * NG;
   const bool vec = aligned32(mg) && aligned32(fbg);  // 256-bit accesses (ld8/st8_s64)
   bool bad_range = false, bad_ovf = false;  // flagged once after the pass
+  // later tiles' messages requested into L2 now (their loads then wait on L2, not
+  // DRAM, behind each tile's block scan)
+  for (long long t0 = (long long)blockDim.x * IPT; t0 < NG; t0 += (long long)blockDim.x * IPT) {
+    const long long m0 = t0 + (long long)threadIdx.x * IPT;
+    if (m0 < NG) asm volatile("prefetch.global.L2 [%0];" ::"l"(mg + m0));
+  }
   for (long long t0 = 0; t0 < NG; t0 += (long long)blockDim.x * IPT) {
     const long long m0 = t0 + (long long)threadIdx.x * IPT;
     const bool whole = vec && m0 + IPT <= NG;
