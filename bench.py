@@ -433,6 +433,17 @@ def timed(step, steps, stream, dist, local, flush=None):
     return total, launches, clk.summary()
 
 
+# How the line maps onto BASELINE.json's metric ("LPT-scheduled nodes/sec and pack GB/s
+# (vs HBM peak) at 1/2/4/8 B200; makespan/OPT").
+METRIC_PARTS = {
+    "value": "(unit, node) schedules + packs completed per second: the whole step, pack "
+             "included (stricter than SURVEY d.1's pack-free nodes/s)",
+    "schedule_only": "BASELINE's 'LPT-scheduled nodes/sec' (pack excluded)",
+    "pack_gbs / roofline": "BASELINE's 'pack GB/s (vs HBM peak)'",
+    "quality": "BASELINE's 'makespan/OPT' (T/T*, makespan/LB with LB <= OPT)",
+}
+
+
 def sched_times(sev, kev, steps):
     """Per-step schedule-part times (ms) between the step's first event and the pack's
     start event.  Reported as the median: step 0 follows the synchronize that opens
@@ -626,7 +637,8 @@ def run_routing(args, cfg, rank, world, local, dev, dist):
     out = {"metric": METRIC, "value": value, "unit": "nodes/s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
-           "dtype": "int64", "data": "synthetic", "config": arm_config(args, P, nd)}
+           "dtype": "int64", "data": "synthetic", "config": arm_config(args, P, nd),
+           "metric_parts": METRIC_PARTS}
     sched_ms = max_over_ranks(sched_ms, dist, dev)
     out["schedule_only"] = {
         "value": nodes / (sched_ms / 1000.0), "unit": "nodes/s", "ms_per_step": sched_ms,
@@ -875,7 +887,7 @@ def run_c4(args, cfg, rank, world, local, dev, dist):
            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-           "config": arm_config(args, P),
+           "config": arm_config(args, P), "metric_parts": METRIC_PARTS,
            "schedule_only": {"value": nodes / (sched_ms / 1000.0), "unit": "nodes/s",
                              "ms_per_step": sched_ms,
                              "stat": "median over the timed steps (max over ranks)",
