@@ -15,8 +15,10 @@
 //    ties: the rail is the low key bits) and an assignment is one compare/select
 //    merge.  Loads are relative to an exact int64 `base`, rebased when the minimum
 //    passes 2^23.  Runs of equal sizes (routing traffic has only C / row_bytes
-//    distinct remainder sizes) are dealt by an exact closed form written by all 32
-//    lanes; aligned groups of 8 equal sizes by a warp scan; other items 8 at a time.
+//    distinct remainder sizes) are dealt by an exact closed form: written by all 32
+//    lanes, or -- given a RunList (the fused node kernel) -- recorded as (start
+//    state, length) and written by the whole CTA after the chain; aligned groups of
+//    8 equal sizes by a warp scan; other items 8 at a time.
 //  * lpt_chain_generic (any N <= 32, any C): lane j holds rail j's load; the
 //    argmin with lowest-index tie is one redux.sync.min on (rel << 5) | j when
 //    C < 2^26, else a 64-bit butterfly over (load, lane).
