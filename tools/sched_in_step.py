@@ -73,9 +73,12 @@ def main():
                 before(mode)
                 pipe.schedule_part(topk, lut)
             torch.cuda.synchronize()
-            one, hist, node = [], [], []
+            one, hist, node, pk = [], [], [], []
             for _ in range(40):
+                p0, p1 = ev(), ev()
+                p0.record()
                 before(mode)
+                p1.record()
                 a, b = ev(), ev()
                 a.record()
                 pipe.schedule_part(topk, lut)
@@ -89,12 +92,13 @@ def main():
                 e.record()
                 torch.cuda.synchronize()
                 one.append(a.elapsed_time(b) * 1e3)
+                pk.append(p0.elapsed_time(p1) * 1e3)
                 hist.append(c.elapsed_time(d) * 1e3)
                 node.append(d.elapsed_time(e) * 1e3)
             rails.check()
             med = lambda v: round(sorted(v)[len(v) // 2], 2)  # noqa: E731
             res[mode] = {"schedule_part_us": med(one), "histogram_us": med(hist),
-                         "schedule_eval_us": med(node)}
+                         "schedule_eval_us": med(node), "before_us": med(pk)}
     res["clocks"] = clk.summary()
     print(json.dumps(res, indent=1))
 
