@@ -235,14 +235,15 @@ __global__ void __launch_bounds__(CHAIN_WARPS * 32)
 }
 
 // Few long chains or many: one chain per warp.  All 32 lanes stream the sorted
-// remainder list through a double-buffered shared-memory stage with coalesced loads,
-// one batch ahead, and all run the same (warp-uniform) register state.  A run of
+// remainder list through a double-buffered shared-memory stage filled by cp.async
+// (512 sizes per batch, one batch ahead, no staging registers: 62 registers), and all
+// run the same (warp-uniform) register state.  A run of
 // >= 32 equal sizes -- routing traffic has only C / row_bytes distinct remainder
 // sizes -- is assigned by single network steps until the cyclic condition holds,
 // then written by the whole warp (lpt_run_cyclic); other items go eight at a time
 // through lpt_group8_v with lane 0 storing.
 constexpr int WS_WARPS = 4;
-constexpr int WS_BATCH = 256;
+constexpr int WS_BATCH = 512;
 
 template <int NT>
 __global__ void __launch_bounds__(WS_WARPS * 32, 7)  // <= 72 registers: C4 (1024 CTAs) fits one wave
@@ -267,27 +268,26 @@ __global__ void __launch_bounds__(WS_WARPS * 32, 7)  // <= 72 registers: C4 (102
     K[i] = (((i < NT - r) ? 0u : (uint32_t)C) << 5) | (uint32_t)rail;
   }
   constexpr int PL = WS_BATCH / 32;
-  uint32_t pw[PL];
+  // batch b (WS_BATCH sizes) -> sW[wid][buf] by cp.async (zero-filled past nr): the
+  // next batch lands in shared memory while this one is assigned, with no registers
+  auto issue = [&](int b, int buf) {
 #pragma unroll
-  for (int p = 0; p < PL; ++p) {
-    const int i = p * 32 + lane;
-    pw[p] = i < nr ? gw[i] : 0u;
-  }
+    for (int p = 0; p < PL; ++p) {
+      const int i = b + p * 32 + lane;
+      const bool in = i < nr;
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(&sW[wid][buf][p * 32 + lane]);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst),
+                   "l"(in ? gw + i : gw), "r"(in ? 4 : 0)
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  issue(0, 0);
   int cur = 0;
   for (int b0 = 0; b0 < nr; b0 += WS_BATCH) {
-    uint32_t cw[PL];
-#pragma unroll
-    for (int p = 0; p < PL; ++p) {
-      sW[wid][cur][p * 32 + lane] = pw[p];
-      cw[p] = pw[p];
-    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncwarp();
-    const int nb = b0 + WS_BATCH;  // prefetch the next batch while this one is assigned
-#pragma unroll
-    for (int p = 0; p < PL; ++p) {
-      const int i = nb + p * 32 + lane;
-      pw[p] = i < nr ? gw[i] : 0u;
-    }
+    if (b0 + WS_BATCH < nr) issue(b0 + WS_BATCH, cur ^ 1);
     const int cnt = min(WS_BATCH, nr - b0);
     const uint32_t* w_ = sW[wid][cur];
     uint64_t* rb = res + b0;
@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(WS_WARPS * 32, 7)  // <= 72 registers: C4 (102
 #pragma unroll
         for (int p = 0; p < PL; ++p) {
           const int j = p * 32 + lane;
-          e += __popc(__ballot_sync(0xffffffffu, j >= i && j < cnt && cw[p] == w));
+          e += __popc(__ballot_sync(0xffffffffu, j >= i && j < cnt && w_[j] == w));
         }
         while (i < e && K[NT - 1] - K[0] >= (w << 5)) {
           const uint64_t r = lpt_step_v<NT>(K, w, base);
