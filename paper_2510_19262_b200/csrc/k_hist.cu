@@ -88,11 +88,13 @@ __global__ void __launch_bounds__(HR_MAX_WARPS * 32, 4)  // 4 x 16 warps per SM:
   for (int off = 0; beg + off < end; off += 32 * UNR) {
     int hv[UNR];
     fetch(off, hv);
+    const bool full = beg + off + 32 * UNR <= end;  // warp-uniform: no per-entry bounds test
 #pragma unroll
     for (int j = 0; j < UNR; ++j) {
-      bad |= hv[j] < 0 && beg + off + j * 32 + lane < end;
+      const bool in = full || beg + off + j * 32 + lane < end;
+      bad |= hv[j] < 0 && in;
       if (hv[j] >= 0) atomicAdd(&my[hv[j]], 1);  // private to this warp: order-free count
-      if (STASH && beg + off + j * 32 + lane < end) stash[off + j * 32] = (uint16_t)hv[j];
+      if (STASH && in) stash[off + j * 32] = (uint16_t)hv[j];
     }
   }
   if (bad) flag_error(err, ERR_RANGE);
@@ -118,10 +120,11 @@ __global__ void __launch_bounds__(HR_MAX_WARPS * 32, 4)  // 4 x 16 warps per SM:
   const unsigned lt = lanemask_lt();
   for (int off = 0; beg + off < end; off += 32 * UNR) {
     int hv[UNR];
+    const bool full = beg + off + 32 * UNR <= end;
     if (STASH) {
 #pragma unroll
       for (int j = 0; j < UNR; ++j) {
-        const int v = beg + off + j * 32 + lane < end ? stash[off + j * 32] : 0xffff;
+        const int v = (full || beg + off + j * 32 + lane < end) ? stash[off + j * 32] : 0xffff;
         hv[j] = v == 0xffff ? -1 : v;  // invalid entries were stashed as 0xffff
       }
     } else {
@@ -129,7 +132,7 @@ __global__ void __launch_bounds__(HR_MAX_WARPS * 32, 4)  // 4 x 16 warps per SM:
     }
 #pragma unroll
     for (int j = 0; j < UNR; ++j) {
-      const bool in = beg + off + j * 32 + lane < end;
+      const bool in = full || beg + off + j * 32 + lane < end;
       const int h = hv[j];
       const bool valid = h >= 0;
       if constexpr (TAG) {
