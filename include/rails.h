@@ -85,6 +85,8 @@ typedef struct {
  *              source node (R#2);
  *   row_rank   int32 [U][nd][N][T][k]  number of earlier (t',s') (in (t,s) order)
  *              of the same GPU g with the same destination h; may be NULL.
+ *   T, k       tokens per GPU >= 1, slots per token 1..32, T*k <= 2^30 (else
+ *              RAILS_EINVAL before any launch).
  * Out-of-range ids set RAILS_ERANGE in the device flag; such slots are skipped. */
 int rails_histogram(const rails_topo_t* topo, const rails_shard_t* shard,
                     int32_t T, int32_t k, const int32_t* topk_inst,

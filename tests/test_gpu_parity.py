@@ -334,6 +334,8 @@ def _oracle_pack_check(pipe, topk, lut, x, u, dl, scheds_oracle=None):
     (5, 8, 128, 2, 8, 12288, 32768, 1, 0, 5),   # C4 row size (12 KiB) straddling 32 KiB
     (3, 2, 40, 2, 4, 20480, 8192, 1, 0, 3),     # rows > 16 KiB window, multi-piece
     (2, 32, 64, 4, 32, 256, 1024, 1, 0, 2),     # N = 32 rails (maximum), G = 64
+    (4, 4, 1, 2, 8, 8192, 32768, 1, 0, 4),      # T = 1: one token row per GPU
+    (3, 4, 2, 1, 8, 16, 4096, 2, 0, 3),         # T = 2, 16-byte rows, every message < C
 ])
 def test_pack_parity(M, N, T, k, E, RB, C, U, d0, nd):
     topk_all, lut = routing_inputs(M, N, T, k, E, 7, 0, U)
@@ -560,6 +562,8 @@ def _hist_check(M, N, T, k, E, U, nd, RB=4096, with_rank=True, seed=17, nodes=No
     (64, 8, 777, 2, 8, 5, 64, True),        # ragged last batch, shared LUT
     (128, 8, 300, 2, 8, 3, 128, False),     # no ranks
     (600, 8, 64, 2, 8, 1, 300, True),       # n_inst = 4800: LUT read through L1
+    (4, 4, 1, 2, 8, 600, 4, True),          # T = 1: two entries per segment
+    (8, 4, 5, 3, 8, 300, 8, True),          # T*k = 15 < 32: one partial group
 ])
 def test_histogram_parity_batched(M, N, T, k, E, U, nd, with_rank):
     """>= 16 segments per SM: the warp-per-segment atomic-ranking kernel."""
@@ -574,10 +578,23 @@ def test_histogram_parity_batched(M, N, T, k, E, U, nd, with_rank):
     (300, 8, 500, 2, 8, 2),       # G = 2400: 4 warps (sub-histograms in 64 KiB)
     (1500, 8, 200, 2, 8, 1),      # G = 12000: 2 warps
     (5000, 4, 64, 2, 4, 1),       # G = 20000: 1 warp
+    (4, 4, 1, 1, 8, 2),           # T*k = 1: 15 of the 16 warps have no entries
+    (64, 8, 3, 2, 8, 2),          # T*k = 6, G = 512
+    (16, 8, 37, 3, 8, 2),         # T*k = 111: ragged, fewer entries than 16 x 32
 ])
 def test_histogram_parity_few_segments(M, N, T, k, E, nd):
     """Few segments: W warps per segment (by G), two passes, tag-trick ranks."""
     _hist_check(M, N, T, k, E, 1, nd)
+
+
+def test_histogram_zero_tokens_rejected():
+    """T = 0 is not a routing step (rails.h: T >= 1): EINVAL before any launch."""
+    M, N = 2, 2
+    topk = torch.zeros((1, 2, N, 0, 2), dtype=torch.int32, device=DEV)
+    lut = torch.arange(4, dtype=torch.int32, device=DEV)
+    with pytest.raises(rails.RailsError) as ei:
+        rails.histogram(rails.topo(M, N, 4096), rails.shard(1, 0, 2), topk, lut, 16)
+    assert ei.value.code == rails.RAILS_EINVAL
 
 
 def test_histogram_parity_huge_segment():
