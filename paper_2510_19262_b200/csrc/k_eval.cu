@@ -31,8 +31,12 @@ namespace rails {
 
 constexpr int EV2_THREADS = 256;
 
-template <int NT>  // NT = 8 (divisions by shifts) or 0 (runtime N)
-__global__ void __launch_bounds__(EV2_THREADS, 4)
+// NT = 8 (divisions by shifts) or 0 (runtime N).  MINB: CTAs per SM the registers
+// are capped for -- 4 (64 registers) in general; 6 (40) when one tile holds every
+// destination (M*N < 256, several source GPUs per thread: C2 757 -> 714 us, while
+// C4's wide tiles lose 35 us at 6)
+template <int NT, int MINB = 4>
+__global__ void __launch_bounds__(EV2_THREADS, MINB)
     k_eval_node(int M, int N_rt, int nd, int d0, long long C, int cshift, uint64_t seed, int FT,
                 const int64_t* __restrict__ msg, const int64_t* __restrict__ full_base,
                 const int8_t* __restrict__ rem_rail, const int64_t* __restrict__ n_full,
@@ -405,7 +409,8 @@ cudaError_t launch_eval(const LaunchCtx& c, int U, int nd, int d0, int M, int N,
   if (err != cudaSuccess) return err;
   const int FT = (EV2_THREADS / N) < 64 ? (EV2_THREADS / N) : 64;
   const size_t smem = 16 + (size_t)N * (FT + 1) * (8 + 4);
-  auto kern = N == 8 ? k_eval_node<8> : k_eval_node<0>;
+  const bool narrow = (long long)M * N < EV2_THREADS;
+  auto kern = N == 8 ? (narrow ? k_eval_node<8, 6> : k_eval_node<8>) : k_eval_node<0>;
   err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   kern<<<(unsigned)((long long)U * nd), EV2_THREADS, smem, c.stream>>>(
