@@ -21,9 +21,10 @@
 namespace rails {
 
 constexpr int SORT_THREADS = 256;
+constexpr int CS_NARROW_MINB = 8;  // 128-thread sorts (N*G <= 2048): 64 registers, 8 CTAs per SM
 
-template <typename KeyT, typename IdxT, bool SMEM>
-__global__ void __launch_bounds__(SORT_THREADS, 3)
+template <typename KeyT, typename IdxT, bool SMEM, int MAXT = SORT_THREADS, int MINB = 3>
+__global__ void __launch_bounds__(MAXT, MINB)
     k_chunk_sort(const int64_t* __restrict__ msg, long long NG, int N, int d0, int nd,
                  long long C, int cshift, int nbits, int64_t* __restrict__ full_base,
                  int32_t* __restrict__ ws_inv, int64_t* __restrict__ n_full_out,
@@ -443,7 +444,11 @@ cudaError_t launch_chains(const LaunchCtx& c, int U, int nd, int d0, int M, int 
   if (NG <= 16384 && smem <= 200 * 1024) {
     // 16-bit keys when C <= 65536 and 16-bit indices: several CTAs per SM
     const int thr = NG <= 2048 ? 128 : SORT_THREADS;
-    auto kern = k16 ? k_chunk_sort<uint16_t, uint16_t, true> : k_chunk_sort<uint32_t, uint16_t, true>;
+    auto kern = thr == 128
+                    ? (k16 ? k_chunk_sort<uint16_t, uint16_t, true, 128, CS_NARROW_MINB>
+                           : k_chunk_sort<uint32_t, uint16_t, true, 128, CS_NARROW_MINB>)
+                    : (k16 ? k_chunk_sort<uint16_t, uint16_t, true>
+                           : k_chunk_sort<uint32_t, uint16_t, true>);
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     kern<<<(unsigned)nseg, thr, smem, c.stream>>>(msg, NG, N, d0, nd, C, cshift, nbits,
